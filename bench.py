@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""Benchmark: earliest-arrival traversal on BASELINE config 2 (RMAT-22).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json): temporal edges traversed per second (TEPS) on one
+B200, TEPS = E_adm / t with E_adm the admissible window edges of the reached
+vertices, plus the roofline of the traversal kernel against
+the measured HBM copy bandwidth. A step is one EA query over the whole
+device-resident graph (labels re-initialised every step).
+
+N > 1 runs N independent replicas (one process per GPU, no data-path
+collective: the path does not shard); value = all ranks'
+edges / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG = "c2"
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.index = index
+        self.period = period
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profile_traffic():
+    """DRAM bytes per traversal launch from the committed ncu --set full capture."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(CONFIG)
+    return None
+
+
+def pick_queries(T, g, wl):
+    out_deg = g.degrees(T.Direction.OUT)
+    in_deg = g.degrees(T.Direction.IN)
+    return wl.queries(out_deg, in_deg, g.vertex_count())
+
+
+def cpu_reference_run(wl, edges, n, q, threads, steps, warmup):
+    """Times the reference library (oracle/_ref, compiled unmodified from the
+    reference sources) on the same edge list and query: returns per-query s."""
+    from oracle.pyoracle import Reference
+
+    Reference.set_workers(threads)
+    t0 = time.perf_counter()
+    ref = Reference(edges, n, True, wl.index_cutoff)
+    build_s = time.perf_counter() - t0
+    labels = None
+    for _ in range(warmup):
+        labels = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        labels = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+        times.append(time.perf_counter() - t)
+    ref.close()
+    return times, build_s, labels
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return 0
+    import paper_2401_02563_b200 as T
+    from paper_2401_02563_b200.configs import workload
+    from oracle.pyoracle import Oracle, Reference
+
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtgxref.so missing"}))
+        return 0
+    wl = workload(CONFIG)
+    edges = T.generate_edges(wl.gen)
+    n = wl.gen.n_vertices
+    out_deg = np.bincount(edges[0], minlength=n)
+    in_deg = np.bincount(edges[1], minlength=n)
+    q = wl.queries(out_deg, in_deg, n)[0]
+    threads = os.cpu_count() or 1
+    times, build_s, labels = cpu_reference_run(wl, edges, n, q, threads, args.steps, args.warmup)
+    o = Oracle(edges, n)
+    e_adm, v_reached = o.work(q.kind, q.vertex, q.window.t_a, q.window.t_b, labels)
+    o.close()
+    t = sum(times) / len(times)
+    value = e_adm / t
+    line = {
+        "impl": "reference",
+        "metric": "temporal edges traversed/sec (TEPS)",
+        "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{CONFIG}: {wl.describe}", "source": q.vertex,
+                   "window": [q.window.t_a, q.window.t_b], "n": n, "m": int(len(edges[0])),
+                   "e_adm": e_adm, "v_reached": v_reached, "graph_build_s": build_s},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} full {CONFIG} EA queries"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    rank, world, local = _dist()
+    import paper_2401_02563_b200 as T
+    from paper_2401_02563_b200.configs import workload
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_mod
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    else:
+        try:
+            import torch
+            torch.cuda.set_device(local)
+        except Exception:
+            torch = None
+    import torch  # noqa: F811
+
+    lib = T.load_library()
+    wl = workload(CONFIG)
+    g = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
+    q = pick_queries(T, g, wl)[0]
+    n = g.vertex_count()
+
+    # unit of work from the final labels (untimed)
+    T.query_batch(g, q.kind, [q.vertex], [q.window], width=4)
+    e_adm, v_reached = T.last_work(g, 0)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        total_ms, kernel_ms = T.time_queries(g, q.kind, [q.vertex], [q.window],
+                                             warmup=args.warmup, steps=args.steps)
+    barrier()
+    ms_step = total_ms / args.steps
+    if dist:
+        t = torch.tensor([ms_step, kernel_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, kernel_ms = float(t[0]), float(t[1])
+    value = world * e_adm / (ms_step * 1e-3)
+
+    # end to end through the reference-facing C-ABI call with a host output
+    # (int64 PathResult values): H2D of the query, D2H of the labels per step
+    out = np.empty(n, np.int64)
+    import ctypes
+    for _ in range(args.warmup):
+        T._check(lib.tgxd_earliest_arrival(g.handle, q.vertex, q.window.t_a, q.window.t_b, 1,
+                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                           None))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        T._check(lib.tgxd_earliest_arrival(g.handle, q.vertex, q.window.t_a, q.window.t_b, 1,
+                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                           None))
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e_value = world * e_adm / e2e_s
+
+    peak, peak_kind = measured_peak()
+    b_alg = 16 * e_adm + 12 * v_reached + 4 * n
+    achieved = b_alg / (kernel_ms * 1e-3) / 1e9
+    traffic = profile_traffic()
+    line = {
+        "metric": "temporal edges traversed/sec (TEPS)",
+        "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{CONFIG}: {wl.describe}", "source": q.vertex,
+                   "window": [q.window.t_a, q.window.t_b], "n": n, "m": g.edge_count(),
+                   "e_adm": e_adm, "v_reached": v_reached,
+                   "l2": "inputs larger than L2 (edge arrays 12 B/edge x 67M = 805 MB)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "traverse_kernel", "kernel_ms": kernel_ms,
+                     "algorithmic_bytes": b_alg, "peak_kind": peak_kind},
+        "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": 4 * args.steps,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, q, n)
+    if rank == 0:
+        print(json.dumps(line))
+    g.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(wl, q, n):
+    """The reference CPU path on the box's host cores, one full C2 query
+    (graph generation and build untimed), or the C oracle if the reference
+    library did not travel."""
+    import paper_2401_02563_b200 as T
+    from oracle.pyoracle import Oracle, Reference
+
+    edges = T.generate_edges(wl.gen)
+    threads = os.cpu_count() or 1
+    if Reference.available():
+        times, _, labels = cpu_reference_run(wl, edges, n, q, threads, 1, 0)
+        kind = "reference"
+    else:
+        o = Oracle(edges, n)
+        t = time.perf_counter()
+        labels = o.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+        times = [time.perf_counter() - t]
+        o.close()
+        kind, threads = "port", 1
+    o = Oracle(edges, n)
+    e_adm, _ = o.work(q.kind, q.vertex, q.window.t_a, q.window.t_b, labels)
+    o.close()
+    return {"value": e_adm / times[0], "unit": "edges/s", "cores": threads, "kind": kind,
+            "sample": f"1 full {CONFIG} EA query ({times[0]:.3f} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

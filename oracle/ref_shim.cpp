@@ -1,0 +1,135 @@
+// TEST INFRASTRUCTURE ONLY — never linked into or called by the product.
+//
+// extern "C" wrapper around the UNMODIFIED reference library (`tgx`, compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It lets
+// the Python tests, the golden-vector script and bench.py's reference arm call
+// the reference's own entry points through ctypes:
+//   TemporalGraph::build           /root/reference/proj/include/tgx/engine.hpp:32-33
+//   earliest_arrival / latest_departure / fastest_path
+//                                  /root/reference/proj/include/tgx/algorithms.hpp:46-58
+//   oracle::enumerate_paths        /root/reference/proj/tests/support/oracle.hpp:27-29
+//   set_workers / num_workers      /root/reference/proj/include/tgx/parallel.hpp:19-21
+// Exceptions are mapped to integer codes (1 out_of_range, 2 invalid_argument,
+// 3 anything else) and the message is kept for tgxref_last_error().
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "support/oracle.hpp"
+#include "tgx/algorithms.hpp"
+#include "tgx/digest.hpp"
+#include "tgx/engine.hpp"
+#include "tgx/parallel.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+std::vector<tgx::TemporalEdge> edges_of(std::uint64_t m, const std::uint32_t* src,
+                                        const std::uint32_t* dst, const std::uint64_t* start,
+                                        const std::uint64_t* end) {
+  std::vector<tgx::TemporalEdge> edges(m);
+  for (std::uint64_t i = 0; i < m; ++i) {
+    edges[i] = tgx::TemporalEdge{src[i], dst[i], start[i], end[i], 1.0};
+  }
+  return edges;
+}
+
+tgx::Ordering ordering_of(int o) {
+  switch (o) {
+    case 0: return tgx::Ordering::Succeeds;
+    case 2: return tgx::Ordering::Overlaps;
+    default: return tgx::Ordering::StrictlySucceeds;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tgxref_last_error() { return g_err.c_str(); }
+
+void tgxref_set_workers(int n) { tgx::set_workers(n); }
+int tgxref_num_workers() { return tgx::num_workers(); }
+
+int tgxref_build(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
+                 const std::uint32_t* dst, const std::uint64_t* start, const std::uint64_t* end,
+                 int directed, std::uint64_t index_cutoff, void** out) {
+  *out = nullptr;
+  return guarded([&] {
+    tgx::EngineConfig cfg;
+    if (index_cutoff != 0) cfg.index_cutoff = index_cutoff;
+    auto* g = new tgx::TemporalGraph(
+        tgx::TemporalGraph::build(edges_of(m, src, dst, start, end), n, directed != 0, cfg));
+    *out = g;
+  });
+}
+
+void tgxref_free(void* g) { delete static_cast<tgx::TemporalGraph*>(g); }
+
+// kind: 0 earliest arrival, 1 latest departure, 2 fastest.
+// force: -1 graph default, 0 auto, 1 index, 2 scan.
+int tgxref_query(void* gp, int kind, std::uint32_t vertex, std::uint64_t ta, std::uint64_t tb,
+                 int ordering, int force, std::int64_t* out) {
+  return guarded([&] {
+    const auto& g = *static_cast<const tgx::TemporalGraph*>(gp);
+    tgx::AlgoOptions opts;
+    opts.ordering = ordering_of(ordering);
+    if (force >= 0) {
+      opts.force_access = force == 1   ? tgx::ForceAccess::Index
+                          : force == 2 ? tgx::ForceAccess::Scan
+                                       : tgx::ForceAccess::Auto;
+    }
+    const tgx::QueryWindow w{ta, tb};
+    tgx::PathResult r;
+    switch (kind) {
+      case 0: r = tgx::earliest_arrival(g, vertex, w, opts); break;
+      case 1: r = tgx::latest_departure(g, vertex, w, opts); break;
+      case 2: r = tgx::fastest_path(g, vertex, w, opts); break;
+      default: throw std::invalid_argument("unknown query kind");
+    }
+    std::memcpy(out, r.values.data(), r.values.size() * sizeof(std::int64_t));
+  });
+}
+
+// metric: 0 EA, 1 LD, 2 fastest (oracle::PathMetric order).
+int tgxref_enumerate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
+                     const std::uint32_t* dst, const std::uint64_t* start,
+                     const std::uint64_t* end, std::uint32_t vertex, std::uint64_t ta,
+                     std::uint64_t tb, int ordering, int metric, std::int64_t* out) {
+  return guarded([&] {
+    const auto edges = edges_of(m, src, dst, start, end);
+    const auto pm = static_cast<tgx::oracle::PathMetric>(metric);
+    const tgx::PathResult r =
+        tgx::oracle::enumerate_paths(edges, n, vertex, tgx::QueryWindow{ta, tb},
+                                     ordering_of(ordering), pm);
+    std::memcpy(out, r.values.data(), r.values.size() * sizeof(std::int64_t));
+  });
+}
+
+std::uint64_t tgxref_digest(const std::int64_t* values, std::uint64_t n) {
+  return tgx::digest_of(std::span<const std::int64_t>(values, n));
+}
+
+}  // extern "C"

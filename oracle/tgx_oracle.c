@@ -1,0 +1,568 @@
+/* TEST INFRASTRUCTURE ONLY — the checker, never the product.
+ *
+ * Plain-C restatement of the reference (Kairos "tgx", /root/reference/proj)
+ * algorithms on the traversal hot path. Every function cites the reference
+ * lines it follows. The restatement keeps the reference's data model
+ * (u64 timestamps, int64 labels, INT64_MAX / INT64_MIN sentinels) and its
+ * round-synchronous label-correcting schedule (snapshot per round, stamp
+ * claim per round). Like the reference's engine it relaxes only a frontier
+ * vertex's window edges; it always uses the sparse (push) representation —
+ * the reference pins push/pull equivalence in test_engine.cpp:153-176 — and
+ * it locates a segment's first admissible edge by binary search instead of
+ * scanning from the segment start (tcsr.hpp:60-69 scans and filters; the set
+ * of edges handed to `update` is identical because segments are sorted by
+ * start).
+ *
+ * Pinned by tests/test_oracle.py against the compiled reference
+ * (oracle/_ref/libtgxref.so) on thousands of random instances and against
+ * the committed golden vectors in tests/golden/.
+ */
+#include "tgx_oracle.h"
+
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define INF64 ((int64_t)0x7fffffffffffffffLL)    /* PathResult::kUnreachedMin, algorithms.hpp:17 */
+#define NEGINF64 ((int64_t)(-0x7fffffffffffffffLL - 1)) /* kUnreachedMax, algorithms.hpp:18 */
+#define TIME_LIMIT ((uint64_t)0x7fffffffffffffffULL)    /* internal.hpp:17-25, types.cpp:29 */
+
+static _Thread_local char g_err[256];
+
+const char* tgxo_last_error(void) { return g_err; }
+
+static int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+/* One T-CSR layout (tcsr.hpp:27-85): offsets, neighbor, start, end. */
+typedef struct {
+  uint64_t* off;
+  uint32_t* nbr;
+  uint64_t* st;
+  uint64_t* en;
+} ocsr;
+
+struct tgxo_graph {
+  uint32_t n;
+  uint64_t m; /* materialized edge count per layout */
+  ocsr out, in;
+};
+
+typedef struct {
+  uint64_t s, e;
+  uint32_t nbr;
+} orec;
+
+/* Segment order (start, end, neighbor), tcsr.cpp:12-15 (weights are all 1.0
+ * through this interface, so the weight tiebreak never fires). */
+static int rec_cmp(const void* a, const void* b) {
+  const orec* x = (const orec*)a;
+  const orec* y = (const orec*)b;
+  if (x->s != y->s) return x->s < y->s ? -1 : 1;
+  if (x->e != y->e) return x->e < y->e ? -1 : 1;
+  if (x->nbr != y->nbr) return x->nbr < y->nbr ? -1 : 1;
+  return 0;
+}
+
+/* TemporalCsr::build, tcsr.cpp:19-84: count, exclusive scan, placement,
+ * per-segment sort, split into flat arrays. */
+static int build_csr(ocsr* c, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                     const uint64_t* st, const uint64_t* en, int by_dst) {
+  c->off = calloc((size_t)n + 1, sizeof(uint64_t));
+  c->nbr = malloc((m ? m : 1) * sizeof(uint32_t));
+  c->st = malloc((m ? m : 1) * sizeof(uint64_t));
+  c->en = malloc((m ? m : 1) * sizeof(uint64_t));
+  orec* rec = malloc((m ? m : 1) * sizeof(orec));
+  uint64_t* cur = malloc(((size_t)n + 1) * sizeof(uint64_t));
+  if (!c->off || !c->nbr || !c->st || !c->en || !rec || !cur) {
+    free(rec);
+    free(cur);
+    return fail(TGXO_INVALID_ARGUMENT, "oracle: out of host memory");
+  }
+  for (uint64_t i = 0; i < m; ++i) c->off[(by_dst ? dst[i] : src[i]) + 1]++;
+  for (uint32_t v = 0; v < n; ++v) c->off[v + 1] += c->off[v];
+  memcpy(cur, c->off, ((size_t)n + 1) * sizeof(uint64_t));
+  for (uint64_t i = 0; i < m; ++i) {
+    const uint32_t key = by_dst ? dst[i] : src[i];
+    const uint64_t slot = cur[key]++;
+    rec[slot].s = st[i];
+    rec[slot].e = en[i];
+    rec[slot].nbr = by_dst ? src[i] : dst[i];
+  }
+  for (uint32_t v = 0; v < n; ++v) {
+    const uint64_t lo = c->off[v], hi = c->off[v + 1];
+    if (hi - lo > 1) qsort(rec + lo, hi - lo, sizeof(orec), rec_cmp);
+  }
+  for (uint64_t i = 0; i < m; ++i) {
+    c->nbr[i] = rec[i].nbr;
+    c->st[i] = rec[i].s;
+    c->en[i] = rec[i].e;
+  }
+  free(rec);
+  free(cur);
+  return TGXO_OK;
+}
+
+static void free_csr(ocsr* c) {
+  free(c->off);
+  free(c->nbr);
+  free(c->st);
+  free(c->en);
+}
+
+void tgxo_graph_free(tgxo_graph* g) {
+  if (!g) return;
+  free_csr(&g->out);
+  free_csr(&g->in);
+  free(g);
+}
+
+uint64_t tgxo_graph_edges(const tgxo_graph* g) { return g->m; }
+
+/* TemporalGraph::build, engine.cpp:7-34, with compute_meta's validation
+ * (types.cpp:19-56): endpoints < n, end >= start, end <= 2^63-1, first
+ * offending edge reported; undirected inputs materialize the reverse of every
+ * non-self-loop edge (engine.cpp:13-22). */
+int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                     const uint64_t* start, const uint64_t* end, int directed, tgxo_graph** out) {
+  *out = NULL;
+  for (uint64_t i = 0; i < m; ++i) {
+    char msg[160];
+    if (src[i] >= n || dst[i] >= n) {
+      snprintf(msg, sizeof msg, "edge %llu: endpoint outside vertex range", (unsigned long long)i);
+      return fail(TGXO_OUT_OF_RANGE, msg);
+    }
+    if (end[i] < start[i]) {
+      snprintf(msg, sizeof msg, "edge %llu: end precedes start", (unsigned long long)i);
+      return fail(TGXO_OUT_OF_RANGE, msg);
+    }
+    if (end[i] > TIME_LIMIT) {
+      snprintf(msg, sizeof msg, "edge %llu: end beyond 2^63-1", (unsigned long long)i);
+      return fail(TGXO_OUT_OF_RANGE, msg);
+    }
+  }
+  const uint32_t* s = src;
+  const uint32_t* d = dst;
+  const uint64_t* a = start;
+  const uint64_t* b = end;
+  uint64_t mm = m;
+  uint32_t *s2 = NULL, *d2 = NULL;
+  uint64_t *a2 = NULL, *b2 = NULL;
+  if (!directed) {
+    uint64_t extra = 0;
+    for (uint64_t i = 0; i < m; ++i) extra += src[i] != dst[i];
+    mm = m + extra;
+    s2 = malloc((mm ? mm : 1) * 4);
+    d2 = malloc((mm ? mm : 1) * 4);
+    a2 = malloc((mm ? mm : 1) * 8);
+    b2 = malloc((mm ? mm : 1) * 8);
+    memcpy(s2, src, m * 4);
+    memcpy(d2, dst, m * 4);
+    memcpy(a2, start, m * 8);
+    memcpy(b2, end, m * 8);
+    uint64_t k = m;
+    for (uint64_t i = 0; i < m; ++i) {
+      if (src[i] == dst[i]) continue;
+      s2[k] = dst[i];
+      d2[k] = src[i];
+      a2[k] = start[i];
+      b2[k] = end[i];
+      ++k;
+    }
+    s = s2;
+    d = d2;
+    a = a2;
+    b = b2;
+  }
+  tgxo_graph* g = calloc(1, sizeof(tgxo_graph));
+  g->n = n;
+  g->m = mm;
+  int rc = build_csr(&g->out, n, mm, s, d, a, b, 0);
+  if (rc == TGXO_OK) rc = build_csr(&g->in, n, mm, s, d, a, b, 1);
+  free(s2);
+  free(d2);
+  free(a2);
+  free(b2);
+  if (rc != TGXO_OK) {
+    tgxo_graph_free(g);
+    return rc;
+  }
+  *out = g;
+  return TGXO_OK;
+}
+
+/* First position in [lo, hi) whose start >= t (segment sorted by start). */
+static uint64_t lower_start(const ocsr* c, uint64_t lo, uint64_t hi, uint64_t t) {
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (c->st[mid] < t) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+/* Growable vertex list. */
+typedef struct {
+  uint32_t* v;
+  uint64_t n, cap;
+} vlist;
+
+static void vpush(vlist* l, uint32_t x) {
+  if (l->n == l->cap) {
+    l->cap = l->cap ? 2 * l->cap : 64;
+    l->v = realloc(l->v, l->cap * sizeof(uint32_t));
+  }
+  l->v[l->n++] = x;
+}
+
+static int u32_cmp(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* VertexSubset::from_ids: sort + unique (engine.cpp:36-42). */
+static void sort_unique(vlist* l) {
+  if (l->n < 2) return;
+  qsort(l->v, l->n, sizeof(uint32_t), u32_cmp);
+  uint64_t k = 1;
+  for (uint64_t i = 1; i < l->n; ++i)
+    if (l->v[i] != l->v[k - 1]) l->v[k++] = l->v[i];
+  l->n = k;
+}
+
+/* checked_window + clamp_window (path_algorithms.cpp:22-25,
+ * internal.hpp:17-25). */
+static int check_window(uint64_t* ta, uint64_t* tb) {
+  if (*ta > *tb) return fail(TGXO_INVALID_ARGUMENT, "query window with t_a > t_b");
+  if (*ta > TIME_LIMIT)
+    return fail(TGXO_INVALID_ARGUMENT, "window start beyond the supported time range (2^63 - 1)");
+  if (*tb > TIME_LIMIT) *tb = TIME_LIMIT;
+  return TGXO_OK;
+}
+
+/* earliest_arrival, path_algorithms.cpp:262-308. Frontier expansion through
+ * temporal_edge_map's sparse branch (engine.hpp:297-320); min_start hook
+ * :287-291, update :294-304. */
+static void earliest_arrival(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb,
+                             int strict, int64_t* L) {
+  const uint32_t n = g->n;
+  const ocsr* c = &g->out;
+  for (uint32_t v = 0; v < n; ++v) L[v] = INF64;
+  L[source] = (int64_t)ta;
+  uint32_t* stamp = calloc(n ? n : 1, sizeof(uint32_t));
+  uint32_t round = 0;
+  vlist fr = {0}, nx = {0};
+  int64_t* snapv = NULL;
+  uint64_t snapcap = 0;
+  vpush(&fr, source);
+  while (fr.n) {
+    ++round;
+    if (fr.n > snapcap) {
+      snapcap = fr.n;
+      snapv = realloc(snapv, snapcap * sizeof(int64_t));
+    }
+    /* snap = r.values (:283), read only at frontier vertices */
+    for (uint64_t i = 0; i < fr.n; ++i) snapv[i] = L[fr.v[i]];
+    nx.n = 0;
+    for (uint64_t i = 0; i < fr.n; ++i) {
+      const uint32_t s = fr.v[i];
+      const int64_t ps = snapv[i];
+      uint64_t lo_t = ta;
+      if (s != source) {
+        const uint64_t b = (uint64_t)ps;
+        lo_t = strict ? b + 1 : b;
+      }
+      if (lo_t < ta) lo_t = ta;
+      if (lo_t > tb) continue; /* effective_window crossed, engine.hpp:264 */
+      const uint64_t hi = c->off[s + 1];
+      for (uint64_t e = lower_start(c, c->off[s], hi, lo_t); e < hi; ++e) {
+        const uint64_t ts = c->st[e], te = c->en[e];
+        if (ts > tb) break;
+        if (te > tb) continue;
+        if (s != source) {
+          if (ps == INF64) continue;
+          if (strict ? (int64_t)ts <= ps : (int64_t)ts < ps) continue;
+        }
+        const uint32_t d = c->nbr[e];
+        if ((int64_t)te < L[d]) { /* write_min, parallel.hpp:91-99 */
+          L[d] = (int64_t)te;
+          if (stamp[d] != round) { /* claim_stamp, parallel.hpp:113-121 */
+            stamp[d] = round;
+            vpush(&nx, d);
+          }
+        }
+      }
+    }
+    sort_unique(&nx);
+    vlist t = fr;
+    fr = nx;
+    nx = t;
+  }
+  free(stamp);
+  free(snapv);
+  free(fr.v);
+  free(nx.v);
+}
+
+/* First position in [lo, hi) whose start > t. */
+static uint64_t upper_start(const ocsr* c, uint64_t lo, uint64_t hi, uint64_t t) {
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (c->st[mid] <= t) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+/* latest_departure, path_algorithms.cpp:310-357: the mirror over the In
+ * layout; max_end hook :337-342, update :344-352. */
+static void latest_departure(const tgxo_graph* g, uint32_t target, uint64_t ta, uint64_t tb,
+                             int strict, int64_t* L) {
+  const uint32_t n = g->n;
+  const ocsr* c = &g->in;
+  for (uint32_t v = 0; v < n; ++v) L[v] = NEGINF64;
+  L[target] = (int64_t)tb;
+  uint32_t* stamp = calloc(n ? n : 1, sizeof(uint32_t));
+  uint32_t round = 0;
+  vlist fr = {0}, nx = {0};
+  int64_t* snapv = NULL;
+  uint64_t snapcap = 0;
+  vpush(&fr, target);
+  while (fr.n) {
+    ++round;
+    if (fr.n > snapcap) {
+      snapcap = fr.n;
+      snapv = realloc(snapv, snapcap * sizeof(int64_t));
+    }
+    for (uint64_t i = 0; i < fr.n; ++i) snapv[i] = L[fr.v[i]];
+    nx.n = 0;
+    for (uint64_t i = 0; i < fr.n; ++i) {
+      const uint32_t s = fr.v[i];
+      const int64_t ps = snapv[i];
+      uint64_t hi_t = tb;
+      if (s != target) {
+        const uint64_t b = (uint64_t)ps;
+        if (strict && b == 0) hi_t = 0;
+        else hi_t = strict ? b - 1 : b;
+      }
+      if (hi_t > tb) hi_t = tb;
+      if (ta > hi_t) continue;
+      /* in-edges (u -> s) with start in [ta, hi_t] (ends are >= starts) */
+      const uint64_t lo = lower_start(c, c->off[s], c->off[s + 1], ta);
+      const uint64_t hi = upper_start(c, lo, c->off[s + 1], hi_t);
+      for (uint64_t e = lo; e < hi; ++e) {
+        const uint64_t ts = c->st[e], te = c->en[e];
+        if (te > hi_t) continue;
+        if (s != target) {
+          if (ps == NEGINF64) continue;
+          if (strict ? (int64_t)te >= ps : (int64_t)te > ps) continue;
+        }
+        const uint32_t u = c->nbr[e];
+        if ((int64_t)ts > L[u]) { /* write_max, parallel.hpp:101-109 */
+          L[u] = (int64_t)ts;
+          if (stamp[u] != round) {
+            stamp[u] = round;
+            vpush(&nx, u);
+          }
+        }
+      }
+    }
+    sort_unique(&nx);
+    vlist t = fr;
+    fr = nx;
+    nx = t;
+  }
+  free(stamp);
+  free(snapv);
+  free(fr.v);
+  free(nx.v);
+}
+
+typedef struct {
+  uint64_t ts, te;
+  uint32_t d;
+} first_edge;
+
+static int fe_desc(const void* a, const void* b) {
+  const first_edge* x = (const first_edge*)a;
+  const first_edge* y = (const first_edge*)b;
+  return x->ts > y->ts ? -1 : x->ts < y->ts;
+}
+
+/* fastest_path, path_algorithms.cpp:436-528: candidate departures are the
+ * distinct starts of the source's window out-edges (read from the T-CSR,
+ * :452-458) in decreasing order; arrivals persist across candidates; each
+ * candidate seeds its first edges (:476-486) then relaxes without a source
+ * exemption (:489-517); touched vertices take r = min(r, arrival - depart)
+ * (:519-524); r[source] = 0 last (:526). */
+static void fastest(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb, int strict,
+                    int64_t* R) {
+  const uint32_t n = g->n;
+  const ocsr* c = &g->out;
+  for (uint32_t v = 0; v < n; ++v) R[v] = INF64;
+  R[source] = 0;
+  uint64_t nfe = 0;
+  first_edge* fe = malloc((c->off[source + 1] - c->off[source] + 1) * sizeof(first_edge));
+  for (uint64_t e = c->off[source]; e < c->off[source + 1]; ++e) {
+    if (c->st[e] > tb) break;
+    if (c->st[e] >= ta && c->en[e] <= tb) {
+      fe[nfe].ts = c->st[e];
+      fe[nfe].te = c->en[e];
+      fe[nfe].d = c->nbr[e];
+      ++nfe;
+    }
+  }
+  if (nfe == 0) {
+    free(fe);
+    return;
+  }
+  qsort(fe, nfe, sizeof(first_edge), fe_desc);
+  int64_t* A = malloc((size_t)n * sizeof(int64_t));
+  for (uint32_t v = 0; v < n; ++v) A[v] = INF64;
+  uint32_t* stamp = calloc(n, sizeof(uint32_t));
+  uint32_t* touch = calloc(n, sizeof(uint32_t));
+  uint32_t round = 0, cand = 0;
+  vlist fr = {0}, nx = {0}, touched = {0};
+  int64_t* snapv = NULL;
+  uint64_t snapcap = 0;
+  uint64_t i = 0;
+  while (i < nfe) {
+    const uint64_t depart = fe[i].ts;
+    ++cand;
+    fr.n = 0;
+    touched.n = 0;
+    for (; i < nfe && fe[i].ts == depart; ++i) {
+      const uint32_t d = fe[i].d;
+      if ((int64_t)fe[i].te < A[d]) {
+        A[d] = (int64_t)fe[i].te;
+        if (touch[d] != cand) {
+          touch[d] = cand;
+          vpush(&touched, d);
+        }
+        vpush(&fr, d);
+      }
+    }
+    sort_unique(&fr);
+    while (fr.n) {
+      ++round;
+      if (fr.n > snapcap) {
+        snapcap = fr.n;
+        snapv = realloc(snapv, snapcap * sizeof(int64_t));
+      }
+      for (uint64_t k = 0; k < fr.n; ++k) snapv[k] = A[fr.v[k]];
+      nx.n = 0;
+      for (uint64_t k = 0; k < fr.n; ++k) {
+        const uint32_t s = fr.v[k];
+        const int64_t ps = snapv[k];
+        if (ps == INF64) continue;
+        uint64_t lo_t = strict ? (uint64_t)ps + 1 : (uint64_t)ps;
+        if (lo_t < ta) lo_t = ta;
+        if (lo_t > tb) continue;
+        const uint64_t hi = c->off[s + 1];
+        for (uint64_t e = lower_start(c, c->off[s], hi, lo_t); e < hi; ++e) {
+          const uint64_t ts = c->st[e], te = c->en[e];
+          if (ts > tb) break;
+          if (te > tb) continue;
+          if (strict ? (int64_t)ts <= ps : (int64_t)ts < ps) continue;
+          const uint32_t d = c->nbr[e];
+          if ((int64_t)te < A[d]) {
+            A[d] = (int64_t)te;
+            if (touch[d] != cand) {
+              touch[d] = cand;
+              vpush(&touched, d);
+            }
+            if (stamp[d] != round) {
+              stamp[d] = round;
+              vpush(&nx, d);
+            }
+          }
+        }
+      }
+      sort_unique(&nx);
+      vlist t = fr;
+      fr = nx;
+      nx = t;
+    }
+    const int64_t dep = (int64_t)depart;
+    for (uint64_t k = 0; k < touched.n; ++k) {
+      const uint32_t v = touched.v[k];
+      if (A[v] - dep < R[v]) R[v] = A[v] - dep;
+    }
+  }
+  R[source] = 0;
+  free(fe);
+  free(A);
+  free(stamp);
+  free(touch);
+  free(snapv);
+  free(fr.v);
+  free(nx.v);
+  free(touched.v);
+}
+
+int tgxo_query(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint64_t tb,
+               int ordering, int64_t* out) {
+  if (vertex >= g->n) return fail(TGXO_OUT_OF_RANGE, "vertex outside vertex range");
+  int rc = check_window(&ta, &tb);
+  if (rc) return rc;
+  if (ordering == TGXO_OVERLAPS)
+    return fail(TGXO_UNSUPPORTED, "the Overlaps ordering is outside the restated path");
+  const int strict = ordering == TGXO_STRICTLY_SUCCEEDS;
+  switch (kind) {
+    case TGXO_EA: earliest_arrival(g, vertex, ta, tb, strict, out); break;
+    case TGXO_LD: latest_departure(g, vertex, ta, tb, strict, out); break;
+    case TGXO_FASTEST: fastest(g, vertex, ta, tb, strict, out); break;
+    default: return fail(TGXO_INVALID_ARGUMENT, "unknown query kind");
+  }
+  return TGXO_OK;
+}
+
+/* E_adm = sum over reached u of the window edges of u that
+ * are admissible under u's final label (all window edges for the root);
+ * V_reached = finite labels. kind is TGXO_EA or TGXO_LD; a fastest sweep
+ * relaxes exactly the edges its earliest-arrival fixpoint admits (every
+ * source window edge is a seed), so callers count it with TGXO_EA. */
+int tgxo_work(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint64_t tb,
+              int ordering, const int64_t* labels, uint64_t* e_adm, uint64_t* v_reached) {
+  if (vertex >= g->n) return fail(TGXO_OUT_OF_RANGE, "vertex outside vertex range");
+  int rc = check_window(&ta, &tb);
+  if (rc) return rc;
+  if (kind != TGXO_EA && kind != TGXO_LD) return fail(TGXO_INVALID_ARGUMENT, "work: EA or LD");
+  const int strict = ordering == TGXO_STRICTLY_SUCCEEDS;
+  uint64_t ea = 0, vr = 0;
+  const int ld = kind == TGXO_LD;
+  const ocsr* c = ld ? &g->in : &g->out;
+  for (uint32_t u = 0; u < g->n; ++u) {
+    const int64_t x = labels[u];
+    if (x == (ld ? NEGINF64 : INF64)) continue;
+    ++vr;
+    for (uint64_t e = c->off[u]; e < c->off[u + 1]; ++e) {
+      const uint64_t ts = c->st[e], te = c->en[e];
+      if (ts < ta || te > tb) continue;
+      if (u != vertex) {
+        if (ld) {
+          if (strict ? (int64_t)te >= x : (int64_t)te > x) continue;
+        } else {
+          if (strict ? (int64_t)ts <= x : (int64_t)ts < x) continue;
+        }
+      }
+      ++ea;
+    }
+  }
+  *e_adm = ea;
+  *v_reached = vr;
+  return TGXO_OK;
+}
+
+/* Digest (FNV-1a over the little-endian label bytes), digest.hpp:12-52. */
+uint64_t tgxo_digest(const int64_t* values, uint64_t n) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  const unsigned char* p = (const unsigned char*)values;
+  for (uint64_t i = 0; i < n * 8; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}

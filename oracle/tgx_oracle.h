@@ -1,0 +1,45 @@
+/* TEST INFRASTRUCTURE ONLY — the checker, never the product.
+ *
+ * Plain-C restatement of the reference's temporal path algorithms
+ * (earliest arrival, latest departure, fastest) over a host T-CSR, with the
+ * reference's u64 timestamps, int64 labels and sentinels. Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg may load it.
+ * Pinned against the compiled reference (oracle/_ref/libtgxref.so) and the
+ * golden vectors in tests/golden/ (see tests/test_oracle.py).
+ */
+#ifndef TGX_ORACLE_H
+#define TGX_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TGXO_OK = 0, TGXO_OUT_OF_RANGE = 1, TGXO_INVALID_ARGUMENT = 2, TGXO_UNSUPPORTED = 3 };
+enum { TGXO_EA = 0, TGXO_LD = 1, TGXO_FASTEST = 2 };
+/* Ordering values follow tgx::Ordering (types.hpp:64-68). */
+enum { TGXO_SUCCEEDS = 0, TGXO_STRICTLY_SUCCEEDS = 1, TGXO_OVERLAPS = 2 };
+
+typedef struct tgxo_graph tgxo_graph;
+
+int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                     const uint64_t* start, const uint64_t* end, int directed, tgxo_graph** out);
+void tgxo_graph_free(tgxo_graph* g);
+uint64_t tgxo_graph_edges(const tgxo_graph* g);
+
+int tgxo_query(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint64_t tb,
+               int ordering, int64_t* out);
+
+/* SURVEY.md 8(d) unit of work from final labels: admissible window edges of
+ * reached vertices, and the reached count. */
+int tgxo_work(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint64_t tb,
+              int ordering, const int64_t* labels, uint64_t* e_adm, uint64_t* v_reached);
+
+uint64_t tgxo_digest(const int64_t* values, uint64_t n);
+const char* tgxo_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,475 @@
+"""B200-native temporal traversal (Kairos, arXiv 2401.02563) — host API.
+
+A Python mirror of the reference's algorithm entry points
+(/root/reference/proj/include/tgx/algorithms.hpp:46-58) and graph build
+(engine.hpp:32-33), over the C-ABI in include/tgxd.h. Names, argument meaning
+and error behaviour follow the reference:
+
+    g = TemporalGraph.build(edges, n_v, directed=True, config=EngineConfig())
+    r = earliest_arrival(g, source, QueryWindow(t_a, t_b), AlgoOptions(...))
+    r.values  # numpy int64, PathResult::values semantics
+
+Exceptions map the reference's C++ ones: std::out_of_range -> OutOfRange
+(an IndexError), std::invalid_argument -> InvalidArgument (a ValueError).
+
+Every call runs on the GPU through libtgxd.so. There is no CPU fallback: if
+the library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "Ordering", "ForceAccess", "Direction", "QueryWindow", "TemporalEdge", "EngineConfig",
+    "AlgoOptions", "EdgeMapStats", "PathResult", "TemporalGraph", "GenConfig",
+    "earliest_arrival", "latest_departure", "fastest_path", "query_batch", "digest_of",
+    "generate_edges", "OutOfRange", "InvalidArgument", "Unsupported", "DeviceError",
+    "TimeRangeError", "load_library", "K_MAX_TIMESTAMP",
+]
+
+K_MAX_TIMESTAMP = (1 << 64) - 1          # types.hpp:18
+K_UNREACHED_MIN = (1 << 63) - 1          # PathResult::kUnreachedMin, algorithms.hpp:17
+K_UNREACHED_MAX = -(1 << 63)             # PathResult::kUnreachedMax, algorithms.hpp:18
+
+
+class Ordering(enum.IntEnum):            # types.hpp:64-68
+    SUCCEEDS = 0
+    STRICTLY_SUCCEEDS = 1
+    OVERLAPS = 2
+
+
+class ForceAccess(enum.IntEnum):         # engine.hpp:17 (results-neutral; accepted, not needed)
+    AUTO = 0
+    INDEX = 1
+    SCAN = 2
+
+
+class Direction(enum.IntEnum):           # types.hpp:87
+    OUT = 0
+    IN = 1
+
+
+class Mode(enum.IntEnum):                # frontier representation policy (tgxd_mode)
+    AUTO = 0
+    SPARSE = 1
+    DENSE = 2
+
+
+class OutOfRange(IndexError):
+    """std::out_of_range in the reference."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class Unsupported(NotImplementedError):
+    """Ordering::Overlaps: not on the device path."""
+
+
+class TimeRangeError(ValueError):
+    """An edge time outside the device time domain [0, 2^31 - 2]."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no usable GPU."""
+
+
+_ERRORS = {1: OutOfRange, 2: InvalidArgument, 3: TimeRangeError, 4: Unsupported, 5: DeviceError,
+           6: ValueError, 7: OutOfRange}
+
+
+@dataclass(frozen=True)
+class QueryWindow:                       # types.hpp:43-50 (closed window)
+    t_a: int = 0
+    t_b: int = K_MAX_TIMESTAMP
+
+    def valid(self) -> bool:
+        return self.t_a <= self.t_b
+
+
+@dataclass(frozen=True)
+class TemporalEdge:                      # types.hpp:29-40
+    source: int
+    destination: int
+    start: int
+    end: int
+    weight: float = 1.0
+
+
+@dataclass
+class EngineConfig:                      # engine.hpp:19-24
+    index_cutoff: int = 2048
+    ordering: Ordering = Ordering.STRICTLY_SUCCEEDS
+    force_access: ForceAccess = ForceAccess.AUTO
+
+
+@dataclass
+class EdgeMapStats:                      # engine.hpp:141-144, plus device counters
+    index_decisions: int = 0
+    scan_decisions: int = 0
+    rounds: int = 0
+    candidates: int = 0
+    edges_relaxed: int = 0
+    kernel_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class AlgoOptions:                       # algorithms.hpp:31-40
+    ordering: Optional[Ordering] = None
+    force_access: Optional[ForceAccess] = None
+    stats: Optional[EdgeMapStats] = None
+    mode: Mode = Mode.AUTO
+
+
+@dataclass
+class PathResult:                        # algorithms.hpp:16-21
+    values: np.ndarray
+    kUnreachedMin = K_UNREACHED_MIN
+    kUnreachedMax = K_UNREACHED_MAX
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_uint32), ("candidates", ctypes.c_uint32),
+                ("expansions", ctypes.c_uint64), ("edges_relaxed", ctypes.c_uint64),
+                ("index_lookups", ctypes.c_uint64), ("kernel_ms", ctypes.c_float),
+                ("total_ms", ctypes.c_float)]
+
+
+class GenConfig(ctypes.Structure):       # tgxd_gen_config
+    _fields_ = [("kind", ctypes.c_int), ("scale", ctypes.c_uint32), ("n", ctypes.c_uint32),
+                ("m", ctypes.c_uint64), ("a", ctypes.c_double), ("b", ctypes.c_double),
+                ("c", ctypes.c_double), ("start_dist", ctypes.c_int),
+                ("t_range", ctypes.c_uint32), ("geo_p", ctypes.c_double),
+                ("seed", ctypes.c_uint64)]
+
+    @property
+    def n_vertices(self) -> int:
+        return (1 << self.scale) if self.kind == 1 else self.n
+
+    @staticmethod
+    def uniform(n: int, m: int, t_range: int, geo_p: float, seed: int,
+                cube_root_starts: bool = False) -> "GenConfig":
+        return GenConfig(0, 0, n, m, 0.0, 0.0, 0.0, 1 if cube_root_starts else 0, t_range, geo_p,
+                         seed)
+
+    @staticmethod
+    def rmat(scale: int, edge_factor: int, a: float, b: float, c: float, t_range: int,
+             geo_p: float, seed: int, cube_root_starts: bool = False) -> "GenConfig":
+        return GenConfig(1, scale, 0, edge_factor << scale, a, b, c,
+                         1 if cube_root_starts else 0, t_range, geo_p, seed)
+
+
+_LIB: Optional[ctypes.CDLL] = None
+_P = ctypes.POINTER
+_u32p = _P(ctypes.c_uint32)
+_u64p = _P(ctypes.c_uint64)
+_i64p = _P(ctypes.c_int64)
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libtgxd.so (building it first if sources are newer); raise if that fails."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    from . import _build
+    path = _build.LIB
+    if _build.needs_build():
+        try:
+            _build.build()
+        except Exception as e:  # no nvcc on the box: use what travelled, if anything
+            if not path.exists():
+                raise DeviceError(f"libtgxd.so is not built and cannot be built: {e}") from e
+    lib = ctypes.CDLL(str(path))
+    vp = ctypes.c_void_p
+    sig = {
+        "tgxd_last_error": ([], ctypes.c_char_p),
+        "tgxd_version": ([], ctypes.c_int),
+        "tgxd_device_count": ([_P(ctypes.c_int)], ctypes.c_int),
+        "tgxd_graph_build": ([ctypes.c_uint32, ctypes.c_uint64, _u32p, _u32p, _u64p, _u64p,
+                              ctypes.c_int, ctypes.c_uint64, _P(vp)], ctypes.c_int),
+        "tgxd_graph_generate": ([_P(GenConfig), ctypes.c_int, ctypes.c_uint64, _P(vp)],
+                                ctypes.c_int),
+        "tgxd_generate_host": ([_P(GenConfig), ctypes.c_uint64, _u64p, _u32p, _u32p, _u64p,
+                                _u64p], ctypes.c_int),
+        "tgxd_graph_destroy": ([vp], None),
+        "tgxd_graph_info": ([vp, _u32p, _u64p, _u64p, _u64p], ctypes.c_int),
+        "tgxd_graph_degrees": ([vp, ctypes.c_int, _u32p], ctypes.c_int),
+        "tgxd_graph_flatten": ([vp, ctypes.c_int, _u32p, _u32p, _u64p, _u64p], ctypes.c_int),
+        "tgxd_earliest_arrival": ([vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                   ctypes.c_int, _i64p, _P(_Stats)], ctypes.c_int),
+        "tgxd_latest_departure": ([vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                   ctypes.c_int, _i64p, _P(_Stats)], ctypes.c_int),
+        "tgxd_fastest": ([vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                          _i64p, _P(_Stats)], ctypes.c_int),
+        "tgxd_query": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p, ctypes.c_int,
+                        ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, _P(_Stats)], ctypes.c_int),
+        "tgxd_last_work": ([vp, ctypes.c_uint32, _u64p, _u64p], ctypes.c_int),
+        "tgxd_time_queries": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p,
+                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
+        "tgxd_digest": ([_i64p, ctypes.c_uint64], ctypes.c_uint64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _LIB = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _LIB.tgxd_last_error().decode(errors="replace") if _LIB else "tgxd error"
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(_P(ct))
+
+
+def device_count() -> int:
+    lib = load_library()
+    c = ctypes.c_int(0)
+    _check(lib.tgxd_device_count(ctypes.byref(c)))
+    return c.value
+
+
+def _edge_arrays(edges) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    if isinstance(edges, tuple) and len(edges) == 4:
+        s, d, a, b = edges
+    elif isinstance(edges, dict):
+        s, d, a, b = edges["src"], edges["dst"], edges["start"], edges["end"]
+    else:
+        el = list(edges)
+        s = [e.source for e in el]
+        d = [e.destination for e in el]
+        a = [e.start for e in el]
+        b = [e.end for e in el]
+    return (np.ascontiguousarray(s, dtype=np.uint32), np.ascontiguousarray(d, dtype=np.uint32),
+            np.ascontiguousarray(a, dtype=np.uint64), np.ascontiguousarray(b, dtype=np.uint64))
+
+
+class TemporalGraph:
+    """Device-resident temporal graph (both T-CSR layouts + selective index).
+    Mirrors tgx::TemporalGraph (engine.hpp:30-84); immutable after build."""
+
+    def __init__(self, handle: int, config: EngineConfig, directed: bool):
+        self._h = ctypes.c_void_p(handle)
+        self.config = config
+        self.directed = directed
+        lib = load_library()
+        n = ctypes.c_uint32()
+        m = ctypes.c_uint64()
+        io = ctypes.c_uint64()
+        ii = ctypes.c_uint64()
+        _check(lib.tgxd_graph_info(self._h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(io),
+                                   ctypes.byref(ii)))
+        self._n, self._m, self._indexed = n.value, m.value, (io.value, ii.value)
+
+    @staticmethod
+    def build(edges, n_v: int, directed: bool = True,
+              config: Optional[EngineConfig] = None) -> "TemporalGraph":
+        """TemporalGraph::build (engine.cpp:7-34). `edges`: iterable of
+        TemporalEdge, a (src, dst, start, end) tuple of arrays, or a dict."""
+        config = config or EngineConfig()
+        if config.index_cutoff < 1:
+            raise InvalidArgument("index cutoff must be >= 1")  # selective_index.cpp:156
+        lib = load_library()
+        s, d, a, b = _edge_arrays(edges)
+        h = ctypes.c_void_p()
+        _check(lib.tgxd_graph_build(n_v, len(s), _ptr(s, ctypes.c_uint32),
+                                    _ptr(d, ctypes.c_uint32), _ptr(a, ctypes.c_uint64),
+                                    _ptr(b, ctypes.c_uint64), 1 if directed else 0,
+                                    config.index_cutoff, ctypes.byref(h)))
+        return TemporalGraph(h.value, config, directed)
+
+    @staticmethod
+    def generate(gen: GenConfig, directed: bool = True,
+                 config: Optional[EngineConfig] = None) -> "TemporalGraph":
+        """Build from the deterministic synthetic generator, on the device."""
+        config = config or EngineConfig()
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.tgxd_graph_generate(ctypes.byref(gen), 1 if directed else 0,
+                                       config.index_cutoff, ctypes.byref(h)))
+        return TemporalGraph(h.value, config, directed)
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            load_library().tgxd_graph_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def vertex_count(self) -> int:
+        return self._n
+
+    def edge_count(self) -> int:
+        """Materialized edges per layout (TemporalCsr::edge_count)."""
+        return self._m
+
+    def indexed_count(self, d: Direction) -> int:
+        return self._indexed[int(d)]
+
+    def ordering(self) -> Ordering:
+        return self.config.ordering
+
+    def degrees(self, d: Direction = Direction.OUT) -> np.ndarray:
+        out = np.empty(self._n, dtype=np.uint32)
+        _check(load_library().tgxd_graph_degrees(self._h, int(d), _ptr(out, ctypes.c_uint32)))
+        return out
+
+    def flatten(self, d: Direction = Direction.OUT):
+        m = self._m
+        s = np.empty(m, np.uint32)
+        t = np.empty(m, np.uint32)
+        a = np.empty(m, np.uint64)
+        b = np.empty(m, np.uint64)
+        _check(load_library().tgxd_graph_flatten(self._h, int(d), _ptr(s, ctypes.c_uint32),
+                                                 _ptr(t, ctypes.c_uint32),
+                                                 _ptr(a, ctypes.c_uint64),
+                                                 _ptr(b, ctypes.c_uint64)))
+        return s, t, a, b
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+
+def _fill_stats(opts: Optional[AlgoOptions], st: _Stats) -> None:
+    if opts is None or opts.stats is None:
+        return
+    s = opts.stats
+    s.index_decisions += st.index_lookups
+    s.scan_decisions += max(0, st.expansions - st.index_lookups)
+    s.rounds += st.rounds
+    s.candidates += st.candidates
+    s.edges_relaxed += st.edges_relaxed
+    s.kernel_ms += st.kernel_ms
+    s.total_ms += st.total_ms
+
+
+def _run(kind: int, g: TemporalGraph, vertex: int, w: QueryWindow,
+         opts: Optional[AlgoOptions]) -> PathResult:
+    if not isinstance(vertex, (int, np.integer)) or vertex < 0 or vertex >= (1 << 32):
+        raise OutOfRange(f"vertex {vertex} outside vertex range [0, {g.vertex_count()})")
+    ordering = (opts.ordering if opts and opts.ordering is not None else g.ordering())
+    mode = int(opts.mode) if opts else 0
+    out = np.empty(g.vertex_count(), dtype=np.int64)
+    v = np.array([vertex], np.uint32)
+    ta = np.array([w.t_a], np.uint64)
+    tb = np.array([w.t_b], np.uint64)
+    st = _Stats()
+    _check(load_library().tgxd_query(g.handle, kind, 1, _ptr(v, ctypes.c_uint32),
+                                     _ptr(ta, ctypes.c_uint64), _ptr(tb, ctypes.c_uint64),
+                                     int(ordering), mode, out.ctypes.data_as(ctypes.c_void_p), 8,
+                                     0, ctypes.byref(st)))
+    _fill_stats(opts, st)
+    return PathResult(out)
+
+
+def earliest_arrival(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
+                     opts: Optional[AlgoOptions] = None) -> PathResult:
+    """algorithms.hpp:46-47 / path_algorithms.cpp:262-308."""
+    return _run(0, g, source, w, opts)
+
+
+def latest_departure(g: TemporalGraph, target: int, w: QueryWindow = QueryWindow(),
+                     opts: Optional[AlgoOptions] = None) -> PathResult:
+    """algorithms.hpp:53-54 / path_algorithms.cpp:310-357."""
+    return _run(1, g, target, w, opts)
+
+
+def fastest_path(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
+                 opts: Optional[AlgoOptions] = None) -> PathResult:
+    """algorithms.hpp:57-58 / path_algorithms.cpp:436-528."""
+    return _run(2, g, source, w, opts)
+
+
+KINDS = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2}
+
+
+def query_batch(g: TemporalGraph, kind: str, vertices: Sequence[int],
+                windows: Sequence[QueryWindow], ordering: Optional[Ordering] = None,
+                mode: Mode = Mode.AUTO, width: int = 8,
+                stats: Optional[EdgeMapStats] = None) -> np.ndarray:
+    """k queries of one kind as one batched traversal (configs 3 and 5):
+    returns a (k, n) label array (int64 for width 8, int32 for width 4)."""
+    k = len(vertices)
+    if len(windows) != k:
+        raise InvalidArgument("one window per query")
+    v = np.ascontiguousarray(vertices, np.uint32)
+    ta = np.array([w.t_a for w in windows], np.uint64)
+    tb = np.array([w.t_b for w in windows], np.uint64)
+    out = np.empty((k, g.vertex_count()), dtype=np.int64 if width == 8 else np.int32)
+    st = _Stats()
+    ordering = g.ordering() if ordering is None else ordering
+    _check(load_library().tgxd_query(g.handle, KINDS[kind], k, _ptr(v, ctypes.c_uint32),
+                                     _ptr(ta, ctypes.c_uint64), _ptr(tb, ctypes.c_uint64),
+                                     int(ordering), int(mode),
+                                     out.ctypes.data_as(ctypes.c_void_p), width, 0,
+                                     ctypes.byref(st)))
+    if stats is not None:
+        _fill_stats(AlgoOptions(stats=stats), st)
+    return out
+
+
+def last_work(g: TemporalGraph, q: int = 0) -> tuple[int, int]:
+    """(E_adm, V_reached) of slot q of the last query on g."""
+    e = ctypes.c_uint64()
+    r = ctypes.c_uint64()
+    _check(load_library().tgxd_last_work(g.handle, q, ctypes.byref(e), ctypes.byref(r)))
+    return e.value, r.value
+
+
+def time_queries(g: TemporalGraph, kind: str, vertices: Sequence[int],
+                 windows: Sequence[QueryWindow], ordering: Optional[Ordering] = None,
+                 mode: Mode = Mode.AUTO, warmup: int = 3, steps: int = 10) -> tuple[float, float]:
+    """(total ms for `steps` back-to-back queries, mean traversal-kernel ms),
+    device-timed with CUDA events on the graph's stream, outputs in HBM."""
+    v = np.ascontiguousarray(vertices, np.uint32)
+    ta = np.array([w.t_a for w in windows], np.uint64)
+    tb = np.array([w.t_b for w in windows], np.uint64)
+    tot = ctypes.c_float()
+    ker = ctypes.c_float()
+    ordering = g.ordering() if ordering is None else ordering
+    _check(load_library().tgxd_time_queries(g.handle, KINDS[kind], len(v),
+                                            _ptr(v, ctypes.c_uint32), _ptr(ta, ctypes.c_uint64),
+                                            _ptr(tb, ctypes.c_uint64), int(ordering), int(mode),
+                                            warmup, steps, ctypes.byref(tot),
+                                            ctypes.byref(ker)))
+    return tot.value, ker.value
+
+
+def generate_edges(gen: GenConfig):
+    """The generator's edge list on the host: (src u32, dst u32, start u64, end u64)."""
+    lib = load_library()
+    cap = int(gen.m)
+    m = ctypes.c_uint64()
+    s = np.empty(cap, np.uint32)
+    d = np.empty(cap, np.uint32)
+    a = np.empty(cap, np.uint64)
+    b = np.empty(cap, np.uint64)
+    _check(lib.tgxd_generate_host(ctypes.byref(gen), cap, ctypes.byref(m),
+                                  _ptr(s, ctypes.c_uint32), _ptr(d, ctypes.c_uint32),
+                                  _ptr(a, ctypes.c_uint64), _ptr(b, ctypes.c_uint64)))
+    k = m.value
+    return s[:k], d[:k], a[:k], b[:k]
+
+
+def digest_of(values: np.ndarray) -> int:
+    """FNV-1a over the int64 label bytes (digest.hpp:12-52)."""
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    return int(load_library().tgxd_digest(_ptr(v, ctypes.c_int64), len(v)))

@@ -1,0 +1,959 @@
+// C-ABI of the B200 temporal traversal engine (include/tgxd.h).
+//
+// Host orchestration only: argument validation with the reference's error
+// semantics, workspace management, kernel launches on the handle's stream,
+// output widening. All per-edge work is in build.cuh / traverse.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "build.cuh"
+#include "gen.cuh"
+#include "tgxd_internal.cuh"
+#include "traverse.cuh"
+
+namespace tgxd {
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define TGXD_CUDA(expr)                                                          \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess)                                                       \
+      return fail(TGXD_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+constexpr uint64_t kTimeLimit63 = 0x7fffffffffffffffULL;
+
+struct Seed {
+  uint32_t root;
+  uint32_t pad;
+  long long value;
+};
+
+// Geometric table thr[k] = floor(2^64 (1 - p)^k), k >= 1, until it reaches 0.
+int geo_table(double p, std::vector<uint64_t>& thr) {
+  if (!(p > 0.0 && p <= 1.0)) return fail(TGXD_ERR_ARGUMENT, "geo_p must lie in (0, 1]");
+  thr.assign(1, ~0ULL);
+  const long double q = 1.0L - (long double)p;
+  long double cur = 18446744073709551616.0L;  // 2^64
+  for (int k = 1; k < kGeoTableMax; ++k) {
+    cur *= q;
+    const long double f = floorl(cur);
+    const uint64_t t = f >= 18446744073709551615.0L ? ~0ULL : (uint64_t)f;
+    thr.push_back(t);
+    if (t == 0) return TGXD_OK;
+  }
+  return fail(TGXD_ERR_ARGUMENT, "geo_p too small for the duration table");
+}
+
+uint64_t prob_threshold(long double x) {
+  if (x <= 0) return 0;
+  if (x >= 1) return ~0ULL;
+  return (uint64_t)floorl(x * 18446744073709551616.0L);
+}
+
+int gen_params(const tgxd_gen_config* c, GenParams& p, std::vector<uint64_t>& thr) {
+  if (!c) return fail(TGXD_ERR_ARGUMENT, "null generator config");
+  std::memset(&p, 0, sizeof p);
+  p.kind = c->kind;
+  p.seed = c->seed;
+  p.start_dist = c->start_dist;
+  p.t_range = c->t_range;
+  p.m_draws = c->m;
+  if (c->t_range == 0 || c->t_range > 1u << 30)
+    return fail(TGXD_ERR_ARGUMENT, "t_range must lie in [1, 2^30]");
+  if (c->kind == TGXD_GEN_RMAT) {
+    if (c->scale > 31) return fail(TGXD_ERR_ARGUMENT, "RMAT scale must be <= 31");
+    p.scale = c->scale;
+    p.n_vertices = c->scale == 32 ? 0 : (1u << c->scale);
+    if (c->a < 0 || c->b < 0 || c->c < 0 || c->a + c->b + c->c > 1.0)
+      return fail(TGXD_ERR_ARGUMENT, "RMAT probabilities must be non-negative and sum <= 1");
+    p.thr_a = prob_threshold((long double)c->a);
+    p.thr_ab = prob_threshold((long double)c->a + (long double)c->b);
+    p.thr_abc = prob_threshold((long double)c->a + (long double)c->b + (long double)c->c);
+    for (int r = 0; r < 3; ++r) {
+      p.perm_mul[r] = mix64(c->seed ^ (0x5851f42d4c957f2dULL * (r + 1))) | 1ULL;
+      p.perm_add[r] = mix64(c->seed + 0x14057b7ef767814fULL * (r + 7));
+    }
+  } else if (c->kind == TGXD_GEN_UNIFORM) {
+    if (c->n == 0) return fail(TGXD_ERR_ARGUMENT, "uniform generator needs n >= 1");
+    p.n_vertices = c->n;
+  } else {
+    return fail(TGXD_ERR_ARGUMENT, "unknown generator kind");
+  }
+  int rc = geo_table(c->geo_p, thr);
+  if (rc) return rc;
+  p.geo_len = (int)thr.size();
+  return TGXD_OK;
+}
+
+template <class T>
+T* dalloc(DeviceBuffer& b, size_t count) {
+  if (b.ensure(count * sizeof(T) + 16) != cudaSuccess) return nullptr;
+  return b.as<T>();
+}
+
+}  // namespace
+
+DeviceBuffer::~DeviceBuffer() { release(); }
+
+void DeviceBuffer::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+cudaError_t DeviceBuffer::ensure(size_t nbytes) {
+  if (nbytes <= bytes && p) return cudaSuccess;
+  release();
+  cudaError_t e = cudaMalloc(&p, nbytes);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    return e;
+  }
+  bytes = nbytes;
+  return cudaSuccess;
+}
+
+// Builds both layouts from device edge arrays (m edges, already validated and
+// materialized). Frees nothing it does not own.
+static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d_dst,
+                         const int32_t* d_st, const int32_t* d_en, uint64_t m) {
+  cudaStream_t s = G->stream;
+  const uint32_t n = G->n;
+  G->m = m;
+  DeviceBuffer keys_a, keys_b, idx_a, idx_b, temp, cnt, counter;
+  unsigned long long* ka = dalloc<unsigned long long>(keys_a, m);
+  unsigned long long* kb = dalloc<unsigned long long>(keys_b, m);
+  uint32_t* ia = dalloc<uint32_t>(idx_a, m);
+  uint32_t* ib = dalloc<uint32_t>(idx_b, m);
+  uint32_t* dc = dalloc<uint32_t>(cnt, (size_t)n + 1);
+  unsigned long long* dctr = dalloc<unsigned long long>(counter, 2);
+  if (!ka || !kb || !ia || !ib || !dc || !dctr)
+    return fail(TGXD_ERR_CUDA, "device allocation failed while building the graph");
+  int end_bit = 32;
+  while (end_bit < 64 && (1ULL << (end_bit - 32)) < (uint64_t)n) ++end_bit;
+  if (end_bit == 32) end_bit = 33;
+  size_t temp_bytes = 0, scan_bytes = 0;
+  TGXD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
+                                            end_bit, s));
+  TGXD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, dc, dc, (int64_t)n + 1, s));
+  if (temp.ensure(std::max(temp_bytes, scan_bytes) + 16) != cudaSuccess)
+    return fail(TGXD_ERR_CUDA, "device allocation failed (sort scratch)");
+  TGXD_CUDA(cudaMemsetAsync(dctr, 0, 16, s));
+  const int gb = grid_for(m, G->sm_count);
+  const uint64_t nf = (m + kFenceStride - 1) >> kFenceShift;
+  for (int dir = 0; dir < 2; ++dir) {
+    const uint32_t* owner = dir == 0 ? d_src : d_dst;
+    const uint32_t* other = dir == 0 ? d_dst : d_src;
+    const int32_t* kk = dir == 0 ? d_st : d_en;
+    const int32_t* vv = dir == 0 ? d_en : d_st;
+    DeviceBuffer& b_off = dir == 0 ? G->out_off : G->in_off;
+    DeviceBuffer& b_nbr = dir == 0 ? G->out_nbr : G->in_nbr;
+    DeviceBuffer& b_key = dir == 0 ? G->out_key : G->in_key;
+    DeviceBuffer& b_val = dir == 0 ? G->out_val : G->in_val;
+    DeviceBuffer& b_fence = dir == 0 ? G->out_fence : G->in_fence;
+    uint32_t* off = dalloc<uint32_t>(b_off, (size_t)n + 1);
+    uint32_t* nbr = dalloc<uint32_t>(b_nbr, m);
+    int32_t* key = dalloc<int32_t>(b_key, m);
+    int32_t* val = dalloc<int32_t>(b_val, m);
+    int32_t* fence = dalloc<int32_t>(b_fence, nf);
+    if (!off || !nbr || !key || !val || !fence)
+      return fail(TGXD_ERR_CUDA, "device allocation failed (T-CSR arrays)");
+    if (m) {
+      make_sort_keys<<<gb, 256, 0, s>>>(owner, kk, dir, m, ka, ia);
+      TGXD_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
+                                                end_bit, s));
+      gather_layout<<<gb, 256, 0, s>>>(ib, other, kk, vv, dir, m, nbr, key, val);
+      make_fences<<<grid_for(nf, G->sm_count), 256, 0, s>>>(key, m, fence);
+    }
+    TGXD_CUDA(cudaMemsetAsync(dc, 0, ((size_t)n + 1) * 4, s));
+    if (m) degree_count<<<gb, 256, 0, s>>>(owner, m, dc);
+    size_t sb = scan_bytes;
+    TGXD_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, sb, dc, off, (int64_t)n + 1, s));
+    if (n) count_indexed<<<grid_for(n, G->sm_count), 256, 0, s>>>(off, n, G->index_cutoff, dctr + dir);
+    DevCsr& c = dir == 0 ? G->out : G->in;
+    c.off = off;
+    c.nbr = nbr;
+    c.key = key;
+    c.val = val;
+    c.fence = fence;
+    c.n = n;
+    c.m = (uint32_t)m;
+  }
+  unsigned long long h[2];
+  TGXD_CUDA(cudaMemcpyAsync(h, dctr, 16, cudaMemcpyDeviceToHost, s));
+  TGXD_CUDA(cudaStreamSynchronize(s));
+  TGXD_CUDA(cudaGetLastError());
+  G->indexed[0] = h[0];
+  G->indexed[1] = h[1];
+  return TGXD_OK;
+}
+
+static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph** out) {
+  int dev = 0, count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(TGXD_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+  TGXD_CUDA(cudaGetDevice(&dev));
+  auto* G = new tgxd_graph();
+  G->device = dev;
+  G->n = n;
+  G->directed = directed ? 1 : 0;
+  G->index_cutoff = index_cutoff ? index_cutoff : 2048;
+  cudaError_t e = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&G->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel, kThreads, 0);
+  for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreate(&G->ws.ev[i]);
+  if (e != cudaSuccess) {
+    delete G;
+    return fail(TGXD_ERR_CUDA, std::string("graph setup: ") + cudaGetErrorString(e));
+  }
+  G->coop_blocks = std::max(1, per_sm) * G->sm_count;
+  *out = G;
+  return TGXD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Queries
+
+struct Prepared {
+  int kind;
+  int strict;
+  uint32_t Q;
+  std::vector<QueryParam> qp;
+  std::vector<Seed> seeds;
+  // fastest
+  std::vector<uint32_t> cand_lo, cand_cnt;
+  std::vector<int32_t> cand_key;
+};
+
+// Validation in the reference's order: require_vertex (out_of_range), then
+// checked_window (invalid_argument), then the ordering.
+static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, const uint64_t* ta,
+                   const uint64_t* tb, int ordering, Prepared& P) {
+  if (kind < 0 || kind > 2) return fail(TGXD_ERR_ARGUMENT, "unknown query kind");
+  if (k == 0 || !verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "empty or null query batch");
+  if ((uint64_t)k * G->n >= 0xffffffffULL)
+    return fail(TGXD_ERR_ARGUMENT, "batch too large: k * n must stay below 2^32");
+  if (ordering < 0 || ordering > 2) return fail(TGXD_ERR_ARGUMENT, "unknown ordering");
+  P.kind = kind;
+  P.Q = k;
+  P.strict = ordering == TGXD_STRICTLY_SUCCEEDS ? 1 : 0;
+  P.qp.resize(k);
+  P.seeds.resize(k);
+  for (uint32_t q = 0; q < k; ++q) {
+    const char* what = kind == TGXD_LATEST_DEPARTURE ? "target " : "source ";
+    if (verts[q] >= G->n)
+      return fail(TGXD_ERR_VERTEX_RANGE, std::string(what) + std::to_string(verts[q]) +
+                                             " outside vertex range [0, " + std::to_string(G->n) +
+                                             ")");
+    if (ta[q] > tb[q]) return fail(TGXD_ERR_WINDOW, "query window with t_a > t_b");
+    if (ta[q] > kTimeLimit63)
+      return fail(TGXD_ERR_WINDOW, "window start beyond the supported time range (2^63 - 1)");
+  }
+  if (ordering == TGXD_OVERLAPS)
+    return fail(TGXD_ERR_UNSUPPORTED, "the Overlaps ordering is not on the device path");
+  for (uint32_t q = 0; q < k; ++q) {
+    const uint64_t tb63 = std::min<uint64_t>(tb[q], kTimeLimit63);
+    const int64_t ta_c = (int64_t)std::min<uint64_t>(ta[q], (uint64_t)kTimeMax + 1);
+    const int64_t tb_c = (int64_t)std::min<uint64_t>(tb63, (uint64_t)kTimeMax);
+    QueryParam& p = P.qp[q];
+    p.depart = 0;
+    Seed& sd = P.seeds[q];
+    sd.root = verts[q];
+    sd.pad = 0;
+    if (kind == TGXD_LATEST_DEPARTURE) {
+      p.root = verts[q];
+      p.klo = (int32_t)(-tb_c);
+      p.vhi = (int32_t)(-ta_c);
+      sd.value = (long long)tb63;
+    } else {
+      p.root = kind == TGXD_FASTEST ? kNoRoot : verts[q];
+      p.klo = (int32_t)ta_c;  // == kInf when t_a lies beyond every edge time
+      p.vhi = (int32_t)tb_c;
+      sd.value = kind == TGXD_FASTEST ? 0 : (long long)ta[q];
+    }
+  }
+  return TGXD_OK;
+}
+
+// Candidate departures of a fastest query (path_algorithms.cpp:449-458):
+// distinct starts of the source's window out-edges, descending. Each
+// candidate's seed range is its whole key group; the relax step applies the
+// end <= t_b filter, so a group whose edges all end too late seeds nothing.
+static int fastest_candidates(tgxd_graph* G, Prepared& P) {
+  const QueryParam& p = P.qp[0];
+  const uint32_t src = P.seeds[0].root;
+  uint32_t se[2];
+  TGXD_CUDA(cudaMemcpyAsync(se, G->out.off + src, 8, cudaMemcpyDeviceToHost, G->stream));
+  TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  const uint32_t deg = se[1] - se[0];
+  std::vector<int32_t> key(deg), val(deg);
+  if (deg) {
+    TGXD_CUDA(cudaMemcpyAsync(key.data(), G->out.key + se[0], deg * 4ull, cudaMemcpyDeviceToHost,
+                              G->stream));
+    TGXD_CUDA(cudaMemcpyAsync(val.data(), G->out.val + se[0], deg * 4ull, cudaMemcpyDeviceToHost,
+                              G->stream));
+    TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  }
+  P.cand_lo.clear();
+  P.cand_cnt.clear();
+  P.cand_key.clear();
+  uint32_t i = deg;
+  while (i > 0) {  // walk key groups from the top
+    uint32_t j = i;
+    const int32_t kv = key[i - 1];
+    bool any = false;
+    while (j > 0 && key[j - 1] == kv) {
+      any |= val[j - 1] <= p.vhi;
+      --j;
+    }
+    if (kv >= p.klo && kv <= p.vhi && any) {
+      P.cand_lo.push_back(se[0] + j);
+      P.cand_cnt.push_back(i - j);
+      P.cand_key.push_back(kv);
+    }
+    i = j;
+  }
+  return TGXD_OK;
+}
+
+static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool fastest) {
+  Workspace& w = G->ws;
+  const uint64_t slots = (uint64_t)Q * G->n;
+  const uint64_t words = (slots + 31) / 32 + 1;
+  bool ok = dalloc<int32_t>(w.X, slots) && dalloc<int32_t>(w.Ex, slots) &&
+            dalloc<uint32_t>(w.bitmap, words) && dalloc<uint32_t>(w.fa, slots) &&
+            dalloc<uint32_t>(w.fb, slots) && dalloc<uint32_t>(w.cnt, slots) &&
+            dalloc<uint32_t>(w.lo, slots) && dalloc<RangeEntry>(w.ranges, slots + 2) &&
+            dalloc<unsigned long long>(w.bsum, G->coop_blocks) &&
+            dalloc<uint32_t>(w.bnz, G->coop_blocks) && dalloc<uint32_t>(w.bidx, G->coop_blocks) &&
+            dalloc<Control>(w.ctl, 1) && dalloc<QueryParam>(w.params, Q) &&
+            dalloc<Seed>(w.seeds, Q);
+  if (ok && fastest) ok = dalloc<int32_t>(w.R, slots) != nullptr;
+  if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (traversal workspace)");
+  w.slots = std::max(w.slots, slots);
+  return TGXD_OK;
+}
+
+__global__ void convert_kernel(int kind, const int32_t* X, const int32_t* R, uint64_t total,
+                               uint32_t n, const Seed* seeds, void* out, int width) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint32_t q = (uint32_t)(i / n);
+    const uint32_t v = (uint32_t)(i - (uint64_t)q * n);
+    long long o;
+    if (kind == TGXD_FASTEST) {
+      const int32_t r = R[i];
+      o = r == kInf ? 0x7fffffffffffffffLL : (long long)r;
+    } else {
+      const int32_t x = X[i];
+      if (kind == TGXD_LATEST_DEPARTURE) o = x == kInf ? (-0x7fffffffffffffffLL - 1) : -(long long)x;
+      else o = x == kInf ? 0x7fffffffffffffffLL : (long long)x;
+    }
+    if (v == seeds[q].root) o = seeds[q].value;
+    if (width == 8) {
+      static_cast<long long*>(out)[i] = o;
+    } else {
+      const long long c = o > 0x7fffffffLL ? 0x7fffffffLL : (o < -0x80000000LL ? -0x80000000LL : o);
+      static_cast<int32_t*>(out)[i] = (int32_t)c;
+    }
+  }
+}
+
+// Enqueues one traversal (init, seeds, the persistent kernel, widening into
+// out_dev). ev_k0/ev_k1 bracket the traversal kernel when non-null.
+static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int width,
+                  cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  Workspace& w = G->ws;
+  cudaStream_t s = G->stream;
+  const bool fast = P.kind == TGXD_FASTEST;
+  const DevCsr& g = P.kind == TGXD_LATEST_DEPARTURE ? G->in : G->out;
+  const uint64_t slots = (uint64_t)P.Q * G->n;
+  TGXD_CUDA(cudaMemcpyAsync(w.params.p, P.qp.data(), P.Q * sizeof(QueryParam),
+                            cudaMemcpyHostToDevice, s));
+  TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), P.Q * sizeof(Seed), cudaMemcpyHostToDevice,
+                            s));
+  const uint32_t ncand = (uint32_t)P.cand_key.size();
+  if (fast && ncand) {
+    if (!dalloc<uint32_t>(w.cand_lo, ncand) || !dalloc<uint32_t>(w.cand_cnt, ncand) ||
+        !dalloc<int32_t>(w.cand_key, ncand))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (candidates)");
+    TGXD_CUDA(cudaMemcpyAsync(w.cand_lo.p, P.cand_lo.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
+    TGXD_CUDA(cudaMemcpyAsync(w.cand_cnt.p, P.cand_cnt.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
+    TGXD_CUDA(cudaMemcpyAsync(w.cand_key.p, P.cand_key.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
+  }
+  const uint64_t words = (slots + 31) / 32 + 1;
+  init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
+      w.X.as<int32_t>(), w.Ex.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr,
+      w.bitmap.as<uint32_t>(), slots, words);
+  seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
+                                                 w.X.as<int32_t>(), w.bitmap.as<uint32_t>(),
+                                                 w.fa.as<uint32_t>(), w.ctl.as<Control>(), fast);
+  TravArgs a;
+  a.g = g;
+  a.qp = w.params.as<QueryParam>();
+  a.X = w.X.as<int32_t>();
+  a.Ex = w.Ex.as<int32_t>();
+  a.R = fast ? w.R.as<int32_t>() : nullptr;
+  a.bitmap = w.bitmap.as<uint32_t>();
+  a.fa = w.fa.as<uint32_t>();
+  a.fb = w.fb.as<uint32_t>();
+  a.cnt = w.cnt.as<uint32_t>();
+  a.lo = w.lo.as<uint32_t>();
+  a.ranges = w.ranges.as<RangeEntry>();
+  a.bsum = w.bsum.as<unsigned long long>();
+  a.bnz = w.bnz.as<uint32_t>();
+  a.bidx = w.bidx.as<uint32_t>();
+  a.ctl = w.ctl.as<Control>();
+  a.n = G->n;
+  a.Q = P.Q;
+  a.strict = P.strict;
+  a.cutoff = (uint32_t)std::min<uint64_t>(G->index_cutoff, 0xffffffffULL);
+  a.mode = mode;
+  a.fastest = fast ? 1 : 0;
+  a.n_cand = ncand;
+  a.cand_lo = w.cand_lo.as<uint32_t>();
+  a.cand_cnt = w.cand_cnt.as<uint32_t>();
+  a.cand_key = w.cand_key.as<int32_t>();
+  if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
+  if (!fast || ncand) {
+    void* args[] = {&a};
+    TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)traverse_kernel, dim3(G->coop_blocks),
+                                          dim3(kThreads), args, 0, s));
+  } else {
+    Control z;
+    std::memset(&z, 0, sizeof z);
+    TGXD_CUDA(cudaMemcpyAsync(w.ctl.p, &z, sizeof z, cudaMemcpyHostToDevice, s));
+  }
+  if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
+  if (out_dev) {
+    convert_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
+        P.kind, w.X.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr, slots, G->n,
+        w.seeds.as<Seed>(), out_dev, width);
+  }
+  TGXD_CUDA(cudaGetLastError());
+  w.last_kind = P.kind;
+  w.last_q = P.Q;
+  w.last_strict = P.strict;
+  w.last_params = P.qp;
+  if (fast) {  // count the arrival fixpoint with the source as root (all seeds)
+    w.last_params[0].root = P.seeds[0].root;
+  }
+  return TGXD_OK;
+}
+
+static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float total_ms) {
+  if (!st) return TGXD_OK;
+  Control c;
+  TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ctl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
+  TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  st->rounds = c.rounds;
+  st->candidates = c.candidates;
+  st->expansions = c.expansions;
+  st->edges_relaxed = c.work_all;
+  st->index_lookups = c.index_lookups;
+  st->kernel_ms = kernel_ms;
+  st->total_ms = total_ms;
+  return TGXD_OK;
+}
+
+static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts,
+                      const uint64_t* ta, const uint64_t* tb, int ordering, int mode, void* out,
+                      int width, int out_on_device, tgxd_stats* stats) {
+  if (!G) return fail(TGXD_ERR_ARGUMENT, "null graph");
+  if (!out) return fail(TGXD_ERR_ARGUMENT, "null output");
+  if (width != 4 && width != 8) return fail(TGXD_ERR_ARGUMENT, "width must be 4 or 8");
+  if (kind == TGXD_FASTEST && k > 1) {  // one sweep per source
+    if (!verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "null query arrays");
+    tgxd_stats acc;
+    std::memset(&acc, 0, sizeof acc);
+    for (uint32_t q = 0; q < k; ++q) {
+      char* o = static_cast<char*>(out) + (size_t)q * G->n * width;
+      tgxd_stats one;
+      const int rc = query_impl(G, kind, 1, verts + q, ta + q, tb + q, ordering, mode, o, width,
+                                out_on_device, &one);
+      if (rc) return rc;
+      acc.rounds += one.rounds;
+      acc.candidates += one.candidates;
+      acc.expansions += one.expansions;
+      acc.edges_relaxed += one.edges_relaxed;
+      acc.index_lookups += one.index_lookups;
+      acc.kernel_ms += one.kernel_ms;
+      acc.total_ms += one.total_ms;
+    }
+    if (stats) *stats = acc;
+    return TGXD_OK;
+  }
+  std::lock_guard<std::mutex> lock(G->mu);
+  TGXD_CUDA(cudaSetDevice(G->device));
+  Prepared P;
+  int rc = prepare(G, kind, k, verts, ta, tb, ordering, P);
+  if (rc) return rc;
+  if (kind == TGXD_FASTEST) {
+    rc = fastest_candidates(G, P);
+    if (rc) return rc;
+  }
+  rc = ensure_workspace(G, P.Q, kind == TGXD_FASTEST);
+  if (rc) return rc;
+  Workspace& w = G->ws;
+  const uint64_t slots = (uint64_t)P.Q * G->n;
+  void* dout = out;
+  if (!out_on_device) {
+    if (!dalloc<char>(w.timing_out, slots * width))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (output staging)");
+    dout = w.timing_out.p;
+  }
+  TGXD_CUDA(cudaEventRecord(w.ev[2], G->stream));
+  rc = launch(G, P, mode, dout, width, w.ev[0], w.ev[1]);
+  if (rc) return rc;
+  if (!out_on_device)
+    TGXD_CUDA(cudaMemcpyAsync(out, dout, slots * width, cudaMemcpyDeviceToHost, G->stream));
+  TGXD_CUDA(cudaEventRecord(w.ev[3], G->stream));
+  TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  float km = 0, tm = 0;
+  TGXD_CUDA(cudaEventElapsedTime(&km, w.ev[0], w.ev[1]));
+  TGXD_CUDA(cudaEventElapsedTime(&tm, w.ev[2], w.ev[3]));
+  return read_stats(G, stats, km, tm);
+}
+
+// E_adm / V_reached of slot q from the final labels; warp
+// per vertex.
+__global__ void work_kernel(DevCsr g, const int32_t* X, QueryParam qp, int strict,
+                            unsigned long long* acc) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long e_adm = 0, reached = 0;
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < g.n; v += nw) {
+    const int32_t x = X[v];
+    if (x == kInf && v != qp.root) continue;
+    if (lane == 0) ++reached;
+    int32_t lb = v == qp.root ? qp.klo : x + strict;
+    if (lb < qp.klo) lb = qp.klo;
+    const uint32_t s = g.off[v], t = g.off[v + 1];
+    for (uint32_t j = s + lane; j < t; j += 32) {
+      const int32_t k = g.key[j];
+      e_adm += (k >= lb && g.val[j] <= qp.vhi) ? 1 : 0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    e_adm += __shfl_xor_sync(0xffffffffu, e_adm, o);
+    reached += __shfl_xor_sync(0xffffffffu, reached, o);
+  }
+  if (lane == 0) {
+    atomicAdd(acc, e_adm);
+    atomicAdd(acc + 1, reached);
+  }
+}
+
+}  // namespace tgxd
+
+using namespace tgxd;
+
+extern "C" {
+
+const char* tgxd_last_error(void) { return g_err.c_str(); }
+int tgxd_version(void) { return TGXD_VERSION; }
+
+int tgxd_device_count(int* count) {
+  if (!count) return fail(TGXD_ERR_ARGUMENT, "null count");
+  *count = 0;
+  if (cudaGetDeviceCount(count) != cudaSuccess) *count = 0;
+  cudaGetLastError();
+  return TGXD_OK;
+}
+
+int tgxd_generate_host(const tgxd_gen_config* cfg, uint64_t capacity, uint64_t* m_out,
+                       uint32_t* src, uint32_t* dst, uint64_t* start, uint64_t* end) {
+  GenParams p;
+  std::vector<uint64_t> thr;
+  int rc = gen_params(cfg, p, thr);
+  if (rc) return rc;
+  if (!m_out) return fail(TGXD_ERR_ARGUMENT, "null m_out");
+  const uint64_t m = cfg->m;
+  const bool drop = cfg->kind == TGXD_GEN_UNIFORM;
+  std::vector<GenEdge> tmp(m);
+  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) {
+    th.emplace_back([&, t] {
+      const uint64_t b = m * t / nt, e = m * (t + 1) / nt;
+      for (uint64_t i = b; i < e; ++i) tmp[i] = gen_edge(p, thr.data(), i);
+    });
+  }
+  for (auto& x : th) x.join();
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < m; ++i) {
+    const GenEdge& e = tmp[i];
+    if (drop && e.src == e.dst) continue;
+    if (k < capacity && src) {
+      src[k] = e.src;
+      dst[k] = e.dst;
+      start[k] = (uint64_t)e.start;
+      end[k] = (uint64_t)e.end;
+    }
+    ++k;
+  }
+  *m_out = k;
+  if (k > capacity && src) return fail(TGXD_ERR_ARGUMENT, "capacity smaller than the edge count");
+  return TGXD_OK;
+}
+
+int tgxd_graph_generate(const tgxd_gen_config* cfg, int directed, uint64_t index_cutoff,
+                        tgxd_graph** out) {
+  if (!out) return fail(TGXD_ERR_ARGUMENT, "null out");
+  *out = nullptr;
+  GenParams p;
+  std::vector<uint64_t> thr;
+  int rc = gen_params(cfg, p, thr);
+  if (rc) return rc;
+  const uint32_t n = p.n_vertices;
+  const uint64_t m = cfg->m;
+  const uint64_t cap = directed ? m : 2 * m;
+  if (cap >= 0xffffffffULL) return fail(TGXD_ERR_ARGUMENT, "edge count must stay below 2^32");
+  tgxd_graph* G = nullptr;
+  rc = new_graph(n, index_cutoff, directed, &G);
+  if (rc) return rc;
+  G->m_logical = m;
+  cudaStream_t s = G->stream;
+  DeviceBuffer bthr, bs, bd, bst, ben, bflag, bpos, cs, cd, cst, cen, temp;
+  uint64_t* dthr = dalloc<uint64_t>(bthr, thr.size());
+  uint32_t* ds = dalloc<uint32_t>(bs, cap);
+  uint32_t* dd = dalloc<uint32_t>(bd, cap);
+  int32_t* dst_ = dalloc<int32_t>(bst, cap);
+  int32_t* den = dalloc<int32_t>(ben, cap);
+  uint32_t* fl = dalloc<uint32_t>(bflag, m + 1);
+  uint32_t* pos = dalloc<uint32_t>(bpos, m + 1);
+  if (!dthr || !ds || !dd || !dst_ || !den || !fl || !pos) {
+    tgxd_graph_destroy(G);
+    return fail(TGXD_ERR_CUDA, "device allocation failed (generator)");
+  }
+  auto cleanup = [&](int code) {
+    if (code) tgxd_graph_destroy(G);
+    return code;
+  };
+#define GEN_CUDA(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return cleanup(fail(TGXD_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
+  } while (0)
+  GEN_CUDA(cudaMemcpyAsync(dthr, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, s));
+  const int gb = grid_for(m, G->sm_count);
+  if (m) gen_kernel<<<gb, 256, 0, s>>>(p, dthr, m, ds, dd, dst_, den);
+  uint64_t mm = m;
+  size_t tb = 0;
+  GEN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, fl, pos, (int64_t)m + 1, s));
+  if (temp.ensure(tb + 16) != cudaSuccess) return cleanup(fail(TGXD_ERR_CUDA, "scan scratch"));
+  auto count_non_loops = [&](const uint32_t* a, const uint32_t* b) -> int {
+    if (m) non_loop_flags<<<gb, 256, 0, s>>>(a, b, m, fl);
+    GEN_CUDA(cudaMemsetAsync(fl + m, 0, 4, s));
+    size_t t2 = tb;
+    GEN_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, t2, fl, pos, (int64_t)m + 1, s));
+    return TGXD_OK;
+  };
+  if (cfg->kind == TGXD_GEN_UNIFORM) {  // self-loops dropped (BASELINE config 1)
+    if ((rc = count_non_loops(ds, dd))) return cleanup(rc);
+    uint32_t kept = 0;
+    GEN_CUDA(cudaMemcpyAsync(&kept, pos + m, 4, cudaMemcpyDeviceToHost, s));
+    GEN_CUDA(cudaStreamSynchronize(s));
+    uint32_t* o_s = dalloc<uint32_t>(cs, cap);
+    uint32_t* o_d = dalloc<uint32_t>(cd, cap);
+    int32_t* o_st = dalloc<int32_t>(cst, cap);
+    int32_t* o_en = dalloc<int32_t>(cen, cap);
+    if (!o_s || !o_d || !o_st || !o_en) return cleanup(fail(TGXD_ERR_CUDA, "allocation (compact)"));
+    if (m) compact_edges<<<gb, 256, 0, s>>>(ds, dd, dst_, den, fl, pos, m, o_s, o_d, o_st, o_en);
+    std::swap(bs.p, cs.p);
+    std::swap(bs.bytes, cs.bytes);
+    std::swap(bd.p, cd.p);
+    std::swap(bd.bytes, cd.bytes);
+    std::swap(bst.p, cst.p);
+    std::swap(bst.bytes, cst.bytes);
+    std::swap(ben.p, cen.p);
+    std::swap(ben.bytes, cen.bytes);
+    ds = bs.as<uint32_t>();
+    dd = bd.as<uint32_t>();
+    dst_ = bst.as<int32_t>();
+    den = ben.as<int32_t>();
+    mm = kept;
+    G->m_logical = kept;
+  }
+  if (!directed) {
+    const uint64_t m0 = mm;
+    if (m0) non_loop_flags<<<grid_for(m0, G->sm_count), 256, 0, s>>>(ds, dd, m0, fl);
+    GEN_CUDA(cudaMemsetAsync(fl + m0, 0, 4, s));
+    size_t t2 = tb;
+    GEN_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, t2, fl, pos, (int64_t)m0 + 1, s));
+    uint32_t extra = 0;
+    GEN_CUDA(cudaMemcpyAsync(&extra, pos + m0, 4, cudaMemcpyDeviceToHost, s));
+    GEN_CUDA(cudaStreamSynchronize(s));
+    if (m0) append_reverse<<<grid_for(m0, G->sm_count), 256, 0, s>>>(ds, dd, dst_, den, fl, pos, m0);
+    mm = m0 + extra;
+  }
+  bflag.release();
+  bpos.release();
+  temp.release();
+  rc = build_layouts(G, ds, dd, dst_, den, mm);
+  if (rc) return cleanup(rc);
+  *out = G;
+  return TGXD_OK;
+#undef GEN_CUDA
+}
+
+int tgxd_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                     const uint64_t* start, const uint64_t* end, int directed,
+                     uint64_t index_cutoff, tgxd_graph** out) {
+  if (!out) return fail(TGXD_ERR_ARGUMENT, "null out");
+  *out = nullptr;
+  if (m && (!src || !dst || !start || !end)) return fail(TGXD_ERR_ARGUMENT, "null edge arrays");
+  // compute_meta (types.cpp:29-54): first offending edge, reference wording.
+  for (uint64_t i = 0; i < m; ++i) {
+    if (src[i] >= n || dst[i] >= n)
+      return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": endpoint (" +
+                                     std::to_string(src[i]) + " -> " + std::to_string(dst[i]) +
+                                     ") outside vertex range [0, " + std::to_string(n) + ")");
+    if (end[i] < start[i])
+      return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": end " + std::to_string(end[i]) +
+                                     " precedes start " + std::to_string(start[i]));
+    if (end[i] > kTimeLimit63)
+      return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": end " + std::to_string(end[i]) +
+                                     " beyond the supported time range (2^63 - 1)");
+  }
+  for (uint64_t i = 0; i < m; ++i) {
+    if (end[i] > (uint64_t)kTimeMax)
+      return fail(TGXD_ERR_TIME_RANGE, "edge " + std::to_string(i) + ": end " +
+                                           std::to_string(end[i]) +
+                                           " outside the device time domain [0, 2^31 - 2]");
+  }
+  uint64_t mm = m;
+  if (!directed)
+    for (uint64_t i = 0; i < m; ++i) mm += src[i] != dst[i];
+  if (mm >= 0xffffffffULL) return fail(TGXD_ERR_ARGUMENT, "edge count must stay below 2^32");
+  std::vector<uint32_t> hs(src, src + m), hd(dst, dst + m);
+  std::vector<int32_t> hst(m), hen(m);
+  for (uint64_t i = 0; i < m; ++i) {
+    hst[i] = (int32_t)start[i];
+    hen[i] = (int32_t)end[i];
+  }
+  if (!directed) {  // engine.cpp:13-22
+    for (uint64_t i = 0; i < m; ++i) {
+      if (src[i] == dst[i]) continue;
+      hs.push_back(dst[i]);
+      hd.push_back(src[i]);
+      hst.push_back((int32_t)start[i]);
+      hen.push_back((int32_t)end[i]);
+    }
+  }
+  tgxd_graph* G = nullptr;
+  int rc = new_graph(n, index_cutoff, directed, &G);
+  if (rc) return rc;
+  G->m_logical = m;
+  DeviceBuffer bs, bd, bst, ben;
+  uint32_t* ds = dalloc<uint32_t>(bs, mm);
+  uint32_t* dd = dalloc<uint32_t>(bd, mm);
+  int32_t* dst_ = dalloc<int32_t>(bst, mm);
+  int32_t* den = dalloc<int32_t>(ben, mm);
+  cudaError_t e = (ds && dd && dst_ && den) ? cudaSuccess : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess && mm) e = cudaMemcpyAsync(ds, hs.data(), mm * 4, cudaMemcpyHostToDevice, G->stream);
+  if (e == cudaSuccess && mm) e = cudaMemcpyAsync(dd, hd.data(), mm * 4, cudaMemcpyHostToDevice, G->stream);
+  if (e == cudaSuccess && mm) e = cudaMemcpyAsync(dst_, hst.data(), mm * 4, cudaMemcpyHostToDevice, G->stream);
+  if (e == cudaSuccess && mm) e = cudaMemcpyAsync(den, hen.data(), mm * 4, cudaMemcpyHostToDevice, G->stream);
+  if (e != cudaSuccess) {
+    tgxd_graph_destroy(G);
+    return fail(TGXD_ERR_CUDA, std::string("edge upload: ") + cudaGetErrorString(e));
+  }
+  rc = build_layouts(G, ds, dd, dst_, den, mm);
+  if (rc) {
+    tgxd_graph_destroy(G);
+    return rc;
+  }
+  *out = G;
+  return TGXD_OK;
+}
+
+void tgxd_graph_destroy(tgxd_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  for (auto& e : g->ws.ev)
+    if (e) cudaEventDestroy(e);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+int tgxd_graph_info(const tgxd_graph* g, uint32_t* n, uint64_t* m, uint64_t* indexed_out,
+                    uint64_t* indexed_in) {
+  if (!g) return fail(TGXD_ERR_ARGUMENT, "null graph");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (indexed_out) *indexed_out = g->indexed[0];
+  if (indexed_in) *indexed_in = g->indexed[1];
+  return TGXD_OK;
+}
+
+int tgxd_graph_degrees(tgxd_graph* g, int direction, uint32_t* out) {
+  if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  TGXD_CUDA(cudaSetDevice(g->device));
+  const DevCsr& c = direction == 0 ? g->out : g->in;
+  DeviceBuffer b;
+  uint32_t* d = dalloc<uint32_t>(b, g->n);
+  if (!d) return fail(TGXD_ERR_CUDA, "allocation");
+  if (g->n) degrees_kernel<<<grid_for(g->n, g->sm_count), 256, 0, g->stream>>>(c.off, g->n, d);
+  TGXD_CUDA(cudaMemcpyAsync(out, d, g->n * 4ull, cudaMemcpyDeviceToHost, g->stream));
+  TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  return TGXD_OK;
+}
+
+int tgxd_graph_flatten(tgxd_graph* g, int direction, uint32_t* src, uint32_t* dst,
+                       uint64_t* start, uint64_t* end) {
+  if (!g || !src || !dst || !start || !end) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  TGXD_CUDA(cudaSetDevice(g->device));
+  const DevCsr& c = direction == 0 ? g->out : g->in;
+  const uint64_t m = g->m;
+  DeviceBuffer b;
+  uint32_t* own = dalloc<uint32_t>(b, m);
+  if (!own) return fail(TGXD_ERR_CUDA, "allocation");
+  if (g->n) owners_kernel<<<grid_for(g->n, g->sm_count), 256, 0, g->stream>>>(c.off, g->n, own);
+  std::vector<uint32_t> o(m), nb(m);
+  std::vector<int32_t> k(m), v(m);
+  if (m) {
+    TGXD_CUDA(cudaMemcpyAsync(o.data(), own, m * 4, cudaMemcpyDeviceToHost, g->stream));
+    TGXD_CUDA(cudaMemcpyAsync(nb.data(), c.nbr, m * 4, cudaMemcpyDeviceToHost, g->stream));
+    TGXD_CUDA(cudaMemcpyAsync(k.data(), c.key, m * 4, cudaMemcpyDeviceToHost, g->stream));
+    TGXD_CUDA(cudaMemcpyAsync(v.data(), c.val, m * 4, cudaMemcpyDeviceToHost, g->stream));
+  }
+  TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  for (uint64_t i = 0; i < m; ++i) {
+    if (direction == 0) {
+      src[i] = o[i];
+      dst[i] = nb[i];
+      start[i] = (uint64_t)k[i];
+      end[i] = (uint64_t)v[i];
+    } else {
+      src[i] = nb[i];
+      dst[i] = o[i];
+      start[i] = (uint64_t)(-(int64_t)v[i]);
+      end[i] = (uint64_t)(-(int64_t)k[i]);
+    }
+  }
+  return TGXD_OK;
+}
+
+int tgxd_query(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices, const uint64_t* t_a,
+               const uint64_t* t_b, int ordering, int mode, void* out, int width,
+               int out_on_device, tgxd_stats* stats) {
+  return query_impl(g, kind, k, vertices, t_a, t_b, ordering, mode, out, width, out_on_device,
+                    stats);
+}
+
+int tgxd_earliest_arrival(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b,
+                          int ordering, int64_t* out, tgxd_stats* stats) {
+  return query_impl(g, TGXD_EARLIEST_ARRIVAL, 1, &source, &t_a, &t_b, ordering, TGXD_MODE_AUTO,
+                    out, 8, 0, stats);
+}
+
+int tgxd_latest_departure(tgxd_graph* g, uint32_t target, uint64_t t_a, uint64_t t_b,
+                          int ordering, int64_t* out, tgxd_stats* stats) {
+  return query_impl(g, TGXD_LATEST_DEPARTURE, 1, &target, &t_a, &t_b, ordering, TGXD_MODE_AUTO,
+                    out, 8, 0, stats);
+}
+
+int tgxd_fastest(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int ordering,
+                 int64_t* out, tgxd_stats* stats) {
+  return query_impl(g, TGXD_FASTEST, 1, &source, &t_a, &t_b, ordering, TGXD_MODE_AUTO, out, 8, 0,
+                    stats);
+}
+
+int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reached) {
+  if (!g || !e_adm || !v_reached) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  Workspace& w = g->ws;
+  if (w.last_kind < 0 || q >= w.last_q) return fail(TGXD_ERR_ARGUMENT, "no such query slot");
+  TGXD_CUDA(cudaSetDevice(g->device));
+  const DevCsr& c = w.last_kind == TGXD_LATEST_DEPARTURE ? g->in : g->out;
+  DeviceBuffer acc;
+  unsigned long long* d = dalloc<unsigned long long>(acc, 2);
+  if (!d) return fail(TGXD_ERR_CUDA, "allocation");
+  TGXD_CUDA(cudaMemsetAsync(d, 0, 16, g->stream));
+  work_kernel<<<g->sm_count * 8, 256, 0, g->stream>>>(
+      c, w.X.as<int32_t>() + (size_t)q * g->n, w.last_params[q], w.last_strict, d);
+  unsigned long long h[2];
+  TGXD_CUDA(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, g->stream));
+  TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  *e_adm = h[0];
+  *v_reached = h[1];
+  return TGXD_OK;
+}
+
+int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
+                      const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode, int warmup,
+                      int steps, float* total_ms, float* kernel_ms) {
+  if (!g || !total_ms || !kernel_ms || steps < 1 || warmup < 0)
+    return fail(TGXD_ERR_ARGUMENT, "bad timing arguments");
+  if (kind == TGXD_FASTEST && k != 1) return fail(TGXD_ERR_ARGUMENT, "timed fastest: one source");
+  std::lock_guard<std::mutex> lock(g->mu);
+  TGXD_CUDA(cudaSetDevice(g->device));
+  Prepared P;
+  int rc = prepare(g, kind, k, vertices, t_a, t_b, ordering, P);
+  if (rc) return rc;
+  if (kind == TGXD_FASTEST && (rc = fastest_candidates(g, P))) return rc;
+  if ((rc = ensure_workspace(g, P.Q, kind == TGXD_FASTEST))) return rc;
+  Workspace& w = g->ws;
+  const uint64_t slots = (uint64_t)P.Q * g->n;
+  if (!dalloc<int32_t>(w.timing_out, slots)) return fail(TGXD_ERR_CUDA, "allocation (output)");
+  std::vector<cudaEvent_t> ev(2 * (size_t)steps);
+  for (auto& e : ev) TGXD_CUDA(cudaEventCreate(&e));
+  auto destroy = [&] {
+    for (auto& e : ev) cudaEventDestroy(e);
+  };
+  for (int i = 0; i < warmup; ++i) {
+    if ((rc = launch(g, P, mode, w.timing_out.p, 4, nullptr, nullptr))) return destroy(), rc;
+  }
+  TGXD_CUDA(cudaEventRecord(w.ev[2], g->stream));
+  for (int i = 0; i < steps; ++i) {
+    if ((rc = launch(g, P, mode, w.timing_out.p, 4, ev[2 * i], ev[2 * i + 1]))) return destroy(), rc;
+  }
+  TGXD_CUDA(cudaEventRecord(w.ev[3], g->stream));
+  TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  float tot = 0, ksum = 0;
+  TGXD_CUDA(cudaEventElapsedTime(&tot, w.ev[2], w.ev[3]));
+  for (int i = 0; i < steps; ++i) {
+    float x = 0;
+    TGXD_CUDA(cudaEventElapsedTime(&x, ev[2 * i], ev[2 * i + 1]));
+    ksum += x;
+  }
+  destroy();
+  *total_ms = tot;
+  *kernel_ms = ksum / steps;
+  return TGXD_OK;
+}
+
+uint64_t tgxd_digest(const int64_t* values, uint64_t n) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(values);
+  for (uint64_t i = 0; i < n * 8; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+}  // extern "C"

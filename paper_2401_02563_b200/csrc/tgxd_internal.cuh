@@ -1,0 +1,111 @@
+// Internal device-side structures of the B200 temporal traversal engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tgxd.h"
+
+namespace tgxd {
+
+// Largest representable edge time. Keys are stored as start (Out) and -end
+// (In), the strict bound adds 1 to a label, so times stay inside
+// [0, 2^31 - 2] to keep every derived bound inside int32.
+constexpr int64_t kTimeMax = 2147483646LL;
+constexpr int32_t kInf = 0x7fffffff;  // unreached label in key space
+
+// Fence stride of the selective index ("bucketed timeline"): fence[j] =
+// key[32 j], so a fence probe narrows a search to one 128-byte key line.
+constexpr uint32_t kFenceShift = 5;
+constexpr uint32_t kFenceStride = 1u << kFenceShift;
+
+// One direction of the device T-CSR. Segments are sorted by key ascending.
+//   Out layout: key = start, val = end           (earliest arrival / fastest)
+//   In layout : key = -end,  val = -start        (latest departure, mirrored)
+// With that mirror, both traversals are "relax val over edges whose key lies
+// at or above the frontier vertex's bound", so one kernel family serves both.
+struct DevCsr {
+  const uint32_t* off = nullptr;  // n + 1
+  const uint32_t* nbr = nullptr;  // m
+  const int32_t* key = nullptr;   // m
+  const int32_t* val = nullptr;   // m
+  const int32_t* fence = nullptr; // ceil(m / 32): key[32 j]
+  uint32_t n = 0;
+  uint32_t m = 0;
+};
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DeviceBuffer();
+  cudaError_t ensure(size_t nbytes);
+  void release();
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Per-query parameters in key space.
+struct QueryParam {
+  uint32_t root;  // vertex exempt from the ordering check (kNoRoot for none)
+  int32_t klo;    // lowest admissible key (window start, mirrored for In)
+  int32_t vhi;    // highest admissible val (window end, mirrored for In)
+  int32_t depart; // fastest: departure of the current candidate
+};
+constexpr uint32_t kNoRoot = 0xffffffffu;
+
+// Range of the frontier: the edges [lo, lo + cnt) of one frontier item, whose
+// exclusive work prefix is pfx. Only non-empty ranges are kept.
+struct RangeEntry {
+  unsigned long long pfx;
+  uint32_t lo;
+  uint32_t item;
+};
+
+// Traversal workspace, sized for q_cap concurrent queries.
+struct Workspace {
+  uint64_t slots = 0;  // Q x n label slots currently allocated
+  DeviceBuffer X, Ex, R, bitmap, fa, fb, cnt, lo, ranges, bsum, bnz, bidx, ctl, params, seeds;
+  DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // what the last query left in X (for tgxd_last_work)
+  int last_kind = -1;
+  uint32_t last_q = 0;
+  int last_strict = 1;
+  std::vector<QueryParam> last_params;
+};
+
+// Device control block (one per workspace), see traverse.cu.
+struct Control {
+  unsigned int fc[2];              // frontier sizes, indexed by round parity
+  unsigned long long work_all;     // edges handed to the relax step, all rounds
+  unsigned long long expansions;   // non-empty ranges, all rounds
+  unsigned long long index_lookups;
+  unsigned int rounds;
+  unsigned int candidates;
+  unsigned long long e_adm;        // tgxd_last_work accumulators
+  unsigned long long v_reached;
+};
+
+}  // namespace tgxd
+
+struct tgxd_graph {
+  int device = 0;
+  uint32_t n = 0;
+  uint64_t m_logical = 0;
+  uint64_t m = 0;  // materialized per layout
+  int directed = 1;
+  uint64_t index_cutoff = 2048;
+  uint64_t indexed[2] = {0, 0};
+  tgxd::DeviceBuffer out_off, out_nbr, out_key, out_val, out_fence;
+  tgxd::DeviceBuffer in_off, in_nbr, in_key, in_val, in_fence;
+  tgxd::DevCsr out, in;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  int coop_blocks = 0;
+  std::mutex mu;
+  tgxd::Workspace ws;
+};
