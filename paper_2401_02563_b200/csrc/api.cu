@@ -338,14 +338,13 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool fastest) {
   Workspace& w = G->ws;
   const uint64_t slots = (uint64_t)Q * G->n;
   const uint64_t words = (slots + 31) / 32 + 1;
+  // chunks per round <= frontier items + edges / kChunk (per query slot)
+  const uint64_t max_chunks = slots + (uint64_t)Q * (G->m / kChunk + 1);
   bool ok = dalloc<int32_t>(w.X, slots) && dalloc<int32_t>(w.Ex, slots) &&
             dalloc<uint32_t>(w.bitmap, words) && dalloc<uint32_t>(w.fa, slots) &&
-            dalloc<uint32_t>(w.fb, slots) && dalloc<uint32_t>(w.cnt, slots) &&
-            dalloc<uint32_t>(w.lo, slots) && dalloc<RangeEntry>(w.ranges, slots + 2) &&
-            dalloc<unsigned long long>(w.bsum, G->coop_blocks) &&
-            dalloc<uint32_t>(w.bnz, G->coop_blocks) && dalloc<uint32_t>(w.bidx, G->coop_blocks) &&
-            dalloc<Control>(w.ctl, 1) && dalloc<QueryParam>(w.params, Q) &&
-            dalloc<Seed>(w.seeds, Q);
+            dalloc<uint32_t>(w.fb, slots) && dalloc<uint2>(w.chunks, max_chunks) &&
+            dalloc<uint2>(w.smalls, slots) && dalloc<Control>(w.ctl, 1) &&
+            dalloc<QueryParam>(w.params, Q) && dalloc<Seed>(w.seeds, Q);
   if (ok && fastest) ok = dalloc<int32_t>(w.R, slots) != nullptr;
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (traversal workspace)");
   w.slots = std::max(w.slots, slots);
@@ -415,12 +414,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.bitmap = w.bitmap.as<uint32_t>();
   a.fa = w.fa.as<uint32_t>();
   a.fb = w.fb.as<uint32_t>();
-  a.cnt = w.cnt.as<uint32_t>();
-  a.lo = w.lo.as<uint32_t>();
-  a.ranges = w.ranges.as<RangeEntry>();
-  a.bsum = w.bsum.as<unsigned long long>();
-  a.bnz = w.bnz.as<uint32_t>();
-  a.bidx = w.bidx.as<uint32_t>();
+  a.chunks = w.chunks.as<uint2>();
+  a.smalls = w.smalls.as<uint2>();
   a.ctl = w.ctl.as<Control>();
   a.n = G->n;
   a.Q = P.Q;

@@ -57,18 +57,10 @@ struct QueryParam {
 };
 constexpr uint32_t kNoRoot = 0xffffffffu;
 
-// Range of the frontier: the edges [lo, lo + cnt) of one frontier item, whose
-// exclusive work prefix is pfx. Only non-empty ranges are kept.
-struct RangeEntry {
-  unsigned long long pfx;
-  uint32_t lo;
-  uint32_t item;
-};
-
 // Traversal workspace, sized for q_cap concurrent queries.
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
-  DeviceBuffer X, Ex, R, bitmap, fa, fb, cnt, lo, ranges, bsum, bnz, bidx, ctl, params, seeds;
+  DeviceBuffer X, Ex, R, bitmap, fa, fb, chunks, smalls, ctl, params, seeds;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // what the last query left in X (for tgxd_last_work)
@@ -78,16 +70,18 @@ struct Workspace {
   std::vector<QueryParam> last_params;
 };
 
-// Device control block (one per workspace), see traverse.cu.
+// Device control block (one per workspace), see traverse.cuh. The three
+// work counters only ever grow during a query; each round works on the
+// difference between its start and end values.
 struct Control {
-  unsigned int fc[2];              // frontier sizes, indexed by round parity
-  unsigned long long work_all;     // edges handed to the relax step, all rounds
-  unsigned long long expansions;   // non-empty ranges, all rounds
-  unsigned long long index_lookups;
+  unsigned long long pushes;        // frontier appends (queue position)
+  unsigned long long chunks;        // big-range chunks emitted
+  unsigned long long smalls;        // small ranges emitted
+  unsigned long long work_all;      // edges handed to the relax step
+  unsigned long long expansions;    // non-empty ranges (chunks + small ranges)
+  unsigned long long index_lookups; // expansions that used the fence index
   unsigned int rounds;
   unsigned int candidates;
-  unsigned long long e_adm;        // tgxd_last_work accumulators
-  unsigned long long v_reached;
 };
 
 }  // namespace tgxd

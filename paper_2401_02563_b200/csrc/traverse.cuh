@@ -3,17 +3,18 @@
 // (reference: path_algorithms.cpp:262-357,436-528 driving temporal_edge_map,
 // engine.hpp:239-353).
 //
-// One persistent cooperative kernel runs the whole query: every round is
-//   A1  expand: per frontier item, locate the not-yet-relaxed admissible key
-//       range of its segment (selective index: fence search for hubs, plain
-//       binary search otherwise) and record its size;
-//   A2  scan: grid-wide exclusive scan of range sizes, compacting non-empty
-//       ranges into a merge-path table;
-//   B   relax: every warp takes an equal slab of the round's edge work,
-//       resolves its lanes' ranges with shuffles, streams dst/val coalesced,
-//       relaxes labels with atomicMin and appends improved vertices to the
-//       next frontier (bitmap dedup + warp-aggregated append);
-// separated by grid barriers. No host round trip per round.
+// One persistent cooperative kernel runs the whole query. Each round is
+//   A  expand: every frontier item locates the not-yet-relaxed admissible key
+//      range of its segment (selective index: fence search for hubs, plain
+//      binary search otherwise) and emits it as work: ranges of >= 32 edges
+//      as fixed-size chunks, shorter ones into a small-range list
+//      (warp-aggregated atomic emission — no ordered scan needed);
+//   B  relax: warps stream chunks (coalesced, unrolled) and pack 32 small
+//      ranges per warp (lane ownership from a redux.or start mask), relax
+//      labels with atomicMin and append improved vertices to the next
+//      frontier through per-warp shared-memory push buffers;
+// separated by grid barriers. No host round trip per round. All counters
+// are monotone, so no round ever resets one (no extra barrier).
 //
 // Work efficiency. Labels only decrease (key space) and the relaxed value of
 // an edge (its val) does not depend on the label that admitted it, so once an
@@ -33,29 +34,29 @@ namespace tgxd {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 4;                       // 32-edge steps in flight per warp
+constexpr uint32_t kChunk = 32u * kUnroll;       // edges per chunk of a big range
+constexpr uint32_t kSmall = 32;                  // ranges below this go to the small list
+constexpr uint32_t kChunkLenBits = 9;            // kChunk <= 256
+constexpr uint32_t kSmallCntBits = 6;
 
 struct TravArgs {
   DevCsr g;
   const QueryParam* qp;
-  int32_t* X;         // labels, Q x n (key space)
-  int32_t* Ex;        // bound each vertex was last expanded with
-  int32_t* R;         // fastest durations (nullptr otherwise)
-  uint32_t* bitmap;   // queued flags, Q x n bits
-  uint32_t* fa;       // frontier queues (items = q * n + v)
+  int32_t* X;          // labels, Q x n (key space)
+  int32_t* Ex;         // bound each vertex was last expanded with
+  int32_t* R;          // fastest durations (nullptr otherwise)
+  uint32_t* bitmap;    // queued flags, Q x n bits
+  uint32_t* fa;        // frontier queues (items = q * n + v)
   uint32_t* fb;
-  uint32_t* cnt;      // per frontier slot: range size
-  uint32_t* lo;       // per frontier slot: range start
-  RangeEntry* ranges; // compacted non-empty ranges + sentinel
-  unsigned long long* bsum;
-  uint32_t* bnz;
-  uint32_t* bidx;
+  uint2* chunks;       // {lo, q << 9 | len}
+  uint2* smalls;       // {lo, q << 6 | cnt}
   Control* ctl;
   uint32_t n;
   uint32_t Q;
   int strict;
   uint32_t cutoff;
-  int mode;           // tgxd_mode
+  int mode;            // tgxd_mode
   // fastest sweep (Q == 1)
   int fastest;
   uint32_t n_cand;
@@ -64,12 +65,12 @@ struct TravArgs {
   const int32_t* cand_key;
 };
 
-__device__ __forceinline__ int32_t ld_nc(const int32_t* p) {
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   int32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
-__device__ __forceinline__ uint32_t ld_nc(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
   uint32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
@@ -104,370 +105,329 @@ __device__ __forceinline__ uint32_t lower_key(const DevCsr& g, uint32_t s, uint3
   return s;
 }
 
-struct Sums {
-  unsigned long long w;
-  uint32_t nz;
-  uint32_t ix;
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+// Per-warp push buffer: improved vertices are staged in shared memory and
+// appended to the next frontier 32 at a time (one global atomic per 32).
+struct PushBuf {
+  uint32_t* buf;  // 64 entries of this warp
+  uint32_t n;     // staged entries (warp-uniform)
 };
 
-// Block-wide exclusive scan of (w, nz) pairs; returns the block totals.
-__device__ __forceinline__ void block_scan2(unsigned long long w, uint32_t nz,
-                                            unsigned long long& ew, uint32_t& enz,
-                                            unsigned long long& tw, uint32_t& tnz) {
-  __shared__ unsigned long long s_w[kWarps];
-  __shared__ uint32_t s_nz[kWarps];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned long long iw = w;
-  uint32_t inz = nz;
+__device__ __forceinline__ void push_flush32(PushBuf& pb, Control* ctl,
+                                             unsigned long long pstart, uint32_t* fout) {
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  const uint32_t v = pb.buf[lane];
+  const uint32_t tail = pb.buf[32 + lane];
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&ctl->pushes, 32ull);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  fout[base - pstart + lane] = v;
+  __syncwarp();
+  if (lane + 32 < pb.n) pb.buf[lane] = tail;
+  pb.n -= 32;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void push(PushBuf& pb, bool p, uint32_t item, Control* ctl,
+                                     unsigned long long pstart, uint32_t* fout) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, p);
+  if (bal == 0) return;
+  const uint32_t lane = lane_id();
+  if (p) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = item;
+  pb.n += __popc(bal);
+  if (pb.n >= 32) push_flush32(pb, ctl, pstart, fout);
+}
+
+__device__ __forceinline__ void push_drain(PushBuf& pb, Control* ctl, unsigned long long pstart,
+                                           uint32_t* fout) {
+  if (pb.n == 0) return;
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&ctl->pushes, (unsigned long long)pb.n);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < pb.n) fout[base - pstart + lane] = pb.buf[lane];
+  pb.n = 0;
+  __syncwarp();
+}
+
+// Relax kUnroll 32-edge steps: e[u] edge ids, q[u] query slots, act[u] lane
+// validity. write_min (parallel.hpp:91-99) + claim_stamp (:113-121) become a
+// plain label probe, atomicMin, and an atomicOr on the queued bitmap.
+__device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&e)[kUnroll],
+                                            const uint32_t (&q)[kUnroll],
+                                            const bool (&act)[kUnroll], int32_t vhi0,
+                                            int32_t depart, PushBuf& pb,
+                                            unsigned long long pstart, uint32_t* fout) {
+  int32_t v[kUnroll];
+  uint32_t d[kUnroll];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long yw = __shfl_up_sync(0xffffffffu, iw, o);
-    const uint32_t ynz = __shfl_up_sync(0xffffffffu, inz, o);
-    if (lane >= o) {
-      iw += yw;
-      inz += ynz;
-    }
+  for (int u = 0; u < kUnroll; ++u) {
+    v[u] = act[u] ? ld_stream(a.g.val + e[u]) : kInf;
+    d[u] = act[u] ? ld_stream(a.g.nbr + e[u]) : 0u;
   }
-  if (lane == 31) {
-    s_w[wid] = iw;
-    s_nz[wid] = inz;
-  }
-  __syncthreads();
-  unsigned long long bw = 0, totw = 0;
-  uint32_t bnz = 0, totnz = 0;
+  uint32_t idx[kUnroll];
+  int32_t cur[kUnroll];
 #pragma unroll
-  for (int k = 0; k < kWarps; ++k) {
-    if (k < wid) {
-      bw += s_w[k];
-      bnz += s_nz[k];
-    }
-    totw += s_w[k];
-    totnz += s_nz[k];
+  for (int u = 0; u < kUnroll; ++u) {
+    const int32_t vhi = a.Q == 1 ? vhi0 : __ldg(&a.qp[q[u]].vhi);
+    // window containment: end <= t_b (types.hpp:55-57)
+    const bool ok = act[u] && v[u] <= vhi;
+    idx[u] = q[u] * a.n + d[u];
+    cur[u] = ok ? __ldcg(a.X + idx[u]) : kInf;
+    if (!ok) v[u] = kInf;
   }
-  __syncthreads();
-  ew = bw + iw - w;
-  enz = bnz + inz - nz;
-  tw = totw;
-  tnz = totnz;
-}
-
-__device__ __forceinline__ void block_sum2(unsigned long long& w, uint32_t& nz) {
-  __shared__ unsigned long long r_w[kWarps];
-  __shared__ uint32_t r_nz[kWarps];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    w += __shfl_xor_sync(0xffffffffu, w, o);
-    nz += __shfl_xor_sync(0xffffffffu, nz, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    r_w[threadIdx.x >> 5] = w;
-    r_nz[threadIdx.x >> 5] = nz;
-  }
-  __syncthreads();
-  w = 0;
-  nz = 0;
-#pragma unroll
-  for (int k = 0; k < kWarps; ++k) {
-    w += r_w[k];
-    nz += r_nz[k];
-  }
-  __syncthreads();
-}
-
-// Expansion of one frontier item: clears its queued flag, computes the range
-// of keys [bound, previous bound) still to relax and records it.
-__device__ __forceinline__ uint32_t expand_item(const TravArgs& a, uint32_t item, uint32_t& lo_out,
-                                                uint32_t& ix) {
-  const uint32_t q = a.Q == 1 ? 0u : item / a.n;
-  const uint32_t v = item - q * a.n;
-  const QueryParam qp = a.qp[q];
-  const int32_t x = __ldcg(a.X + item);
-  // min_start / max_end hook (path_algorithms.cpp:287-291, :337-342): the
-  // root leaves at any time inside the window; everyone else strictly
-  // (or weakly) after its own label.
-  int32_t lb = (v == qp.root) ? qp.klo : (x == kInf ? kInf : x + a.strict);
-  if (lb < qp.klo) lb = qp.klo;
-  const int32_t old = __ldcg(a.Ex + item);
-  lo_out = 0;
-  if (lb >= old) return 0;
-  a.Ex[item] = lb;
-  const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
-  if (lb >= hik) return 0;
-  const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-  const bool idx = a.cutoff != 0 && t - s >= a.cutoff;
-  ix += idx;
-  const uint32_t p0 = lower_key(a.g, s, t, lb, idx);
-  const uint32_t p1 = lower_key(a.g, p0, t, hik, idx);
-  lo_out = p0;
-  return p1 - p0;
-}
-
-// Phase A1: contiguous frontier chunk per block.
-__device__ void phase_a1(const TravArgs& a, const uint32_t* fin, uint32_t F) {
-  const uint32_t chunk = (F + gridDim.x - 1) / gridDim.x;
-  const uint32_t beg = min(F, blockIdx.x * chunk), end = min(F, beg + chunk);
-  unsigned long long w = 0;
-  uint32_t nz = 0, ix = 0;
-  for (uint32_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    const uint32_t item = __ldcg(fin + i);
-    a.bitmap[item >> 5] = 0u;  // every set bit belongs to a frontier item
-    uint32_t lo;
-    const uint32_t c = expand_item(a, item, lo, ix);
-    a.cnt[i] = c;
-    a.lo[i] = lo;
-    w += c;
-    nz += c != 0;
-  }
-  block_sum2(w, nz);
-  unsigned long long dummy = ix;
-  uint32_t ixs = 0;
-  block_sum2(dummy, ixs);
-  if (threadIdx.x == 0) {
-    a.bsum[blockIdx.x] = w;
-    a.bnz[blockIdx.x] = nz;
-    a.bidx[blockIdx.x] = (uint32_t)dummy;
-  }
-}
-
-// Phase A2: block offsets from the per-block sums, then an in-order scan of
-// the block's chunk writing compacted, prefix-annotated ranges.
-__device__ void phase_a2(const TravArgs& a, const uint32_t* fin, uint32_t F,
-                         unsigned long long& W, uint32_t& NR, uint32_t& IX) {
-  __shared__ unsigned long long s_pre_w, s_tot_w;
-  __shared__ uint32_t s_pre_nz, s_tot_nz, s_tot_ix;
-  unsigned long long pw = 0, tw = 0, ix = 0;
-  uint32_t pnz = 0, tnz = 0, dz = 0;
-  for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
-    const unsigned long long bw = __ldcg(a.bsum + j);
-    const uint32_t bn = __ldcg(a.bnz + j);
-    if (j < blockIdx.x) {
-      pw += bw;
-      pnz += bn;
-    }
-    tw += bw;
-    tnz += bn;
-    ix += __ldcg(a.bidx + j);
-  }
-  block_sum2(pw, pnz);
-  block_sum2(tw, tnz);
-  block_sum2(ix, dz);
-  if (threadIdx.x == 0) {
-    s_pre_w = pw;
-    s_pre_nz = pnz;
-    s_tot_w = tw;
-    s_tot_nz = tnz;
-    s_tot_ix = (uint32_t)ix;
-  }
-  __syncthreads();
-  unsigned long long base_w = s_pre_w;
-  uint32_t base_nz = s_pre_nz;
-  W = s_tot_w;
-  NR = s_tot_nz;
-  IX = s_tot_ix;
-  const uint32_t chunk = (F + gridDim.x - 1) / gridDim.x;
-  const uint32_t beg = min(F, blockIdx.x * chunk), end = min(F, beg + chunk);
-  for (uint32_t tile = beg; tile < end; tile += blockDim.x) {
-    const uint32_t i = tile + threadIdx.x;
-    const uint32_t c = i < end ? __ldcg(a.cnt + i) : 0u;
-    unsigned long long ew, bw;
-    uint32_t enz, bnz;
-    block_scan2(c, c != 0, ew, enz, bw, bnz);
-    if (c != 0) {
-      const uint32_t item = __ldcg(fin + i);
-      RangeEntry r;
-      r.pfx = base_w + ew;
-      r.lo = __ldcg(a.lo + i);
-      r.item = a.Q == 1 ? 0u : item / a.n;
-      a.ranges[base_nz + enz] = r;
-    }
-    base_w += bw;
-    base_nz += bnz;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.ranges[NR].pfx = W;  // merge-path sentinel
-  }
-}
-
-// Phase B: merge-path relax of W edge-work items over NR ranges. With
-// `single`, the table is the one explicit range (lo0, q = 0) — the seed
-// edges of a fastest candidate.
-__device__ void phase_b(const TravArgs& a, unsigned long long W, uint32_t NR, bool single,
-                        uint32_t lo0, int32_t depart, uint32_t* fout, unsigned int* fcn) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t nw = gridDim.x * kWarps;
-  unsigned long long S = (W + nw - 1) / nw;
-  S = (S + 31) & ~31ull;
-  if (S < 32) S = 32;
-  const unsigned long long s0 = (unsigned long long)gw * S;
-  if (s0 >= W) return;
-  const unsigned long long s1 = min(W, s0 + S);
-
-  uint32_t i = 0;
-  if (!single) {
-    uint32_t lo = 0, hi = NR;  // first range with pfx > s0
-    if (lane == 0) {
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldcg(&a.ranges[mid].pfx) <= s0) lo = mid + 1;
-        else hi = mid;
+  for (int u = 0; u < kUnroll; ++u) {
+    bool p = false;
+    if (v[u] < cur[u]) {
+      const int32_t old = atomicMin(a.X + idx[u], v[u]);
+      if (v[u] < old) {
+        if (a.R) atomicMin(a.R + idx[u], v[u] - depart);
+        const uint32_t m = 1u << (idx[u] & 31);
+        p = (atomicOr(a.bitmap + (idx[u] >> 5), m) & m) == 0;
       }
     }
-    i = __shfl_sync(0xffffffffu, lo, 0) - 1;
+    push(pb, p, idx[u], a.ctl, pstart, fout);
   }
-  const int32_t vhi0 = a.qp[0].vhi;
-  uint32_t wi = 0xffffffffu;
-  unsigned long long endP = 0, Pi = 0;
-  uint32_t wlo = 0, wq = 0;
+}
 
-  for (unsigned long long base = s0; base < s1; base += 32ull * kUnroll) {
-    uint32_t e[kUnroll], qq[kUnroll];
+// Phase A: expand the frontier and emit work.
+__device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
+                        unsigned long long cstart, unsigned long long sstart,
+                        unsigned long long& work, unsigned long long& ix) {
+  const uint32_t lane = lane_id();
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  const uint32_t tbase = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  for (uint32_t base = tbase; base < F; base += nthreads) {
+    const uint32_t i = base + lane;
+    uint32_t cnt = 0, lo = 0, q = 0;
+    if (i < F) {
+      const uint32_t item = __ldcg(fin + i);
+      a.bitmap[item >> 5] = 0u;  // every set bit belongs to a frontier item
+      q = a.Q == 1 ? 0u : item / a.n;
+      const uint32_t v = item - q * a.n;
+      const QueryParam qp = a.qp[q];
+      const int32_t x = __ldcg(a.X + item);
+      // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342):
+      // the root leaves at any time inside the window; everyone else
+      // strictly (or weakly) after its own label.
+      int32_t lb = (v == qp.root) ? qp.klo : (x == kInf ? kInf : x + a.strict);
+      if (lb < qp.klo) lb = qp.klo;
+      const int32_t old = __ldcg(a.Ex + item);
+      if (lb < old) {
+        a.Ex[item] = lb;
+        const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
+        if (lb < hik) {
+          const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
+          const bool use_idx = a.cutoff != 0 && t - s >= a.cutoff;
+          ix += use_idx;
+          const uint32_t p0 = lower_key(a.g, s, t, lb, use_idx);
+          const uint32_t p1 = lower_key(a.g, p0, t, hik, use_idx);
+          lo = p0;
+          cnt = p1 - p0;
+          work += cnt;
+        }
+      }
+    }
+    // warp-aggregated emission
+    const bool small = cnt != 0 && cnt < kSmall;
+    const uint32_t nch = cnt >= kSmall ? (cnt + kChunk - 1) / kChunk : 0u;
+    const uint32_t sbal = __ballot_sync(0xffffffffu, small);
+    uint32_t incl = nch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long cb = 0, sb = 0;
+    if (lane == 0) {
+      if (tot) cb = atomicAdd(&a.ctl->chunks, (unsigned long long)tot);
+      if (sbal) sb = atomicAdd(&a.ctl->smalls, (unsigned long long)__popc(sbal));
+    }
+    cb = __shfl_sync(0xffffffffu, cb, 0);
+    sb = __shfl_sync(0xffffffffu, sb, 0);
+    if (small) {
+      const uint64_t pos = sb - sstart + __popc(sbal & ((1u << lane) - 1));
+      a.smalls[pos] = make_uint2(lo, (q << kSmallCntBits) | cnt);
+    }
+    if (nch) {
+      uint64_t pos = cb - cstart + incl - nch;
+      for (uint32_t c = 0; c < nch; ++c, ++pos) {
+        const uint32_t off = c * kChunk;
+        const uint32_t len = min(kChunk, cnt - off);
+        a.chunks[pos] = make_uint2(lo + off, (q << kChunkLenBits) | len);
+      }
+    }
+  }
+}
+
+// Phase B: relax the round's chunks and small ranges (plus, for a fastest
+// seed round, the virtual chunks of one explicit range).
+__device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned long long nsmall,
+                        uint32_t xlo, uint32_t xcnt, int32_t depart, unsigned long long pstart,
+                        uint32_t* fout, uint32_t* wbuf) {
+  const uint32_t lane = lane_id();
+  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t nw = gridDim.x * kWarps;
+  const int32_t vhi0 = a.qp[0].vhi;
+  PushBuf pb{wbuf, 0};
+
+  // explicit range (fastest seeds), split into virtual chunks
+  const uint32_t nx = (xcnt + kChunk - 1) / kChunk;
+  for (uint32_t c = gw; c < nx; c += nw) {
+    uint32_t e[kUnroll], q[kUnroll];
     bool act[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const unsigned long long b = base + 32ull * u;
-      act[u] = false;
-      e[u] = 0;
-      qq[u] = 0;
-      if (b < s1) {
-        if (i != wi) {  // (re)load the 32-range window starting at range i
-          wi = i;
-          if (single) {
-            endP = lane == 0 ? W : ~0ull;
-            wlo = lo0;
-            wq = 0;
-            Pi = 0;
-          } else {
-            const uint32_t r = i + lane;
-            unsigned long long p = ~0ull;
-            if (r <= NR) {
-              const RangeEntry re = a.ranges[r];
-              p = re.pfx;
-              wlo = re.lo;
-              wq = re.item;
-            }
-            Pi = __shfl_sync(0xffffffffu, p, 0);
-            endP = __shfl_down_sync(0xffffffffu, p, 1);
-            if (lane == 31) endP = (r + 1 <= NR) ? __ldcg(&a.ranges[r + 1].pfx) : ~0ull;
-            if (r >= NR) endP = ~0ull;
-          }
-        }
-        const unsigned long long t = b + lane;
-        uint32_t pos = 0;
-#pragma unroll
-        for (uint32_t step = 16; step >= 1; step >>= 1) {
-          const unsigned long long ev = __shfl_sync(0xffffffffu, endP, pos + step - 1);
-          if (ev <= t) pos += step;
-        }
-        const unsigned long long prev = __shfl_sync(0xffffffffu, endP, pos > 0 ? pos - 1 : 0);
-        const unsigned long long startP = pos ? prev : Pi;
-        const uint32_t rlo = __shfl_sync(0xffffffffu, wlo, pos);
-        const uint32_t rq = __shfl_sync(0xffffffffu, wq, pos);
-        act[u] = t < s1;
-        e[u] = rlo + (uint32_t)(t - startP);
-        qq[u] = rq;
-        i += __popc(__ballot_sync(0xffffffffu, endP <= b + 32));
-      }
+      const uint32_t off = c * kChunk + u * 32 + lane;
+      act[u] = off < xcnt;
+      e[u] = xlo + off;
+      q[u] = 0;
     }
-    int32_t v[kUnroll];
-    uint32_t d[kUnroll];
+    relax_steps(a, e, q, act, vhi0, depart, pb, pstart, fout);
+  }
+
+  // chunks of big ranges: coalesced kChunk-edge bursts
+  for (unsigned long long c = gw; c < nchunks; c += nw) {
+    const uint2 ch = a.chunks[c];
+    const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
+    const uint32_t cq = ch.y >> kChunkLenBits;
+    uint32_t e[kUnroll], q[kUnroll];
+    bool act[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      if (act[u]) {
-        v[u] = ld_nc(a.g.val + e[u]);
-        d[u] = ld_nc(a.g.nbr + e[u]);
-      }
+      const uint32_t off = u * 32 + lane;
+      act[u] = off < len;
+      e[u] = ch.x + off;
+      q[u] = cq;
     }
-    uint32_t idx[kUnroll];
-    bool cand[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      cand[u] = false;
-      idx[u] = 0;
-      if (act[u]) {
-        const int32_t vhi = a.Q == 1 ? vhi0 : a.qp[qq[u]].vhi;
-        if (v[u] <= vhi) {  // window containment: end <= t_b (types.hpp:55-57)
-          idx[u] = qq[u] * a.n + d[u];
-          cand[u] = true;
-        }
-      }
+    relax_steps(a, e, q, act, vhi0, depart, pb, pstart, fout);
+  }
+
+  // small ranges: 32 per warp window; lane l owns range l, items are packed
+  // densely and each lane finds its owner from the mask of range starts.
+  const unsigned long long nwin = (nsmall + 31) / 32;
+  for (unsigned long long w = gw; w < nwin; w += nw) {
+    const unsigned long long r = w * 32 + lane;
+    uint32_t lo = 0, cnt = 0, rq = 0;
+    if (r < nsmall) {
+      const uint2 s = a.smalls[r];
+      lo = s.x;
+      cnt = s.y & ((1u << kSmallCntBits) - 1);
+      rq = s.y >> kSmallCntBits;
     }
-    int32_t cur[kUnroll];
+    uint32_t incl = cnt;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) cur[u] = cand[u] ? __ldcg(a.X + idx[u]) : kInf;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t start = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
+      uint32_t e[kUnroll], q[kUnroll];
+      bool act[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      bool push = false;
-      if (cand[u] && v[u] < cur[u]) {
-        const int32_t old = atomicMin(a.X + idx[u], v[u]);  // write_min, parallel.hpp:91-99
-        if (v[u] < old) {
-          if (a.R) atomicMin(a.R + idx[u], v[u] - depart);
-          const uint32_t m = 1u << (idx[u] & 31);
-          const uint32_t ob = atomicOr(a.bitmap + (idx[u] >> 5), m);  // frontier claim
-          push = (ob & m) == 0;
-        }
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t sb = base + u * 32;
+        // owner of item sb: last range starting at or before it
+        const uint32_t before = __ballot_sync(0xffffffffu, cnt != 0 && start <= sb);
+        const uint32_t i0 = before ? 31 - __clz(before) : 0;
+        // ranges starting strictly inside (sb, sb + 32)
+        const uint32_t rel = start - sb;
+        const uint32_t bit = (cnt != 0 && start > sb && rel < 32) ? (1u << rel) : 0u;
+        const uint32_t mask = __reduce_or_sync(0xffffffffu, bit);
+        const uint32_t own = i0 + __popc(mask & ((2u << lane) - 1));
+        const uint32_t olo = __shfl_sync(0xffffffffu, lo, own & 31);
+        const uint32_t ost = __shfl_sync(0xffffffffu, start, own & 31);
+        const uint32_t oq = __shfl_sync(0xffffffffu, rq, own & 31);
+        const uint32_t t = sb + lane;
+        act[u] = t < total;
+        e[u] = olo + (t - ost);
+        q[u] = oq;
       }
-      const uint32_t bal = __ballot_sync(0xffffffffu, push);
-      if (bal) {
-        uint32_t basep = 0;
-        const uint32_t leader = __ffs(bal) - 1;
-        if (lane == leader) basep = atomicAdd(fcn, __popc(bal));
-        basep = __shfl_sync(0xffffffffu, basep, leader);
-        if (push) fout[basep + __popc(bal & ((1u << lane) - 1))] = idx[u];
-      }
+      relax_steps(a, e, q, act, vhi0, depart, pb, pstart, fout);
     }
   }
+  push_drain(pb, a.ctl, pstart, fout);
 }
 
-__global__ void __launch_bounds__(kThreads) traverse_kernel(TravArgs a) {
+struct RoundCounters {
+  unsigned long long pushes, chunks, smalls;
+};
+
+__device__ __forceinline__ RoundCounters read_counters(const Control* ctl) {
+  RoundCounters r;
+  r.pushes = __ldcg(&ctl->pushes);
+  r.chunks = __ldcg(&ctl->chunks);
+  r.smalls = __ldcg(&ctl->smalls);
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
+  __shared__ uint32_t s_buf[kWarps][64];
   cg::grid_group grid = cg::this_grid();
+  uint32_t* wbuf = s_buf[threadIdx.x >> 5];
   uint32_t* fin = a.fa;
   uint32_t* fout = a.fb;
-  uint32_t round = 0;
-  unsigned long long work = 0, expansions = 0, index_lookups = 0;
   Control* ctl = a.ctl;
+  uint32_t rounds = 0;
+  unsigned long long work = 0, ix = 0, expansions = 0;
+  // the initial frontier (seed_kernel) occupies pushes [0, Q) of fa
+  unsigned long long prev_p = 0;
   for (uint32_t cand = 0;; ++cand) {
+    int32_t depart = 0;
     if (a.fastest) {
       if (cand >= a.n_cand) break;
       // Seed round (path_algorithms.cpp:476-486): the candidate's first
       // edges, relaxed without an admissibility check.
+      depart = a.cand_key[cand];
       const uint32_t c0 = a.cand_cnt[cand];
-      phase_b(a, c0, 1, true, a.cand_lo[cand], a.cand_key[cand], fout, &ctl->fc[(round + 1) & 1]);
-      work += c0;
+      const RoundCounters rc = read_counters(ctl);
+      phase_b(a, 0, 0, a.cand_lo[cand], c0, depart, rc.pushes, fout, wbuf);
+      if (blockIdx.x == 0 && threadIdx.x == 0) work += c0;
+      prev_p = rc.pushes;
       grid.sync();
-      ++round;
+      ++rounds;
       uint32_t* t = fin;
       fin = fout;
       fout = t;
     }
-    const int32_t depart = a.fastest ? a.cand_key[cand] : 0;
     for (;;) {
-      const uint32_t F = __ldcg(&ctl->fc[round & 1]);
+      const RoundCounters rc = read_counters(ctl);
+      const uint32_t F = (uint32_t)(rc.pushes - prev_p);
       if (F == 0) break;
-      phase_a1(a, fin, F);
+      phase_a(a, fin, F, rc.chunks, rc.smalls, work, ix);
       grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->fc[round & 1] = 0;
-      unsigned long long W;
-      uint32_t NR, IX;
-      phase_a2(a, fin, F, W, NR, IX);
+      const RoundCounters rb = read_counters(ctl);
+      const unsigned long long nch = rb.chunks - rc.chunks, nsm = rb.smalls - rc.smalls;
+      phase_b(a, nch, nsm, 0, 0, depart, rc.pushes, fout, wbuf);
+      expansions += nch + nsm;
+      prev_p = rc.pushes;
       grid.sync();
-      if (W) phase_b(a, W, NR, false, 0, depart, fout, &ctl->fc[(round + 1) & 1]);
-      work += W;
-      expansions += NR;
-      index_lookups += IX;
-      grid.sync();
-      ++round;
+      ++rounds;
       uint32_t* t = fin;
       fin = fout;
       fout = t;
     }
     if (!a.fastest) break;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    work += __shfl_xor_sync(0xffffffffu, work, o);
+    ix += __shfl_xor_sync(0xffffffffu, ix, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (work) atomicAdd(&ctl->work_all, work);
+    if (ix) atomicAdd(&ctl->index_lookups, ix);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->rounds = round;
-    ctl->work_all = work;
+    ctl->rounds = rounds;
     ctl->expansions = expansions;
-    ctl->index_lookups = index_lookups;
     ctl->candidates = a.fastest ? a.n_cand : 0;
   }
 }
@@ -476,7 +436,14 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(TravArgs a) {
 __global__ void init_kernel(int32_t* X, int32_t* Ex, int32_t* R, uint32_t* bitmap, size_t nl,
                             size_t nwords) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+  const size_t n4 = nl / 4;
+  const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    reinterpret_cast<int4*>(X)[i] = inf4;
+    reinterpret_cast<int4*>(Ex)[i] = inf4;
+    if (R) reinterpret_cast<int4*>(R)[i] = inf4;
+  }
+  for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
     X[i] = kInf;
     Ex[i] = kInf;
     if (R) R[i] = kInf;
@@ -490,8 +457,12 @@ __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_
                             uint32_t* bitmap, uint32_t* fa, Control* ctl, int fastest) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q == 0) {
-    ctl->fc[0] = fastest ? 0u : Q;
-    ctl->fc[1] = 0u;
+    ctl->pushes = fastest ? 0ull : Q;
+    ctl->chunks = 0;
+    ctl->smalls = 0;
+    ctl->work_all = 0;
+    ctl->expansions = 0;
+    ctl->index_lookups = 0;
   }
   if (q >= Q || fastest) return;
   const uint32_t item = q * n + qp[q].root;
