@@ -356,18 +356,6 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
   push_drain(pb, a.ctl, pstart, fout);
 }
 
-struct RoundCounters {
-  unsigned long long pushes, chunks, smalls;
-};
-
-__device__ __forceinline__ RoundCounters read_counters(const Control* ctl) {
-  RoundCounters r;
-  r.pushes = __ldcg(&ctl->pushes);
-  r.chunks = __ldcg(&ctl->chunks);
-  r.smalls = __ldcg(&ctl->smalls);
-  return r;
-}
-
 __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
   cg::grid_group grid = cg::this_grid();
@@ -377,20 +365,23 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
   Control* ctl = a.ctl;
   uint32_t rounds = 0;
   unsigned long long work = 0, ix = 0, expansions = 0;
-  // the initial frontier (seed_kernel) occupies pushes [0, Q) of fa
-  unsigned long long prev_p = 0;
+  // Counter discipline: `pushes` only grows in phase B and is read at round
+  // start (phase A); `chunks` / `smalls` only grow in phase A and are read
+  // in phase B. A counter is never read while another block may be moving
+  // it, so every block sees the same round boundaries.
+  unsigned long long prev_p = 0;         // queue position where fin's items start
+  unsigned long long c_cur = 0, s_cur = 0;
   for (uint32_t cand = 0;; ++cand) {
     int32_t depart = 0;
     if (a.fastest) {
       if (cand >= a.n_cand) break;
       // Seed round (path_algorithms.cpp:476-486): the candidate's first
-      // edges, relaxed without an admissibility check.
+      // edges, relaxed without an admissibility check. The queue is empty
+      // here, so pushes == prev_p for every block.
       depart = a.cand_key[cand];
       const uint32_t c0 = a.cand_cnt[cand];
-      const RoundCounters rc = read_counters(ctl);
-      phase_b(a, 0, 0, a.cand_lo[cand], c0, depart, rc.pushes, fout, wbuf);
+      phase_b(a, 0, 0, a.cand_lo[cand], c0, depart, prev_p, fout, wbuf);
       if (blockIdx.x == 0 && threadIdx.x == 0) work += c0;
-      prev_p = rc.pushes;
       grid.sync();
       ++rounds;
       uint32_t* t = fin;
@@ -398,16 +389,17 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
       fout = t;
     }
     for (;;) {
-      const RoundCounters rc = read_counters(ctl);
-      const uint32_t F = (uint32_t)(rc.pushes - prev_p);
+      const unsigned long long p_now = __ldcg(&ctl->pushes);
+      const uint32_t F = (uint32_t)(p_now - prev_p);
       if (F == 0) break;
-      phase_a(a, fin, F, rc.chunks, rc.smalls, work, ix);
+      phase_a(a, fin, F, c_cur, s_cur, work, ix);
       grid.sync();
-      const RoundCounters rb = read_counters(ctl);
-      const unsigned long long nch = rb.chunks - rc.chunks, nsm = rb.smalls - rc.smalls;
-      phase_b(a, nch, nsm, 0, 0, depart, rc.pushes, fout, wbuf);
-      expansions += nch + nsm;
-      prev_p = rc.pushes;
+      const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
+      phase_b(a, c_end - c_cur, s_end - s_cur, 0, 0, depart, p_now, fout, wbuf);
+      expansions += (c_end - c_cur) + (s_end - s_cur);
+      c_cur = c_end;
+      s_cur = s_end;
+      prev_p = p_now;
       grid.sync();
       ++rounds;
       uint32_t* t = fin;
