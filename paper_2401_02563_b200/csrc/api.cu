@@ -427,6 +427,9 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.cand_lo = w.cand_lo.as<uint32_t>();
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
+  a.trace = w.trace_cap ? w.trace.as<unsigned long long>() : nullptr;
+  a.trace_cap = w.trace_cap;
+  if (a.trace) TGXD_CUDA(cudaMemsetAsync(w.trace.p, 0, w.trace_cap * 64ull, s));
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
     void* args[] = {&a};
@@ -938,6 +941,27 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
   destroy();
   *total_ms = tot;
   *kernel_ms = ksum / steps;
+  return TGXD_OK;
+}
+
+int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds) {
+  if (!g) return fail(TGXD_ERR_ARGUMENT, "null graph");
+  std::lock_guard<std::mutex> lock(g->mu);
+  TGXD_CUDA(cudaSetDevice(g->device));
+  if (max_rounds && !dalloc<unsigned long long>(g->ws.trace, max_rounds * 8ull))
+    return fail(TGXD_ERR_CUDA, "allocation (trace)");
+  g->ws.trace_cap = max_rounds;
+  return TGXD_OK;
+}
+
+int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds) {
+  if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  const uint32_t r = std::min(max_rounds, g->ws.trace_cap);
+  if (r) {
+    TGXD_CUDA(cudaMemcpyAsync(out, g->ws.trace.p, r * 64ull, cudaMemcpyDeviceToHost, g->stream));
+    TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  }
   return TGXD_OK;
 }
 

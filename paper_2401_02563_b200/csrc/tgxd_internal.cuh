@@ -61,7 +61,8 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
   DeviceBuffer X, Ex, R, bitmap, fa, fb, chunks, smalls, ctl, params, seeds;
-  DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
+  DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out, trace;
+  uint32_t trace_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // what the last query left in X (for tgxd_last_work)
   int last_kind = -1;

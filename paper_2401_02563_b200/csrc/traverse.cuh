@@ -63,7 +63,17 @@ struct TravArgs {
   const uint32_t* cand_lo;
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
+  // optional per-round trace (block 0): {t_start, t_after_A, t_after_B, F,
+  // chunks, smalls, pushes, 0} per round, globaltimer ns
+  unsigned long long* trace;
+  uint32_t trace_cap;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   int32_t r;
@@ -392,15 +402,29 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
       const unsigned long long p_now = __ldcg(&ctl->pushes);
       const uint32_t F = (uint32_t)(p_now - prev_p);
       if (F == 0) break;
+      const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0 && rounds < a.trace_cap;
+      if (tr) {
+        a.trace[rounds * 8 + 0] = gtimer();
+        a.trace[rounds * 8 + 3] = F;
+      }
       phase_a(a, fin, F, c_cur, s_cur, work, ix);
       grid.sync();
       const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
+      if (tr) {
+        a.trace[rounds * 8 + 1] = gtimer();
+        a.trace[rounds * 8 + 4] = c_end - c_cur;
+        a.trace[rounds * 8 + 5] = s_end - s_cur;
+      }
       phase_b(a, c_end - c_cur, s_end - s_cur, 0, 0, depart, p_now, fout, wbuf);
       expansions += (c_end - c_cur) + (s_end - s_cur);
       c_cur = c_end;
       s_cur = s_end;
       prev_p = p_now;
       grid.sync();
+      if (tr) {
+        a.trace[rounds * 8 + 2] = gtimer();
+        a.trace[rounds * 8 + 6] = __ldcg(&ctl->pushes) - p_now;
+      }
       ++rounds;
       uint32_t* t = fin;
       fin = fout;
