@@ -337,11 +337,10 @@ static int fastest_candidates(tgxd_graph* G, Prepared& P) {
 static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool fastest) {
   Workspace& w = G->ws;
   const uint64_t slots = (uint64_t)Q * G->n;
-  const uint64_t words = (slots + 31) / 32 + 1;
   // chunks per round <= frontier items + edges / kChunk (per query slot)
   const uint64_t max_chunks = slots + (uint64_t)Q * (G->m / kChunk + 1);
   bool ok = dalloc<int32_t>(w.X, slots) && dalloc<int32_t>(w.Ex, slots) &&
-            dalloc<uint32_t>(w.bitmap, words) && dalloc<uint32_t>(w.fa, slots) &&
+            dalloc<uint32_t>(w.fa, slots) &&
             dalloc<uint32_t>(w.fb, slots) && dalloc<uint2>(w.chunks, max_chunks) &&
             dalloc<uint2>(w.smalls, slots) && dalloc<Control>(w.ctl, 1) &&
             dalloc<QueryParam>(w.params, Q) && dalloc<Seed>(w.seeds, Q);
@@ -398,20 +397,17 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     TGXD_CUDA(cudaMemcpyAsync(w.cand_cnt.p, P.cand_cnt.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
     TGXD_CUDA(cudaMemcpyAsync(w.cand_key.p, P.cand_key.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
   }
-  const uint64_t words = (slots + 31) / 32 + 1;
   init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
-      w.X.as<int32_t>(), w.Ex.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr,
-      w.bitmap.as<uint32_t>(), slots, words);
+      w.X.as<int32_t>(), w.Ex.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr, slots);
   seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
-                                                 w.X.as<int32_t>(), w.bitmap.as<uint32_t>(),
-                                                 w.fa.as<uint32_t>(), w.ctl.as<Control>(), fast);
+                                                 w.X.as<int32_t>(), w.fa.as<uint32_t>(),
+                                                 w.ctl.as<Control>(), fast);
   TravArgs a;
   a.g = g;
   a.qp = w.params.as<QueryParam>();
   a.X = w.X.as<int32_t>();
   a.Ex = w.Ex.as<int32_t>();
   a.R = fast ? w.R.as<int32_t>() : nullptr;
-  a.bitmap = w.bitmap.as<uint32_t>();
   a.fa = w.fa.as<uint32_t>();
   a.fb = w.fb.as<uint32_t>();
   a.chunks = w.chunks.as<uint2>();
@@ -422,6 +418,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.strict = P.strict;
   a.cutoff = (uint32_t)std::min<uint64_t>(G->index_cutoff, 0xffffffffULL);
   a.mode = mode;
+  a.dense_f = std::max<uint64_t>(1024, slots / 64);
+  a.push_w = std::max<uint64_t>(4096, slots / 8);
   a.fastest = fast ? 1 : 0;
   a.n_cand = ncand;
   a.cand_lo = w.cand_lo.as<uint32_t>();
@@ -465,7 +463,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   st->rounds = c.rounds;
   st->candidates = c.candidates;
   st->expansions = c.expansions;
-  st->edges_relaxed = c.work_all;
+  st->edges_relaxed = c.edges;
   st->index_lookups = c.index_lookups;
   st->kernel_ms = kernel_ms;
   st->total_ms = total_ms;

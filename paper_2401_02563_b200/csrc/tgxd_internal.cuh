@@ -60,7 +60,7 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 // Traversal workspace, sized for q_cap concurrent queries.
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
-  DeviceBuffer X, Ex, R, bitmap, fa, fb, chunks, smalls, ctl, params, seeds;
+  DeviceBuffer X, Ex, R, fa, fb, chunks, smalls, ctl, params, seeds;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out, trace;
   uint32_t trace_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -76,13 +76,15 @@ struct Workspace {
 // difference between its start and end values.
 struct Control {
   unsigned long long pushes;        // frontier appends (queue position)
+  unsigned long long improved;      // label improvements in non-pushing rounds
   unsigned long long chunks;        // big-range chunks emitted
   unsigned long long smalls;        // small ranges emitted
-  unsigned long long work_all;      // edges handed to the relax step
+  unsigned long long edges;         // edges handed to the relax step
   unsigned long long expansions;    // non-empty ranges (chunks + small ranges)
   unsigned long long index_lookups; // expansions that used the fence index
   unsigned int rounds;
   unsigned int candidates;
+  unsigned long long state[8];      // CTA-local rounds hand their state over here
 };
 
 }  // namespace tgxd

@@ -4,17 +4,23 @@
 // engine.hpp:239-353).
 //
 // One persistent cooperative kernel runs the whole query. Each round is
-//   A  expand: every frontier item locates the not-yet-relaxed admissible key
-//      range of its segment (selective index: fence search for hubs, plain
-//      binary search otherwise) and emits it as work: ranges of >= 32 edges
-//      as fixed-size chunks, shorter ones into a small-range list
-//      (warp-aggregated atomic emission — no ordered scan needed);
-//   B  relax: warps stream chunks (coalesced, unrolled) and pack 32 small
-//      ranges per warp (lane ownership from a redux.or start mask), relax
-//      labels with atomicMin and append improved vertices to the next
-//      frontier through per-warp shared-memory push buffers;
-// separated by grid barriers. No host round trip per round. All counters
-// are monotone, so no round ever resets one (no extra barrier).
+//   A  expand: every frontier vertex locates the not-yet-relaxed admissible
+//      key range of its segment (selective index: fence search for hubs,
+//      plain binary search otherwise) and emits it as work — ranges of >= 32
+//      edges as fixed-size chunks, shorter ones into a small-range list
+//      (warp-aggregated atomic emission, no ordered scan). The frontier is
+//      either the sparse queue of vertices pushed last round or, when large,
+//      implicit (dense): every vertex whose label moved below the bound it
+//      was last expanded with (temporal_edge_map's sparse/dense switch,
+//      engine.hpp:280-295).
+//   B  relax: warps stream chunks (coalesced, unrolled, L2 evict-first) and
+//      pack 32 small ranges per warp (lane ownership from a redux.or start
+//      mask), relax labels with atomicMin and, when the next round is
+//      sparse, append each vertex's first improvement of the round to the
+//      next frontier through per-warp shared-memory push buffers.
+// Rounds are separated by grid barriers; no host round trip per round.
+// Rounds with a tiny frontier run on one CTA with CTA barriers only
+// ("local" rounds) and hand back to the whole grid when work grows.
 //
 // Work efficiency. Labels only decrease (key space) and the relaxed value of
 // an edge (its val) does not depend on the label that admitted it, so once an
@@ -24,6 +30,11 @@
 // once per query (once per sweep for fastest), whatever the schedule — the
 // labels are the unique least fixpoint the reference's round-synchronous
 // loop also reaches, so results are bit-identical.
+//
+// Frontier dedup without flags. After every expand phase each reached vertex
+// v satisfies Ex[v] == bound(X[v]). During relax, the atomicMin that returns
+// old with bound(old) == Ex[v] is therefore the first improvement of v in
+// this round: exactly one thread pushes v (claim_stamp, parallel.hpp:113-121).
 #include <cooperative_groups.h>
 
 #include "tgxd_internal.cuh"
@@ -39,6 +50,8 @@ constexpr uint32_t kChunk = 32u * kUnroll;       // edges per chunk of a big ran
 constexpr uint32_t kSmall = 32;                  // ranges below this go to the small list
 constexpr uint32_t kChunkLenBits = 9;            // kChunk <= 256
 constexpr uint32_t kSmallCntBits = 6;
+constexpr uint32_t kLocalMaxF = 1024;            // frontier that one CTA expands
+constexpr uint32_t kLocalMaxW = 4096;            // edge work that one CTA relaxes
 
 struct TravArgs {
   DevCsr g;
@@ -46,7 +59,6 @@ struct TravArgs {
   int32_t* X;          // labels, Q x n (key space)
   int32_t* Ex;         // bound each vertex was last expanded with
   int32_t* R;          // fastest durations (nullptr otherwise)
-  uint32_t* bitmap;    // queued flags, Q x n bits
   uint32_t* fa;        // frontier queues (items = q * n + v)
   uint32_t* fb;
   uint2* chunks;       // {lo, q << 9 | len}
@@ -57,14 +69,15 @@ struct TravArgs {
   int strict;
   uint32_t cutoff;
   int mode;            // tgxd_mode
+  unsigned long long dense_f;  // AUTO: frontier above this expands densely
+  unsigned long long push_w;   // AUTO: rounds relaxing more edges do not push
   // fastest sweep (Q == 1)
   int fastest;
   uint32_t n_cand;
   const uint32_t* cand_lo;
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
-  // optional per-round trace (block 0): {t_start, t_after_A, t_after_B, F,
-  // chunks, smalls, pushes, 0} per round, globaltimer ns
+  // optional per-round trace (block 0), 8 u64 per round
   unsigned long long* trace;
   uint32_t trace_cap;
 };
@@ -75,14 +88,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Streaming read of immutable edge data: no L1 allocation, L2 evict-first
+// so the edge stream does not push labels out of L2.
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
   int32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(r) : "l"(p), "l"(pol));
   return r;
 }
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
   uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+// Coherent (L2) read of mutable state, kept resident in L2.
+__device__ __forceinline__ int32_t ld_state(const int32_t* p, uint64_t pol) {
+  int32_t r;
+  asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
   return r;
 }
 
@@ -117,6 +151,12 @@ __device__ __forceinline__ uint32_t lower_key(const DevCsr& g, uint32_t s, uint3
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// The bound a label implies for its vertex's next expansion (min_start /
+// max_end hooks, path_algorithms.cpp:287-291, :337-342).
+__device__ __forceinline__ int32_t bound_of(int32_t x, int strict) {
+  return x == kInf ? kInf : x + strict;
+}
+
 // Per-warp push buffer: improved vertices are staged in shared memory and
 // appended to the next frontier 32 at a time (one global atomic per 32).
 struct PushBuf {
@@ -140,16 +180,6 @@ __device__ __forceinline__ void push_flush32(PushBuf& pb, Control* ctl,
   __syncwarp();
 }
 
-__device__ __forceinline__ void push(PushBuf& pb, bool p, uint32_t item, Control* ctl,
-                                     unsigned long long pstart, uint32_t* fout) {
-  const uint32_t bal = __ballot_sync(0xffffffffu, p);
-  if (bal == 0) return;
-  const uint32_t lane = lane_id();
-  if (p) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = item;
-  pb.n += __popc(bal);
-  if (pb.n >= 32) push_flush32(pb, ctl, pstart, fout);
-}
-
 __device__ __forceinline__ void push_drain(PushBuf& pb, Control* ctl, unsigned long long pstart,
                                            uint32_t* fout) {
   if (pb.n == 0) return;
@@ -163,127 +193,176 @@ __device__ __forceinline__ void push_drain(PushBuf& pb, Control* ctl, unsigned l
   __syncwarp();
 }
 
+struct RelaxCtx {
+  int32_t vhi0;
+  int32_t depart;
+  bool push;                 // append first improvements to the next frontier
+  unsigned long long pstart; // queue position of the next frontier's start
+  uint32_t* fout;
+  uint64_t pol_stream, pol_keep;
+  uint32_t improved;         // per-lane improvement count (no-push rounds)
+};
+
 // Relax kUnroll 32-edge steps: e[u] edge ids, q[u] query slots, act[u] lane
-// validity. write_min (parallel.hpp:91-99) + claim_stamp (:113-121) become a
-// plain label probe, atomicMin, and an atomicOr on the queued bitmap.
+// validity. write_min (parallel.hpp:91-99) is a plain label probe followed by
+// atomicMin when the probe says the edge can improve.
 __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&e)[kUnroll],
                                             const uint32_t (&q)[kUnroll],
-                                            const bool (&act)[kUnroll], int32_t vhi0,
-                                            int32_t depart, PushBuf& pb,
-                                            unsigned long long pstart, uint32_t* fout) {
+                                            const bool (&act)[kUnroll], RelaxCtx& rx,
+                                            PushBuf& pb) {
   int32_t v[kUnroll];
   uint32_t d[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    v[u] = act[u] ? ld_stream(a.g.val + e[u]) : kInf;
-    d[u] = act[u] ? ld_stream(a.g.nbr + e[u]) : 0u;
+    v[u] = act[u] ? ld_stream(a.g.val + e[u], rx.pol_stream) : kInf;
+    d[u] = act[u] ? ld_stream(a.g.nbr + e[u], rx.pol_stream) : 0u;
   }
   uint32_t idx[kUnroll];
   int32_t cur[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    const int32_t vhi = a.Q == 1 ? vhi0 : __ldg(&a.qp[q[u]].vhi);
+    const int32_t vhi = a.Q == 1 ? rx.vhi0 : __ldg(&a.qp[q[u]].vhi);
     // window containment: end <= t_b (types.hpp:55-57)
     const bool ok = act[u] && v[u] <= vhi;
     idx[u] = q[u] * a.n + d[u];
-    cur[u] = ok ? __ldcg(a.X + idx[u]) : kInf;
+    cur[u] = ok ? ld_state(a.X + idx[u], rx.pol_keep) : kInf;
     if (!ok) v[u] = kInf;
   }
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     bool p = false;
     if (v[u] < cur[u]) {
+      int32_t ex = 0;
+      if (rx.push) ex = ld_state(a.Ex + idx[u], rx.pol_keep);
       const int32_t old = atomicMin(a.X + idx[u], v[u]);
       if (v[u] < old) {
-        if (a.R) atomicMin(a.R + idx[u], v[u] - depart);
-        const uint32_t m = 1u << (idx[u] & 31);
-        p = (atomicOr(a.bitmap + (idx[u] >> 5), m) & m) == 0;
+        if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
+        if (rx.push) p = bound_of(old, a.strict) == ex;
+        else ++rx.improved;
       }
     }
-    push(pb, p, idx[u], a.ctl, pstart, fout);
+    if (rx.push) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, p);
+      if (bal) {
+        const uint32_t lane = lane_id();
+        if (p) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = idx[u];
+        pb.n += __popc(bal);
+        if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
+      }
+    }
   }
 }
 
-// Phase A: expand the frontier and emit work.
-__device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
-                        unsigned long long cstart, unsigned long long sstart,
-                        unsigned long long& work, unsigned long long& ix) {
+// Expansion of one slot (q * n + v) with label x: returns the range of keys
+// still to relax, [lo, lo + cnt), and records the new bound.
+__device__ __forceinline__ uint32_t expand_slot(const TravArgs& a, uint32_t item, int32_t x,
+                                                int32_t old, uint32_t& lo, uint32_t& q,
+                                                unsigned long long& ix) {
+  q = a.Q == 1 ? 0u : item / a.n;
+  const uint32_t v = item - q * a.n;
+  const QueryParam& qp = a.qp[q];
+  int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
+  if (lb < qp.klo) lb = qp.klo;
+  lo = 0;
+  if (lb >= old) return 0;
+  a.Ex[item] = lb;
+  const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
+  if (lb >= hik) return 0;
+  const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
+  const bool use_idx = a.cutoff != 0 && t - s >= a.cutoff;
+  ix += use_idx;
+  const uint32_t p0 = lower_key(a.g, s, t, lb, use_idx);
+  const uint32_t p1 = lower_key(a.g, p0, t, hik, use_idx);
+  lo = p0;
+  return p1 - p0;
+}
+
+// Warp-aggregated emission of one range per lane (cnt == 0: nothing).
+__device__ __forceinline__ void emit(const TravArgs& a, uint32_t lo, uint32_t cnt, uint32_t q,
+                                     unsigned long long cstart, unsigned long long sstart) {
   const uint32_t lane = lane_id();
-  const uint32_t nthreads = gridDim.x * blockDim.x;
-  const uint32_t tbase = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-  for (uint32_t base = tbase; base < F; base += nthreads) {
+  const bool small = cnt != 0 && cnt < kSmall;
+  const uint32_t nch = cnt >= kSmall ? (cnt + kChunk - 1) / kChunk : 0u;
+  const uint32_t sbal = __ballot_sync(0xffffffffu, small);
+  uint32_t incl = nch;
+  unsigned long long w = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+    w += __shfl_xor_sync(0xffffffffu, w, o);
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long cb = 0, sb = 0;
+  if (lane == 0) {
+    if (tot) cb = atomicAdd(&a.ctl->chunks, (unsigned long long)tot);
+    if (sbal) sb = atomicAdd(&a.ctl->smalls, (unsigned long long)__popc(sbal));
+    if (w) atomicAdd(&a.ctl->edges, w);
+  }
+  cb = __shfl_sync(0xffffffffu, cb, 0);
+  sb = __shfl_sync(0xffffffffu, sb, 0);
+  if (small) {
+    const uint64_t pos = sb - sstart + __popc(sbal & ((1u << lane) - 1));
+    a.smalls[pos] = make_uint2(lo, (q << kSmallCntBits) | cnt);
+  }
+  if (nch) {
+    uint64_t pos = cb - cstart + incl - nch;
+    for (uint32_t c = 0; c < nch; ++c, ++pos) {
+      const uint32_t off = c * kChunk;
+      a.chunks[pos] = make_uint2(lo + off, (q << kChunkLenBits) | min(kChunk, cnt - off));
+    }
+  }
+}
+
+// Phase A over a sparse frontier queue (items [0, F) of fin).
+__device__ void phase_a_sparse(const TravArgs& a, const uint32_t* fin, uint32_t F,
+                               unsigned long long cstart, unsigned long long sstart,
+                               uint32_t bid, uint32_t nblk, uint64_t pol_keep,
+                               unsigned long long& ix) {
+  const uint32_t lane = lane_id();
+  const uint32_t nthreads = nblk * blockDim.x;
+  for (uint32_t base = bid * blockDim.x + (threadIdx.x & ~31u); base < F; base += nthreads) {
     const uint32_t i = base + lane;
     uint32_t cnt = 0, lo = 0, q = 0;
     if (i < F) {
       const uint32_t item = __ldcg(fin + i);
-      a.bitmap[item >> 5] = 0u;  // every set bit belongs to a frontier item
-      q = a.Q == 1 ? 0u : item / a.n;
-      const uint32_t v = item - q * a.n;
-      const QueryParam qp = a.qp[q];
-      const int32_t x = __ldcg(a.X + item);
-      // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342):
-      // the root leaves at any time inside the window; everyone else
-      // strictly (or weakly) after its own label.
-      int32_t lb = (v == qp.root) ? qp.klo : (x == kInf ? kInf : x + a.strict);
-      if (lb < qp.klo) lb = qp.klo;
-      const int32_t old = __ldcg(a.Ex + item);
-      if (lb < old) {
-        a.Ex[item] = lb;
-        const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
-        if (lb < hik) {
-          const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-          const bool use_idx = a.cutoff != 0 && t - s >= a.cutoff;
-          ix += use_idx;
-          const uint32_t p0 = lower_key(a.g, s, t, lb, use_idx);
-          const uint32_t p1 = lower_key(a.g, p0, t, hik, use_idx);
-          lo = p0;
-          cnt = p1 - p0;
-          work += cnt;
-        }
-      }
+      cnt = expand_slot(a, item, ld_state(a.X + item, pol_keep), ld_state(a.Ex + item, pol_keep),
+                        lo, q, ix);
     }
-    // warp-aggregated emission
-    const bool small = cnt != 0 && cnt < kSmall;
-    const uint32_t nch = cnt >= kSmall ? (cnt + kChunk - 1) / kChunk : 0u;
-    const uint32_t sbal = __ballot_sync(0xffffffffu, small);
-    uint32_t incl = nch;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+    emit(a, lo, cnt, q, cstart, sstart);
+  }
+}
+
+// Phase A over the implicit dense frontier: every slot whose label bound is
+// below its expansion bound.
+__device__ void phase_a_dense(const TravArgs& a, unsigned long long cstart,
+                              unsigned long long sstart, uint64_t pol_keep,
+                              unsigned long long& ix) {
+  const uint32_t lane = lane_id();
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  const uint32_t slots = a.Q * a.n;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < slots;
+       base += nthreads) {
+    const uint32_t i = base + lane;
+    uint32_t cnt = 0, lo = 0, q = 0;
+    if (i < slots) {
+      const int32_t x = ld_state(a.X + i, pol_keep);
+      const int32_t old = ld_state(a.Ex + i, pol_keep);
+      if (x != kInf) cnt = expand_slot(a, i, x, old, lo, q, ix);
     }
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned long long cb = 0, sb = 0;
-    if (lane == 0) {
-      if (tot) cb = atomicAdd(&a.ctl->chunks, (unsigned long long)tot);
-      if (sbal) sb = atomicAdd(&a.ctl->smalls, (unsigned long long)__popc(sbal));
-    }
-    cb = __shfl_sync(0xffffffffu, cb, 0);
-    sb = __shfl_sync(0xffffffffu, sb, 0);
-    if (small) {
-      const uint64_t pos = sb - sstart + __popc(sbal & ((1u << lane) - 1));
-      a.smalls[pos] = make_uint2(lo, (q << kSmallCntBits) | cnt);
-    }
-    if (nch) {
-      uint64_t pos = cb - cstart + incl - nch;
-      for (uint32_t c = 0; c < nch; ++c, ++pos) {
-        const uint32_t off = c * kChunk;
-        const uint32_t len = min(kChunk, cnt - off);
-        a.chunks[pos] = make_uint2(lo + off, (q << kChunkLenBits) | len);
-      }
-    }
+    emit(a, lo, cnt, q, cstart, sstart);
   }
 }
 
 // Phase B: relax the round's chunks and small ranges (plus, for a fastest
 // seed round, the virtual chunks of one explicit range).
-__device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned long long nsmall,
-                        uint32_t xlo, uint32_t xcnt, int32_t depart, unsigned long long pstart,
-                        uint32_t* fout, uint32_t* wbuf) {
+__device__ void phase_b(const TravArgs& a, unsigned long long chunk0, unsigned long long nchunks,
+                        unsigned long long small0, unsigned long long nsmall, uint32_t xlo,
+                        uint32_t xcnt, RelaxCtx& rx, uint32_t bid, uint32_t nblk,
+                        uint32_t* wbuf) {
   const uint32_t lane = lane_id();
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t nw = gridDim.x * kWarps;
-  const int32_t vhi0 = a.qp[0].vhi;
+  const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
+  const uint32_t nw = nblk * kWarps;
   PushBuf pb{wbuf, 0};
 
   // explicit range (fastest seeds), split into virtual chunks
@@ -298,12 +377,12 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
       e[u] = xlo + off;
       q[u] = 0;
     }
-    relax_steps(a, e, q, act, vhi0, depart, pb, pstart, fout);
+    relax_steps(a, e, q, act, rx, pb);
   }
 
   // chunks of big ranges: coalesced kChunk-edge bursts
   for (unsigned long long c = gw; c < nchunks; c += nw) {
-    const uint2 ch = a.chunks[c];
+    const uint2 ch = a.chunks[chunk0 + c];
     const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
     const uint32_t cq = ch.y >> kChunkLenBits;
     uint32_t e[kUnroll], q[kUnroll];
@@ -315,7 +394,7 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
       e[u] = ch.x + off;
       q[u] = cq;
     }
-    relax_steps(a, e, q, act, vhi0, depart, pb, pstart, fout);
+    relax_steps(a, e, q, act, rx, pb);
   }
 
   // small ranges: 32 per warp window; lane l owns range l, items are packed
@@ -325,7 +404,7 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
     const unsigned long long r = w * 32 + lane;
     uint32_t lo = 0, cnt = 0, rq = 0;
     if (r < nsmall) {
-      const uint2 s = a.smalls[r];
+      const uint2 s = a.smalls[small0 + r];
       lo = s.x;
       cnt = s.y & ((1u << kSmallCntBits) - 1);
       rq = s.y >> kSmallCntBits;
@@ -351,106 +430,261 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
         const uint32_t rel = start - sb;
         const uint32_t bit = (cnt != 0 && start > sb && rel < 32) ? (1u << rel) : 0u;
         const uint32_t mask = __reduce_or_sync(0xffffffffu, bit);
-        const uint32_t own = i0 + __popc(mask & ((2u << lane) - 1));
-        const uint32_t olo = __shfl_sync(0xffffffffu, lo, own & 31);
-        const uint32_t ost = __shfl_sync(0xffffffffu, start, own & 31);
-        const uint32_t oq = __shfl_sync(0xffffffffu, rq, own & 31);
+        const uint32_t own = (i0 + __popc(mask & ((2u << lane) - 1))) & 31;
+        const uint32_t olo = __shfl_sync(0xffffffffu, lo, own);
+        const uint32_t ost = __shfl_sync(0xffffffffu, start, own);
+        const uint32_t oq = __shfl_sync(0xffffffffu, rq, own);
         const uint32_t t = sb + lane;
         act[u] = t < total;
         e[u] = olo + (t - ost);
         q[u] = oq;
       }
-      relax_steps(a, e, q, act, vhi0, depart, pb, pstart, fout);
+      relax_steps(a, e, q, act, rx, pb);
     }
   }
-  push_drain(pb, a.ctl, pstart, fout);
+  if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
+}
+
+// Traversal state; identical in every block at every grid barrier.
+struct TState {
+  unsigned long long prev_p;   // queue position where fin's items start
+  unsigned long long prev_i;   // improvement counter at the start of the last relax
+  unsigned long long c_cur, s_cur, e_cur;
+  unsigned long long p_now;    // (pending) queue position for its pushes
+  uint32_t rounds;
+  uint32_t flip;               // fin/fout parity
+  int dense;                   // the next expand scans densely
+  int pending;                 // expand done, relax of [c_cur..c_end) pending
+};
+
+__device__ __forceinline__ void save_state(Control* ctl, const TState& s) {
+  static_assert(sizeof(TState) <= sizeof(ctl->state), "state slot too small");
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s);
+  unsigned long long* dst = ctl->state;
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(TState) / 8); ++i) dst[i] = src[i];
+}
+__device__ __forceinline__ void load_state(const Control* ctl, TState& s) {
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(TState) / 8); ++i) dst[i] = __ldcg(ctl->state + i);
+}
+
+__device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int slot,
+                                            unsigned long long v) {
+  if (a.trace && r < a.trace_cap) a.trace[r * 8 + slot] = v;
+}
+
+// Rounds with a tiny frontier on one CTA (block 0). Returns with st updated
+// and, if the expand produced more edge work than one CTA should relax,
+// st.pending set with the relax left to the grid.
+__device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32_t xcnt,
+                             int32_t depart, int32_t vhi0, uint64_t pol_stream,
+                             uint64_t pol_keep, uint32_t* wbuf, unsigned long long& ix) {
+  __shared__ unsigned long long s_val[4];
+  Control* ctl = a.ctl;
+  bool seed = xcnt != 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_val[0] = __ldcg(&ctl->pushes);
+    __syncthreads();
+    const unsigned long long p_now = s_val[0];
+    uint32_t* fin = st.flip ? a.fb : a.fa;
+    uint32_t* fout = st.flip ? a.fa : a.fb;
+    RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
+    const bool tr = threadIdx.x == 0;
+    if (seed) {
+      if (tr) {
+        trace_round(a, st.rounds, 0, gtimer());
+        trace_round(a, st.rounds, 1, gtimer());
+        trace_round(a, st.rounds, 7, 1);
+      }
+      phase_b(a, 0, 0, 0, 0, xlo, xcnt, rx, 0, 1, wbuf);
+      if (tr) trace_round(a, st.rounds, 2, gtimer());
+      seed = false;
+    } else {
+      const uint32_t F = (uint32_t)(p_now - st.prev_p);
+      if (F == 0 || F > kLocalMaxF) return;
+      if (tr) {
+        trace_round(a, st.rounds, 0, gtimer());
+        trace_round(a, st.rounds, 3, F);
+        trace_round(a, st.rounds, 7, 1);
+      }
+      phase_a_sparse(a, fin, F, st.c_cur, st.s_cur, 0, 1, pol_keep, ix);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_val[1] = __ldcg(&ctl->chunks);
+        s_val[2] = __ldcg(&ctl->smalls);
+        s_val[3] = __ldcg(&ctl->edges);
+      }
+      __syncthreads();
+      const unsigned long long c_end = s_val[1], s_end = s_val[2], e_end = s_val[3];
+      if (tr) {
+        trace_round(a, st.rounds, 1, gtimer());
+        trace_round(a, st.rounds, 4, c_end - st.c_cur);
+        trace_round(a, st.rounds, 5, s_end - st.s_cur);
+      }
+      if (e_end - st.e_cur > kLocalMaxW) {  // hand the relax to the grid
+        st.pending = 1;
+        st.p_now = p_now;
+        return;
+      }
+      phase_b(a, st.c_cur, c_end - st.c_cur, st.s_cur, s_end - st.s_cur, 0, 0, rx, 0, 1, wbuf);
+      st.c_cur = c_end;
+      st.s_cur = s_end;
+      st.e_cur = e_end;
+      if (tr) trace_round(a, st.rounds, 2, gtimer());
+    }
+    __syncthreads();
+    if (tr) trace_round(a, st.rounds, 6, __ldcg(&ctl->pushes) - p_now);
+    st.prev_p = p_now;
+    st.flip ^= 1u;
+    st.dense = 0;
+    ++st.rounds;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
   cg::grid_group grid = cg::this_grid();
   uint32_t* wbuf = s_buf[threadIdx.x >> 5];
-  uint32_t* fin = a.fa;
-  uint32_t* fout = a.fb;
   Control* ctl = a.ctl;
-  uint32_t rounds = 0;
-  unsigned long long work = 0, ix = 0, expansions = 0;
-  // Counter discipline: `pushes` only grows in phase B and is read at round
-  // start (phase A); `chunks` / `smalls` only grow in phase A and are read
-  // in phase B. A counter is never read while another block may be moving
-  // it, so every block sees the same round boundaries.
-  unsigned long long prev_p = 0;         // queue position where fin's items start
-  unsigned long long c_cur = 0, s_cur = 0;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  const int32_t vhi0 = a.qp[0].vhi;
+  unsigned long long ix = 0;
+  // Counter discipline: `pushes` / `improved` only grow in relax and are read
+  // in expand; `chunks` / `smalls` / `edges` only grow in expand and are read
+  // in relax. A counter is never read while another block may move it, so
+  // every block derives the same round boundaries.
+  TState st;
+  st.prev_p = 0;
+  st.prev_i = 0;
+  st.c_cur = st.s_cur = st.e_cur = 0;
+  st.p_now = 0;
+  st.rounds = 0;
+  st.flip = 0;
+  st.dense = a.mode == TGXD_MODE_DENSE;
+  st.pending = 0;
   for (uint32_t cand = 0;; ++cand) {
     int32_t depart = 0;
+    uint32_t xlo = 0, xcnt = 0;
     if (a.fastest) {
       if (cand >= a.n_cand) break;
       // Seed round (path_algorithms.cpp:476-486): the candidate's first
-      // edges, relaxed without an admissibility check. The queue is empty
-      // here, so pushes == prev_p for every block.
+      // edges, relaxed without an admissibility check.
       depart = a.cand_key[cand];
-      const uint32_t c0 = a.cand_cnt[cand];
-      phase_b(a, 0, 0, a.cand_lo[cand], c0, depart, prev_p, fout, wbuf);
-      if (blockIdx.x == 0 && threadIdx.x == 0) work += c0;
-      grid.sync();
-      ++rounds;
-      uint32_t* t = fin;
-      fin = fout;
-      fout = t;
+      xlo = a.cand_lo[cand];
+      xcnt = a.cand_cnt[cand];
     }
     for (;;) {
       const unsigned long long p_now = __ldcg(&ctl->pushes);
-      const uint32_t F = (uint32_t)(p_now - prev_p);
-      if (F == 0) break;
-      const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0 && rounds < a.trace_cap;
-      if (tr) {
-        a.trace[rounds * 8 + 0] = gtimer();
-        a.trace[rounds * 8 + 3] = F;
+      const unsigned long long i_now = __ldcg(&ctl->improved);
+      const unsigned long long F = xcnt ? 0 : (st.dense ? i_now - st.prev_i : p_now - st.prev_p);
+      if (!xcnt && F == 0) break;
+      const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
+                            (xcnt ? xcnt <= kLocalMaxW : F <= kLocalMaxF);
+      if (go_local) {
+        if (blockIdx.x == 0) {
+          local_rounds(a, st, xlo, xcnt, depart, vhi0, pol_stream, pol_keep, wbuf, ix);
+          if (threadIdx.x == 0) save_state(ctl, st);
+        }
+        xcnt = 0;
+        grid.sync();
+        load_state(ctl, st);
+        if (!st.pending) continue;
+        // the grid relaxes what the CTA expanded
+        const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
+        uint32_t* fout = st.flip ? a.fa : a.fb;
+        RelaxCtx rx{vhi0, depart, true, st.p_now, fout, pol_stream, pol_keep, 0};
+        phase_b(a, st.c_cur, c_end - st.c_cur, st.s_cur, s_end - st.s_cur, 0, 0, rx,
+                blockIdx.x, gridDim.x, wbuf);
+        st.c_cur = c_end;
+        st.s_cur = s_end;
+        st.e_cur = __ldcg(&ctl->edges);
+        st.prev_p = st.p_now;
+        st.pending = 0;
+        st.flip ^= 1u;
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          trace_round(a, st.rounds, 2, gtimer());
+          trace_round(a, st.rounds, 6, __ldcg(&ctl->pushes) - st.prev_p);
+        }
+        ++st.rounds;
+        continue;
       }
-      phase_a(a, fin, F, c_cur, s_cur, work, ix);
+      const bool tr = blockIdx.x == 0 && threadIdx.x == 0;
+      uint32_t* fin = st.flip ? a.fb : a.fa;
+      uint32_t* fout = st.flip ? a.fa : a.fb;
+      if (tr) {
+        trace_round(a, st.rounds, 0, gtimer());
+        trace_round(a, st.rounds, 3, F);
+        trace_round(a, st.rounds, 7, st.dense ? 2 : 0);
+      }
+      unsigned long long c_end = st.c_cur, s_end = st.s_cur, e_end = st.e_cur;
+      if (!xcnt) {
+        if (st.dense) phase_a_dense(a, st.c_cur, st.s_cur, pol_keep, ix);
+        else phase_a_sparse(a, fin, (uint32_t)F, st.c_cur, st.s_cur, blockIdx.x, gridDim.x,
+                            pol_keep, ix);
+        grid.sync();
+        c_end = __ldcg(&ctl->chunks);
+        s_end = __ldcg(&ctl->smalls);
+        e_end = __ldcg(&ctl->edges);
+      }
+      if (tr) {
+        trace_round(a, st.rounds, 1, gtimer());
+        trace_round(a, st.rounds, 4, c_end - st.c_cur);
+        trace_round(a, st.rounds, 5, s_end - st.s_cur);
+      }
+      const unsigned long long w = (e_end - st.e_cur) + xcnt;
+      const bool push = a.mode == TGXD_MODE_SPARSE ||
+                        (a.mode == TGXD_MODE_AUTO && w <= a.push_w);
+      RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0};
+      phase_b(a, st.c_cur, c_end - st.c_cur, st.s_cur, s_end - st.s_cur, xlo, xcnt, rx,
+              blockIdx.x, gridDim.x, wbuf);
+      if (!push) {  // improvements only feed the dense frontier's size
+        uint32_t imp = rx.improved;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) imp += __shfl_xor_sync(0xffffffffu, imp, o);
+        if (lane_id() == 0 && imp) atomicAdd(&ctl->improved, (unsigned long long)imp);
+      }
+      st.c_cur = c_end;
+      st.s_cur = s_end;
+      st.e_cur = e_end;
+      st.prev_p = p_now;
+      st.prev_i = i_now;
+      xcnt = 0;
       grid.sync();
-      const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
+      const unsigned long long pushed = __ldcg(&ctl->pushes) - p_now;
       if (tr) {
-        a.trace[rounds * 8 + 1] = gtimer();
-        a.trace[rounds * 8 + 4] = c_end - c_cur;
-        a.trace[rounds * 8 + 5] = s_end - s_cur;
+        trace_round(a, st.rounds, 2, gtimer());
+        trace_round(a, st.rounds, 6, push ? pushed : __ldcg(&ctl->improved) - i_now);
       }
-      phase_b(a, c_end - c_cur, s_end - s_cur, 0, 0, depart, p_now, fout, wbuf);
-      expansions += (c_end - c_cur) + (s_end - s_cur);
-      c_cur = c_end;
-      s_cur = s_end;
-      prev_p = p_now;
-      grid.sync();
-      if (tr) {
-        a.trace[rounds * 8 + 2] = gtimer();
-        a.trace[rounds * 8 + 6] = __ldcg(&ctl->pushes) - p_now;
+      ++st.rounds;
+      if (push) st.flip ^= 1u;
+      // the next expand is dense when nothing was queued or the queue is big;
+      // a dense expand sizes its frontier by improvements since this relax
+      if (a.mode == TGXD_MODE_DENSE || !push) {
+        st.dense = 1;
+      } else {
+        st.dense = a.mode == TGXD_MODE_AUTO && pushed > a.dense_f;
+        if (st.dense) st.prev_i = __ldcg(&ctl->improved) - pushed;
       }
-      ++rounds;
-      uint32_t* t = fin;
-      fin = fout;
-      fout = t;
     }
     if (!a.fastest) break;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    work += __shfl_xor_sync(0xffffffffu, work, o);
-    ix += __shfl_xor_sync(0xffffffffu, ix, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (work) atomicAdd(&ctl->work_all, work);
-    if (ix) atomicAdd(&ctl->index_lookups, ix);
-  }
+  for (int o = 16; o > 0; o >>= 1) ix += __shfl_xor_sync(0xffffffffu, ix, o);
+  if (lane_id() == 0 && ix) atomicAdd(&ctl->index_lookups, ix);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->rounds = rounds;
-    ctl->expansions = expansions;
+    ctl->rounds = st.rounds;
+    ctl->expansions = __ldcg(&ctl->chunks) + __ldcg(&ctl->smalls);
     ctl->candidates = a.fastest ? a.n_cand : 0;
   }
 }
 
-// Labels to INF, expansion bounds to INF, durations to INF, flags cleared.
-__global__ void init_kernel(int32_t* X, int32_t* Ex, int32_t* R, uint32_t* bitmap, size_t nl,
-                            size_t nwords) {
+// Labels, expansion bounds and durations to INF.
+__global__ void init_kernel(int32_t* X, int32_t* Ex, int32_t* R, size_t nl) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t n4 = nl / 4;
   const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
@@ -464,26 +698,24 @@ __global__ void init_kernel(int32_t* X, int32_t* Ex, int32_t* R, uint32_t* bitma
     Ex[i] = kInf;
     if (R) R[i] = kInf;
   }
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride)
-    bitmap[i] = 0u;
 }
 
 // Seeds: X[root] = klo (EA: t_a, LD: -t_b), root queued as round-0 frontier.
 __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_t* X,
-                            uint32_t* bitmap, uint32_t* fa, Control* ctl, int fastest) {
+                            uint32_t* fa, Control* ctl, int fastest) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q == 0) {
     ctl->pushes = fastest ? 0ull : Q;
+    ctl->improved = fastest ? 0ull : Q;
     ctl->chunks = 0;
     ctl->smalls = 0;
-    ctl->work_all = 0;
+    ctl->edges = 0;
     ctl->expansions = 0;
     ctl->index_lookups = 0;
   }
   if (q >= Q || fastest) return;
   const uint32_t item = q * n + qp[q].root;
   X[item] = qp[q].klo;
-  atomicOr(bitmap + (item >> 5), 1u << (item & 31));
   fa[q] = item;
 }
 
