@@ -277,36 +277,52 @@ __device__ __forceinline__ uint32_t expand_slot(const TravArgs& a, uint32_t item
   return p1 - p0;
 }
 
-// Warp-aggregated emission of one range per lane (cnt == 0: nothing).
+// Block-aggregated emission of one range per thread (cnt == 0: nothing):
+// one block-wide scan and two global atomics per 256 expanded slots. Every
+// thread of the block must call it (it synchronizes the block).
 __device__ __forceinline__ void emit(const TravArgs& a, uint32_t lo, uint32_t cnt, uint32_t q,
-                                     unsigned long long cstart, unsigned long long sstart) {
-  const uint32_t lane = lane_id();
+                                     unsigned long long cstart, unsigned long long sstart,
+                                     unsigned long long& work) {
+  __shared__ uint32_t s_ch[kWarps], s_sm[kWarps];
+  __shared__ unsigned long long s_base[2];
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
   const bool small = cnt != 0 && cnt < kSmall;
   const uint32_t nch = cnt >= kSmall ? (cnt + kChunk - 1) / kChunk : 0u;
+  work += cnt;
   const uint32_t sbal = __ballot_sync(0xffffffffu, small);
   uint32_t incl = nch;
-  unsigned long long w = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
-    w += __shfl_xor_sync(0xffffffffu, w, o);
   }
-  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-  unsigned long long cb = 0, sb = 0;
-  if (lane == 0) {
-    if (tot) cb = atomicAdd(&a.ctl->chunks, (unsigned long long)tot);
-    if (sbal) sb = atomicAdd(&a.ctl->smalls, (unsigned long long)__popc(sbal));
-    if (w) atomicAdd(&a.ctl->edges, w);
+  if (lane == 31) {
+    s_ch[wid] = incl;
+    s_sm[wid] = __popc(sbal);
   }
-  cb = __shfl_sync(0xffffffffu, cb, 0);
-  sb = __shfl_sync(0xffffffffu, sb, 0);
+  __syncthreads();
+  uint32_t ch_before = 0, sm_before = 0, ch_tot = 0, sm_tot = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) {
+    const uint32_t c = s_ch[k], m = s_sm[k];
+    if (k < (int)wid) {
+      ch_before += c;
+      sm_before += m;
+    }
+    ch_tot += c;
+    sm_tot += m;
+  }
+  if (threadIdx.x == 0) {
+    s_base[0] = ch_tot ? atomicAdd(&a.ctl->chunks, (unsigned long long)ch_tot) : 0ull;
+    s_base[1] = sm_tot ? atomicAdd(&a.ctl->smalls, (unsigned long long)sm_tot) : 0ull;
+  }
+  __syncthreads();
   if (small) {
-    const uint64_t pos = sb - sstart + __popc(sbal & ((1u << lane) - 1));
+    const uint64_t pos = s_base[1] - sstart + sm_before + __popc(sbal & ((1u << lane) - 1));
     a.smalls[pos] = make_uint2(lo, (q << kSmallCntBits) | cnt);
   }
   if (nch) {
-    uint64_t pos = cb - cstart + incl - nch;
+    uint64_t pos = s_base[0] - cstart + ch_before + incl - nch;
     for (uint32_t c = 0; c < nch; ++c, ++pos) {
       const uint32_t off = c * kChunk;
       a.chunks[pos] = make_uint2(lo + off, (q << kChunkLenBits) | min(kChunk, cnt - off));
@@ -314,23 +330,40 @@ __device__ __forceinline__ void emit(const TravArgs& a, uint32_t lo, uint32_t cn
   }
 }
 
+// Adds a block's relax-work count to the edges counter (one atomic per block).
+__device__ __forceinline__ void flush_work(Control* ctl, unsigned long long work) {
+  __shared__ unsigned long long s_w[kWarps];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
+  if (lane_id() == 0) s_w[threadIdx.x >> 5] = work;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+#pragma unroll
+    for (int k = 0; k < kWarps; ++k) t += s_w[k];
+    if (t) atomicAdd(&ctl->edges, t);
+  }
+  __syncthreads();
+}
+
 // Phase A over a sparse frontier queue (items [0, F) of fin).
 __device__ void phase_a_sparse(const TravArgs& a, const uint32_t* fin, uint32_t F,
                                unsigned long long cstart, unsigned long long sstart,
                                uint32_t bid, uint32_t nblk, uint64_t pol_keep,
                                unsigned long long& ix) {
-  const uint32_t lane = lane_id();
   const uint32_t nthreads = nblk * blockDim.x;
-  for (uint32_t base = bid * blockDim.x + (threadIdx.x & ~31u); base < F; base += nthreads) {
-    const uint32_t i = base + lane;
+  unsigned long long work = 0;
+  for (uint32_t base = bid * blockDim.x; base < F; base += nthreads) {
+    const uint32_t i = base + threadIdx.x;
     uint32_t cnt = 0, lo = 0, q = 0;
     if (i < F) {
       const uint32_t item = __ldcg(fin + i);
       cnt = expand_slot(a, item, ld_state(a.X + item, pol_keep), ld_state(a.Ex + item, pol_keep),
                         lo, q, ix);
     }
-    emit(a, lo, cnt, q, cstart, sstart);
+    emit(a, lo, cnt, q, cstart, sstart, work);
   }
+  flush_work(a.ctl, work);
 }
 
 // Phase A over the implicit dense frontier: every slot whose label bound is
@@ -338,26 +371,26 @@ __device__ void phase_a_sparse(const TravArgs& a, const uint32_t* fin, uint32_t 
 __device__ void phase_a_dense(const TravArgs& a, unsigned long long cstart,
                               unsigned long long sstart, uint64_t pol_keep,
                               unsigned long long& ix) {
-  const uint32_t lane = lane_id();
   const uint32_t nthreads = gridDim.x * blockDim.x;
   const uint32_t slots = a.Q * a.n;
-  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < slots;
-       base += nthreads) {
-    const uint32_t i = base + lane;
+  unsigned long long work = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < slots; base += nthreads) {
+    const uint32_t i = base + threadIdx.x;
     uint32_t cnt = 0, lo = 0, q = 0;
     if (i < slots) {
       const int32_t x = ld_state(a.X + i, pol_keep);
       const int32_t old = ld_state(a.Ex + i, pol_keep);
       if (x != kInf) cnt = expand_slot(a, i, x, old, lo, q, ix);
     }
-    emit(a, lo, cnt, q, cstart, sstart);
+    emit(a, lo, cnt, q, cstart, sstart, work);
   }
+  flush_work(a.ctl, work);
 }
 
 // Phase B: relax the round's chunks and small ranges (plus, for a fastest
 // seed round, the virtual chunks of one explicit range).
-__device__ void phase_b(const TravArgs& a, unsigned long long chunk0, unsigned long long nchunks,
-                        unsigned long long small0, unsigned long long nsmall, uint32_t xlo,
+__device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned long long nsmall,
+                        uint32_t xlo,
                         uint32_t xcnt, RelaxCtx& rx, uint32_t bid, uint32_t nblk,
                         uint32_t* wbuf) {
   const uint32_t lane = lane_id();
@@ -382,7 +415,7 @@ __device__ void phase_b(const TravArgs& a, unsigned long long chunk0, unsigned l
 
   // chunks of big ranges: coalesced kChunk-edge bursts
   for (unsigned long long c = gw; c < nchunks; c += nw) {
-    const uint2 ch = a.chunks[chunk0 + c];
+    const uint2 ch = a.chunks[c];
     const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
     const uint32_t cq = ch.y >> kChunkLenBits;
     uint32_t e[kUnroll], q[kUnroll];
@@ -404,7 +437,7 @@ __device__ void phase_b(const TravArgs& a, unsigned long long chunk0, unsigned l
     const unsigned long long r = w * 32 + lane;
     uint32_t lo = 0, cnt = 0, rq = 0;
     if (r < nsmall) {
-      const uint2 s = a.smalls[small0 + r];
+      const uint2 s = a.smalls[r];
       lo = s.x;
       cnt = s.y & ((1u << kSmallCntBits) - 1);
       rq = s.y >> kSmallCntBits;
@@ -499,7 +532,7 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
         trace_round(a, st.rounds, 1, gtimer());
         trace_round(a, st.rounds, 7, 1);
       }
-      phase_b(a, 0, 0, 0, 0, xlo, xcnt, rx, 0, 1, wbuf);
+      phase_b(a, 0, 0, xlo, xcnt, rx, 0, 1, wbuf);
       if (tr) trace_round(a, st.rounds, 2, gtimer());
       seed = false;
     } else {
@@ -529,7 +562,7 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
         st.p_now = p_now;
         return;
       }
-      phase_b(a, st.c_cur, c_end - st.c_cur, st.s_cur, s_end - st.s_cur, 0, 0, rx, 0, 1, wbuf);
+      phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, 0, 1, wbuf);
       st.c_cur = c_end;
       st.s_cur = s_end;
       st.e_cur = e_end;
@@ -597,8 +630,7 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
         const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
         uint32_t* fout = st.flip ? a.fa : a.fb;
         RelaxCtx rx{vhi0, depart, true, st.p_now, fout, pol_stream, pol_keep, 0};
-        phase_b(a, st.c_cur, c_end - st.c_cur, st.s_cur, s_end - st.s_cur, 0, 0, rx,
-                blockIdx.x, gridDim.x, wbuf);
+        phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
         st.c_cur = c_end;
         st.s_cur = s_end;
         st.e_cur = __ldcg(&ctl->edges);
@@ -640,8 +672,7 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
       const bool push = a.mode == TGXD_MODE_SPARSE ||
                         (a.mode == TGXD_MODE_AUTO && w <= a.push_w);
       RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0};
-      phase_b(a, st.c_cur, c_end - st.c_cur, st.s_cur, s_end - st.s_cur, xlo, xcnt, rx,
-              blockIdx.x, gridDim.x, wbuf);
+      phase_b(a, c_end - st.c_cur, s_end - st.s_cur, xlo, xcnt, rx, blockIdx.x, gridDim.x, wbuf);
       if (!push) {  // improvements only feed the dense frontier's size
         uint32_t imp = rx.improved;
 #pragma unroll
