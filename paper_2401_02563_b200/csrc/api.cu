@@ -427,6 +427,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.cand_key = w.cand_key.as<int32_t>();
   a.trace = w.trace_cap ? w.trace.as<unsigned long long>() : nullptr;
   a.trace_cap = w.trace_cap;
+  a.round_limit = (uint32_t)std::min<uint64_t>(
+      0xfffffff0ULL, ((uint64_t)ncand + 1) * ((uint64_t)slots + 2) + 16);
   if (a.trace) TGXD_CUDA(cudaMemsetAsync(w.trace.p, 0, w.trace_cap * 64ull, s));
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
@@ -456,10 +458,11 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
 }
 
 static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float total_ms) {
-  if (!st) return TGXD_OK;
   Control c;
   TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ctl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  if (c.error) return fail(TGXD_ERR_CUDA, "traversal watchdog: round limit exceeded");
+  if (!st) return TGXD_OK;
   st->rounds = c.rounds;
   st->candidates = c.candidates;
   st->expansions = c.expansions;

@@ -84,6 +84,8 @@ struct Control {
   unsigned long long index_lookups; // expansions that used the fence index
   unsigned int rounds;
   unsigned int candidates;
+  unsigned int error;               // watchdog tripped
+  unsigned int pad;
   unsigned long long state[8];      // CTA-local rounds hand their state over here
 };
 

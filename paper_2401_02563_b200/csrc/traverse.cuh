@@ -80,6 +80,7 @@ struct TravArgs {
   // optional per-round trace (block 0), 8 u64 per round
   unsigned long long* trace;
   uint32_t trace_cap;
+  uint32_t round_limit;  // watchdog: a correct traversal never gets near it
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -518,6 +519,7 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
   Control* ctl = a.ctl;
   bool seed = xcnt != 0;
   for (;;) {
+    if (st.rounds > a.round_limit) return;
     __syncthreads();
     if (threadIdx.x == 0) s_val[0] = __ldcg(&ctl->pushes);
     __syncthreads();
@@ -611,6 +613,10 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
       xcnt = a.cand_cnt[cand];
     }
     for (;;) {
+      if (st.rounds > a.round_limit) {  // identical in every block: all stop together
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->error = 1;
+        break;
+      }
       const unsigned long long p_now = __ldcg(&ctl->pushes);
       const unsigned long long i_now = __ldcg(&ctl->improved);
       const unsigned long long F = xcnt ? 0 : (st.dense ? i_now - st.prev_i : p_now - st.prev_p);
@@ -702,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
         if (st.dense) st.prev_i = __ldcg(&ctl->improved) - pushed;
       }
     }
-    if (!a.fastest) break;
+    if (!a.fastest || st.rounds > a.round_limit) break;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ix += __shfl_xor_sync(0xffffffffu, ix, o);
@@ -743,6 +749,7 @@ __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_
     ctl->edges = 0;
     ctl->expansions = 0;
     ctl->index_lookups = 0;
+    ctl->error = 0;
   }
   if (q >= Q || fastest) return;
   const uint32_t item = q * n + qp[q].root;
