@@ -624,6 +624,9 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
       const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
                             (xcnt ? xcnt <= kLocalMaxW : F <= kLocalMaxF);
       if (go_local) {
+        // every block must have read this round's counters before block 0
+        // starts moving them
+        grid.sync();
         if (blockIdx.x == 0) {
           local_rounds(a, st, xlo, xcnt, depart, vhi0, pol_stream, pol_keep, wbuf, ix);
           if (threadIdx.x == 0) save_state(ctl, st);
