@@ -163,22 +163,20 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     const int32_t* kk = dir == 0 ? d_st : d_en;
     const int32_t* vv = dir == 0 ? d_en : d_st;
     DeviceBuffer& b_off = dir == 0 ? G->out_off : G->in_off;
-    DeviceBuffer& b_nbr = dir == 0 ? G->out_nbr : G->in_nbr;
     DeviceBuffer& b_key = dir == 0 ? G->out_key : G->in_key;
-    DeviceBuffer& b_val = dir == 0 ? G->out_val : G->in_val;
+    DeviceBuffer& b_pay = dir == 0 ? G->out_pay : G->in_pay;
     DeviceBuffer& b_fence = dir == 0 ? G->out_fence : G->in_fence;
     uint32_t* off = dalloc<uint32_t>(b_off, (size_t)n + 1);
-    uint32_t* nbr = dalloc<uint32_t>(b_nbr, m);
     int32_t* key = dalloc<int32_t>(b_key, m);
-    int32_t* val = dalloc<int32_t>(b_val, m);
+    uint2* pay = dalloc<uint2>(b_pay, m);
     int32_t* fence = dalloc<int32_t>(b_fence, nf);
-    if (!off || !nbr || !key || !val || !fence)
+    if (!off || !key || !pay || !fence)
       return fail(TGXD_ERR_CUDA, "device allocation failed (T-CSR arrays)");
     if (m) {
       make_sort_keys<<<gb, 256, 0, s>>>(owner, kk, dir, m, ka, ia);
       TGXD_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
                                                 end_bit, s));
-      gather_layout<<<gb, 256, 0, s>>>(ib, other, kk, vv, dir, m, nbr, key, val);
+      gather_layout<<<gb, 256, 0, s>>>(ib, other, kk, vv, dir, m, key, pay);
       make_fences<<<grid_for(nf, G->sm_count), 256, 0, s>>>(key, m, fence);
     }
     TGXD_CUDA(cudaMemsetAsync(dc, 0, ((size_t)n + 1) * 4, s));
@@ -188,9 +186,8 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     if (n) count_indexed<<<grid_for(n, G->sm_count), 256, 0, s>>>(off, n, G->index_cutoff, dctr + dir);
     DevCsr& c = dir == 0 ? G->out : G->in;
     c.off = off;
-    c.nbr = nbr;
     c.key = key;
-    c.val = val;
+    c.pay = pay;
     c.fence = fence;
     c.n = n;
     c.m = (uint32_t)m;
@@ -305,12 +302,14 @@ static int fastest_candidates(tgxd_graph* G, Prepared& P) {
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
   const uint32_t deg = se[1] - se[0];
   std::vector<int32_t> key(deg), val(deg);
+  std::vector<uint2> pay(deg);
   if (deg) {
     TGXD_CUDA(cudaMemcpyAsync(key.data(), G->out.key + se[0], deg * 4ull, cudaMemcpyDeviceToHost,
                               G->stream));
-    TGXD_CUDA(cudaMemcpyAsync(val.data(), G->out.val + se[0], deg * 4ull, cudaMemcpyDeviceToHost,
+    TGXD_CUDA(cudaMemcpyAsync(pay.data(), G->out.pay + se[0], deg * 8ull, cudaMemcpyDeviceToHost,
                               G->stream));
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
+    for (uint32_t i = 0; i < deg; ++i) val[i] = (int32_t)pay[i].y;
   }
   P.cand_lo.clear();
   P.cand_cnt.clear();
@@ -548,7 +547,7 @@ __global__ void work_kernel(DevCsr g, const int32_t* X, QueryParam qp, int stric
     const uint32_t s = g.off[v], t = g.off[v + 1];
     for (uint32_t j = s + lane; j < t; j += 32) {
       const int32_t k = g.key[j];
-      e_adm += (k >= lb && g.val[j] <= qp.vhi) ? 1 : 0;
+      e_adm += (k >= lb && (int32_t)g.pay[j].y <= qp.vhi) ? 1 : 0;
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -833,13 +832,17 @@ int tgxd_graph_flatten(tgxd_graph* g, int direction, uint32_t* src, uint32_t* ds
   if (g->n) owners_kernel<<<grid_for(g->n, g->sm_count), 256, 0, g->stream>>>(c.off, g->n, own);
   std::vector<uint32_t> o(m), nb(m);
   std::vector<int32_t> k(m), v(m);
+  std::vector<uint2> pay(m);
   if (m) {
     TGXD_CUDA(cudaMemcpyAsync(o.data(), own, m * 4, cudaMemcpyDeviceToHost, g->stream));
-    TGXD_CUDA(cudaMemcpyAsync(nb.data(), c.nbr, m * 4, cudaMemcpyDeviceToHost, g->stream));
     TGXD_CUDA(cudaMemcpyAsync(k.data(), c.key, m * 4, cudaMemcpyDeviceToHost, g->stream));
-    TGXD_CUDA(cudaMemcpyAsync(v.data(), c.val, m * 4, cudaMemcpyDeviceToHost, g->stream));
+    TGXD_CUDA(cudaMemcpyAsync(pay.data(), c.pay, m * 8, cudaMemcpyDeviceToHost, g->stream));
   }
   TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  for (uint64_t i = 0; i < m; ++i) {
+    nb[i] = pay[i].x;
+    v[i] = (int32_t)pay[i].y;
+  }
   for (uint64_t i = 0; i < m; ++i) {
     if (direction == 0) {
       src[i] = o[i];

@@ -83,14 +83,13 @@ __global__ void make_sort_keys(const uint32_t* owner, const int32_t* kk, int neg
 }
 
 __global__ void gather_layout(const uint32_t* idx, const uint32_t* other, const int32_t* kk,
-                              const int32_t* vv, int negate, uint64_t m, uint32_t* nbr,
-                              int32_t* key, int32_t* val) {
+                              const int32_t* vv, int negate, uint64_t m, int32_t* key,
+                              uint2* pay) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
     const uint32_t i = idx[j];
-    nbr[j] = other[i];
     key[j] = negate ? -kk[i] : kk[i];
-    val[j] = negate ? -vv[i] : vv[i];
+    pay[j] = make_uint2(other[i], (uint32_t)(negate ? -vv[i] : vv[i]));
   }
 }
 

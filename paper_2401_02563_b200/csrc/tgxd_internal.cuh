@@ -26,13 +26,15 @@ constexpr uint32_t kFenceStride = 1u << kFenceShift;
 // One direction of the device T-CSR. Segments are sorted by key ascending.
 //   Out layout: key = start, val = end           (earliest arrival / fastest)
 //   In layout : key = -end,  val = -start        (latest departure, mirrored)
+// Keys live in their own array (searched, never streamed); neighbor and val
+// are interleaved so the relax step reads one 8-byte word per edge and a
+// short range touches as few 32-byte sectors as possible.
 // With that mirror, both traversals are "relax val over edges whose key lies
 // at or above the frontier vertex's bound", so one kernel family serves both.
 struct DevCsr {
   const uint32_t* off = nullptr;  // n + 1
-  const uint32_t* nbr = nullptr;  // m
-  const int32_t* key = nullptr;   // m
-  const int32_t* val = nullptr;   // m
+  const int32_t* key = nullptr;   // m: search keys (binary search / fences only)
+  const uint2* pay = nullptr;     // m: relax payload {neighbor, val} (one 8-byte load)
   const int32_t* fence = nullptr; // ceil(m / 32): key[32 j]
   uint32_t n = 0;
   uint32_t m = 0;
@@ -99,8 +101,8 @@ struct tgxd_graph {
   int directed = 1;
   uint64_t index_cutoff = 2048;
   uint64_t indexed[2] = {0, 0};
-  tgxd::DeviceBuffer out_off, out_nbr, out_key, out_val, out_fence;
-  tgxd::DeviceBuffer in_off, in_nbr, in_key, in_val, in_fence;
+  tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence;
+  tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence;
   tgxd::DevCsr out, in;
   cudaStream_t stream = nullptr;
   int sm_count = 0;

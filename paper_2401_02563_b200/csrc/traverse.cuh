@@ -114,40 +114,17 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
                : "=r"(r) : "l"(p), "l"(pol));
   return r;
 }
+__device__ __forceinline__ uint2 ld_stream2(const uint2* p, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
 // Coherent (L2) read of mutable state, kept resident in L2.
 __device__ __forceinline__ int32_t ld_state(const int32_t* p, uint64_t pol) {
   int32_t r;
   asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
   return r;
-}
-
-// First position in [s, t) whose key >= x. Vertices at or above the index
-// cutoff first search the fence array (every 32nd key of the layout, a
-// compact "bucketed timeline"), which narrows the search to one 128-byte key
-// line; the rest binary-search their segment directly. Results-neutral, like
-// the reference's TGER-vs-scan choice (test_algorithms.cpp:196-217).
-__device__ __forceinline__ uint32_t lower_key(const DevCsr& g, uint32_t s, uint32_t t, int32_t x,
-                                              bool use_index) {
-  if (use_index && t > s) {
-    const uint32_t jlo = (s + kFenceStride - 1) >> kFenceShift;
-    const uint32_t jhi = (t - 1) >> kFenceShift;
-    if (jlo <= jhi) {
-      uint32_t a = jlo, b = jhi + 1;
-      while (a < b) {
-        const uint32_t mid = (a + b) >> 1;
-        if (__ldg(g.fence + mid) < x) a = mid + 1;
-        else b = mid;
-      }
-      if (a > jlo) s = max(s, ((a - 1) << kFenceShift) + 1);
-      if (a <= jhi) t = min(t, a << kFenceShift);
-    }
-  }
-  while (s < t) {
-    const uint32_t mid = (s + t) >> 1;
-    if (__ldg(g.key + mid) < x) s = mid + 1;
-    else t = mid;
-  }
-  return s;
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -215,8 +192,9 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
   uint32_t d[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    v[u] = act[u] ? ld_stream(a.g.val + e[u], rx.pol_stream) : kInf;
-    d[u] = act[u] ? ld_stream(a.g.nbr + e[u], rx.pol_stream) : 0u;
+    const uint2 pl = act[u] ? ld_stream2(a.g.pay + e[u], rx.pol_stream) : make_uint2(0u, kInf);
+    d[u] = pl.x;
+    v[u] = (int32_t)pl.y;
   }
   uint32_t idx[kUnroll];
   int32_t cur[kUnroll];
@@ -254,81 +232,181 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
   }
 }
 
-// Expansion of one slot (q * n + v) with label x: returns the range of keys
-// still to relax, [lo, lo + cnt), and records the new bound.
-__device__ __forceinline__ uint32_t expand_slot(const TravArgs& a, uint32_t item, int32_t x,
-                                                int32_t old, uint32_t& lo, uint32_t& q,
-                                                unsigned long long& ix) {
-  q = a.Q == 1 ? 0u : item / a.n;
-  const uint32_t v = item - q * a.n;
-  const QueryParam& qp = a.qp[q];
-  int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
-  if (lb < qp.klo) lb = qp.klo;
-  lo = 0;
-  if (lb >= old) return 0;
-  a.Ex[item] = lb;
-  const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
-  if (lb >= hik) return 0;
-  const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-  const bool use_idx = a.cutoff != 0 && t - s >= a.cutoff;
-  ix += use_idx;
-  const uint32_t p0 = lower_key(a.g, s, t, lb, use_idx);
-  const uint32_t p1 = lower_key(a.g, p0, t, hik, use_idx);
-  lo = p0;
-  return p1 - p0;
+// ---------------------------------------------------------------------------
+// Phase A: expansion, kExpand slots per thread per step. All per-slot memory
+// chains (label, offsets, the binary searches) advance in lockstep so each
+// step keeps kExpand independent loads in flight per thread.
+
+constexpr int kExpand = 4;
+
+// Lockstep lower_bound: pos[k] = first position in [s[k], t[k]) whose key is
+// >= x[k]. Slots with use_idx[k] first search the fence array (every 32nd
+// key of the layout, a compact "bucketed timeline"), which narrows the
+// search to one 128-byte key line; the rest binary-search their segment
+// directly. Results-neutral, like the reference's TGER-vs-scan choice
+// (test_algorithms.cpp:196-217).
+__device__ __forceinline__ void lower_bound_k(const DevCsr& g, const uint32_t (&s)[kExpand],
+                                              const uint32_t (&t)[kExpand],
+                                              const int32_t (&x)[kExpand],
+                                              const bool (&use_idx)[kExpand],
+                                              const bool (&act)[kExpand],
+                                              uint32_t (&pos)[kExpand]) {
+  uint32_t lo[kExpand], hi[kExpand], jlo[kExpand], jhi[kExpand];
+  bool fence[kExpand];
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    lo[k] = s[k];
+    hi[k] = act[k] ? t[k] : s[k];
+    jlo[k] = (s[k] + kFenceStride - 1) >> kFenceShift;
+    jhi[k] = t[k] > 0 ? (t[k] - 1) >> kFenceShift : 0;
+    fence[k] = act[k] && use_idx[k] && t[k] > s[k] && jlo[k] <= jhi[k];
+    if (fence[k]) {
+      lo[k] = jlo[k];
+      hi[k] = jhi[k] + 1;
+    }
+  }
+  for (;;) {
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kExpand; ++k) {
+      if (lo[k] < hi[k]) {
+        const uint32_t mid = (lo[k] + hi[k]) >> 1;
+        const int32_t probe = fence[k] ? __ldg(g.fence + mid) : __ldg(g.key + mid);
+        if (probe < x[k]) lo[k] = mid + 1;
+        else hi[k] = mid;
+        any = true;
+      } else if (fence[k]) {  // fence stage done: continue inside one key line
+        const uint32_t a = lo[k];
+        lo[k] = a > jlo[k] ? max(s[k], ((a - 1) << kFenceShift) + 1) : s[k];
+        hi[k] = a <= jhi[k] ? min(t[k], a << kFenceShift) : t[k];
+        fence[k] = false;
+        any = true;
+      }
+    }
+    if (!any) break;
+  }
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) pos[k] = lo[k];
 }
 
-// Block-aggregated emission of one range per thread (cnt == 0: nothing):
-// one block-wide scan and two global atomics per 256 expanded slots. Every
-// thread of the block must call it (it synchronizes the block).
-__device__ __forceinline__ void emit(const TravArgs& a, uint32_t lo, uint32_t cnt, uint32_t q,
-                                     unsigned long long cstart, unsigned long long sstart,
-                                     unsigned long long& work) {
+// Expansion of kExpand slots (q * n + v) with labels x[k] and previous
+// bounds old[k]: records the new bounds and returns the key ranges still to
+// relax, [lo[k], lo[k] + cnt[k]).
+__device__ __forceinline__ void expand_k(const TravArgs& a, const uint32_t (&item)[kExpand],
+                                         const bool (&valid)[kExpand],
+                                         const int32_t (&x)[kExpand],
+                                         const int32_t (&old)[kExpand], uint32_t (&lo)[kExpand],
+                                         uint32_t (&cnt)[kExpand], uint32_t (&q)[kExpand],
+                                         unsigned long long& ix) {
+  bool act[kExpand], idx[kExpand], need1[kExpand];
+  int32_t lb[kExpand], hik[kExpand], last[kExpand];
+  uint32_t v[kExpand], s[kExpand], t[kExpand], p0[kExpand], p1[kExpand];
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    q[k] = a.Q == 1 ? 0u : item[k] / a.n;
+    v[k] = item[k] - q[k] * a.n;
+    const QueryParam& qp = a.qp[q[k]];
+    lb[k] = (v[k] == qp.root) ? qp.klo : bound_of(x[k], a.strict);
+    if (lb[k] < qp.klo) lb[k] = qp.klo;
+    act[k] = valid[k] && lb[k] < old[k];
+    if (act[k]) a.Ex[item[k]] = lb[k];
+    hik[k] = min(old[k], qp.vhi + 1);  // keys above vhi cannot fit the window
+    act[k] = act[k] && lb[k] < hik[k];
+    cnt[k] = 0;
+    lo[k] = 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    s[k] = act[k] ? __ldg(a.g.off + v[k]) : 0u;
+    t[k] = act[k] ? __ldg(a.g.off + v[k] + 1) : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    act[k] = act[k] && t[k] > s[k];
+    idx[k] = act[k] && a.cutoff != 0 && t[k] - s[k] >= a.cutoff;
+    ix += idx[k];
+    // the common case hik > last key needs no second search
+    last[k] = act[k] ? __ldg(a.g.key + t[k] - 1) : 0;
+  }
+  lower_bound_k(a.g, s, t, lb, idx, act, p0);
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) need1[k] = act[k] && last[k] >= hik[k];
+  lower_bound_k(a.g, p0, t, hik, idx, need1, p1);
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    if (act[k]) {
+      const uint32_t e1 = need1[k] ? p1[k] : t[k];
+      lo[k] = p0[k];
+      cnt[k] = e1 - p0[k];
+    }
+  }
+}
+
+// Block-aggregated emission of kExpand ranges per thread (cnt == 0:
+// nothing): one block-wide scan and at most two global atomics per step.
+// Every thread of the block must call it (it synchronizes the block).
+__device__ __forceinline__ void emit_k(const TravArgs& a, const uint32_t (&lo)[kExpand],
+                                       const uint32_t (&cnt)[kExpand],
+                                       const uint32_t (&q)[kExpand], unsigned long long cstart,
+                                       unsigned long long sstart, unsigned long long& work) {
   __shared__ uint32_t s_ch[kWarps], s_sm[kWarps];
   __shared__ unsigned long long s_base[2];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-  const bool small = cnt != 0 && cnt < kSmall;
-  const uint32_t nch = cnt >= kSmall ? (cnt + kChunk - 1) / kChunk : 0u;
-  work += cnt;
-  const uint32_t sbal = __ballot_sync(0xffffffffu, small);
-  uint32_t incl = nch;
+  uint32_t my_ch = 0, my_sm = 0;
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    work += cnt[k];
+    my_ch += cnt[k] >= kSmall ? (cnt[k] + kChunk - 1) / kChunk : 0u;
+    my_sm += (cnt[k] != 0 && cnt[k] < kSmall) ? 1u : 0u;
+  }
+  uint32_t ich = my_ch, ism = my_sm;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+    const uint32_t y = __shfl_up_sync(0xffffffffu, ich, o);
+    const uint32_t z = __shfl_up_sync(0xffffffffu, ism, o);
+    if (lane >= o) {
+      ich += y;
+      ism += z;
+    }
   }
   if (lane == 31) {
-    s_ch[wid] = incl;
-    s_sm[wid] = __popc(sbal);
+    s_ch[wid] = ich;
+    s_sm[wid] = ism;
   }
   __syncthreads();
   uint32_t ch_before = 0, sm_before = 0, ch_tot = 0, sm_tot = 0;
 #pragma unroll
-  for (int k = 0; k < kWarps; ++k) {
-    const uint32_t c = s_ch[k], m = s_sm[k];
-    if (k < (int)wid) {
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t c = s_ch[w], m = s_sm[w];
+    if (w < (int)wid) {
       ch_before += c;
       sm_before += m;
     }
     ch_tot += c;
     sm_tot += m;
   }
+  if (ch_tot + sm_tot == 0) {  // uniform: nothing to emit in the whole block
+    __syncthreads();
+    return;
+  }
   if (threadIdx.x == 0) {
     s_base[0] = ch_tot ? atomicAdd(&a.ctl->chunks, (unsigned long long)ch_tot) : 0ull;
     s_base[1] = sm_tot ? atomicAdd(&a.ctl->smalls, (unsigned long long)sm_tot) : 0ull;
   }
   __syncthreads();
-  if (small) {
-    const uint64_t pos = s_base[1] - sstart + sm_before + __popc(sbal & ((1u << lane) - 1));
-    a.smalls[pos] = make_uint2(lo, (q << kSmallCntBits) | cnt);
-  }
-  if (nch) {
-    uint64_t pos = s_base[0] - cstart + ch_before + incl - nch;
-    for (uint32_t c = 0; c < nch; ++c, ++pos) {
-      const uint32_t off = c * kChunk;
-      a.chunks[pos] = make_uint2(lo + off, (q << kChunkLenBits) | min(kChunk, cnt - off));
+  uint64_t cpos = s_base[0] - cstart + ch_before + ich - my_ch;
+  uint64_t spos = s_base[1] - sstart + sm_before + ism - my_sm;
+#pragma unroll
+  for (int k = 0; k < kExpand; ++k) {
+    const uint32_t c = cnt[k];
+    if (c != 0 && c < kSmall) {
+      a.smalls[spos++] = make_uint2(lo[k], (q[k] << kSmallCntBits) | c);
+    } else if (c >= kSmall) {
+      for (uint32_t off = 0; off < c; off += kChunk)
+        a.chunks[cpos++] = make_uint2(lo[k] + off, (q[k] << kChunkLenBits) | min(kChunk, c - off));
     }
   }
+  __syncthreads();  // s_ch / s_base are reused by the next step
 }
 
 // Adds a block's relax-work count to the edges counter (one atomic per block).
@@ -352,17 +430,25 @@ __device__ void phase_a_sparse(const TravArgs& a, const uint32_t* fin, uint32_t 
                                unsigned long long cstart, unsigned long long sstart,
                                uint32_t bid, uint32_t nblk, uint64_t pol_keep,
                                unsigned long long& ix) {
-  const uint32_t nthreads = nblk * blockDim.x;
+  const uint32_t step = nblk * blockDim.x * kExpand;
   unsigned long long work = 0;
-  for (uint32_t base = bid * blockDim.x; base < F; base += nthreads) {
-    const uint32_t i = base + threadIdx.x;
-    uint32_t cnt = 0, lo = 0, q = 0;
-    if (i < F) {
-      const uint32_t item = __ldcg(fin + i);
-      cnt = expand_slot(a, item, ld_state(a.X + item, pol_keep), ld_state(a.Ex + item, pol_keep),
-                        lo, q, ix);
+  for (uint32_t base = bid * blockDim.x * kExpand; base < F; base += step) {
+    uint32_t item[kExpand], lo[kExpand], cnt[kExpand], q[kExpand];
+    bool valid[kExpand];
+    int32_t x[kExpand], old[kExpand];
+#pragma unroll
+    for (int k = 0; k < kExpand; ++k) {
+      const uint32_t i = base + k * blockDim.x + threadIdx.x;
+      valid[k] = i < F;
+      item[k] = valid[k] ? __ldcg(fin + i) : 0u;
     }
-    emit(a, lo, cnt, q, cstart, sstart, work);
+#pragma unroll
+    for (int k = 0; k < kExpand; ++k) {
+      x[k] = valid[k] ? ld_state(a.X + item[k], pol_keep) : kInf;
+      old[k] = valid[k] ? ld_state(a.Ex + item[k], pol_keep) : kInf;
+    }
+    expand_k(a, item, valid, x, old, lo, cnt, q, ix);
+    emit_k(a, lo, cnt, q, cstart, sstart, work);
   }
   flush_work(a.ctl, work);
 }
@@ -372,18 +458,23 @@ __device__ void phase_a_sparse(const TravArgs& a, const uint32_t* fin, uint32_t 
 __device__ void phase_a_dense(const TravArgs& a, unsigned long long cstart,
                               unsigned long long sstart, uint64_t pol_keep,
                               unsigned long long& ix) {
-  const uint32_t nthreads = gridDim.x * blockDim.x;
   const uint32_t slots = a.Q * a.n;
+  const uint32_t step = gridDim.x * blockDim.x * kExpand;
   unsigned long long work = 0;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < slots; base += nthreads) {
-    const uint32_t i = base + threadIdx.x;
-    uint32_t cnt = 0, lo = 0, q = 0;
-    if (i < slots) {
-      const int32_t x = ld_state(a.X + i, pol_keep);
-      const int32_t old = ld_state(a.Ex + i, pol_keep);
-      if (x != kInf) cnt = expand_slot(a, i, x, old, lo, q, ix);
+  for (uint32_t base = blockIdx.x * blockDim.x * kExpand; base < slots; base += step) {
+    uint32_t item[kExpand], lo[kExpand], cnt[kExpand], q[kExpand];
+    bool valid[kExpand];
+    int32_t x[kExpand], old[kExpand];
+#pragma unroll
+    for (int k = 0; k < kExpand; ++k) {
+      item[k] = base + k * blockDim.x + threadIdx.x;
+      const bool in = item[k] < slots;
+      x[k] = in ? ld_state(a.X + item[k], pol_keep) : kInf;
+      old[k] = in ? ld_state(a.Ex + item[k], pol_keep) : kInf;
+      valid[k] = in && x[k] != kInf;
     }
-    emit(a, lo, cnt, q, cstart, sstart, work);
+    expand_k(a, item, valid, x, old, lo, cnt, q, ix);
+    emit_k(a, lo, cnt, q, cstart, sstart, work);
   }
   flush_work(a.ctl, work);
 }
