@@ -233,180 +233,206 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
 }
 
 // ---------------------------------------------------------------------------
-// Phase A: expansion, kExpand slots per thread per step. All per-slot memory
-// chains (label, offsets, the binary searches) advance in lockstep so each
-// step keeps kExpand independent loads in flight per thread.
+// Phase A: expansion. Each warp takes 32 frontier slots at a time. Short
+// segments (<= 32 keys) are counted in registers from a handful of 16-byte
+// loads; medium segments binary-search per lane; segments at or above the
+// index cutoff go through the selective index: a warp-cooperative 32-ary
+// search of the fence array (every 32nd key, a compact "bucketed timeline")
+// that lands on one 128-byte key line. All three are results-neutral, like
+// the reference's TGER-vs-scan choice (test_algorithms.cpp:196-217).
+// Emission is buffered per warp in shared memory (no block barriers).
 
-constexpr int kExpand = 4;
+constexpr uint32_t kLinear = 32;   // segments up to this length are counted, not searched
 
-// Lockstep lower_bound: pos[k] = first position in [s[k], t[k]) whose key is
-// >= x[k]. Slots with use_idx[k] first search the fence array (every 32nd
-// key of the layout, a compact "bucketed timeline"), which narrows the
-// search to one 128-byte key line; the rest binary-search their segment
-// directly. Results-neutral, like the reference's TGER-vs-scan choice
-// (test_algorithms.cpp:196-217).
-__device__ __forceinline__ void lower_bound_k(const DevCsr& g, const uint32_t (&s)[kExpand],
-                                              const uint32_t (&t)[kExpand],
-                                              const int32_t (&x)[kExpand],
-                                              const bool (&use_idx)[kExpand],
-                                              const bool (&act)[kExpand],
-                                              uint32_t (&pos)[kExpand]) {
-  uint32_t lo[kExpand], hi[kExpand], jlo[kExpand], jhi[kExpand];
-  bool fence[kExpand];
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    lo[k] = s[k];
-    hi[k] = act[k] ? t[k] : s[k];
-    jlo[k] = (s[k] + kFenceStride - 1) >> kFenceShift;
-    jhi[k] = t[k] > 0 ? (t[k] - 1) >> kFenceShift : 0;
-    fence[k] = act[k] && use_idx[k] && t[k] > s[k] && jlo[k] <= jhi[k];
-    if (fence[k]) {
-      lo[k] = jlo[k];
-      hi[k] = jhi[k] + 1;
+// Per-warp staging of emitted work: appended 32 entries at a time.
+struct WarpList {
+  uint2* buf;       // 64 entries of this warp
+  uint32_t n;       // staged entries (warp-uniform)
+};
+
+__device__ __forceinline__ void list_flush(WarpList& wl, uint32_t count, unsigned long long* ctr,
+                                           unsigned long long start, uint2* list) {
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  const uint2 v = wl.buf[lane];
+  const uint2 tail = wl.buf[32 + lane];
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(ctr, (unsigned long long)count);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < count) list[base - start + lane] = v;
+  __syncwarp();
+  if (lane + count < wl.n && lane < 32) wl.buf[lane] = tail;
+  wl.n -= count;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void list_append(WarpList& wl, bool p, uint2 v, unsigned long long* ctr,
+                                            unsigned long long start, uint2* list) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, p);
+  if (bal == 0) return;
+  if (p) wl.buf[wl.n + __popc(bal & ((1u << lane_id()) - 1))] = v;
+  wl.n += __popc(bal);
+  if (wl.n >= 32) list_flush(wl, 32, ctr, start, list);
+}
+
+__device__ __forceinline__ void list_drain(WarpList& wl, unsigned long long* ctr,
+                                           unsigned long long start, uint2* list) {
+  if (wl.n) list_flush(wl, wl.n, ctr, start, list);
+}
+
+__device__ __forceinline__ uint32_t lane_lower_bound(const int32_t* key, uint32_t lo, uint32_t hi,
+                                                     int32_t x) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(key + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Warp-cooperative lower_bound over arr[lo, hi): 32 probes per level.
+// Every lane must call it with the same arguments; the result is uniform.
+__device__ __forceinline__ uint32_t warp_lower_bound(const int32_t* arr, uint32_t lo, uint32_t hi,
+                                                     int32_t x) {
+  const uint32_t lane = lane_id();
+  while (hi - lo > 32) {
+    const uint32_t len = hi - lo;
+    const uint32_t pos = lo + (uint32_t)(((unsigned long long)(lane + 1) * len) / 33);
+    const uint32_t b = __ballot_sync(0xffffffffu, __ldg(arr + pos) >= x);
+    if (b == 0) {
+      lo = __shfl_sync(0xffffffffu, pos, 31) + 1;
+    } else {
+      const uint32_t f = __ffs(b) - 1;
+      const uint32_t pf = __shfl_sync(0xffffffffu, pos, f);
+      const uint32_t pp = __shfl_sync(0xffffffffu, pos, f ? f - 1 : 0);
+      hi = pf;  // arr[pf] >= x: the answer is at most pf
+      if (f) lo = pp + 1;
     }
   }
-  for (;;) {
-    bool any = false;
+  const uint32_t pos = lo + lane;
+  const uint32_t b = __ballot_sync(0xffffffffu, pos < hi && __ldg(arr + pos) >= x);
+  return b ? lo + __ffs(b) - 1 : hi;
+}
+
+// Selective-index lookup: fence search, then one key line.
+__device__ __forceinline__ uint32_t index_lower_bound(const DevCsr& g, uint32_t s, uint32_t t,
+                                                      int32_t x) {
+  const uint32_t jlo = (s + kFenceStride - 1) >> kFenceShift;
+  const uint32_t jhi = (t - 1) >> kFenceShift;
+  if (jlo <= jhi) {
+    const uint32_t f = warp_lower_bound(g.fence, jlo, jhi + 1, x);
+    if (f > jlo) s = max(s, ((f - 1) << kFenceShift) + 1);
+    if (f <= jhi) t = min(t, f << kFenceShift);
+  }
+  return warp_lower_bound(g.key, s, t, x);
+}
+
+// Keys below lb and below hik in a short segment [s, t), t - s <= kLinear,
+// from aligned 16-byte loads.
+__device__ __forceinline__ void linear_count(const int32_t* key, uint32_t s, uint32_t t, int32_t lb,
+                                             int32_t hik, uint32_t& c0, uint32_t& c1) {
+  c0 = c1 = 0;
+  const uint32_t a0 = s & ~3u;
 #pragma unroll
-    for (int k = 0; k < kExpand; ++k) {
-      if (lo[k] < hi[k]) {
-        const uint32_t mid = (lo[k] + hi[k]) >> 1;
-        const int32_t probe = fence[k] ? __ldg(g.fence + mid) : __ldg(g.key + mid);
-        if (probe < x[k]) lo[k] = mid + 1;
-        else hi[k] = mid;
-        any = true;
-      } else if (fence[k]) {  // fence stage done: continue inside one key line
-        const uint32_t a = lo[k];
-        lo[k] = a > jlo[k] ? max(s[k], ((a - 1) << kFenceShift) + 1) : s[k];
-        hi[k] = a <= jhi[k] ? min(t[k], a << kFenceShift) : t[k];
-        fence[k] = false;
-        any = true;
+  for (uint32_t j = 0; j < (kLinear + 4) / 4; ++j) {
+    const uint32_t p = a0 + 4 * j;
+    if (p < t) {
+      const int4 k4 = __ldg(reinterpret_cast<const int4*>(key + p));
+      const int32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const bool in = p + c >= s && p + c < t;
+        c0 += (in && kk[c] < lb) ? 1u : 0u;
+        c1 += (in && kk[c] < hik) ? 1u : 0u;
       }
     }
-    if (!any) break;
-  }
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) pos[k] = lo[k];
-}
-
-// Expansion of kExpand slots (q * n + v) with labels x[k] and previous
-// bounds old[k]: records the new bounds and returns the key ranges still to
-// relax, [lo[k], lo[k] + cnt[k]).
-__device__ __forceinline__ void expand_k(const TravArgs& a, const uint32_t (&item)[kExpand],
-                                         const bool (&valid)[kExpand],
-                                         const int32_t (&x)[kExpand],
-                                         const int32_t (&old)[kExpand], uint32_t (&lo)[kExpand],
-                                         uint32_t (&cnt)[kExpand], uint32_t (&q)[kExpand],
-                                         unsigned long long& ix) {
-  bool act[kExpand], idx[kExpand], need1[kExpand];
-  int32_t lb[kExpand], hik[kExpand], last[kExpand];
-  uint32_t v[kExpand], s[kExpand], t[kExpand], p0[kExpand], p1[kExpand];
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    q[k] = a.Q == 1 ? 0u : item[k] / a.n;
-    v[k] = item[k] - q[k] * a.n;
-    const QueryParam& qp = a.qp[q[k]];
-    lb[k] = (v[k] == qp.root) ? qp.klo : bound_of(x[k], a.strict);
-    if (lb[k] < qp.klo) lb[k] = qp.klo;
-    act[k] = valid[k] && lb[k] < old[k];
-    if (act[k]) a.Ex[item[k]] = lb[k];
-    hik[k] = min(old[k], qp.vhi + 1);  // keys above vhi cannot fit the window
-    act[k] = act[k] && lb[k] < hik[k];
-    cnt[k] = 0;
-    lo[k] = 0;
-  }
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    s[k] = act[k] ? __ldg(a.g.off + v[k]) : 0u;
-    t[k] = act[k] ? __ldg(a.g.off + v[k] + 1) : 0u;
-  }
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    act[k] = act[k] && t[k] > s[k];
-    idx[k] = act[k] && a.cutoff != 0 && t[k] - s[k] >= a.cutoff;
-    ix += idx[k];
-    // the common case hik > last key needs no second search
-    last[k] = act[k] ? __ldg(a.g.key + t[k] - 1) : 0;
-  }
-  lower_bound_k(a.g, s, t, lb, idx, act, p0);
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) need1[k] = act[k] && last[k] >= hik[k];
-  lower_bound_k(a.g, p0, t, hik, idx, need1, p1);
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    if (act[k]) {
-      const uint32_t e1 = need1[k] ? p1[k] : t[k];
-      lo[k] = p0[k];
-      cnt[k] = e1 - p0[k];
-    }
   }
 }
 
-// Block-aggregated emission of kExpand ranges per thread (cnt == 0:
-// nothing): one block-wide scan and at most two global atomics per step.
-// Every thread of the block must call it (it synchronizes the block).
-__device__ __forceinline__ void emit_k(const TravArgs& a, const uint32_t (&lo)[kExpand],
-                                       const uint32_t (&cnt)[kExpand],
-                                       const uint32_t (&q)[kExpand], unsigned long long cstart,
-                                       unsigned long long sstart, unsigned long long& work) {
-  __shared__ uint32_t s_ch[kWarps], s_sm[kWarps];
-  __shared__ unsigned long long s_base[2];
-  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-  uint32_t my_ch = 0, my_sm = 0;
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    work += cnt[k];
-    my_ch += cnt[k] >= kSmall ? (cnt[k] + kChunk - 1) / kChunk : 0u;
-    my_sm += (cnt[k] != 0 && cnt[k] < kSmall) ? 1u : 0u;
-  }
-  uint32_t ich = my_ch, ism = my_sm;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, ich, o);
-    const uint32_t z = __shfl_up_sync(0xffffffffu, ism, o);
-    if (lane >= o) {
-      ich += y;
-      ism += z;
+struct ExpandBufs {
+  WarpList sm, ch;
+  unsigned long long cstart, sstart;
+};
+
+// Expansion of one slot per lane (item = q * n + v, label x, previous bound
+// old); the emitted ranges go to the warp's lists. All lanes must call it.
+__device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint32_t item, int32_t x,
+                                            int32_t old, ExpandBufs& eb,
+                                            unsigned long long& work, unsigned long long& ix) {
+  const uint32_t lane = lane_id();
+  uint32_t q = 0, v = 0, s = 0, t = 0, p0 = 0, p1 = 0;
+  int32_t lb = 0, hik = 0, last = 0;
+  bool act = false;
+  if (valid) {
+    q = a.Q == 1 ? 0u : item / a.n;
+    v = item - q * a.n;
+    const QueryParam& qp = a.qp[q];
+    // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342):
+    // the root leaves at any time inside the window; everyone else strictly
+    // (or weakly) after its own label.
+    lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
+    if (lb < qp.klo) lb = qp.klo;
+    if (lb < old) {
+      a.Ex[item] = lb;
+      hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
+      if (lb < hik) {
+        s = __ldg(a.g.off + v);
+        t = __ldg(a.g.off + v + 1);
+        act = t > s;
+      }
     }
   }
-  if (lane == 31) {
-    s_ch[wid] = ich;
-    s_sm[wid] = ism;
-  }
-  __syncthreads();
-  uint32_t ch_before = 0, sm_before = 0, ch_tot = 0, sm_tot = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    const uint32_t c = s_ch[w], m = s_sm[w];
-    if (w < (int)wid) {
-      ch_before += c;
-      sm_before += m;
-    }
-    ch_tot += c;
-    sm_tot += m;
-  }
-  if (ch_tot + sm_tot == 0) {  // uniform: nothing to emit in the whole block
-    __syncthreads();
-    return;
-  }
-  if (threadIdx.x == 0) {
-    s_base[0] = ch_tot ? atomicAdd(&a.ctl->chunks, (unsigned long long)ch_tot) : 0ull;
-    s_base[1] = sm_tot ? atomicAdd(&a.ctl->smalls, (unsigned long long)sm_tot) : 0ull;
-  }
-  __syncthreads();
-  uint64_t cpos = s_base[0] - cstart + ch_before + ich - my_ch;
-  uint64_t spos = s_base[1] - sstart + sm_before + ism - my_sm;
-#pragma unroll
-  for (int k = 0; k < kExpand; ++k) {
-    const uint32_t c = cnt[k];
-    if (c != 0 && c < kSmall) {
-      a.smalls[spos++] = make_uint2(lo[k], (q[k] << kSmallCntBits) | c);
-    } else if (c >= kSmall) {
-      for (uint32_t off = 0; off < c; off += kChunk)
-        a.chunks[cpos++] = make_uint2(lo[k] + off, (q[k] << kChunkLenBits) | min(kChunk, c - off));
+  const uint32_t deg = t - s;
+  const bool hub = act && a.cutoff != 0 && deg >= a.cutoff;
+  if (act && !hub) {
+    if (deg <= kLinear) {
+      uint32_t c0, c1;
+      linear_count(a.g.key, s, t, lb, hik, c0, c1);
+      p0 = s + c0;
+      p1 = s + c1;
+    } else {
+      last = __ldg(a.g.key + t - 1);
+      p0 = lane_lower_bound(a.g.key, s, t, lb);
+      p1 = last < hik ? t : lane_lower_bound(a.g.key, p0, t, hik);
     }
   }
-  __syncthreads();  // s_ch / s_base are reused by the next step
+  if (hub) last = __ldg(a.g.key + t - 1);
+  uint32_t hubs = __ballot_sync(0xffffffffu, hub);
+  ix += hub ? 1 : 0;
+  while (hubs) {
+    const uint32_t src = __ffs(hubs) - 1;
+    hubs &= hubs - 1;
+    const uint32_t S = __shfl_sync(0xffffffffu, s, src), Tt = __shfl_sync(0xffffffffu, t, src);
+    const int32_t LB = __shfl_sync(0xffffffffu, lb, src), HK = __shfl_sync(0xffffffffu, hik, src);
+    const int32_t LAST = __shfl_sync(0xffffffffu, last, src);
+    const uint32_t P0 = index_lower_bound(a.g, S, Tt, LB);
+    const uint32_t P1 = LAST < HK ? Tt : index_lower_bound(a.g, P0, Tt, HK);
+    if (lane == src) {
+      p0 = P0;
+      p1 = P1;
+    }
+  }
+  const uint32_t cnt = act ? p1 - p0 : 0u;
+  work += cnt;
+  // short ranges: one small-list entry
+  list_append(eb.sm, cnt != 0 && cnt < kSmall, make_uint2(p0, (q << kSmallCntBits) | cnt),
+              &a.ctl->smalls, eb.sstart, a.smalls);
+  // long ranges: kChunk-edge chunks, appended by the whole warp
+  uint32_t bigs = __ballot_sync(0xffffffffu, cnt >= kSmall);
+  while (bigs) {
+    const uint32_t src = __ffs(bigs) - 1;
+    bigs &= bigs - 1;
+    const uint32_t B0 = __shfl_sync(0xffffffffu, p0, src), BC = __shfl_sync(0xffffffffu, cnt, src);
+    const uint32_t BQ = __shfl_sync(0xffffffffu, q, src);
+    const uint32_t nch = (BC + kChunk - 1) / kChunk;
+    for (uint32_t j0 = 0; j0 < nch; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t off = j * kChunk;
+      list_append(eb.ch, j < nch,
+                  make_uint2(B0 + off, (BQ << kChunkLenBits) | (j < nch ? min(kChunk, BC - off) : 0u)),
+                  &a.ctl->chunks, eb.cstart, a.chunks);
+    }
+  }
 }
 
 // Adds a block's relax-work count to the edges counter (one atomic per block).
@@ -425,57 +451,33 @@ __device__ __forceinline__ void flush_work(Control* ctl, unsigned long long work
   __syncthreads();
 }
 
-// Phase A over a sparse frontier queue (items [0, F) of fin).
-__device__ void phase_a_sparse(const TravArgs& a, const uint32_t* fin, uint32_t F,
-                               unsigned long long cstart, unsigned long long sstart,
-                               uint32_t bid, uint32_t nblk, uint64_t pol_keep,
-                               unsigned long long& ix) {
-  const uint32_t step = nblk * blockDim.x * kExpand;
+// Phase A over a sparse frontier queue (items [0, F) of fin) or, with
+// fin == nullptr, over the implicit dense frontier: every slot whose label
+// bound is below its expansion bound.
+__device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
+                        unsigned long long cstart, unsigned long long sstart, uint32_t bid,
+                        uint32_t nblk, uint64_t pol_keep, uint2* ebuf, unsigned long long& ix) {
+  const uint32_t lane = lane_id();
+  const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
+  const uint32_t nw = nblk * kWarps;
+  const uint32_t total = fin ? F : a.Q * a.n;
+  ExpandBufs eb{{ebuf, 0}, {ebuf + 64, 0}, cstart, sstart};
   unsigned long long work = 0;
-  for (uint32_t base = bid * blockDim.x * kExpand; base < F; base += step) {
-    uint32_t item[kExpand], lo[kExpand], cnt[kExpand], q[kExpand];
-    bool valid[kExpand];
-    int32_t x[kExpand], old[kExpand];
-#pragma unroll
-    for (int k = 0; k < kExpand; ++k) {
-      const uint32_t i = base + k * blockDim.x + threadIdx.x;
-      valid[k] = i < F;
-      item[k] = valid[k] ? __ldcg(fin + i) : 0u;
+  for (uint32_t base = gw * 32; base < total; base += nw * 32) {
+    const uint32_t i = base + lane;
+    bool valid = i < total;
+    uint32_t item = i;
+    int32_t x = kInf, old = kInf;
+    if (valid) {
+      if (fin) item = __ldcg(fin + i);
+      x = ld_state(a.X + item, pol_keep);
+      old = ld_state(a.Ex + item, pol_keep);
+      valid = x != kInf;
     }
-#pragma unroll
-    for (int k = 0; k < kExpand; ++k) {
-      x[k] = valid[k] ? ld_state(a.X + item[k], pol_keep) : kInf;
-      old[k] = valid[k] ? ld_state(a.Ex + item[k], pol_keep) : kInf;
-    }
-    expand_k(a, item, valid, x, old, lo, cnt, q, ix);
-    emit_k(a, lo, cnt, q, cstart, sstart, work);
+    expand_warp(a, valid, item, x, old, eb, work, ix);
   }
-  flush_work(a.ctl, work);
-}
-
-// Phase A over the implicit dense frontier: every slot whose label bound is
-// below its expansion bound.
-__device__ void phase_a_dense(const TravArgs& a, unsigned long long cstart,
-                              unsigned long long sstart, uint64_t pol_keep,
-                              unsigned long long& ix) {
-  const uint32_t slots = a.Q * a.n;
-  const uint32_t step = gridDim.x * blockDim.x * kExpand;
-  unsigned long long work = 0;
-  for (uint32_t base = blockIdx.x * blockDim.x * kExpand; base < slots; base += step) {
-    uint32_t item[kExpand], lo[kExpand], cnt[kExpand], q[kExpand];
-    bool valid[kExpand];
-    int32_t x[kExpand], old[kExpand];
-#pragma unroll
-    for (int k = 0; k < kExpand; ++k) {
-      item[k] = base + k * blockDim.x + threadIdx.x;
-      const bool in = item[k] < slots;
-      x[k] = in ? ld_state(a.X + item[k], pol_keep) : kInf;
-      old[k] = in ? ld_state(a.Ex + item[k], pol_keep) : kInf;
-      valid[k] = in && x[k] != kInf;
-    }
-    expand_k(a, item, valid, x, old, lo, cnt, q, ix);
-    emit_k(a, lo, cnt, q, cstart, sstart, work);
-  }
+  list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
+  list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
   flush_work(a.ctl, work);
 }
 
@@ -605,7 +607,8 @@ __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int s
 // st.pending set with the relax left to the grid.
 __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32_t xcnt,
                              int32_t depart, int32_t vhi0, uint64_t pol_stream,
-                             uint64_t pol_keep, uint32_t* wbuf, unsigned long long& ix) {
+                             uint64_t pol_keep, uint32_t* wbuf, uint2* ebuf,
+                             unsigned long long& ix) {
   __shared__ unsigned long long s_val[4];
   Control* ctl = a.ctl;
   bool seed = xcnt != 0;
@@ -636,7 +639,7 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
         trace_round(a, st.rounds, 3, F);
         trace_round(a, st.rounds, 7, 1);
       }
-      phase_a_sparse(a, fin, F, st.c_cur, st.s_cur, 0, 1, pol_keep, ix);
+      phase_a(a, fin, F, st.c_cur, st.s_cur, 0, 1, pol_keep, ebuf, ix);
       __syncthreads();
       if (threadIdx.x == 0) {
         s_val[1] = __ldcg(&ctl->chunks);
@@ -672,8 +675,10 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
 
 __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
+  __shared__ uint2 s_ebuf[kWarps][128];
   cg::grid_group grid = cg::this_grid();
   uint32_t* wbuf = s_buf[threadIdx.x >> 5];
+  uint2* ebuf = s_ebuf[threadIdx.x >> 5];
   Control* ctl = a.ctl;
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
@@ -719,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
         // starts moving them
         grid.sync();
         if (blockIdx.x == 0) {
-          local_rounds(a, st, xlo, xcnt, depart, vhi0, pol_stream, pol_keep, wbuf, ix);
+          local_rounds(a, st, xlo, xcnt, depart, vhi0, pol_stream, pol_keep, wbuf, ebuf, ix);
           if (threadIdx.x == 0) save_state(ctl, st);
         }
         xcnt = 0;
@@ -755,9 +760,8 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
       }
       unsigned long long c_end = st.c_cur, s_end = st.s_cur, e_end = st.e_cur;
       if (!xcnt) {
-        if (st.dense) phase_a_dense(a, st.c_cur, st.s_cur, pol_keep, ix);
-        else phase_a_sparse(a, fin, (uint32_t)F, st.c_cur, st.s_cur, blockIdx.x, gridDim.x,
-                            pol_keep, ix);
+        phase_a(a, st.dense ? nullptr : fin, (uint32_t)F, st.c_cur, st.s_cur, blockIdx.x,
+                gridDim.x, pol_keep, ebuf, ix);
         grid.sync();
         c_end = __ldcg(&ctl->chunks);
         s_end = __ldcg(&ctl->smalls);
