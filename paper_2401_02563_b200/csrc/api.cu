@@ -424,11 +424,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.cand_lo = w.cand_lo.as<uint32_t>();
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
-  a.trace = w.trace_cap ? w.trace.as<unsigned long long>() : nullptr;
+  a.trace = w.trace_dev;
   a.trace_cap = w.trace_cap;
   a.round_limit = (uint32_t)std::min<uint64_t>(
       0xfffffff0ULL, ((uint64_t)ncand + 1) * ((uint64_t)slots + 2) + 16);
-  if (a.trace) TGXD_CUDA(cudaMemsetAsync(w.trace.p, 0, w.trace_cap * 64ull, s));
+  if (w.trace_host) {
+    TGXD_CUDA(cudaStreamSynchronize(s));
+    std::memset(w.trace_host, 0, w.trace_cap * 64ull);
+  }
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
     void* args[] = {&a};
@@ -791,6 +794,7 @@ void tgxd_graph_destroy(tgxd_graph* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& e : g->ws.ev)
     if (e) cudaEventDestroy(e);
+  if (g->ws.trace_host) cudaFreeHost(g->ws.trace_host);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -948,24 +952,37 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
   return TGXD_OK;
 }
 
+// The trace lives in mapped pinned host memory: the device writes it
+// directly, so it stays readable even while a traversal is still running.
 int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds) {
   if (!g) return fail(TGXD_ERR_ARGUMENT, "null graph");
   std::lock_guard<std::mutex> lock(g->mu);
   TGXD_CUDA(cudaSetDevice(g->device));
-  if (max_rounds && !dalloc<unsigned long long>(g->ws.trace, max_rounds * 8ull))
-    return fail(TGXD_ERR_CUDA, "allocation (trace)");
-  g->ws.trace_cap = max_rounds;
+  if (g->ws.trace_host) {
+    cudaFreeHost(g->ws.trace_host);
+    g->ws.trace_host = nullptr;
+  }
+  g->ws.trace_cap = 0;
+  g->ws.trace_dev = nullptr;
+  if (max_rounds) {
+    void* h = nullptr;
+    TGXD_CUDA(cudaHostAlloc(&h, max_rounds * 64ull, cudaHostAllocMapped));
+    std::memset(h, 0, max_rounds * 64ull);
+    void* d = nullptr;
+    TGXD_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    g->ws.trace_host = static_cast<unsigned long long*>(h);
+    g->ws.trace_dev = static_cast<unsigned long long*>(d);
+    g->ws.trace_cap = max_rounds;
+  }
   return TGXD_OK;
 }
 
+// No lock and no CUDA call: safe to use while a query is in flight.
 int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds) {
   if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
-  std::lock_guard<std::mutex> lock(g->mu);
   const uint32_t r = std::min(max_rounds, g->ws.trace_cap);
-  if (r) {
-    TGXD_CUDA(cudaMemcpyAsync(out, g->ws.trace.p, r * 64ull, cudaMemcpyDeviceToHost, g->stream));
-    TGXD_CUDA(cudaStreamSynchronize(g->stream));
-  }
+  volatile unsigned long long* src = g->ws.trace_host;
+  for (uint64_t i = 0; i < r * 8ull; ++i) out[i] = src[i];
   return TGXD_OK;
 }
 

@@ -63,7 +63,9 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
   DeviceBuffer X, Ex, R, fa, fb, chunks, smalls, ctl, params, seeds;
-  DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out, trace;
+  DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
+  unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
+  unsigned long long* trace_dev = nullptr;
   uint32_t trace_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // what the last query left in X (for tgxd_last_work)

@@ -599,7 +599,11 @@ __device__ __forceinline__ void load_state(const Control* ctl, TState& s) {
 
 __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int slot,
                                             unsigned long long v) {
-  if (a.trace && r < a.trace_cap) a.trace[r * 8 + slot] = v;
+  if (a.trace && r < a.trace_cap) {
+    volatile unsigned long long* t = a.trace;
+    t[r * 8 + slot] = v;
+    __threadfence_system();
+  }
 }
 
 // Rounds with a tiny frontier on one CTA (block 0). Returns with st updated
