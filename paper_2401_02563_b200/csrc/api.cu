@@ -424,6 +424,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.cand_lo = w.cand_lo.as<uint32_t>();
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
+  a.init_pushes = fast ? 0ull : P.Q;
   a.trace = w.trace_dev;
   a.trace_cap = w.trace_cap;
   a.round_limit = (uint32_t)std::min<uint64_t>(

@@ -90,7 +90,7 @@ struct Control {
   unsigned int candidates;
   unsigned int error;               // watchdog tripped
   unsigned int pad;
-  unsigned long long state[8];      // CTA-local rounds hand their state over here
+  unsigned long long state[12];     // CTA-local rounds hand their state over here
 };
 
 }  // namespace tgxd

@@ -81,6 +81,7 @@ struct TravArgs {
   unsigned long long* trace;
   uint32_t trace_cap;
   uint32_t round_limit;  // watchdog: a correct traversal never gets near it
+  unsigned long long init_pushes;  // queue position / improvements after seeding
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -573,15 +574,22 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
 }
 
 // Traversal state; identical in every block at every grid barrier.
+//
+// Counter discipline. The shared counters (pushes, improved, chunks,
+// smalls, edges) are only read immediately after a barrier, into the
+// "known" fields below, and every phase that moves a counter is separated
+// from those reads by at least one more barrier. So every block derives the
+// same round boundaries and the same control flow.
 struct TState {
   unsigned long long prev_p;   // queue position where fin's items start
   unsigned long long prev_i;   // improvement counter at the start of the last relax
-  unsigned long long c_cur, s_cur, e_cur;
-  unsigned long long p_now;    // (pending) queue position for its pushes
+  unsigned long long p_known;  // pushes counter as of the last barrier
+  unsigned long long i_known;  // improved counter as of the last barrier
+  unsigned long long c_cur, s_cur, e_cur;  // emission counters as of the last barrier
   uint32_t rounds;
   uint32_t flip;               // fin/fout parity
   int dense;                   // the next expand scans densely
-  int pending;                 // expand done, relax of [c_cur..c_end) pending
+  int pending;                 // CTA expand done, grid relax of its work pending
 };
 
 __device__ __forceinline__ void save_state(Control* ctl, const TState& s) {
@@ -606,26 +614,32 @@ __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int s
   }
 }
 
-// Rounds with a tiny frontier on one CTA (block 0). Returns with st updated
-// and, if the expand produced more edge work than one CTA should relax,
-// st.pending set with the relax left to the grid.
+// Reads one counter into every thread of the block (block 0 local rounds).
+__device__ __forceinline__ unsigned long long block_read(const unsigned long long* p) {
+  __shared__ unsigned long long s_v;
+  __syncthreads();
+  if (threadIdx.x == 0) s_v = __ldcg(p);
+  __syncthreads();
+  return s_v;
+}
+
+// Rounds with a tiny frontier on one CTA (block 0; it is the only block
+// moving counters meanwhile). Returns with st updated and, if an expand
+// produced more edge work than one CTA should relax, st.pending set with the
+// relax left to the grid.
 __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32_t xcnt,
                              int32_t depart, int32_t vhi0, uint64_t pol_stream,
                              uint64_t pol_keep, uint32_t* wbuf, uint2* ebuf,
                              unsigned long long& ix) {
-  __shared__ unsigned long long s_val[4];
   Control* ctl = a.ctl;
   bool seed = xcnt != 0;
+  const bool tr = threadIdx.x == 0;
   for (;;) {
     if (st.rounds > a.round_limit) return;
-    __syncthreads();
-    if (threadIdx.x == 0) s_val[0] = __ldcg(&ctl->pushes);
-    __syncthreads();
-    const unsigned long long p_now = s_val[0];
+    const unsigned long long p_now = st.p_known;
     uint32_t* fin = st.flip ? a.fb : a.fa;
     uint32_t* fout = st.flip ? a.fa : a.fb;
     RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
-    const bool tr = threadIdx.x == 0;
     if (seed) {
       if (tr) {
         trace_round(a, st.rounds, 0, gtimer());
@@ -633,7 +647,6 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
         trace_round(a, st.rounds, 7, 1);
       }
       phase_b(a, 0, 0, xlo, xcnt, rx, 0, 1, wbuf);
-      if (tr) trace_round(a, st.rounds, 2, gtimer());
       seed = false;
     } else {
       const uint32_t F = (uint32_t)(p_now - st.prev_p);
@@ -644,14 +657,9 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
         trace_round(a, st.rounds, 7, 1);
       }
       phase_a(a, fin, F, st.c_cur, st.s_cur, 0, 1, pol_keep, ebuf, ix);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        s_val[1] = __ldcg(&ctl->chunks);
-        s_val[2] = __ldcg(&ctl->smalls);
-        s_val[3] = __ldcg(&ctl->edges);
-      }
-      __syncthreads();
-      const unsigned long long c_end = s_val[1], s_end = s_val[2], e_end = s_val[3];
+      const unsigned long long c_end = block_read(&ctl->chunks);
+      const unsigned long long s_end = block_read(&ctl->smalls);
+      const unsigned long long e_end = block_read(&ctl->edges);
       if (tr) {
         trace_round(a, st.rounds, 1, gtimer());
         trace_round(a, st.rounds, 4, c_end - st.c_cur);
@@ -659,17 +667,18 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
       }
       if (e_end - st.e_cur > kLocalMaxW) {  // hand the relax to the grid
         st.pending = 1;
-        st.p_now = p_now;
         return;
       }
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, 0, 1, wbuf);
       st.c_cur = c_end;
       st.s_cur = s_end;
       st.e_cur = e_end;
-      if (tr) trace_round(a, st.rounds, 2, gtimer());
     }
-    __syncthreads();
-    if (tr) trace_round(a, st.rounds, 6, __ldcg(&ctl->pushes) - p_now);
+    st.p_known = block_read(&ctl->pushes);
+    if (tr) {
+      trace_round(a, st.rounds, 2, gtimer());
+      trace_round(a, st.rounds, 6, st.p_known - p_now);
+    }
     st.prev_p = p_now;
     st.flip ^= 1u;
     st.dense = 0;
@@ -687,16 +696,14 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
   const int32_t vhi0 = a.qp[0].vhi;
+  const bool tr = blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long ix = 0;
-  // Counter discipline: `pushes` / `improved` only grow in relax and are read
-  // in expand; `chunks` / `smalls` / `edges` only grow in expand and are read
-  // in relax. A counter is never read while another block may move it, so
-  // every block derives the same round boundaries.
   TState st;
   st.prev_p = 0;
   st.prev_i = 0;
+  st.p_known = a.init_pushes;
+  st.i_known = a.init_pushes;
   st.c_cur = st.s_cur = st.e_cur = 0;
-  st.p_now = 0;
   st.rounds = 0;
   st.flip = 0;
   st.dense = a.mode == TGXD_MODE_DENSE;
@@ -706,6 +713,9 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
     uint32_t xlo = 0, xcnt = 0;
     if (a.fastest) {
       if (cand >= a.n_cand) break;
+      // the previous candidate's last post-barrier reads end before this
+      // candidate's seeds move the counters
+      if (cand) grid.sync();
       // Seed round (path_algorithms.cpp:476-486): the candidate's first
       // edges, relaxed without an admissibility check.
       depart = a.cand_key[cand];
@@ -714,19 +724,16 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
     }
     for (;;) {
       if (st.rounds > a.round_limit) {  // identical in every block: all stop together
-        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->error = 1;
+        if (tr) ctl->error = 1;
         break;
       }
-      const unsigned long long p_now = __ldcg(&ctl->pushes);
-      const unsigned long long i_now = __ldcg(&ctl->improved);
-      const unsigned long long F = xcnt ? 0 : (st.dense ? i_now - st.prev_i : p_now - st.prev_p);
+      const unsigned long long F =
+          xcnt ? 0 : (st.dense ? st.i_known - st.prev_i : st.p_known - st.prev_p);
       if (!xcnt && F == 0) break;
       const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
                             (xcnt ? xcnt <= kLocalMaxW : F <= kLocalMaxF);
       if (go_local) {
-        // every block must have read this round's counters before block 0
-        // starts moving them
-        grid.sync();
+        grid.sync();  // post-barrier reads of every block end before block 0 moves counters
         if (blockIdx.x == 0) {
           local_rounds(a, st, xlo, xcnt, depart, vhi0, pol_stream, pol_keep, wbuf, ebuf, ix);
           if (threadIdx.x == 0) save_state(ctl, st);
@@ -737,24 +744,30 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
         if (!st.pending) continue;
         // the grid relaxes what the CTA expanded
         const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
+        const unsigned long long e_end = __ldcg(&ctl->edges);
+        const unsigned long long p_now = st.p_known;
         uint32_t* fout = st.flip ? a.fa : a.fb;
-        RelaxCtx rx{vhi0, depart, true, st.p_now, fout, pol_stream, pol_keep, 0};
+        RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
         phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
+        grid.sync();
+        st.p_known = __ldcg(&ctl->pushes);
+        st.i_known = __ldcg(&ctl->improved);
         st.c_cur = c_end;
         st.s_cur = s_end;
-        st.e_cur = __ldcg(&ctl->edges);
-        st.prev_p = st.p_now;
+        st.e_cur = e_end;
+        st.prev_p = p_now;
         st.pending = 0;
         st.flip ^= 1u;
-        grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (tr) {
           trace_round(a, st.rounds, 2, gtimer());
-          trace_round(a, st.rounds, 6, __ldcg(&ctl->pushes) - st.prev_p);
+          trace_round(a, st.rounds, 6, st.p_known - p_now);
         }
         ++st.rounds;
+        st.dense = a.mode == TGXD_MODE_AUTO && st.p_known - p_now > a.dense_f;
+        if (st.dense) st.prev_i = st.i_known - (st.p_known - p_now);
         continue;
       }
-      const bool tr = blockIdx.x == 0 && threadIdx.x == 0;
+      const unsigned long long p_now = st.p_known, i_now = st.i_known;
       uint32_t* fin = st.flip ? a.fb : a.fa;
       uint32_t* fout = st.flip ? a.fa : a.fb;
       if (tr) {
@@ -787,17 +800,19 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
         for (int o = 16; o > 0; o >>= 1) imp += __shfl_xor_sync(0xffffffffu, imp, o);
         if (lane_id() == 0 && imp) atomicAdd(&ctl->improved, (unsigned long long)imp);
       }
+      grid.sync();
+      st.p_known = __ldcg(&ctl->pushes);
+      st.i_known = __ldcg(&ctl->improved);
       st.c_cur = c_end;
       st.s_cur = s_end;
       st.e_cur = e_end;
       st.prev_p = p_now;
       st.prev_i = i_now;
       xcnt = 0;
-      grid.sync();
-      const unsigned long long pushed = __ldcg(&ctl->pushes) - p_now;
+      const unsigned long long pushed = st.p_known - p_now;
       if (tr) {
         trace_round(a, st.rounds, 2, gtimer());
-        trace_round(a, st.rounds, 6, push ? pushed : __ldcg(&ctl->improved) - i_now);
+        trace_round(a, st.rounds, 6, push ? pushed : st.i_known - i_now);
       }
       ++st.rounds;
       if (push) st.flip ^= 1u;
@@ -807,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
         st.dense = 1;
       } else {
         st.dense = a.mode == TGXD_MODE_AUTO && pushed > a.dense_f;
-        if (st.dense) st.prev_i = __ldcg(&ctl->improved) - pushed;
+        if (st.dense) st.prev_i = st.i_known - pushed;
       }
     }
     if (!a.fastest || st.rounds > a.round_limit) break;
@@ -815,7 +830,7 @@ __global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ix += __shfl_xor_sync(0xffffffffu, ix, o);
   if (lane_id() == 0 && ix) atomicAdd(&ctl->index_lookups, ix);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (tr) {
     ctl->rounds = st.rounds;
     ctl->expansions = __ldcg(&ctl->chunks) + __ldcg(&ctl->smalls);
     ctl->candidates = a.fastest ? a.n_cand : 0;
