@@ -179,9 +179,13 @@ def load_library() -> ctypes.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
+    import os
     from . import _build
     path = _build.LIB
-    if _build.needs_build():
+    override = os.environ.get("TGXD_LIB")  # variant builds for A/B measurements
+    if override:
+        path = Path(override)
+    elif _build.needs_build():
         try:
             _build.build()
         except Exception as e:  # no nvcc on the box: use what travelled, if anything

@@ -43,14 +43,23 @@ namespace cg = cooperative_groups;
 
 namespace tgxd {
 
+#ifndef TGXD_UNROLL
+#define TGXD_UNROLL 4
+#endif
+#ifndef TGXD_MIN_BLOCKS
+#define TGXD_MIN_BLOCKS 3
+#endif
+#ifndef TGXD_LOCAL_F
+#define TGXD_LOCAL_F 128
+#endif
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;                       // 32-edge steps in flight per warp
+constexpr int kUnroll = TGXD_UNROLL;             // 32-edge steps in flight per warp
 constexpr uint32_t kChunk = 32u * kUnroll;       // edges per chunk of a big range
 constexpr uint32_t kSmall = 32;                  // ranges below this go to the small list
-constexpr uint32_t kChunkLenBits = 9;            // kChunk <= 256
+constexpr uint32_t kChunkLenBits = 10;           // kChunk <= 512
 constexpr uint32_t kSmallCntBits = 6;
-constexpr uint32_t kLocalMaxF = 1024;            // frontier that one CTA expands
+constexpr uint32_t kLocalMaxF = TGXD_LOCAL_F;    // frontier that one CTA expands
 constexpr uint32_t kLocalMaxW = 4096;            // edge work that one CTA relaxes
 
 struct TravArgs {
@@ -686,7 +695,7 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) traverse_kernel(TravArgs a) {
+__global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
   __shared__ uint2 s_ebuf[kWarps][128];
   cg::grid_group grid = cg::this_grid();
