@@ -98,6 +98,22 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def max_over_ranks(values, dist=None, device="cpu"):
+    """Element-wise max over ranks (the contract's max-over-ranks timing)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(v) for v in values]
+    import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
+def whole_job_teps(world, e_adm_per_rank, ms_per_step):
+    """Replicas: every rank traverses its own copy; value = all ranks' edges
+    over the slowest rank's step time."""
+    return world * e_adm_per_rank / (ms_per_step * 1e-3)
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -224,12 +240,8 @@ def run_ours(args):
         total_ms, kernel_ms = T.time_queries(g, q.kind, [q.vertex], [q.window],
                                              warmup=args.warmup, steps=args.steps)
     barrier()
-    ms_step = total_ms / args.steps
-    if dist:
-        t = torch.tensor([ms_step, kernel_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, kernel_ms = float(t[0]), float(t[1])
-    value = world * e_adm / (ms_step * 1e-3)
+    ms_step, kernel_ms = max_over_ranks([total_ms / args.steps, kernel_ms], dist, "cuda")
+    value = whole_job_teps(world, e_adm, ms_step)
 
     # end to end through the reference-facing C-ABI call with a host output
     # (int64 PathResult values): H2D of the query, D2H of the labels per step
@@ -246,12 +258,8 @@ def run_ours(args):
                                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                            None))
     barrier()
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
-    e2e_value = world * e_adm / e2e_s
+    e2e_s = max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, "cuda")[0]
+    e2e_value = whole_job_teps(world, e_adm, e2e_s * 1e3)
 
     peak, peak_kind = measured_peak()
     b_alg = 16 * e_adm + 12 * v_reached + 4 * n

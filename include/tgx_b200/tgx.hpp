@@ -1,0 +1,175 @@
+// tgx_b200 — C++ drop-in for the reference's traversal entry points.
+//
+// Header-only shim over the C-ABI (include/tgxd.h, libtgxd.so). It keeps the
+// reference signatures and semantics (/root/reference/proj/include/tgx/):
+//   TemporalGraph::build(edges, n_v, directed, config)   engine.hpp:32-33
+//   earliest_arrival / latest_departure / fastest_path    algorithms.hpp:46-58
+//   PathResult (int64 values, INT64_MAX / INT64_MIN)       algorithms.hpp:16-21
+//   digest_of                                             digest.hpp:42-52
+// and re-throws the reference's exception types: std::out_of_range for a bad
+// vertex or edge, std::invalid_argument for a bad window. Ordering::Overlaps
+// and times outside [0, 2^31 - 2] raise std::domain_error (the device path
+// does not cover them; there is no CPU fallback). force_access is accepted
+// and ignored: results are access-invariant (test_algorithms.cpp:196-217).
+//
+// A user of the reference switches by replacing `#include "tgx/..."` and
+// `tgx::` with this header and `tgx_b200::`, and linking libtgxd.so.
+#pragma once
+
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../tgxd.h"
+
+namespace tgx_b200 {
+
+using Timestamp = std::uint64_t;
+using VertexId = std::uint32_t;
+using EdgeId = std::uint64_t;
+inline constexpr Timestamp kMaxTimestamp = std::numeric_limits<Timestamp>::max();
+
+struct TemporalEdge {
+  VertexId source = 0;
+  VertexId destination = 0;
+  Timestamp start = 0;
+  Timestamp end = 0;
+  double weight = 1.0;
+};
+
+struct QueryWindow {
+  Timestamp t_a = 0;
+  Timestamp t_b = kMaxTimestamp;
+  bool valid() const { return t_a <= t_b; }
+};
+
+enum class Ordering { Succeeds, StrictlySucceeds, Overlaps };
+enum class ForceAccess { Auto, Index, Scan };
+enum class Direction { Out, In };
+
+struct EngineConfig {
+  EdgeId index_cutoff = 2048;
+  Ordering ordering = Ordering::StrictlySucceeds;
+  ForceAccess force_access = ForceAccess::Auto;
+};
+
+struct EdgeMapStats {
+  std::uint64_t index_decisions = 0;
+  std::uint64_t scan_decisions = 0;
+};
+
+struct AlgoOptions {
+  std::optional<Ordering> ordering;
+  std::optional<ForceAccess> force_access;
+  EdgeMapStats* stats = nullptr;
+};
+
+struct PathResult {
+  static constexpr std::int64_t kUnreachedMin = std::numeric_limits<std::int64_t>::max();
+  static constexpr std::int64_t kUnreachedMax = std::numeric_limits<std::int64_t>::min();
+  std::vector<std::int64_t> values;
+};
+
+namespace detail {
+[[noreturn]] inline void raise(int code) {
+  const std::string msg = tgxd_last_error();
+  switch (code) {
+    case TGXD_ERR_VERTEX_RANGE:
+    case TGXD_ERR_EDGE:
+      throw std::out_of_range(msg);
+    case TGXD_ERR_WINDOW:
+      throw std::invalid_argument(msg);
+    case TGXD_ERR_TIME_RANGE:
+    case TGXD_ERR_UNSUPPORTED:
+      throw std::domain_error(msg);
+    default:
+      throw std::runtime_error(msg);
+  }
+}
+inline void check(int code) {
+  if (code != TGXD_OK) raise(code);
+}
+}  // namespace detail
+
+// Device-resident graph: both T-CSR layouts plus the selective index. Cheap
+// to copy (shared handle); immutable after build.
+class TemporalGraph {
+ public:
+  static TemporalGraph build(std::vector<TemporalEdge> edges, VertexId n_v, bool directed,
+                             const EngineConfig& config = {}) {
+    if (config.index_cutoff < 1) throw std::invalid_argument("index cutoff must be >= 1");
+    const std::size_t m = edges.size();
+    std::vector<std::uint32_t> s(m), d(m);
+    std::vector<std::uint64_t> a(m), b(m);
+    for (std::size_t i = 0; i < m; ++i) {
+      s[i] = edges[i].source;
+      d[i] = edges[i].destination;
+      a[i] = edges[i].start;
+      b[i] = edges[i].end;
+    }
+    tgxd_graph* h = nullptr;
+    detail::check(tgxd_graph_build(n_v, m, s.data(), d.data(), a.data(), b.data(),
+                                   directed ? 1 : 0, config.index_cutoff, &h));
+    TemporalGraph g;
+    g.h_ = std::shared_ptr<tgxd_graph>(h, tgxd_graph_destroy);
+    g.config_ = config;
+    g.n_ = n_v;
+    return g;
+  }
+
+  VertexId vertex_count() const { return n_; }
+  const EngineConfig& config() const { return config_; }
+  Ordering ordering() const { return config_.ordering; }
+  tgxd_graph* handle() const { return h_.get(); }
+
+ private:
+  std::shared_ptr<tgxd_graph> h_;
+  EngineConfig config_;
+  VertexId n_ = 0;
+};
+
+namespace detail {
+inline PathResult run(int kind, const TemporalGraph& g, VertexId v, const QueryWindow& w,
+                      const AlgoOptions& opts) {
+  const Ordering ord = opts.ordering.value_or(g.ordering());
+  PathResult r;
+  r.values.resize(g.vertex_count());
+  tgxd_stats st{};
+  const std::uint64_t ta = w.t_a, tb = w.t_b;
+  check(tgxd_query(g.handle(), kind, 1, &v, &ta, &tb, static_cast<int>(ord), TGXD_MODE_AUTO,
+                   r.values.data(), 8, 0, &st));
+  if (opts.stats) {
+    opts.stats->index_decisions += st.index_lookups;
+    opts.stats->scan_decisions += st.expansions - st.index_lookups;
+  }
+  return r;
+}
+}  // namespace detail
+
+inline PathResult earliest_arrival(const TemporalGraph& g, VertexId source, const QueryWindow& w,
+                                   const AlgoOptions& opts = {}) {
+  return detail::run(TGXD_EARLIEST_ARRIVAL, g, source, w, opts);
+}
+
+inline PathResult latest_departure(const TemporalGraph& g, VertexId target, const QueryWindow& w,
+                                   const AlgoOptions& opts = {}) {
+  return detail::run(TGXD_LATEST_DEPARTURE, g, target, w, opts);
+}
+
+inline PathResult fastest_path(const TemporalGraph& g, VertexId source, const QueryWindow& w,
+                               const AlgoOptions& opts = {}) {
+  return detail::run(TGXD_FASTEST, g, source, w, opts);
+}
+
+template <class T>
+std::uint64_t digest_of(const std::vector<T>& values) {
+  static_assert(sizeof(T) == 8, "labels are int64");
+  return tgxd_digest(reinterpret_cast<const std::int64_t*>(values.data()), values.size());
+}
+
+}  // namespace tgx_b200

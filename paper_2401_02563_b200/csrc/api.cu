@@ -417,8 +417,11 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.strict = P.strict;
   a.cutoff = (uint32_t)std::min<uint64_t>(G->index_cutoff, 0xffffffffULL);
   a.mode = mode;
-  a.dense_f = std::max<uint64_t>(1024, slots / 64);
-  a.push_w = std::max<uint64_t>(4096, slots / 8);
+  // AUTO: push every round unless a round relaxes more edges than 4x the
+  // slot count; expand densely only when the queue holds half the slots
+  // (measured on config 2: the queue-driven expand is cheaper below that).
+  a.dense_f = std::max<uint64_t>(1024, slots / 2);
+  a.push_w = std::max<uint64_t>(4096, slots * 4);
   a.fastest = fast ? 1 : 0;
   a.n_cand = ncand;
   a.cand_lo = w.cand_lo.as<uint32_t>();

@@ -1,0 +1,93 @@
+// The reference's hand-computed path cases (test_algorithms.cpp:51-122),
+// written against the drop-in C++ shim exactly as a reference user would.
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "tgx_b200/tgx.hpp"
+
+using namespace tgx_b200;
+
+static int failures = 0;
+#define CHECK(c)                                                   \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c);      \
+      ++failures;                                                  \
+    }                                                              \
+  } while (0)
+
+constexpr std::int64_t kInf = PathResult::kUnreachedMin;
+constexpr std::int64_t kNegInf = PathResult::kUnreachedMax;
+
+int main() {
+  {  // earliest arrival: no edges
+    const auto g = TemporalGraph::build({}, 4, true);
+    const auto r = earliest_arrival(g, 1, QueryWindow{5, 50});
+    CHECK(r.values[1] == 5);
+    CHECK(r.values[0] == kInf && r.values[2] == kInf && r.values[3] == kInf);
+  }
+  {  // single contained edge arrives at its end
+    const auto g = TemporalGraph::build({{0, 1, 3, 5, 1.0}}, 2, true);
+    CHECK(earliest_arrival(g, 0, QueryWindow{0, 10}).values[1] == 5);
+  }
+  {  // strict ordering rejects an equal handoff, weak accepts it
+    const auto g = TemporalGraph::build({{0, 1, 1, 3, 1.0}, {1, 2, 3, 4, 1.0}}, 3, true);
+    AlgoOptions strict, weak;
+    strict.ordering = Ordering::StrictlySucceeds;
+    weak.ordering = Ordering::Succeeds;
+    CHECK(earliest_arrival(g, 0, QueryWindow{}, strict).values[2] == kInf);
+    CHECK(earliest_arrival(g, 0, QueryWindow{}, weak).values[2] == 4);
+  }
+  {  // source out of range
+    const auto g = TemporalGraph::build({}, 2, true);
+    bool thrown = false;
+    try {
+      earliest_arrival(g, 5, QueryWindow{});
+    } catch (const std::out_of_range&) {
+      thrown = true;
+    }
+    CHECK(thrown);
+  }
+  {  // window with t_a > t_b
+    const auto g = TemporalGraph::build({}, 2, true);
+    bool thrown = false;
+    try {
+      earliest_arrival(g, 0, QueryWindow{9, 3});
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    CHECK(thrown);
+  }
+  {  // latest departure
+    const auto g0 = TemporalGraph::build({}, 3, true);
+    const auto r0 = latest_departure(g0, 1, QueryWindow{2, 9});
+    CHECK(r0.values[1] == 9);
+    CHECK(r0.values[0] == kNegInf);
+    const auto g = TemporalGraph::build({{0, 1, 3, 5, 1.0}}, 2, true);
+    CHECK(latest_departure(g, 1, QueryWindow{0, 10}).values[0] == 3);
+  }
+  {  // fastest: two-hop beats the direct edge
+    const auto g =
+        TemporalGraph::build({{0, 1, 2, 6, 1.0}, {0, 2, 3, 4, 1.0}, {2, 1, 4, 5, 1.0}}, 3, true);
+    AlgoOptions weak;
+    weak.ordering = Ordering::Succeeds;
+    CHECK(fastest_path(g, 0, QueryWindow{}, weak).values[1] == 2);
+    const auto g0 = TemporalGraph::build({}, 3, true);
+    const auto r = fastest_path(g0, 2, QueryWindow{});
+    CHECK(r.values[2] == 0);
+    CHECK(r.values[0] == kInf);
+  }
+  {  // edge validation (types.cpp:41-54)
+    bool thrown = false;
+    try {
+      TemporalGraph::build({{0, 7, 1, 2, 1.0}}, 2, true);
+    } catch (const std::out_of_range&) {
+      thrown = true;
+    }
+    CHECK(thrown);
+  }
+  if (failures) return 1;
+  std::printf("shim ok\n");
+  return 0;
+}

@@ -1,0 +1,156 @@
+"""Generate the golden fixtures from the REFERENCE itself.
+
+Runs the unmodified reference library (oracle/_ref/libtgxref.so, compiled
+from /root/reference/proj/src by oracle/Makefile) and the reference's own
+brute-force oracle (tests/support/oracle.cpp) on seeded inputs, and stores
+inputs + outputs as compressed npz files next to this script:
+
+  small_random.npz  300 random small instances (shape of random_instance(rng,
+                    9..12, 28..40), test_algorithms.cpp:171-194) x
+                    {EA, LD, fastest} x {Succeeds, StrictlySucceeds}, checked
+                    against enumerate_paths as well
+  hand_cases.npz    the hand-computed cases of test_algorithms.cpp:51-122
+  rmat12.npz        RMAT scale 12 (config-2 distributions) with 12 queries,
+                    full int64 label vectors + FNV-1a digests
+  uniform14.npz     uniform n=2^14, m=2^18 (config-1 distributions), 6 queries
+
+Only this script touches the reference; tests read the npz files. Re-run
+with:  python tests/golden/make_golden.py
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+from oracle.pyoracle import Reference  # noqa: E402
+
+HERE = Path(__file__).resolve().parent
+KINDS = ["earliest_arrival", "latest_departure", "fastest"]
+
+
+def small_random():
+    rng = np.random.default_rng(20240105)
+    rows = {k: [] for k in ["n", "eoff", "src", "dst", "start", "end", "vertex", "ta", "tb",
+                            "kind", "ordering", "labels", "loff"]}
+    eoff = [0]
+    loff = [0]
+    src, dst, st, en, labels = [], [], [], [], []
+    meta = []
+    for it in range(300):
+        n = int(rng.integers(1, 13))
+        m = int(rng.integers(0, 41))
+        s = rng.integers(0, n, m)
+        d = rng.integers(0, n, m)
+        a = rng.integers(0, 61, m)
+        b = a + rng.integers(0, 9, m)
+        E = (s, d, a, b)
+        ref = Reference(E, n)
+        ta, tb = sorted(int(x) for x in rng.integers(0, 76, 2))
+        v = int(rng.integers(0, n))
+        for ki, kind in enumerate(KINDS):
+            for ordv in (0, 1):
+                out = ref.query(kind, v, ta, tb, ordv)
+                brute = Reference.enumerate(E, n, kind, v, ta, tb, ordv)
+                assert np.array_equal(out, brute), (it, kind, ordv)
+                meta.append((it, n, v, ta, tb, ki, ordv, loff[-1]))
+                labels.append(out)
+                loff.append(loff[-1] + n)
+        ref.close()
+        src.append(s); dst.append(d); st.append(a); en.append(b)
+        eoff.append(eoff[-1] + m)
+    np.savez_compressed(
+        HERE / "small_random.npz",
+        eoff=np.array(eoff, np.int64), src=np.concatenate(src).astype(np.uint32),
+        dst=np.concatenate(dst).astype(np.uint32), start=np.concatenate(st).astype(np.uint64),
+        end=np.concatenate(en).astype(np.uint64), meta=np.array(meta, np.int64),
+        labels=np.concatenate(labels).astype(np.int64))
+
+
+# test_algorithms.cpp:51-122 (inputs, query, expected values of listed vertices)
+HAND = [
+    # (name, n, edges, kind, vertex, ta, tb, ordering, {vertex: expected})
+    ("ea_no_edges", 4, [], "earliest_arrival", 1, 5, 50, 1, None),
+    ("ea_single_edge", 2, [(0, 1, 3, 5)], "earliest_arrival", 0, 0, 10, 1, None),
+    ("ea_strict_rejects_equal_handoff", 3, [(0, 1, 1, 3), (1, 2, 3, 4)], "earliest_arrival", 0,
+     0, (1 << 64) - 1, 1, None),
+    ("ea_weak_accepts_equal_handoff", 3, [(0, 1, 1, 3), (1, 2, 3, 4)], "earliest_arrival", 0,
+     0, (1 << 64) - 1, 0, None),
+    ("ld_no_edges", 3, [], "latest_departure", 1, 2, 9, 1, None),
+    ("ld_single_edge", 2, [(0, 1, 3, 5)], "latest_departure", 1, 0, 10, 1, None),
+    ("fastest_two_hop", 3, [(0, 1, 2, 6), (0, 2, 3, 4), (2, 1, 4, 5)], "fastest", 0, 0,
+     (1 << 64) - 1, 0, None),
+    ("fastest_no_edges", 3, [], "fastest", 2, 0, (1 << 64) - 1, 1, None),
+]
+
+
+def hand_cases():
+    out = {}
+    for name, n, edges, kind, v, ta, tb, ordv, _ in HAND:
+        e = np.array(edges, np.int64).reshape(-1, 4)
+        E = (e[:, 0], e[:, 1], e[:, 2], e[:, 3])
+        ref = Reference(E, n)
+        out[name] = ref.query(kind, v, ta, tb, ordv)
+        ref.close()
+    np.savez_compressed(HERE / "hand_cases.npz", **out)
+
+
+def scaled(name, gen, queries):
+    import paper_2401_02563_b200 as T  # host generator only (no GPU needed)
+    E = T.generate_edges(gen)
+    n = gen.n_vertices
+    ref = Reference(E, n)
+    meta, labels, digests = [], [], []
+    for (kind, v, ta, tb) in queries:
+        out = ref.query(kind, v, ta, tb, 1)
+        meta.append((KINDS.index(kind), v, ta, tb))
+        labels.append(out)
+        digests.append(int(Reference.lib().tgxref_digest(out.ctypes.data_as(
+            __import__("ctypes").POINTER(__import__("ctypes").c_int64)), len(out))))
+    ref.close()
+    # the edge list itself is not stored: tests regenerate it from `gen`
+    # (host generator) and check it against edge_digest first
+    gen_fields = np.array([gen.kind, gen.scale, gen.n, gen.m, gen.start_dist, gen.t_range,
+                           gen.seed], np.uint64)
+    gen_probs = np.array([gen.a, gen.b, gen.c, gen.geo_p], np.float64)
+    np.savez_compressed(HERE / f"{name}.npz", gen_fields=gen_fields, gen_probs=gen_probs,
+                        edge_digest=np.array([edge_digest(E)], np.uint64), n=np.array([n]),
+                        m=np.array([len(E[0])]), meta=np.array(meta, np.int64),
+                        labels=np.array(labels, np.int64), digests=np.array(digests, np.uint64))
+
+
+def edge_digest(E):
+    """FNV-1a (digest.hpp:12-40) over the src|dst|start|end little-endian bytes:
+    pins the generator."""
+    import paper_2401_02563_b200 as T
+    buf = b"".join(np.ascontiguousarray(x).tobytes() for x in (
+        np.asarray(E[0], np.uint32), np.asarray(E[1], np.uint32), np.asarray(E[2], np.uint64),
+        np.asarray(E[3], np.uint64)))
+    return T.digest_of(np.frombuffer(buf, np.int64))
+
+
+def main():
+    import paper_2401_02563_b200 as T
+    small_random()
+    hand_cases()
+    g = T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 7, cube_root_starts=True)
+    E = T.generate_edges(g)
+    deg = np.bincount(E[0], minlength=g.n_vertices)
+    rng = np.random.default_rng(12)
+    srcs = [int(np.argmax(deg))] + [int(x) for x in rng.choice(np.flatnonzero(deg), 3)]
+    qs = []
+    for sidx, s in enumerate(srcs):
+        w = (0, 999_999) if sidx % 2 == 0 else (200_000, 800_000)
+        for kind in KINDS:
+            qs.append((kind, s, w[0], w[1]))
+    scaled("rmat12", g, qs)
+    g2 = T.GenConfig.uniform(1 << 14, 1 << 18, 1_000_000, 0.01, 3)
+    qs2 = [(k, 0, 0, 999_999) for k in KINDS] + [(k, 77, 100_000, 600_000) for k in KINDS]
+    scaled("uniform14", g2, qs2)
+    for p in sorted(HERE.glob("*.npz")):
+        print(p.name, p.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

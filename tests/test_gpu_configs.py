@@ -1,0 +1,101 @@
+"""GPU: the five BASELINE workloads. Reduced scales are checked label for
+label against the C oracle; the full-size configs 1 and 2 are checked
+bit-exactly too (the oracle finishes them in seconds); configs 3-5 at full
+size through size-independent properties (batch == single, mode
+invariance, window monotonicity, work accounting)."""
+import numpy as np
+import pytest
+
+import paper_2401_02563_b200 as T
+from oracle.pyoracle import Oracle
+from paper_2401_02563_b200.configs import NAMES, workload
+
+pytestmark = pytest.mark.gpu
+FN = {"earliest_arrival": T.earliest_arrival, "latest_departure": T.latest_departure,
+      "fastest": T.fastest_path}
+
+
+def setup(name, delta):
+    wl = workload(name, delta)
+    g = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
+    qs = wl.queries(g.degrees(T.Direction.OUT), g.degrees(T.Direction.IN), g.vertex_count())
+    return wl, g, qs
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_reduced_config_parity(name):
+    wl, g, qs = setup(name, -8)
+    E = T.generate_edges(wl.gen)
+    o = Oracle(E, wl.gen.n_vertices)
+    for q in qs:
+        got = FN[q.kind](g, q.vertex, q.window).values
+        want = o.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+        assert np.array_equal(got, want), (name, q)
+    # the same queries as one batched traversal
+    for kind in {q.kind for q in qs}:
+        sub = [q for q in qs if q.kind == kind]
+        out = T.query_batch(g, kind, [q.vertex for q in sub], [q.window for q in sub])
+        for i, q in enumerate(sub):
+            assert np.array_equal(out[i], o.query(kind, q.vertex, q.window.t_a, q.window.t_b))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_full_config_bit_exact(name):
+    wl, g, qs = setup(name, 0)
+    q = qs[0]
+    got = FN[q.kind](g, q.vertex, q.window).values
+    E = T.generate_edges(wl.gen)
+    o = Oracle(E, wl.gen.n_vertices)
+    want = o.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+    assert np.array_equal(got, want)
+    assert T.last_work(g, 0) == o.work(q.kind, q.vertex, q.window.t_a, q.window.t_b, want)
+
+
+@pytest.mark.slow
+def test_full_c3_batch_equals_single_and_modes():
+    wl, g, qs = setup("c3", 0)
+    for kind in ("earliest_arrival", "latest_departure"):
+        sub = [q for q in qs if q.kind == kind]
+        batch = T.query_batch(g, kind, [q.vertex for q in sub], [q.window for q in sub])
+        for i, q in enumerate(sub[:8]):
+            single = FN[kind](g, q.vertex, q.window, T.AlgoOptions(mode=T.Mode.DENSE)).values
+            assert np.array_equal(batch[i], single), (kind, i)
+
+
+@pytest.mark.slow
+def test_full_c4_fastest_and_ld_properties():
+    wl, g, qs = setup("c4", 0)
+    fq, lq = qs
+    r = T.fastest_path(g, fq.vertex, fq.window).values
+    ea = T.earliest_arrival(g, fq.vertex, fq.window).values
+    INF = (1 << 63) - 1
+    assert r[fq.vertex] == 0
+    # reached by fastest <=> reached by earliest arrival (same admissible paths)
+    assert np.array_equal(r != INF, ea != INF)
+    assert np.all(r[r != INF] >= 0)
+    r2 = T.fastest_path(g, fq.vertex, fq.window, T.AlgoOptions(mode=T.Mode.SPARSE)).values
+    assert np.array_equal(r, r2)
+    ld = T.latest_departure(g, lq.vertex, lq.window).values
+    ld2 = T.latest_departure(g, lq.vertex, lq.window, T.AlgoOptions(mode=T.Mode.DENSE)).values
+    assert np.array_equal(ld, ld2)
+
+
+@pytest.mark.slow
+def test_full_c5_batch_properties():
+    wl, g, qs = setup("c5", 0)
+    full = qs[:16]
+    part = qs[16:]
+    bf = T.query_batch(g, "earliest_arrival", [q.vertex for q in full], [q.window for q in full],
+                       width=4)
+    bp = T.query_batch(g, "earliest_arrival", [q.vertex for q in part], [q.window for q in part],
+                       width=4)
+    INT32_MAX = 0x7fffffff
+    for i in range(16):
+        # window monotonicity (test_algorithms.cpp:71-83): the 10% window's
+        # labels are never earlier than the full window's
+        assert np.all(bp[i].astype(np.int64) >= bf[i].astype(np.int64))
+        assert bf[i][full[i].vertex] == 0
+    single = T.earliest_arrival(g, full[3].vertex, full[3].window).values
+    s32 = np.where(single == (1 << 63) - 1, INT32_MAX, single).astype(np.int64)
+    assert np.array_equal(s32, bf[3].astype(np.int64))

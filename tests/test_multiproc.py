@@ -1,0 +1,52 @@
+"""CPU, world_size 2 over gloo: the bench's N>1 path (replicas, no data-path
+collective) — max-over-ranks timing and whole-job aggregation."""
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ms = [2.0 + rank, 1.0 + 3 * rank]  # rank 1 is the slow one
+    got = bench.max_over_ranks(ms, dist, "cpu")
+    teps = bench.whole_job_teps(world, 1_000_000, got[0])
+    q.put((rank, got, teps))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_replica_timing_is_max_over_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, got, teps in res:
+        assert got == [3.0, 4.0]
+        assert teps == pytest.approx(2 * 1_000_000 / 3e-3)
+
+
+def test_single_rank_needs_no_process_group():
+    import bench
+    assert bench.max_over_ranks([1.5, 2.5]) == [1.5, 2.5]
+    assert bench.whole_job_teps(1, 10, 1.0) == pytest.approx(1e4)
