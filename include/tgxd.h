@@ -151,11 +151,14 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
                       const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode,
                       int warmup, int steps, float* total_ms, float* kernel_ms);
 
-/* Diagnostics: record a per-round trace of the next queries (block 0:
- * globaltimer at round start / after expand / after relax, frontier size,
- * chunks, small ranges, pushes; 8 u64 per round), max_rounds = 0 disables. */
+/* Diagnostics: record a per-round trace of the next queries, max_rounds = 0
+ * disables. tgxd_get_trace writes 12 u64 per round: globaltimer (ns) at round
+ * start / after expand / after relax, frontier size, chunks, small ranges,
+ * pushes, flags, then the latest and (2^62 - earliest) warp completion time
+ * of expand and of relax. Without with_device only the first 8 are filled
+ * and the call is safe while a query is still running. */
 int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds);
-int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds);
+int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds, int with_device);
 
 /* FNV-1a digest of int64 labels (digest.hpp:12-52). */
 uint64_t tgxd_digest(const int64_t* values, uint64_t n);

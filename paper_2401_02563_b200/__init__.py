@@ -221,7 +221,7 @@ def load_library() -> ctypes.CDLL:
                                _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
         "tgxd_digest": ([_i64p, ctypes.c_uint64], ctypes.c_uint64),
         "tgxd_set_trace": ([vp, ctypes.c_uint32], ctypes.c_int),
-        "tgxd_get_trace": ([vp, _u64p, ctypes.c_uint32], ctypes.c_int),
+        "tgxd_get_trace": ([vp, _u64p, ctypes.c_uint32, ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -463,11 +463,13 @@ def set_trace(g: TemporalGraph, max_rounds: int) -> None:
     _check(load_library().tgxd_set_trace(g.handle, max_rounds))
 
 
-def get_trace(g: TemporalGraph, max_rounds: int) -> np.ndarray:
-    """Per-round trace rows: t0, t_after_expand, t_after_relax (ns), F, chunks,
-    small ranges, pushes."""
-    out = np.zeros((max_rounds, 8), np.uint64)
-    _check(load_library().tgxd_get_trace(g.handle, _ptr(out, ctypes.c_uint64), max_rounds))
+def get_trace(g: TemporalGraph, max_rounds: int, with_device: bool = True) -> np.ndarray:
+    """Per-round trace rows (12 u64): t0, t_after_expand, t_after_relax (ns), F,
+    chunks, small ranges, pushes, flags, expand last/first warp done, relax
+    last/first warp done (first stored as 2^62 - t)."""
+    out = np.zeros((max_rounds, 12), np.uint64)
+    _check(load_library().tgxd_get_trace(g.handle, _ptr(out, ctypes.c_uint64), max_rounds,
+                                         1 if with_device else 0))
     return out
 
 

@@ -429,12 +429,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.cand_key = w.cand_key.as<int32_t>();
   a.init_pushes = fast ? 0ull : P.Q;
   a.trace = w.trace_dev;
+  a.wtrace = w.trace_cap ? w.wtrace.as<unsigned long long>() : nullptr;
   a.trace_cap = w.trace_cap;
   a.round_limit = (uint32_t)std::min<uint64_t>(
       0xfffffff0ULL, ((uint64_t)ncand + 1) * ((uint64_t)slots + 2) + 16);
   if (w.trace_host) {
     TGXD_CUDA(cudaStreamSynchronize(s));
     std::memset(w.trace_host, 0, w.trace_cap * 64ull);
+    TGXD_CUDA(cudaMemsetAsync(w.wtrace.p, 0, w.trace_cap * 32ull, s));
   }
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
@@ -977,16 +979,27 @@ int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds) {
     g->ws.trace_host = static_cast<unsigned long long*>(h);
     g->ws.trace_dev = static_cast<unsigned long long*>(d);
     g->ws.trace_cap = max_rounds;
+    if (!dalloc<unsigned long long>(g->ws.wtrace, max_rounds * 4ull))
+      return fail(TGXD_ERR_CUDA, "allocation (trace)");
   }
   return TGXD_OK;
 }
 
-// No lock and no CUDA call: safe to use while a query is in flight.
-int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds) {
+// Rows of 12 u64: the 8 block-0 fields (read from mapped host memory, no
+// lock: usable while a query is still running) and the 4 per-warp phase
+// extremes (device memory; copied only when `with_device` is set).
+int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds, int with_device) {
   if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
   const uint32_t r = std::min(max_rounds, g->ws.trace_cap);
   volatile unsigned long long* src = g->ws.trace_host;
-  for (uint64_t i = 0; i < r * 8ull; ++i) out[i] = src[i];
+  std::vector<unsigned long long> wt(r * 4ull, 0);
+  if (with_device && r) {
+    TGXD_CUDA(cudaMemcpy(wt.data(), g->ws.wtrace.p, r * 32ull, cudaMemcpyDeviceToHost));
+  }
+  for (uint64_t i = 0; i < r; ++i) {
+    for (int j = 0; j < 8; ++j) out[i * 12 + j] = src[i * 8 + j];
+    for (int j = 0; j < 4; ++j) out[i * 12 + 8 + j] = wt[i * 4 + j];
+  }
   return TGXD_OK;
 }
 

@@ -66,6 +66,7 @@ struct Workspace {
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
   unsigned long long* trace_dev = nullptr;
+  DeviceBuffer wtrace;
   uint32_t trace_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // what the last query left in X (for tgxd_last_work)

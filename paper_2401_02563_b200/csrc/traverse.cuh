@@ -86,8 +86,10 @@ struct TravArgs {
   const uint32_t* cand_lo;
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
-  // optional per-round trace (block 0), 8 u64 per round
+  // optional per-round trace (block 0), 8 u64 per round, plus per-warp
+  // phase completion extremes (device memory, 4 u64 per round)
   unsigned long long* trace;
+  unsigned long long* wtrace;
   uint32_t trace_cap;
   uint32_t round_limit;  // watchdog: a correct traversal never gets near it
   unsigned long long init_pushes;  // queue position / improvements after seeding
@@ -623,6 +625,17 @@ __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int s
   }
 }
 
+// Per-warp phase completion: wtrace[r*4 + 2*phase] = latest, [+1] = earliest
+// (stored as kTBig - t so both are maxima).
+constexpr unsigned long long kTBig = 1ull << 62;
+__device__ __forceinline__ void trace_warp_done(const TravArgs& a, uint32_t r, int phase) {
+  if (a.wtrace && r < a.trace_cap && lane_id() == 0) {
+    const unsigned long long t = gtimer();
+    atomicMax(a.wtrace + r * 4 + 2 * phase, t);
+    atomicMax(a.wtrace + r * 4 + 2 * phase + 1, kTBig - t);
+  }
+}
+
 // Reads one counter into every thread of the block (block 0 local rounds).
 __device__ __forceinline__ unsigned long long block_read(const unsigned long long* p) {
   __shared__ unsigned long long s_v;
@@ -758,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         uint32_t* fout = st.flip ? a.fa : a.fb;
         RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
         phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
+        trace_warp_done(a, st.rounds, 1);
         grid.sync();
         st.p_known = __ldcg(&ctl->pushes);
         st.i_known = __ldcg(&ctl->improved);
@@ -788,6 +802,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       if (!xcnt) {
         phase_a(a, st.dense ? nullptr : fin, (uint32_t)F, st.c_cur, st.s_cur, blockIdx.x,
                 gridDim.x, pol_keep, ebuf, ix);
+        trace_warp_done(a, st.rounds, 0);
         grid.sync();
         c_end = __ldcg(&ctl->chunks);
         s_end = __ldcg(&ctl->smalls);
@@ -809,6 +824,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         for (int o = 16; o > 0; o >>= 1) imp += __shfl_xor_sync(0xffffffffu, imp, o);
         if (lane_id() == 0 && imp) atomicAdd(&ctl->improved, (unsigned long long)imp);
       }
+      trace_warp_done(a, st.rounds, 1);
       grid.sync();
       st.p_known = __ldcg(&ctl->pushes);
       st.i_known = __ldcg(&ctl->improved);
