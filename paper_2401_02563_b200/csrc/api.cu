@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -430,6 +431,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.init_pushes = fast ? 0ull : P.Q;
   a.trace = w.trace_dev;
   a.wtrace = w.trace_cap ? w.wtrace.as<unsigned long long>() : nullptr;
+  a.wtrace_on = getenv("TGXD_WTRACE") != nullptr;
   a.trace_cap = w.trace_cap;
   a.round_limit = (uint32_t)std::min<uint64_t>(
       0xfffffff0ULL, ((uint64_t)ncand + 1) * ((uint64_t)slots + 2) + 16);

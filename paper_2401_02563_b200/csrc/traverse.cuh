@@ -90,6 +90,7 @@ struct TravArgs {
   // phase completion extremes (device memory, 4 u64 per round)
   unsigned long long* trace;
   unsigned long long* wtrace;
+  int wtrace_on;
   uint32_t trace_cap;
   uint32_t round_limit;  // watchdog: a correct traversal never gets near it
   unsigned long long init_pushes;  // queue position / improvements after seeding
@@ -619,9 +620,8 @@ __device__ __forceinline__ void load_state(const Control* ctl, TState& s) {
 __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int slot,
                                             unsigned long long v) {
   if (a.trace && r < a.trace_cap) {
-    volatile unsigned long long* t = a.trace;
+    volatile unsigned long long* t = a.trace;  // mapped host memory, no fence
     t[r * 8 + slot] = v;
-    __threadfence_system();
   }
 }
 
@@ -629,7 +629,7 @@ __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int s
 // (stored as kTBig - t so both are maxima).
 constexpr unsigned long long kTBig = 1ull << 62;
 __device__ __forceinline__ void trace_warp_done(const TravArgs& a, uint32_t r, int phase) {
-  if (a.wtrace && r < a.trace_cap && lane_id() == 0) {
+  if (a.wtrace && a.wtrace_on && r < a.trace_cap && lane_id() == 0) {
     const unsigned long long t = gtimer();
     atomicMax(a.wtrace + r * 4 + 2 * phase, t);
     atomicMax(a.wtrace + r * 4 + 2 * phase + 1, kTBig - t);

@@ -71,7 +71,9 @@ __global__ void stream_kernel(const uint2* __restrict__ p, size_t n, unsigned lo
   if (acc == 42) out[0] = acc;
 }
 
+int latency_main();
 int main() {
+  latency_main();
   int dev = 0, sms = 0;
   CK(cudaSetDevice(dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -180,6 +182,88 @@ int main() {
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     printf("stream 8B loads: %.0f GB/s\n", n * 8 / (ms * 1e6));
+  }
+  return 0;
+}
+
+// ---- latency probes (appended) ----
+__global__ void chase(const unsigned* __restrict__ nxt, int steps, unsigned* out, long long* cyc) {
+  unsigned p = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < steps; ++i) p = __ldcg(nxt + p);
+  long long t1 = clock64();
+  out[0] = p;
+  cyc[0] = t1 - t0;
+}
+__global__ void chase_atomic(unsigned* nxt, int steps, unsigned* out, long long* cyc) {
+  unsigned p = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < steps; ++i) p = atomicAdd(nxt + p, 0u);
+  long long t1 = clock64();
+  out[0] = p;
+  cyc[0] = t1 - t0;
+}
+// a round = grid.sync + a dependent chain of `deps` L2 loads in one warp per block
+__global__ void rounds_kernel(const unsigned* __restrict__ nxt, int rounds, int deps, unsigned* out) {
+  cg::grid_group g = cg::this_grid();
+  unsigned p = blockIdx.x;
+  for (int r = 0; r < rounds; ++r) {
+    if (threadIdx.x < 32)
+      for (int d = 0; d < deps; ++d) p = __ldcg(nxt + (p & 1023));
+    g.sync();
+  }
+  if (p == 12345) out[0] = p;
+}
+int latency_main() {
+  const size_t n_small = 1 << 20, n_big = 1u << 28;  // 4 MB (L2) and 1 GB (DRAM)
+  unsigned *a, *out;
+  long long* cyc;
+  CK(cudaMalloc(&a, n_big * 4));
+  CK(cudaMalloc(&out, 64));
+  CK(cudaMalloc(&cyc, 64));
+  for (size_t n : {n_small, n_big}) {
+    std::vector<unsigned> h(n);
+    // random cyclic permutation with large strides
+    uint64_t s = 1234567;
+    std::vector<unsigned> perm(n);
+    for (size_t i = 0; i < n; ++i) perm[i] = i;
+    for (size_t i = n - 1; i > 0; --i) {
+      s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+      size_t j = s % (i + 1);
+      std::swap(perm[i], perm[j]);
+    }
+    for (size_t i = 0; i < n; ++i) h[perm[i]] = perm[(i + 1) % n];
+    CK(cudaMemcpy(a, h.data(), n * 4, cudaMemcpyHostToDevice));
+    const int steps = 20000;
+    chase<<<1, 1>>>(a, 1000, out, cyc);  // warm
+    CK(cudaDeviceSynchronize());
+    chase<<<1, 1>>>(a, steps, out, cyc);
+    long long c;
+    CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
+    printf("dependent load latency, %zu MB footprint: %.0f cycles (%.0f ns @1.965GHz)\n",
+           n * 4 >> 20, (double)c / steps, (double)c / steps / 1.965);
+    chase_atomic<<<1, 1>>>(a, steps, out, cyc);
+    CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
+    printf("dependent atomic latency, %zu MB footprint: %.0f cycles\n", n * 4 >> 20,
+           (double)c / steps);
+  }
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int deps : {0, 4, 8}) {
+    int rounds = 500;
+    void* args[] = {&a, &rounds, &deps, &out};
+    CK(cudaLaunchCooperativeKernel((void*)rounds_kernel, sms * 3, 256, args, 0, 0));
+    cudaEventRecord(e0);
+    CK(cudaLaunchCooperativeKernel((void*)rounds_kernel, sms * 3, 256, args, 0, 0));
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("round = %d dependent L2 loads + grid.sync (444 CTAs): %.2f us\n", deps,
+           ms * 1e3 / rounds);
   }
   return 0;
 }
