@@ -339,7 +339,7 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool fastest) {
   const uint64_t slots = (uint64_t)Q * G->n;
   // chunks per round <= frontier items + edges / kChunk (per query slot)
   const uint64_t max_chunks = slots + (uint64_t)Q * (G->m / kChunk + 1);
-  bool ok = dalloc<int32_t>(w.X, slots) && dalloc<int32_t>(w.Ex, slots) &&
+  bool ok = dalloc<int32_t>(w.X, slots) && dalloc<int2>(w.EP, slots) &&
             dalloc<uint32_t>(w.fa, slots) &&
             dalloc<uint32_t>(w.fb, slots) && dalloc<uint2>(w.chunks, max_chunks) &&
             dalloc<uint2>(w.smalls, slots) && dalloc<Control>(w.ctl, 1) &&
@@ -398,7 +398,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     TGXD_CUDA(cudaMemcpyAsync(w.cand_key.p, P.cand_key.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
   }
   init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
-      w.X.as<int32_t>(), w.Ex.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr, slots);
+      w.X.as<int32_t>(), w.EP.as<int2>(), fast ? w.R.as<int32_t>() : nullptr, slots);
   seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
                                                  w.X.as<int32_t>(), w.fa.as<uint32_t>(),
                                                  w.ctl.as<Control>(), fast);
@@ -406,7 +406,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.g = g;
   a.qp = w.params.as<QueryParam>();
   a.X = w.X.as<int32_t>();
-  a.Ex = w.Ex.as<int32_t>();
+  a.EP = w.EP.as<int2>();
   a.R = fast ? w.R.as<int32_t>() : nullptr;
   a.fa = w.fa.as<uint32_t>();
   a.fb = w.fb.as<uint32_t>();

@@ -62,7 +62,7 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 // Traversal workspace, sized for q_cap concurrent queries.
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
-  DeviceBuffer X, Ex, R, fa, fb, chunks, smalls, ctl, params, seeds;
+  DeviceBuffer X, EP, R, fa, fb, chunks, smalls, ctl, params, seeds;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
   unsigned long long* trace_dev = nullptr;

@@ -66,7 +66,8 @@ struct TravArgs {
   DevCsr g;
   const QueryParam* qp;
   int32_t* X;          // labels, Q x n (key space)
-  int32_t* Ex;         // bound each vertex was last expanded with
+  int2* EP;            // per slot {bound it was last expanded with, position of
+                       // that bound in its segment (kNoPos: unknown)}
   int32_t* R;          // fastest durations (nullptr otherwise)
   uint32_t* fa;        // frontier queues (items = q * n + v)
   uint32_t* fb;
@@ -225,7 +226,7 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
     bool p = false;
     if (v[u] < cur[u]) {
       int32_t ex = 0;
-      if (rx.push) ex = ld_state(a.Ex + idx[u], rx.pol_keep);
+      if (rx.push) ex = ld_state(reinterpret_cast<const int32_t*>(a.EP + idx[u]), rx.pol_keep);
       const int32_t old = atomicMin(a.X + idx[u], v[u]);
       if (v[u] < old) {
         if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
@@ -255,7 +256,6 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
 // the reference's TGER-vs-scan choice (test_algorithms.cpp:196-217).
 // Emission is buffered per warp in shared memory (no block barriers).
 
-constexpr uint32_t kLinear = 32;   // segments up to this length are counted, not searched
 
 // Per-warp staging of emitted work: appended 32 entries at a time.
 struct WarpList {
@@ -293,73 +293,55 @@ __device__ __forceinline__ void list_drain(WarpList& wl, unsigned long long* ctr
   if (wl.n) list_flush(wl, wl.n, ctr, start, list);
 }
 
-__device__ __forceinline__ uint32_t lane_lower_bound(const int32_t* key, uint32_t lo, uint32_t hi,
-                                                     int32_t x) {
-  while (lo < hi) {
+constexpr uint32_t kNoPos = 0xffffffffu;
+
+// Keys below x in a short range [lo, hi), hi - lo <= 32, from aligned
+// 16-byte loads (at most 9, all in flight together).
+__device__ __forceinline__ uint32_t line_count(const int32_t* key, uint32_t lo, uint32_t hi,
+                                               int32_t x) {
+  uint32_t c = 0;
+  const uint32_t a0 = lo & ~3u;
+#pragma unroll
+  for (uint32_t j = 0; j < 9; ++j) {
+    const uint32_t p = a0 + 4 * j;
+    if (p < hi) {
+      const int4 k4 = __ldg(reinterpret_cast<const int4*>(key + p));
+      c += (p + 0 >= lo && p + 0 < hi && k4.x < x) ? 1u : 0u;
+      c += (p + 1 >= lo && p + 1 < hi && k4.y < x) ? 1u : 0u;
+      c += (p + 2 >= lo && p + 2 < hi && k4.z < x) ? 1u : 0u;
+      c += (p + 3 >= lo && p + 3 < hi && k4.w < x) ? 1u : 0u;
+    }
+  }
+  return lo + c;
+}
+
+// lower_bound(x) over key[lo, hi) by one lane. With `fence` (the vertex is
+// at or above the index cutoff) the selective index first narrows the range
+// to one 32-key line by binary search over the fence array (every 32nd key
+// of the layout, a compact "bucketed timeline"); otherwise the keys
+// themselves are bisected down to 32. The last line is counted with vector
+// loads. Results-neutral, like the reference's TGER-vs-scan choice
+// (test_algorithms.cpp:196-217).
+__device__ __forceinline__ uint32_t lane_lower_bound(const DevCsr& g, uint32_t lo, uint32_t hi,
+                                                     int32_t x, bool fence) {
+  if (fence && hi - lo > 32) {
+    const uint32_t jlo = (lo + kFenceStride - 1) >> kFenceShift;
+    const uint32_t jhi = (hi - 1) >> kFenceShift;
+    uint32_t a = jlo, b = jhi + 1;  // first fence >= x in [jlo, jhi], else jhi + 1
+    while (a < b) {
+      const uint32_t mid = (a + b) >> 1;
+      if (__ldg(g.fence + mid) < x) a = mid + 1;
+      else b = mid;
+    }
+    if (a > jlo) lo = max(lo, ((a - 1) << kFenceShift) + 1);
+    if (a <= jhi) hi = min(hi, a << kFenceShift);
+  }
+  while (hi - lo > 32) {
     const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(key + mid) < x) lo = mid + 1;
+    if (__ldg(g.key + mid) < x) lo = mid + 1;
     else hi = mid;
   }
-  return lo;
-}
-
-// Warp-cooperative lower_bound over arr[lo, hi): 32 probes per level.
-// Every lane must call it with the same arguments; the result is uniform.
-__device__ __forceinline__ uint32_t warp_lower_bound(const int32_t* arr, uint32_t lo, uint32_t hi,
-                                                     int32_t x) {
-  const uint32_t lane = lane_id();
-  while (hi - lo > 32) {
-    const uint32_t len = hi - lo;
-    const uint32_t pos = lo + (uint32_t)(((unsigned long long)(lane + 1) * len) / 33);
-    const uint32_t b = __ballot_sync(0xffffffffu, __ldg(arr + pos) >= x);
-    if (b == 0) {
-      lo = __shfl_sync(0xffffffffu, pos, 31) + 1;
-    } else {
-      const uint32_t f = __ffs(b) - 1;
-      const uint32_t pf = __shfl_sync(0xffffffffu, pos, f);
-      const uint32_t pp = __shfl_sync(0xffffffffu, pos, f ? f - 1 : 0);
-      hi = pf;  // arr[pf] >= x: the answer is at most pf
-      if (f) lo = pp + 1;
-    }
-  }
-  const uint32_t pos = lo + lane;
-  const uint32_t b = __ballot_sync(0xffffffffu, pos < hi && __ldg(arr + pos) >= x);
-  return b ? lo + __ffs(b) - 1 : hi;
-}
-
-// Selective-index lookup: fence search, then one key line.
-__device__ __forceinline__ uint32_t index_lower_bound(const DevCsr& g, uint32_t s, uint32_t t,
-                                                      int32_t x) {
-  const uint32_t jlo = (s + kFenceStride - 1) >> kFenceShift;
-  const uint32_t jhi = (t - 1) >> kFenceShift;
-  if (jlo <= jhi) {
-    const uint32_t f = warp_lower_bound(g.fence, jlo, jhi + 1, x);
-    if (f > jlo) s = max(s, ((f - 1) << kFenceShift) + 1);
-    if (f <= jhi) t = min(t, f << kFenceShift);
-  }
-  return warp_lower_bound(g.key, s, t, x);
-}
-
-// Keys below lb and below hik in a short segment [s, t), t - s <= kLinear,
-// from aligned 16-byte loads.
-__device__ __forceinline__ void linear_count(const int32_t* key, uint32_t s, uint32_t t, int32_t lb,
-                                             int32_t hik, uint32_t& c0, uint32_t& c1) {
-  c0 = c1 = 0;
-  const uint32_t a0 = s & ~3u;
-#pragma unroll
-  for (uint32_t j = 0; j < (kLinear + 4) / 4; ++j) {
-    const uint32_t p = a0 + 4 * j;
-    if (p < t) {
-      const int4 k4 = __ldg(reinterpret_cast<const int4*>(key + p));
-      const int32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const bool in = p + c >= s && p + c < t;
-        c0 += (in && kk[c] < lb) ? 1u : 0u;
-        c1 += (in && kk[c] < hik) ? 1u : 0u;
-      }
-    }
-  }
+  return line_count(g.key, lo, hi, x);
 }
 
 struct ExpandBufs {
@@ -367,62 +349,48 @@ struct ExpandBufs {
   unsigned long long cstart, sstart;
 };
 
-// Expansion of one slot per lane (item = q * n + v, label x, previous bound
-// old); the emitted ranges go to the warp's lists. All lanes must call it.
+// Expansion of one slot per lane (item = q * n + v, label x, previous
+// expansion state ep = {bound, position}); the emitted ranges go to the
+// warp's lists. All lanes must call it; no lane ever waits on another's
+// search.
 __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint32_t item, int32_t x,
-                                            int32_t old, ExpandBufs& eb,
-                                            unsigned long long& work, unsigned long long& ix) {
+                                            int2 ep, ExpandBufs& eb, unsigned long long& work,
+                                            unsigned long long& ix) {
   const uint32_t lane = lane_id();
-  uint32_t q = 0, v = 0, s = 0, t = 0, p0 = 0, p1 = 0;
-  int32_t lb = 0, hik = 0, last = 0;
+  uint32_t q = 0, p0 = 0, p1 = 0;
   bool act = false;
   if (valid) {
     q = a.Q == 1 ? 0u : item / a.n;
-    v = item - q * a.n;
+    const uint32_t v = item - q * a.n;
     const QueryParam& qp = a.qp[q];
     // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342):
     // the root leaves at any time inside the window; everyone else strictly
     // (or weakly) after its own label.
-    lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
+    int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
     if (lb < qp.klo) lb = qp.klo;
+    const int32_t old = ep.x;
     if (lb < old) {
-      a.Ex[item] = lb;
-      hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
+      const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
+      uint32_t pos = kNoPos;
       if (lb < hik) {
-        s = __ldg(a.g.off + v);
-        t = __ldg(a.g.off + v + 1);
-        act = t > s;
+        const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
+        if (t > s) {
+          act = true;
+          const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
+          ix += fence ? 1 : 0;
+          // upper end: the previous expansion's position when that bound is
+          // the limit (a re-expansion), else the segment end when every key
+          // fits under the window
+          if (old <= qp.vhi + 1 && ep.y != (int32_t)kNoPos) {
+            p1 = (uint32_t)ep.y;
+          } else {
+            p1 = __ldg(a.g.key + t - 1) < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
+          }
+          p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
+          pos = p0;
+        }
       }
-    }
-  }
-  const uint32_t deg = t - s;
-  const bool hub = act && a.cutoff != 0 && deg >= a.cutoff;
-  if (act && !hub) {
-    if (deg <= kLinear) {
-      uint32_t c0, c1;
-      linear_count(a.g.key, s, t, lb, hik, c0, c1);
-      p0 = s + c0;
-      p1 = s + c1;
-    } else {
-      last = __ldg(a.g.key + t - 1);
-      p0 = lane_lower_bound(a.g.key, s, t, lb);
-      p1 = last < hik ? t : lane_lower_bound(a.g.key, p0, t, hik);
-    }
-  }
-  if (hub) last = __ldg(a.g.key + t - 1);
-  uint32_t hubs = __ballot_sync(0xffffffffu, hub);
-  ix += hub ? 1 : 0;
-  while (hubs) {
-    const uint32_t src = __ffs(hubs) - 1;
-    hubs &= hubs - 1;
-    const uint32_t S = __shfl_sync(0xffffffffu, s, src), Tt = __shfl_sync(0xffffffffu, t, src);
-    const int32_t LB = __shfl_sync(0xffffffffu, lb, src), HK = __shfl_sync(0xffffffffu, hik, src);
-    const int32_t LAST = __shfl_sync(0xffffffffu, last, src);
-    const uint32_t P0 = index_lower_bound(a.g, S, Tt, LB);
-    const uint32_t P1 = LAST < HK ? Tt : index_lower_bound(a.g, P0, Tt, HK);
-    if (lane == src) {
-      p0 = P0;
-      p1 = P1;
+      a.EP[item] = make_int2(lb, (int32_t)pos);
     }
   }
   const uint32_t cnt = act ? p1 - p0 : 0u;
@@ -430,20 +398,34 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
   // short ranges: one small-list entry
   list_append(eb.sm, cnt != 0 && cnt < kSmall, make_uint2(p0, (q << kSmallCntBits) | cnt),
               &a.ctl->smalls, eb.sstart, a.smalls);
-  // long ranges: kChunk-edge chunks, appended by the whole warp
-  uint32_t bigs = __ballot_sync(0xffffffffu, cnt >= kSmall);
+  // long ranges: kChunk-edge chunks; medium ones through the warp buffer,
+  // huge ones straight to the list with one reservation
+  const uint32_t nch = cnt >= kSmall ? (cnt + kChunk - 1) / kChunk : 0u;
+  uint32_t bigs = __ballot_sync(0xffffffffu, nch != 0 && nch < 32);
   while (bigs) {
     const uint32_t src = __ffs(bigs) - 1;
     bigs &= bigs - 1;
     const uint32_t B0 = __shfl_sync(0xffffffffu, p0, src), BC = __shfl_sync(0xffffffffu, cnt, src);
     const uint32_t BQ = __shfl_sync(0xffffffffu, q, src);
-    const uint32_t nch = (BC + kChunk - 1) / kChunk;
-    for (uint32_t j0 = 0; j0 < nch; j0 += 32) {
-      const uint32_t j = j0 + lane;
+    const uint32_t bn = __shfl_sync(0xffffffffu, nch, src);
+    const uint32_t off = lane * kChunk;
+    list_append(eb.ch, lane < bn,
+                make_uint2(B0 + off, (BQ << kChunkLenBits) | (lane < bn ? min(kChunk, BC - off) : 0u)),
+                &a.ctl->chunks, eb.cstart, a.chunks);
+  }
+  uint32_t huge = __ballot_sync(0xffffffffu, nch >= 32);
+  while (huge) {
+    const uint32_t src = __ffs(huge) - 1;
+    huge &= huge - 1;
+    const uint32_t B0 = __shfl_sync(0xffffffffu, p0, src), BC = __shfl_sync(0xffffffffu, cnt, src);
+    const uint32_t BQ = __shfl_sync(0xffffffffu, q, src);
+    const uint32_t bn = __shfl_sync(0xffffffffu, nch, src);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&a.ctl->chunks, (unsigned long long)bn);
+    base = __shfl_sync(0xffffffffu, base, 0) - eb.cstart;
+    for (uint32_t j = lane; j < bn; j += 32) {
       const uint32_t off = j * kChunk;
-      list_append(eb.ch, j < nch,
-                  make_uint2(B0 + off, (BQ << kChunkLenBits) | (j < nch ? min(kChunk, BC - off) : 0u)),
-                  &a.ctl->chunks, eb.cstart, a.chunks);
+      a.chunks[base + j] = make_uint2(B0 + off, (BQ << kChunkLenBits) | min(kChunk, BC - off));
     }
   }
 }
@@ -480,14 +462,15 @@ __device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
     const uint32_t i = base + lane;
     bool valid = i < total;
     uint32_t item = i;
-    int32_t x = kInf, old = kInf;
+    int32_t x = kInf;
+    int2 ep = make_int2(kInf, (int32_t)kNoPos);
     if (valid) {
       if (fin) item = __ldcg(fin + i);
       x = ld_state(a.X + item, pol_keep);
-      old = ld_state(a.Ex + item, pol_keep);
+      ep = __ldcg(a.EP + item);
       valid = x != kInf;
     }
-    expand_warp(a, valid, item, x, old, eb, work, ix);
+    expand_warp(a, valid, item, x, ep, eb, work, ix);
   }
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
@@ -863,18 +846,20 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
 }
 
 // Labels, expansion bounds and durations to INF.
-__global__ void init_kernel(int32_t* X, int32_t* Ex, int32_t* R, size_t nl) {
+__global__ void init_kernel(int32_t* X, int2* EP, int32_t* R, size_t nl) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t n4 = nl / 4;
   const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
+  const int4 ep2 = make_int4(kInf, (int32_t)kNoPos, kInf, (int32_t)kNoPos);
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     reinterpret_cast<int4*>(X)[i] = inf4;
-    reinterpret_cast<int4*>(Ex)[i] = inf4;
+    reinterpret_cast<int4*>(EP)[2 * i] = ep2;
+    reinterpret_cast<int4*>(EP)[2 * i + 1] = ep2;
     if (R) reinterpret_cast<int4*>(R)[i] = inf4;
   }
   for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
     X[i] = kInf;
-    Ex[i] = kInf;
+    EP[i] = make_int2(kInf, (int32_t)kNoPos);
     if (R) R[i] = kInf;
   }
 }
