@@ -203,42 +203,49 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
                                             const bool (&act)[kUnroll], RelaxCtx& rx,
                                             PushBuf& pb) {
   int32_t v[kUnroll];
-  uint32_t d[kUnroll];
+  uint32_t idx[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     const uint2 pl = act[u] ? ld_stream2(a.g.pay + e[u], rx.pol_stream) : make_uint2(0u, kInf);
-    d[u] = pl.x;
+    idx[u] = q[u] * a.n + pl.x;
     v[u] = (int32_t)pl.y;
   }
-  uint32_t idx[kUnroll];
   int32_t cur[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     const int32_t vhi = a.Q == 1 ? rx.vhi0 : __ldg(&a.qp[q[u]].vhi);
     // window containment: end <= t_b (types.hpp:55-57)
-    const bool ok = act[u] && v[u] <= vhi;
-    idx[u] = q[u] * a.n + d[u];
-    cur[u] = ok ? ld_state(a.X + idx[u], rx.pol_keep) : kInf;
-    if (!ok) v[u] = kInf;
+    if (!(act[u] && v[u] <= vhi)) v[u] = kInf;
+    cur[u] = v[u] != kInf ? ld_state(a.X + idx[u], rx.pol_keep) : kInf;
   }
+  // all atomics of the batch are in flight before any result is used
+  int32_t old[kUnroll], ex[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    bool p = false;
+    old[u] = kInf;
+    ex[u] = 0;
     if (v[u] < cur[u]) {
-      int32_t ex = 0;
-      if (rx.push) ex = ld_state(reinterpret_cast<const int32_t*>(a.EP + idx[u]), rx.pol_keep);
-      const int32_t old = atomicMin(a.X + idx[u], v[u]);
-      if (v[u] < old) {
-        if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
-        if (rx.push) p = bound_of(old, a.strict) == ex;
-        else ++rx.improved;
-      }
+      if (rx.push) ex[u] = ld_state(reinterpret_cast<const int32_t*>(a.EP + idx[u]), rx.pol_keep);
+      old[u] = atomicMin(a.X + idx[u], v[u]);  // write_min, parallel.hpp:91-99
     }
-    if (rx.push) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, p);
+  }
+  bool p[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    p[u] = false;
+    if (v[u] < old[u]) {
+      if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
+      if (rx.push) p[u] = bound_of(old[u], a.strict) == ex[u];
+      else ++rx.improved;
+    }
+  }
+  if (rx.push) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, p[u]);
       if (bal) {
         const uint32_t lane = lane_id();
-        if (p) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = idx[u];
+        if (p[u]) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = idx[u];
         pb.n += __popc(bal);
         if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
       }
@@ -504,8 +511,10 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
   }
 
   // chunks of big ranges: coalesced kChunk-edge bursts
+  uint2 nxt = gw < nchunks ? __ldcg(a.chunks + gw) : make_uint2(0u, 0u);
   for (unsigned long long c = gw; c < nchunks; c += nw) {
-    const uint2 ch = a.chunks[c];
+    const uint2 ch = nxt;  // descriptor prefetched one iteration ahead
+    if (c + nw < nchunks) nxt = __ldcg(a.chunks + c + nw);
     const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
     const uint32_t cq = ch.y >> kChunkLenBits;
     uint32_t e[kUnroll], q[kUnroll];
@@ -523,15 +532,15 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
   // small ranges: 32 per warp window; lane l owns range l, items are packed
   // densely and each lane finds its owner from the mask of range starts.
   const unsigned long long nwin = (nsmall + 31) / 32;
+  uint2 snx = (gw < nwin && gw * 32 + lane < nsmall) ? __ldcg(a.smalls + gw * 32 + lane)
+                                                     : make_uint2(0u, 0u);
   for (unsigned long long w = gw; w < nwin; w += nw) {
-    const unsigned long long r = w * 32 + lane;
-    uint32_t lo = 0, cnt = 0, rq = 0;
-    if (r < nsmall) {
-      const uint2 s = a.smalls[r];
-      lo = s.x;
-      cnt = s.y & ((1u << kSmallCntBits) - 1);
-      rq = s.y >> kSmallCntBits;
-    }
+    const uint2 sv = snx;  // window prefetched one iteration ahead
+    const unsigned long long rn = (w + nw) * 32 + lane;
+    if (w + nw < nwin) snx = rn < nsmall ? __ldcg(a.smalls + rn) : make_uint2(0u, 0u);
+    const uint32_t lo = sv.x;
+    const uint32_t cnt = sv.y & ((1u << kSmallCntBits) - 1);
+    const uint32_t rq = sv.y >> kSmallCntBits;
     uint32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
