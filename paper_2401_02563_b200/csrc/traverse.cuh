@@ -47,7 +47,7 @@ namespace tgxd {
 #define TGXD_UNROLL 4
 #endif
 #ifndef TGXD_MIN_BLOCKS
-#define TGXD_MIN_BLOCKS 3
+#define TGXD_MIN_BLOCKS 4
 #endif
 #ifndef TGXD_LOCAL_F
 #define TGXD_LOCAL_F 128
