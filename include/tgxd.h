@@ -53,7 +53,12 @@ enum tgxd_ordering { TGXD_SUCCEEDS = 0, TGXD_STRICTLY_SUCCEEDS = 1, TGXD_OVERLAP
 /* Frontier representation policy (temporal_edge_map's representation switch,
  * engine.hpp:280-295). AUTO switches on frontier size; the forced modes exist
  * for the push/pull equivalence tests (test_engine.cpp:153-176). */
-enum tgxd_mode { TGXD_MODE_AUTO = 0, TGXD_MODE_SPARSE = 1, TGXD_MODE_DENSE = 2 };
+enum tgxd_mode {
+  TGXD_MODE_AUTO = 0,    /* engine's choice */
+  TGXD_MODE_SPARSE = 1,  /* round-based, queue frontier every round */
+  TGXD_MODE_DENSE = 2,   /* round-based, implicit (dense) frontier every round */
+  TGXD_MODE_ASYNC = 3    /* barrier-free work queues (no rounds) */
+};
 
 /* Output label width: 8 = int64 exactly as PathResult::values
  * (algorithms.hpp:16-21: INT64_MAX / INT64_MIN sentinels, exact seed values);

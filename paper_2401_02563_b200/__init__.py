@@ -55,10 +55,11 @@ class Direction(enum.IntEnum):           # types.hpp:87
     IN = 1
 
 
-class Mode(enum.IntEnum):                # frontier representation policy (tgxd_mode)
+class Mode(enum.IntEnum):                # traversal schedule (tgxd_mode)
     AUTO = 0
-    SPARSE = 1
-    DENSE = 2
+    SPARSE = 1     # rounds, queue frontier
+    DENSE = 2      # rounds, implicit dense frontier
+    ASYNC = 3      # barrier-free work queues
 
 
 class OutOfRange(IndexError):

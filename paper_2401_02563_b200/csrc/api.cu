@@ -18,6 +18,7 @@
 #include "gen.cuh"
 #include "tgxd_internal.cuh"
 #include "traverse.cuh"
+#include "async.cuh"
 
 namespace tgxd {
 
@@ -223,6 +224,9 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
     return fail(TGXD_ERR_CUDA, std::string("graph setup: ") + cudaGetErrorString(e));
   }
   G->coop_blocks = std::max(1, per_sm) * G->sm_count;
+  int per_sm_a = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, async_kernel, kThreads, 0);
+  G->coop_blocks_async = std::max(1, per_sm_a) * G->sm_count;
   *out = G;
   return TGXD_OK;
 }
@@ -375,6 +379,71 @@ __global__ void convert_kernel(int kind, const int32_t* X, const int32_t* R, uin
   }
 }
 
+static uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// The asynchronous engine: rings and flags persist across queries (every
+// query leaves them empty and clear); the kernel runs after init_kernel.
+static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint32_t ncand,
+                        cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  Workspace& w = G->ws;
+  cudaStream_t s = G->stream;
+  const bool fast = P.kind == TGXD_FASTEST;
+  const uint64_t slots = (uint64_t)P.Q * G->n;
+  const uint64_t vcap = next_pow2(slots + 64);
+  // outstanding chunks <= ranges of >= kAInline edges + their chunks
+  const uint64_t ccap = next_pow2((uint64_t)P.Q * (G->m / kAInline + G->m / kAChunk) + 1024);
+  if (w.a_slots < slots || w.a_vcap < vcap || w.a_ccap < ccap) {
+    if (!dalloc<uint32_t>(w.aflag, slots) || !dalloc<uint32_t>(w.avq, vcap) ||
+        !dalloc<uint2>(w.acq, ccap) || !dalloc<AsyncCtl>(w.actl, 1))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (async queues)");
+    TGXD_CUDA(cudaMemsetAsync(w.actl.p, 0, sizeof(AsyncCtl), s));
+    async_reset_kernel<<<grid_for(std::max(vcap, ccap), G->sm_count), 256, 0, s>>>(
+        w.aflag.as<uint32_t>(), slots, w.avq.as<uint32_t>(), vcap, w.acq.as<uint2>(), ccap,
+        w.actl.as<AsyncCtl>());
+    w.a_slots = slots;
+    w.a_vcap = vcap;
+    w.a_ccap = ccap;
+  }
+  async_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n, w.X.as<int32_t>(),
+                                     w.aflag.as<uint32_t>(), w.avq.as<uint32_t>(),
+                                     (uint32_t)(w.a_vcap - 1), w.actl.as<AsyncCtl>(), fast);
+  AsyncArgs a;
+  a.g = g;
+  a.qp = w.params.as<QueryParam>();
+  a.X = w.X.as<int32_t>();
+  a.EP = w.EP.as<int2>();
+  a.R = fast ? w.R.as<int32_t>() : nullptr;
+  a.flag = w.aflag.as<uint32_t>();
+  a.vq = w.avq.as<uint32_t>();
+  a.cq = w.acq.as<uint2>();
+  a.vmask = (uint32_t)(w.a_vcap - 1);
+  a.cmask = (uint32_t)(w.a_ccap - 1);
+  a.c = w.actl.as<AsyncCtl>();
+  a.n = G->n;
+  a.Q = P.Q;
+  a.strict = P.strict;
+  a.cutoff = (uint32_t)std::min<uint64_t>(G->index_cutoff, 0xffffffffULL);
+  a.fastest = fast ? 1 : 0;
+  a.n_cand = ncand;
+  a.cand_lo = w.cand_lo.as<uint32_t>();
+  a.cand_cnt = w.cand_cnt.as<uint32_t>();
+  a.cand_key = w.cand_key.as<int32_t>();
+  a.time_limit_ns = 20ull * 1000 * 1000 * 1000;  // watchdog: 20 s
+  if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
+  if (!fast || ncand) {
+    void* args[] = {&a};
+    TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel,
+                                          dim3(G->coop_blocks_async), dim3(kThreads), args, 0, s));
+  }
+  if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
+  w.last_async = true;
+  return TGXD_OK;
+}
+
 // Enqueues one traversal (init, seeds, the persistent kernel, widening into
 // out_dev). ev_k0/ev_k1 bracket the traversal kernel when non-null.
 static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int width,
@@ -402,6 +471,23 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
                                                  w.X.as<int32_t>(), w.fa.as<uint32_t>(),
                                                  w.ctl.as<Control>(), fast);
+  if (mode == TGXD_MODE_ASYNC) {
+    const int rc = launch_async(G, P, g, ncand, ev_k0, ev_k1);
+    if (rc) return rc;
+    if (out_dev) {
+      convert_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
+          P.kind, w.X.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr, slots, G->n,
+          w.seeds.as<Seed>(), out_dev, width);
+    }
+    TGXD_CUDA(cudaGetLastError());
+    w.last_kind = P.kind;
+    w.last_q = P.Q;
+    w.last_strict = P.strict;
+    w.last_params = P.qp;
+    if (fast) w.last_params[0].root = P.seeds[0].root;
+    return TGXD_OK;
+  }
+  w.last_async = false;
   TravArgs a;
   a.g = g;
   a.qp = w.params.as<QueryParam>();
@@ -468,6 +554,29 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
 }
 
 static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float total_ms) {
+  if (G->ws.last_async) {
+    AsyncCtl c;
+    TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.actl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
+    TGXD_CUDA(cudaStreamSynchronize(G->stream));
+    if (c.error) {
+      Workspace& w = G->ws;
+      async_reset_kernel<<<grid_for(std::max(w.a_vcap, w.a_ccap), G->sm_count), 256, 0,
+                           G->stream>>>(w.aflag.as<uint32_t>(), w.a_slots, w.avq.as<uint32_t>(),
+                                        w.a_vcap, w.acq.as<uint2>(), w.a_ccap,
+                                        w.actl.as<AsyncCtl>());
+      cudaStreamSynchronize(G->stream);
+      return fail(TGXD_ERR_CUDA, "async traversal watchdog expired");
+    }
+    if (!st) return TGXD_OK;
+    st->rounds = 0;
+    st->candidates = 0;
+    st->expansions = c.vpops + c.cpops;
+    st->edges_relaxed = c.edges;
+    st->index_lookups = c.index_lookups;
+    st->kernel_ms = kernel_ms;
+    st->total_ms = total_ms;
+    return TGXD_OK;
+  }
   Control c;
   TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ctl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
   TGXD_CUDA(cudaStreamSynchronize(G->stream));

@@ -64,6 +64,10 @@ struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
   DeviceBuffer X, EP, R, fa, fb, chunks, smalls, ctl, params, seeds;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
+  // asynchronous engine: queued flags, vertex / chunk rings, control block
+  DeviceBuffer aflag, avq, acq, actl;
+  uint64_t a_slots = 0, a_vcap = 0, a_ccap = 0;
+  bool last_async = false;
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
   unsigned long long* trace_dev = nullptr;
   DeviceBuffer wtrace;
@@ -110,6 +114,7 @@ struct tgxd_graph {
   cudaStream_t stream = nullptr;
   int sm_count = 0;
   int coop_blocks = 0;
+  int coop_blocks_async = 0;
   std::mutex mu;
   tgxd::Workspace ws;
 };

@@ -35,6 +35,8 @@
 // v satisfies Ex[v] == bound(X[v]). During relax, the atomicMin that returns
 // old with bound(old) == Ex[v] is therefore the first improvement of v in
 // this round: exactly one thread pushes v (claim_stamp, parallel.hpp:113-121).
+#pragma once
+
 #include <cooperative_groups.h>
 
 #include "tgxd_internal.cuh"
