@@ -567,6 +567,12 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
       cudaStreamSynchronize(G->stream);
       return fail(TGXD_ERR_CUDA, "async traversal watchdog expired");
     }
+    if (c.bad[0]) {
+      char msg[256];
+      snprintf(msg, sizeof msg, "async validation failed: kind %llu a=%llu b=%llx c=%llx", c.bad[0],
+               c.bad[1], c.bad[2], c.bad[3]);
+      return fail(TGXD_ERR_CUDA, msg);
+    }
     if (!st) return TGXD_OK;
     st->rounds = 0;
     st->candidates = 0;

@@ -48,6 +48,7 @@ struct AsyncCtl {
   unsigned long long edges;
   unsigned long long index_lookups;
   unsigned long long vpops, cpops;
+  unsigned long long bad[4];  // TGXD_VALIDATE: first violation {kind, a, b, c}
 };
 
 struct AsyncArgs {
@@ -136,6 +137,11 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     const int32_t vhi = a.Q == 1 ? rx.vhi0 : __ldg(&a.qp[q[u]].vhi);
+#ifdef TGXD_VALIDATE
+    if (act[u] && __ldg(a.g.key + e[u]) < a.qp[q[u]].klo && atomicCAS(&a.c->bad[0], 0ull, 1ull) == 0)
+      a.c->bad[1] = e[u], a.c->bad[2] = (unsigned long long)(long long)__ldg(a.g.key + e[u]),
+      a.c->bad[3] = q[u];
+#endif
     if (!(act[u] && v[u] <= vhi)) v[u] = kInf;  // window containment (types.hpp:55-57)
     cur[u] = v[u] != kInf ? ld_state(a.X + idx[u], rx.pol_keep) : kInf;
   }
@@ -249,6 +255,14 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
           }
           p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
           pos = p0;
+#ifdef TGXD_VALIDATE
+          bool badr = p0 > p1 || p1 > t || p0 < s;
+          if (!badr && p0 < p1) badr = __ldg(a.g.key + p0) < lb || __ldg(a.g.key + p1 - 1) >= hik;
+          if (!badr && p0 > s) badr = __ldg(a.g.key + p0 - 1) >= lb;
+          if (badr && atomicCAS(&a.c->bad[0], 0ull, 2ull) == 0)
+            a.c->bad[1] = item, a.c->bad[2] = ((unsigned long long)p0 << 32) | p1,
+            a.c->bad[3] = ((unsigned long long)(uint32_t)lb << 32) | (uint32_t)hik;
+#endif
         }
       }
       a.EP[item] = make_int2(lb, (int32_t)pos);
@@ -423,6 +437,7 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, 
   c->index_lookups = 0;
   c->vpops = 0;
   c->cpops = 0;
+  c->bad[0] = c->bad[1] = c->bad[2] = c->bad[3] = 0;
   c->pending.v = 0;
   c->vhead.v = c->vtail.v;
   c->chead.v = c->ctail.v;
