@@ -168,6 +168,15 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
 __device__ __forceinline__ void relax_ranges_packed(const AsyncArgs& a, uint32_t lo, uint32_t cnt,
                                                     uint32_t rq, const ARelax& rx, VBuf& vb) {
   const uint32_t lane = lane_id();
+  // compact the non-empty ranges into the low lanes: the owner search below
+  // needs range l in lane l
+  const uint32_t nz = __ballot_sync(0xffffffffu, cnt != 0);
+  const uint32_t k = __popc(nz);
+  const uint32_t src = lane < k ? __fns(nz, 0, lane + 1) : 0u;
+  lo = __shfl_sync(0xffffffffu, lo, src);
+  rq = __shfl_sync(0xffffffffu, rq, src);
+  cnt = __shfl_sync(0xffffffffu, cnt, src);
+  if (lane >= k) cnt = 0;
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
