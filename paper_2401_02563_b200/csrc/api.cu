@@ -393,24 +393,26 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   cudaStream_t s = G->stream;
   const bool fast = P.kind == TGXD_FASTEST;
   const uint64_t slots = (uint64_t)P.Q * G->n;
-  const uint64_t vcap = next_pow2(slots + 64);
-  // outstanding chunks <= ranges of >= kAInline edges + their chunks
-  const uint64_t ccap = next_pow2((uint64_t)P.Q * (G->m / kAInline + G->m / kAChunk) + 1024);
-  if (w.a_slots < slots || w.a_vcap < vcap || w.a_ccap < ccap) {
-    if (!dalloc<uint32_t>(w.aflag, slots) || !dalloc<uint32_t>(w.avq, vcap) ||
-        !dalloc<uint2>(w.acq, ccap) || !dalloc<AsyncCtl>(w.actl, 1))
-      return fail(TGXD_ERR_CUDA, "device allocation failed (async queues)");
+  // outstanding units <= batches (<= one per queued slot) + chunks (ranges of
+  // >= kAInline edges and their 512-edge pieces) + staging slack
+  const uint64_t nunits =
+      next_pow2(slots + (uint64_t)P.Q * (G->m / kAInline + G->m / kAChunk) +
+                4ull * G->coop_blocks_async * kWarps + 64);
+  if (nunits > (1ull << 26))
+    return fail(TGXD_ERR_UNSUPPORTED, "async engine: batch too large (use a round-based mode)");
+  if (w.a_slots < slots || w.a_units < nunits) {
+    if (!dalloc<uint32_t>(w.aflag, slots) || !dalloc<uint32_t>(w.aunits, nunits * kUnitWords) ||
+        !dalloc<AsyncCtl>(w.actl, 1))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (async queue)");
     TGXD_CUDA(cudaMemsetAsync(w.actl.p, 0, sizeof(AsyncCtl), s));
-    async_reset_kernel<<<grid_for(std::max(vcap, ccap), G->sm_count), 256, 0, s>>>(
-        w.aflag.as<uint32_t>(), slots, w.avq.as<uint32_t>(), vcap, w.acq.as<uint2>(), ccap,
-        w.actl.as<AsyncCtl>());
+    async_reset_kernel<<<grid_for(std::max(slots, nunits), G->sm_count), 256, 0, s>>>(
+        w.aflag.as<uint32_t>(), slots, w.aunits.as<uint32_t>(), nunits, w.actl.as<AsyncCtl>());
     w.a_slots = slots;
-    w.a_vcap = vcap;
-    w.a_ccap = ccap;
+    w.a_units = nunits;
   }
   async_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n, w.X.as<int32_t>(),
-                                     w.aflag.as<uint32_t>(), w.avq.as<uint32_t>(),
-                                     (uint32_t)(w.a_vcap - 1), w.actl.as<AsyncCtl>(), fast);
+                                     w.aflag.as<uint32_t>(), w.aunits.as<uint32_t>(),
+                                     w.a_units - 1, w.actl.as<AsyncCtl>(), fast);
   AsyncArgs a;
   a.g = g;
   a.qp = w.params.as<QueryParam>();
@@ -418,10 +420,8 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   a.EP = w.EP.as<int2>();
   a.R = fast ? w.R.as<int32_t>() : nullptr;
   a.flag = w.aflag.as<uint32_t>();
-  a.vq = w.avq.as<uint32_t>();
-  a.cq = w.acq.as<uint2>();
-  a.vmask = (uint32_t)(w.a_vcap - 1);
-  a.cmask = (uint32_t)(w.a_ccap - 1);
+  a.units = w.aunits.as<uint32_t>();
+  a.umask = w.a_units - 1;
   a.c = w.actl.as<AsyncCtl>();
   a.n = G->n;
   a.Q = P.Q;
@@ -560,10 +560,9 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
     if (c.error) {
       Workspace& w = G->ws;
-      async_reset_kernel<<<grid_for(std::max(w.a_vcap, w.a_ccap), G->sm_count), 256, 0,
-                           G->stream>>>(w.aflag.as<uint32_t>(), w.a_slots, w.avq.as<uint32_t>(),
-                                        w.a_vcap, w.acq.as<uint2>(), w.a_ccap,
-                                        w.actl.as<AsyncCtl>());
+      async_reset_kernel<<<grid_for(std::max(w.a_slots, w.a_units), G->sm_count), 256, 0,
+                           G->stream>>>(w.aflag.as<uint32_t>(), w.a_slots, w.aunits.as<uint32_t>(),
+                                        w.a_units, w.actl.as<AsyncCtl>());
       cudaStreamSynchronize(G->stream);
       return fail(TGXD_ERR_CUDA, "async traversal watchdog expired");
     }
@@ -576,7 +575,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     if (!st) return TGXD_OK;
     st->rounds = 0;
     st->candidates = 0;
-    st->expansions = c.vpops + c.cpops;
+    st->expansions = c.batches + c.chunks;
     st->edges_relaxed = c.edges;
     st->index_lookups = c.index_lookups;
     st->kernel_ms = kernel_ms;

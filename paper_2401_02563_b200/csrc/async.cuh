@@ -1,16 +1,19 @@
 // Asynchronous (barrier-free) traversal — the same fixpoint as traverse.cuh
 // without rounds.
 //
-// Every warp loops over two multi-producer / multi-consumer ring queues:
-//   CQ  edge chunks (up to kAChunk edges of one vertex's admissible range),
-//   VQ  vertex slots whose label improved since their last expansion.
-// A warp pops a chunk and relaxes it, or pops up to 32 vertices, expands
-// them (the same key-range search and selective index as the round kernel),
-// relaxes their short ranges itself (packed 32 ranges per warp) and pushes
-// long ranges to CQ as chunks. Improved vertices are enqueued once per
-// improvement "epoch": a per-slot queued flag is set with atomicExch by the
-// improver and cleared (then fenced) by the expander before it reads the
-// label, so no improvement is ever left unexpanded.
+// All warps share ONE ticket queue of 64-byte work units:
+//   * a vertex batch — up to kBatch slots whose label improved since their
+//     last expansion, or
+//   * an edge chunk — up to kAChunk edges of one vertex's admissible range.
+// A warp takes the next ticket with one atomicAdd, waits on that unit's
+// header (its own address: no hot spot), and processes it: a chunk is
+// relaxed; a batch is expanded (the same key-range search and selective
+// index as the round kernel), its short ranges relaxed by the warp itself
+// (packed 32 ranges per warp) and its long ranges published as chunks.
+// Improved vertices are enqueued once per improvement "epoch": a per-slot
+// queued flag is set with atomicExch by the improver and cleared (then
+// fenced) by the expander before it reads the label, so no improvement is
+// ever left unexpanded.
 //
 // Work efficiency is unchanged: an expansion only walks keys in
 // [bound, previous bound), so every admissible edge is relaxed once per
@@ -18,10 +21,11 @@
 // which is idempotent). Labels are the unique least fixpoint
 // — bit-identical to the reference.
 //
-// Termination: `pending` counts items that exist (queued, staged or being
+// Termination: `pending` counts units that exist (published or being
 // processed). Producers add before publishing; a warp subtracts what it has
-// completed only when it is idle with empty staging buffers, so pending
-// reaches zero exactly when all work is done.
+// completed only while it waits with nothing staged. The warp whose
+// subtraction reaches zero raises `quiesce`; waiting warps abandon their
+// tickets (the next query or candidate restarts the queue at its tail).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -30,10 +34,12 @@
 
 namespace tgxd {
 
-constexpr uint32_t kAChunk = 512;        // edges per async chunk (4 x 128-edge bursts)
+constexpr uint32_t kAChunk = 512;        // edges per chunk unit (4 x 128-edge bursts)
 constexpr uint32_t kAInline = 64;        // shorter ranges are relaxed by the expanding warp
-constexpr uint32_t kAChunkLenBits = 10;  // len <= 512
+constexpr uint32_t kUnitWords = 16;      // 64-byte units
+constexpr uint32_t kBatch = kUnitWords - 1;  // vertices per batch unit
 constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr uint32_t kChunkTag = 0x80000000u;  // header: tag | q << 10 | len (len <= 512)
 
 struct alignas(128) PaddedCounter {
   unsigned long long v;
@@ -41,13 +47,14 @@ struct alignas(128) PaddedCounter {
 };
 
 struct AsyncCtl {
-  PaddedCounter vhead, vtail, chead, ctail, pending;
+  PaddedCounter head, tail, pending;
+  alignas(128) unsigned int quiesce;  // epoch whose work is complete
   unsigned int abort;
   unsigned int error;
-  unsigned long long expansions;
+  unsigned int pad0;
   unsigned long long edges;
   unsigned long long index_lookups;
-  unsigned long long vpops, cpops;
+  unsigned long long batches, chunks;
   unsigned long long bad[4];  // TGXD_VALIDATE: first violation {kind, a, b, c}
 };
 
@@ -58,9 +65,8 @@ struct AsyncArgs {
   int2* EP;
   int32_t* R;
   uint32_t* flag;   // per slot: 1 while queued
-  uint32_t* vq;     // vertex ring, kEmpty when free
-  uint2* cq;        // chunk ring, .y == kEmpty when free
-  uint32_t vmask, cmask;
+  uint32_t* units;  // ring of 64-byte units, header word kEmpty when free
+  unsigned long long umask;
   AsyncCtl* c;
   uint32_t n, Q;
   int strict;
@@ -79,6 +85,16 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
+__device__ __forceinline__ uint32_t* unit_ptr(const AsyncArgs& a, unsigned long long pos) {
+  return a.units + (pos & a.umask) * kUnitWords;
+}
+
+// Reserves k units: counted as pending before they can be seen.
+__device__ __forceinline__ unsigned long long reserve_units(const AsyncArgs& a, uint32_t k) {
+  atomicAdd(&a.c->pending.v, (unsigned long long)k);
+  __threadfence();
+  return atomicAdd(&a.c->tail.v, (unsigned long long)k);
+}
 
 // Per-warp staging of vertex pushes (64 entries of shared memory).
 struct VBuf {
@@ -86,31 +102,31 @@ struct VBuf {
   uint32_t n;  // warp-uniform
 };
 
-__device__ __forceinline__ void vq_flush(const AsyncArgs& a, VBuf& vb, uint32_t count) {
+// Publishes the first `count` (<= kBatch) staged vertices as one batch unit.
+__device__ __forceinline__ void vb_publish(const AsyncArgs& a, VBuf& vb, uint32_t count) {
   const uint32_t lane = lane_id();
   __syncwarp();
   const uint32_t v = vb.buf[lane];
-  const uint32_t tail = vb.buf[32 + lane];
-  unsigned long long base = 0;
-  if (lane == 0) {
-    atomicAdd(&a.c->pending.v, (unsigned long long)count);  // before the items exist
-    __threadfence();
-    base = atomicAdd(&a.c->vtail.v, (unsigned long long)count);
-  }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (lane < count) st_volatile(a.vq + ((base + lane) & a.vmask), v);
+  const uint32_t rest = vb.buf[(lane + count) & 63];
+  unsigned long long pos = 0;
+  if (lane == 0) pos = reserve_units(a, 1);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  uint32_t* u = unit_ptr(a, pos);
+  if (lane < count) u[1 + lane] = v;
+  __threadfence();
   __syncwarp();
-  if (lane + count < vb.n) vb.buf[lane] = tail;
+  if (lane == 0) st_volatile(u, count);
+  if (lane + count < vb.n) vb.buf[lane] = rest;
   vb.n -= count;
   __syncwarp();
 }
 
-__device__ __forceinline__ void vq_append(const AsyncArgs& a, VBuf& vb, bool p, uint32_t item) {
+__device__ __forceinline__ void vb_append(const AsyncArgs& a, VBuf& vb, bool p, uint32_t item) {
   const uint32_t bal = __ballot_sync(0xffffffffu, p);
   if (bal == 0) return;
   if (p) vb.buf[vb.n + __popc(bal & ((1u << lane_id()) - 1))] = item;
   vb.n += __popc(bal);
-  if (vb.n >= 32) vq_flush(a, vb, 32);
+  while (vb.n >= kBatch) vb_publish(a, vb, kBatch);
 }
 
 struct ARelax {
@@ -159,17 +175,16 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
     }
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) vq_append(a, vb, was[u] == 0u, idx[u]);
+  for (int u = 0; u < kUnroll; ++u) vb_append(a, vb, was[u] == 0u, idx[u]);
 }
 
-// Relax ranges given one per lane (lo, cnt, q), packed 32 per warp: lane l
-// owns range l, items are numbered densely and each lane finds its owner
+// Relax ranges given one per lane (lo, cnt, q), packed 32 per warp: range l
+// sits in lane l, items are numbered densely and each lane finds its owner
 // from the redux.or mask of range starts (as phase_b's small windows).
 __device__ __forceinline__ void relax_ranges_packed(const AsyncArgs& a, uint32_t lo, uint32_t cnt,
                                                     uint32_t rq, const ARelax& rx, VBuf& vb) {
   const uint32_t lane = lane_id();
-  // compact the non-empty ranges into the low lanes: the owner search below
-  // needs range l in lane l
+  // compact the non-empty ranges into the low lanes
   const uint32_t nz = __ballot_sync(0xffffffffu, cnt != 0);
   const uint32_t k = __popc(nz);
   const uint32_t src = lane < k ? __fns(nz, 0, lane + 1) : 0u;
@@ -210,7 +225,7 @@ __device__ __forceinline__ void relax_ranges_packed(const AsyncArgs& a, uint32_t
 }
 
 // Relax one contiguous range [lo, lo + len) of query slot q (a chunk, or a
-// seed range), 128 edges per step.
+// seed piece), 128 edges per step.
 __device__ __forceinline__ void relax_span(const AsyncArgs& a, uint32_t lo, uint32_t len,
                                            uint32_t q, const ARelax& rx, VBuf& vb) {
   const uint32_t lane = lane_id();
@@ -228,7 +243,7 @@ __device__ __forceinline__ void relax_span(const AsyncArgs& a, uint32_t lo, uint
   }
 }
 
-// Expansion of up to 32 popped slots (one per lane).
+// Expansion of one batch (one slot per lane, `valid` lanes only).
 __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uint32_t item,
                                              const ARelax& rx, VBuf& vb,
                                              unsigned long long& work, unsigned long long& ix) {
@@ -245,6 +260,7 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
     q = a.Q == 1 ? 0u : item / a.n;
     const uint32_t v = item - q * a.n;
     const QueryParam& qp = a.qp[q];
+    // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342)
     int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
     if (lb < qp.klo) lb = qp.klo;
     const int32_t old = ep.x;
@@ -264,14 +280,6 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
           }
           p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
           pos = p0;
-#ifdef TGXD_VALIDATE
-          bool badr = p0 > p1 || p1 > t || p0 < s;
-          if (!badr && p0 < p1) badr = __ldg(a.g.key + p0) < lb || __ldg(a.g.key + p1 - 1) >= hik;
-          if (!badr && p0 > s) badr = __ldg(a.g.key + p0 - 1) >= lb;
-          if (badr && atomicCAS(&a.c->bad[0], 0ull, 2ull) == 0)
-            a.c->bad[1] = item, a.c->bad[2] = ((unsigned long long)p0 << 32) | p1,
-            a.c->bad[3] = ((unsigned long long)(uint32_t)lb << 32) | (uint32_t)hik;
-#endif
         }
       }
       a.EP[item] = make_int2(lb, (int32_t)pos);
@@ -279,7 +287,7 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
   }
   const uint32_t cnt = act ? p1 - p0 : 0u;
   work += cnt;
-  // long ranges: chunks to CQ (one reservation for the whole warp)
+  // long ranges: chunk units (one reservation for the whole warp)
   const uint32_t nch = cnt >= kAInline ? (cnt + kAChunk - 1) / kAChunk : 0u;
   uint32_t incl = nch;
 #pragma unroll
@@ -290,18 +298,13 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
   const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
   if (tot) {
     unsigned long long base = 0;
-    if (lane == 0) {
-      atomicAdd(&a.c->pending.v, (unsigned long long)tot);
-      __threadfence();
-      base = atomicAdd(&a.c->ctail.v, (unsigned long long)tot);
-    }
+    if (lane == 0) base = reserve_units(a, tot);
     base = __shfl_sync(0xffffffffu, base, 0) + incl - nch;
-    for (uint32_t j = 0; j < nch; ++j)  // payload words first ...
-      a.cq[(base + j) & a.cmask].x = p0 + j * kAChunk;
+    for (uint32_t j = 0; j < nch; ++j) unit_ptr(a, base + j)[1] = p0 + j * kAChunk;
     __threadfence();
-    for (uint32_t j = 0; j < nch; ++j)  // ... then the words that publish them
-      st_volatile(&a.cq[(base + j) & a.cmask].y,
-                  (q << kAChunkLenBits) | min(kAChunk, cnt - j * kAChunk));
+    for (uint32_t j = 0; j < nch; ++j)
+      st_volatile(unit_ptr(a, base + j),
+                  kChunkTag | (q << 10) | min(kAChunk, cnt - j * kAChunk));
   }
   // short ranges: relaxed right here
   const bool inl = cnt != 0 && cnt < kAInline;
@@ -309,86 +312,65 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
     relax_ranges_packed(a, inl ? p0 : 0u, inl ? cnt : 0u, q, rx, vb);
 }
 
-// Claims up to `want` consecutive queue positions; returns how many (uniform).
-__device__ __forceinline__ uint32_t claim(unsigned long long* head, unsigned long long* tailp,
-                                          uint32_t want, unsigned long long& h_out) {
-  unsigned long long h = 0;
-  uint32_t take = 0;
-  if (lane_id() == 0) {
-    h = __ldcg(head);
-    const unsigned long long t = __ldcg(tailp);
-    if (t > h) {
-      take = (uint32_t)((t - h) < want ? (t - h) : want);
-      if (atomicCAS(head, h, h + take) != h) take = 0;
-    }
-  }
-  take = __shfl_sync(0xffffffffu, take, 0);
-  h_out = __shfl_sync(0xffffffffu, h, 0);
-  return take;
-}
-
-__device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb,
+// Takes tickets and processes their units until the epoch's work is done.
+__device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint32_t epoch,
                            unsigned long long t_deadline, unsigned long long& done,
                            unsigned long long& work, unsigned long long& ix,
-                           unsigned long long& vpops, unsigned long long& cpops) {
+                           unsigned long long& nb, unsigned long long& nc) {
   const uint32_t lane = lane_id();
-  uint32_t idle_ns = 0;
   for (;;) {
-    if (ld_volatile(&a.c->abort)) return;
-    unsigned long long h;
-    // chunks first: edge work that is ready
-    if (claim(&a.c->chead.v, &a.c->ctail.v, 1, h)) {
-      uint2* slot = a.cq + (h & a.cmask);
-      uint32_t y = kEmpty;
-      uint32_t x = 0;
-      if (lane == 0) {
-        while ((y = ld_volatile(&slot->y)) == kEmpty) {}
-        __threadfence();
-        x = ld_volatile(&slot->x);
-        st_volatile(&slot->y, kEmpty);
+    unsigned long long h = 0;
+    if (lane == 0) h = atomicAdd(&a.c->head.v, 1ull);
+    h = __shfl_sync(0xffffffffu, h, 0);
+    uint32_t* u = unit_ptr(a, h);
+    uint32_t hdr = kEmpty;
+    uint32_t polls = 0;
+    for (;;) {  // wait for the ticket's unit
+      if (lane == 0) hdr = ld_volatile(u);
+      hdr = __shfl_sync(0xffffffffu, hdr, 0);
+      if (hdr != kEmpty) break;
+      // nothing staged or unsubtracted may be held while waiting
+      if (vb.n) {
+        vb_publish(a, vb, vb.n);
+        continue;
       }
-      y = __shfl_sync(0xffffffffu, y, 0);
-      x = __shfl_sync(0xffffffffu, x, 0);
-      relax_span(a, x, y & ((1u << kAChunkLenBits) - 1), y >> kAChunkLenBits, rx, vb);
-      ++done;
-      ++cpops;
-      idle_ns = 0;
-      continue;
-    }
-    const uint32_t take = claim(&a.c->vhead.v, &a.c->vtail.v, 32, h);
-    if (take) {
-      uint32_t item = 0;
-      if (lane < take) {
-        uint32_t* slot = a.vq + ((h + lane) & a.vmask);
-        while ((item = ld_volatile(slot)) == kEmpty) {}
-        st_volatile(slot, kEmpty);
+      if (done) {
+        if (lane == 0) {
+          __threadfence();
+          const unsigned long long before = atomicAdd(&a.c->pending.v, 0ull - done);
+          if (before == done) st_volatile(&a.c->quiesce, epoch);  // the last unit is done
+        }
+        done = 0;
+        continue;
       }
-      expand_batch(a, lane < take, item, rx, vb, work, ix);
-      done += take;
-      ++vpops;
-      idle_ns = 0;
-      continue;
-    }
-    // idle: publish staged pushes and completed work, then test for the end
-    if (vb.n) vq_flush(a, vb, vb.n);
-    if (done) {
-      if (lane == 0) {
-        __threadfence();
-        atomicAdd(&a.c->pending.v, (unsigned long long)(0ull - done));
+      ++polls;
+      uint32_t stop = 0;
+      if (lane == 0 && (polls & 15) == 0) {
+        stop = ld_volatile(&a.c->quiesce) == epoch || ld_volatile(&a.c->abort);
+        if (!stop && gtimer() > t_deadline) {
+          a.c->error = 1;
+          st_volatile(&a.c->abort, 1u);
+          stop = 1;
+        }
       }
-      done = 0;
-      continue;  // look again before sleeping: others may be waiting on us
+      if (__shfl_sync(0xffffffffu, stop, 0)) return;
+      __nanosleep(polls < 64 ? 64 : 512);
     }
-    unsigned long long p = 0;
-    if (lane == 0) p = __ldcg(&a.c->pending.v);
-    p = __shfl_sync(0xffffffffu, p, 0);
-    if (p == 0) return;
-    if (idle_ns) __nanosleep(idle_ns);
-    idle_ns = min(2 * idle_ns + 64, 2048u);
-    if (lane == 0 && gtimer() > t_deadline) {
-      a.c->error = 1;
-      a.c->abort = 1;
+    __threadfence();
+    if (hdr & kChunkTag) {
+      const uint32_t lo = ld_volatile(u + 1);
+      __syncwarp();
+      if (lane == 0) st_volatile(u, kEmpty);
+      relax_span(a, lo, hdr & 1023u, (hdr & ~kChunkTag) >> 10, rx, vb);
+      ++nc;
+    } else {
+      const uint32_t item = lane < hdr ? ld_volatile(u + 1 + lane) : 0u;
+      __syncwarp();
+      if (lane == 0) st_volatile(u, kEmpty);
+      expand_batch(a, lane < hdr, item, rx, vb, work, ix);
+      ++nb;
     }
+    ++done;
   }
 }
 
@@ -398,11 +380,11 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
   VBuf vb{s_vb[threadIdx.x >> 5], 0};
   const unsigned long long t_deadline = gtimer() + a.time_limit_ns;
   ARelax rx{a.qp[0].vhi, 0, policy_evict_first(), policy_evict_last()};
-  unsigned long long done = 0, work = 0, ix = 0, vpops = 0, cpops = 0;
+  unsigned long long done = 0, work = 0, ix = 0, nb = 0, nc = 0;
   const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kWarps;
   if (!a.fastest) {
-    async_loop(a, rx, vb, t_deadline, done, work, ix, vpops, cpops);
+    async_loop(a, rx, vb, 1, t_deadline, done, work, ix, nb, nc);
   } else {
     for (uint32_t cand = 0; cand < a.n_cand; ++cand) {
       // Seeds (path_algorithms.cpp:476-486): the candidate's first edges,
@@ -411,14 +393,15 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
       const uint32_t lo = a.cand_lo[cand], cnt = a.cand_cnt[cand];
       const uint32_t pieces = (cnt + 127) / 128;
       const uint32_t mine = gw < pieces ? (pieces - gw + nw - 1) / nw : 0u;
-      grid.sync();  // the previous candidate is fully drained everywhere
+      grid.sync();  // the previous candidate is drained everywhere
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.c->head.v = a.c->tail.v;  // drop idle tickets
       if (lane_id() == 0 && mine) atomicAdd(&a.c->pending.v, (unsigned long long)mine);
-      grid.sync();  // no warp sees pending == 0 before all seeds are counted
+      grid.sync();  // every seed piece is counted before anyone can see zero
       for (uint32_t pc = gw; pc < pieces; pc += nw) {
         relax_span(a, lo + pc * 128, min(128u, cnt - pc * 128), 0, rx, vb);
         ++done;
       }
-      async_loop(a, rx, vb, t_deadline, done, work, ix, vpops, cpops);
+      async_loop(a, rx, vb, cand + 1, t_deadline, done, work, ix, nb, nc);
       if (ld_volatile(&a.c->abort)) break;
     }
   }
@@ -430,48 +413,54 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
   if (lane_id() == 0) {
     if (work) atomicAdd(&a.c->edges, work);
     if (ix) atomicAdd(&a.c->index_lookups, ix);
-    if (vpops) atomicAdd(&a.c->vpops, vpops);
-    if (cpops) atomicAdd(&a.c->cpops, cpops);
+    if (nb) atomicAdd(&a.c->batches, nb);
+    if (nc) atomicAdd(&a.c->chunks, nc);
   }
 }
 
-// Seeds of an async EA / LD query: X[root] = klo, roots queued.
+// Query start: counters, and for EA / LD the roots as the first batch units.
 __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_t* X,
-                                  uint32_t* flag, uint32_t* vq, uint32_t vmask, AsyncCtl* c,
-                                  int fastest) {
+                                  uint32_t* flag, uint32_t* units, unsigned long long umask,
+                                  AsyncCtl* c, int fastest) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   c->abort = 0;
   c->error = 0;
+  c->quiesce = 0;
   c->edges = 0;
   c->index_lookups = 0;
-  c->vpops = 0;
-  c->cpops = 0;
+  c->batches = 0;
+  c->chunks = 0;
   c->bad[0] = c->bad[1] = c->bad[2] = c->bad[3] = 0;
   c->pending.v = 0;
-  c->vhead.v = c->vtail.v;
-  c->chead.v = c->ctail.v;
+  c->head.v = c->tail.v;  // tickets left waiting by the previous query are void
   if (fastest) return;
-  const unsigned long long t = c->vtail.v;
-  for (uint32_t q = 0; q < Q; ++q) {
-    const uint32_t item = q * n + qp[q].root;
-    X[item] = qp[q].klo;
-    flag[item] = 1u;
-    vq[(t + q) & vmask] = item;
+  unsigned long long t = c->tail.v;
+  uint32_t nu = 0;
+  for (uint32_t q0 = 0; q0 < Q; q0 += kBatch, ++nu) {
+    uint32_t* u = units + ((t + nu) & umask) * kUnitWords;
+    const uint32_t k = min(kBatch, Q - q0);
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t item = (q0 + j) * n + qp[q0 + j].root;
+      X[item] = qp[q0 + j].klo;
+      flag[item] = 1u;
+      u[1 + j] = item;
+    }
+    u[0] = k;
   }
-  c->vtail.v = t + Q;
-  c->pending.v = Q;
+  c->tail.v = t + nu;
+  c->pending.v = nu;
 }
 
-// After a watchdog abort the rings and flags may hold stale entries.
-__global__ void async_reset_kernel(uint32_t* flag, size_t slots, uint32_t* vq, size_t vcap,
-                                   uint2* cq, size_t ccap, AsyncCtl* c) {
+// Fresh (or post-abort) queue state: flags clear, every unit free.
+__global__ void async_reset_kernel(uint32_t* flag, size_t slots, uint32_t* units, size_t nunits,
+                                   AsyncCtl* c) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += stride) flag[i] = 0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < vcap; i += stride) vq[i] = kEmpty;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < ccap; i += stride)
-    cq[i] = make_uint2(0u, kEmpty);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += stride)
+    flag[i] = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nunits; i += stride)
+    units[i * kUnitWords] = kEmpty;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c->vhead.v = c->vtail.v = c->chead.v = c->ctail.v = 0;
+    c->head.v = c->tail.v = 0;
     c->pending.v = 0;
   }
 }
