@@ -572,6 +572,9 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
                c.bad[1], c.bad[2], c.bad[3]);
       return fail(TGXD_ERR_CUDA, msg);
     }
+    if (getenv("TGXD_ASTATS"))
+      fprintf(stderr, "async: batches %llu chunks %llu edges %llu wait %.3f ms busy %.3f ms (warp-sum)\n",
+              c.batches, c.chunks, c.edges, c.wait_ns / 1e6, c.busy_ns / 1e6);
     if (!st) return TGXD_OK;
     st->rounds = 0;
     st->candidates = 0;

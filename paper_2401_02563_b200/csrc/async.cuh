@@ -55,6 +55,7 @@ struct AsyncCtl {
   unsigned long long edges;
   unsigned long long index_lookups;
   unsigned long long batches, chunks;
+  unsigned long long wait_ns, busy_ns, t_first, t_last;  // time accounting
   unsigned long long bad[4];  // TGXD_VALIDATE: first violation {kind, a, b, c}
 };
 
@@ -316,9 +317,11 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
 __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint32_t epoch,
                            unsigned long long t_deadline, unsigned long long& done,
                            unsigned long long& work, unsigned long long& ix,
-                           unsigned long long& nb, unsigned long long& nc) {
+                           unsigned long long& nb, unsigned long long& nc,
+                           unsigned long long& wait_ns, unsigned long long& busy_ns) {
   const uint32_t lane = lane_id();
   for (;;) {
+    const unsigned long long t0 = gtimer();
     unsigned long long h = 0;
     if (lane == 0) h = atomicAdd(&a.c->head.v, 1ull);
     h = __shfl_sync(0xffffffffu, h, 0);
@@ -353,9 +356,14 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
           stop = 1;
         }
       }
-      if (__shfl_sync(0xffffffffu, stop, 0)) return;
+      if (__shfl_sync(0xffffffffu, stop, 0)) {
+        wait_ns += gtimer() - t0;
+        return;
+      }
       __nanosleep(polls < 64 ? 64 : 512);
     }
+    const unsigned long long t1 = gtimer();
+    wait_ns += t1 - t0;
     __threadfence();
     if (hdr & kChunkTag) {
       const uint32_t lo = ld_volatile(u + 1);
@@ -371,6 +379,7 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
       ++nb;
     }
     ++done;
+    busy_ns += gtimer() - t1;
   }
 }
 
@@ -380,11 +389,11 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
   VBuf vb{s_vb[threadIdx.x >> 5], 0};
   const unsigned long long t_deadline = gtimer() + a.time_limit_ns;
   ARelax rx{a.qp[0].vhi, 0, policy_evict_first(), policy_evict_last()};
-  unsigned long long done = 0, work = 0, ix = 0, nb = 0, nc = 0;
+  unsigned long long done = 0, work = 0, ix = 0, nb = 0, nc = 0, wait_ns = 0, busy_ns = 0;
   const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kWarps;
   if (!a.fastest) {
-    async_loop(a, rx, vb, 1, t_deadline, done, work, ix, nb, nc);
+    async_loop(a, rx, vb, 1, t_deadline, done, work, ix, nb, nc, wait_ns, busy_ns);
   } else {
     for (uint32_t cand = 0; cand < a.n_cand; ++cand) {
       // Seeds (path_algorithms.cpp:476-486): the candidate's first edges,
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
         relax_span(a, lo + pc * 128, min(128u, cnt - pc * 128), 0, rx, vb);
         ++done;
       }
-      async_loop(a, rx, vb, cand + 1, t_deadline, done, work, ix, nb, nc);
+      async_loop(a, rx, vb, cand + 1, t_deadline, done, work, ix, nb, nc, wait_ns, busy_ns);
       if (ld_volatile(&a.c->abort)) break;
     }
   }
@@ -415,6 +424,8 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
     if (ix) atomicAdd(&a.c->index_lookups, ix);
     if (nb) atomicAdd(&a.c->batches, nb);
     if (nc) atomicAdd(&a.c->chunks, nc);
+    atomicAdd(&a.c->wait_ns, wait_ns);
+    atomicAdd(&a.c->busy_ns, busy_ns);
   }
 }
 
@@ -430,6 +441,8 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, 
   c->index_lookups = 0;
   c->batches = 0;
   c->chunks = 0;
+  c->wait_ns = 0;
+  c->busy_ns = 0;
   c->bad[0] = c->bad[1] = c->bad[2] = c->bad[3] = 0;
   c->pending.v = 0;
   c->head.v = c->tail.v;  // tickets left waiting by the previous query are void
