@@ -86,14 +86,36 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
+// Release / acquire primitives (PTX memory model): cheaper than the full
+// fences they replace, and exactly the orderings the handoffs need.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t exch_release(uint32_t* p, uint32_t v) {
+  uint32_t o;
+  asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+  return o;
+}
+__device__ __forceinline__ uint32_t exch_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t o;
+  asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+  return o;
+}
 __device__ __forceinline__ uint32_t* unit_ptr(const AsyncArgs& a, unsigned long long pos) {
   return a.units + (pos & a.umask) * kUnitWords;
 }
 
-// Reserves k units: counted as pending before they can be seen.
+// Reserves k units, counted as pending. No fence is needed between the two
+// atomics: a unit's consumer can only drive pending to zero after the
+// producer's own (still unsubtracted) unit is done, and the producer's later
+// subtraction is ordered after its addition (same address).
 __device__ __forceinline__ unsigned long long reserve_units(const AsyncArgs& a, uint32_t k) {
   atomicAdd(&a.c->pending.v, (unsigned long long)k);
-  __threadfence();
   return atomicAdd(&a.c->tail.v, (unsigned long long)k);
 }
 
@@ -114,9 +136,8 @@ __device__ __forceinline__ void vb_publish(const AsyncArgs& a, VBuf& vb, uint32_
   pos = __shfl_sync(0xffffffffu, pos, 0);
   uint32_t* u = unit_ptr(a, pos);
   if (lane < count) u[1 + lane] = v;
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_volatile(u, count);
+  __syncwarp();                            // payload words happen-before ...
+  if (lane == 0) st_release(u, count);     // ... the releasing header store
   if (lane + count < vb.n) vb.buf[lane] = rest;
   vb.n -= count;
   __syncwarp();
@@ -172,7 +193,7 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
     was[u] = 1u;
     if (v[u] < old[u]) {
       if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
-      was[u] = atomicExch(a.flag + idx[u], 1u);
+      was[u] = exch_release(a.flag + idx[u], 1u);  // the label update precedes the flag
     }
   }
 #pragma unroll
@@ -252,10 +273,10 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
   uint32_t q = 0, p0 = 0, p1 = 0;
   bool act = false;
   if (valid) {
-    // clear the queued flag before reading the label: an improvement after
-    // this point re-enqueues the slot
-    st_volatile(a.flag + item, 0u);
-    __threadfence();
+    // clear the queued flag before reading the label (acq_rel: the label
+    // load cannot move above it): an improvement after this point
+    // re-enqueues the slot, one before it is visible to the load below
+    exch_acq_rel(a.flag + item, 0u);
     const int32_t x = __ldcg(a.X + item);
     const int2 ep = __ldcg(a.EP + item);
     q = a.Q == 1 ? 0u : item / a.n;
@@ -301,11 +322,11 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
     unsigned long long base = 0;
     if (lane == 0) base = reserve_units(a, tot);
     base = __shfl_sync(0xffffffffu, base, 0) + incl - nch;
-    for (uint32_t j = 0; j < nch; ++j) unit_ptr(a, base + j)[1] = p0 + j * kAChunk;
-    __threadfence();
-    for (uint32_t j = 0; j < nch; ++j)
-      st_volatile(unit_ptr(a, base + j),
-                  kChunkTag | (q << 10) | min(kAChunk, cnt - j * kAChunk));
+    for (uint32_t j = 0; j < nch; ++j) {
+      uint32_t* cu = unit_ptr(a, base + j);
+      cu[1] = p0 + j * kAChunk;
+      st_release(cu, kChunkTag | (q << 10) | min(kAChunk, cnt - j * kAChunk));
+    }
   }
   // short ranges: relaxed right here
   const bool inl = cnt != 0 && cnt < kAInline;
@@ -329,7 +350,7 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
     uint32_t hdr = kEmpty;
     uint32_t polls = 0;
     for (;;) {  // wait for the ticket's unit
-      if (lane == 0) hdr = ld_volatile(u);
+      if (lane == 0) hdr = ld_acquire(u);
       hdr = __shfl_sync(0xffffffffu, hdr, 0);
       if (hdr != kEmpty) break;
       // nothing staged or unsubtracted may be held while waiting
@@ -339,7 +360,6 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
       }
       if (done) {
         if (lane == 0) {
-          __threadfence();
           const unsigned long long before = atomicAdd(&a.c->pending.v, 0ull - done);
           if (before == done) st_volatile(&a.c->quiesce, epoch);  // the last unit is done
         }
@@ -364,7 +384,7 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
     }
     const unsigned long long t1 = gtimer();
     wait_ns += t1 - t0;
-    __threadfence();
+    __syncwarp();  // lane 0's acquire orders the payload reads of every lane
     if (hdr & kChunkTag) {
       const uint32_t lo = ld_volatile(u + 1);
       __syncwarp();
