@@ -21,11 +21,12 @@
 // which is idempotent). Labels are the unique least fixpoint
 // — bit-identical to the reference.
 //
-// Termination: `pending` counts units that exist (published or being
-// processed). Producers add before publishing; a warp subtracts what it has
-// completed only while it waits with nothing staged. The warp whose
-// subtraction reaches zero raises `quiesce`; waiting warps abandon their
-// tickets (the next query or candidate restarts the queue at its tail).
+// Termination: `tail` counts published units, `completed` finished ones. A
+// warp adds its finished units only while it waits with nothing staged, so
+// `completed` can equal `tail` only when no unit is unfinished (a
+// producer's own unit always completes after what it published). The warp
+// whose addition makes them equal raises `quiesce`; waiting warps abandon
+// their tickets (the next query or candidate restarts the queue at its tail).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -47,7 +48,7 @@ struct alignas(128) PaddedCounter {
 };
 
 struct AsyncCtl {
-  PaddedCounter head, tail, pending;
+  PaddedCounter head, tail, completed;  // units claimed / published / finished
   alignas(128) unsigned int quiesce;  // epoch whose work is complete
   unsigned int abort;
   unsigned int error;
@@ -110,12 +111,8 @@ __device__ __forceinline__ uint32_t* unit_ptr(const AsyncArgs& a, unsigned long 
   return a.units + (pos & a.umask) * kUnitWords;
 }
 
-// Reserves k units, counted as pending. No fence is needed between the two
-// atomics: a unit's consumer can only drive pending to zero after the
-// producer's own (still unsubtracted) unit is done, and the producer's later
-// subtraction is ordered after its addition (same address).
+// Reserves k units (one atomic on the publish counter).
 __device__ __forceinline__ unsigned long long reserve_units(const AsyncArgs& a, uint32_t k) {
-  atomicAdd(&a.c->pending.v, (unsigned long long)k);
   return atomicAdd(&a.c->tail.v, (unsigned long long)k);
 }
 
@@ -359,9 +356,12 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
         continue;
       }
       if (done) {
+        // completions are published lazily, only from here: `completed`
+        // can reach `tail` only when no unit is unfinished (a producer's own
+        // unit completes after everything it published was reserved)
         if (lane == 0) {
-          const unsigned long long before = atomicAdd(&a.c->pending.v, 0ull - done);
-          if (before == done) st_volatile(&a.c->quiesce, epoch);  // the last unit is done
+          const unsigned long long c = atomicAdd(&a.c->completed.v, done) + done;
+          if (c == __ldcg(&a.c->tail.v)) st_volatile(&a.c->quiesce, epoch);
         }
         done = 0;
         continue;
@@ -423,9 +423,12 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
       const uint32_t pieces = (cnt + 127) / 128;
       const uint32_t mine = gw < pieces ? (pieces - gw + nw - 1) / nw : 0u;
       grid.sync();  // the previous candidate is drained everywhere
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.c->head.v = a.c->tail.v;  // drop idle tickets
-      if (lane_id() == 0 && mine) atomicAdd(&a.c->pending.v, (unsigned long long)mine);
-      grid.sync();  // every seed piece is counted before anyone can see zero
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // drop idle tickets; the seed pieces count as work to complete
+        a.c->head.v = a.c->tail.v;
+        a.c->completed.v = a.c->tail.v - pieces;
+      }
+      grid.sync();
       for (uint32_t pc = gw; pc < pieces; pc += nw) {
         relax_span(a, lo + pc * 128, min(128u, cnt - pc * 128), 0, rx, vb);
         ++done;
@@ -464,8 +467,8 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, 
   c->wait_ns = 0;
   c->busy_ns = 0;
   c->bad[0] = c->bad[1] = c->bad[2] = c->bad[3] = 0;
-  c->pending.v = 0;
   c->head.v = c->tail.v;  // tickets left waiting by the previous query are void
+  c->completed.v = c->tail.v;
   if (fastest) return;
   unsigned long long t = c->tail.v;
   uint32_t nu = 0;
@@ -481,7 +484,6 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, 
     u[0] = k;
   }
   c->tail.v = t + nu;
-  c->pending.v = nu;
 }
 
 // Fresh (or post-abort) queue state: flags clear, every unit free.
@@ -493,8 +495,7 @@ __global__ void async_reset_kernel(uint32_t* flag, size_t slots, uint32_t* units
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nunits; i += stride)
     units[i * kUnitWords] = kEmpty;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c->head.v = c->tail.v = 0;
-    c->pending.v = 0;
+    c->head.v = c->tail.v = c->completed.v = 0;
   }
 }
 
