@@ -401,17 +401,19 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   if (nunits > (1ull << 26))
     return fail(TGXD_ERR_UNSUPPORTED, "async engine: batch too large (use a round-based mode)");
   if (w.a_slots < slots || w.a_units < nunits) {
-    if (!dalloc<uint32_t>(w.aflag, slots) || !dalloc<uint32_t>(w.aunits, nunits * kUnitWords) ||
-        !dalloc<AsyncCtl>(w.actl, 1))
+    if (!dalloc<unsigned long long>(w.axq, slots) ||
+        !dalloc<uint32_t>(w.aunits, nunits * kUnitWords) || !dalloc<AsyncCtl>(w.actl, 1))
       return fail(TGXD_ERR_CUDA, "device allocation failed (async queue)");
     TGXD_CUDA(cudaMemsetAsync(w.actl.p, 0, sizeof(AsyncCtl), s));
-    async_reset_kernel<<<grid_for(std::max(slots, nunits), G->sm_count), 256, 0, s>>>(
-        w.aflag.as<uint32_t>(), slots, w.aunits.as<uint32_t>(), nunits, w.actl.as<AsyncCtl>());
+    async_reset_kernel<<<grid_for(nunits, G->sm_count), 256, 0, s>>>(
+        w.aunits.as<uint32_t>(), nunits, w.actl.as<AsyncCtl>());
     w.a_slots = slots;
     w.a_units = nunits;
   }
-  async_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n, w.X.as<int32_t>(),
-                                     w.aflag.as<uint32_t>(), w.aunits.as<uint32_t>(),
+  async_init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
+      w.axq.as<unsigned long long>(), slots);
+  async_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
+                                     w.axq.as<unsigned long long>(), w.aunits.as<uint32_t>(),
                                      w.a_units - 1, w.actl.as<AsyncCtl>(), fast);
   AsyncArgs a;
   a.g = g;
@@ -419,7 +421,7 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   a.X = w.X.as<int32_t>();
   a.EP = w.EP.as<int2>();
   a.R = fast ? w.R.as<int32_t>() : nullptr;
-  a.flag = w.aflag.as<uint32_t>();
+  a.XQ = w.axq.as<unsigned long long>();
   a.units = w.aunits.as<uint32_t>();
   a.umask = w.a_units - 1;
   a.c = w.actl.as<AsyncCtl>();
@@ -560,9 +562,8 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
     if (c.error) {
       Workspace& w = G->ws;
-      async_reset_kernel<<<grid_for(std::max(w.a_slots, w.a_units), G->sm_count), 256, 0,
-                           G->stream>>>(w.aflag.as<uint32_t>(), w.a_slots, w.aunits.as<uint32_t>(),
-                                        w.a_units, w.actl.as<AsyncCtl>());
+      async_reset_kernel<<<grid_for(w.a_units, G->sm_count), 256, 0, G->stream>>>(
+          w.aunits.as<uint32_t>(), w.a_units, w.actl.as<AsyncCtl>());
       cudaStreamSynchronize(G->stream);
       return fail(TGXD_ERR_CUDA, "async traversal watchdog expired");
     }

@@ -10,10 +10,12 @@
 // relaxed; a batch is expanded (the same key-range search and selective
 // index as the round kernel), its short ranges relaxed by the warp itself
 // (packed 32 ranges per warp) and its long ranges published as chunks.
-// Improved vertices are enqueued once per improvement "epoch": a per-slot
-// queued flag is set with atomicExch by the improver and cleared (then
-// fenced) by the expander before it reads the label, so no improvement is
-// ever left unexpanded.
+// Label and "queued" bit share one 64-bit word per slot (XQ): an improver
+// lowers the label and sets the bit in one CAS and enqueues the slot only if
+// the bit was clear; the expander clears the bit with atomicAnd, whose
+// return value is the label it expands with. All of it is ordered by the
+// coherence of that single address — no fences — so no improvement is ever
+// left unexpanded. Labels are copied back to X when the query is done.
 //
 // Work efficiency is unchanged: an expansion only walks keys in
 // [bound, previous bound), so every admissible edge is relaxed once per
@@ -63,10 +65,10 @@ struct AsyncCtl {
 struct AsyncArgs {
   DevCsr g;
   const QueryParam* qp;
-  int32_t* X;
+  int32_t* X;       // final labels (copied from XQ at the end)
+  unsigned long long* XQ;  // per slot: label << 32 | queued bit
   int2* EP;
   int32_t* R;
-  uint32_t* flag;   // per slot: 1 while queued
   uint32_t* units;  // ring of 64-byte units, header word kEmpty when free
   unsigned long long umask;
   AsyncCtl* c;
@@ -97,16 +99,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t exch_release(uint32_t* p, uint32_t v) {
-  uint32_t o;
-  asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
-  return o;
+__device__ __forceinline__ unsigned long long xq_pack(int32_t label, uint32_t queued) {
+  return ((unsigned long long)(uint32_t)label << 32) | queued;
 }
-__device__ __forceinline__ uint32_t exch_acq_rel(uint32_t* p, uint32_t v) {
-  uint32_t o;
-  asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
-  return o;
-}
+__device__ __forceinline__ int32_t xq_label(unsigned long long w) { return (int32_t)(w >> 32); }
+
 __device__ __forceinline__ uint32_t* unit_ptr(const AsyncArgs& a, unsigned long long pos) {
   return a.units + (pos & a.umask) * kUnitWords;
 }
@@ -155,7 +152,7 @@ struct ARelax {
 };
 
 // Relax kUnroll 32-edge steps (see relax_steps in traverse.cuh); an
-// improvement enqueues its vertex when the queued flag was clear.
+// improvement enqueues its vertex when its queued bit was clear.
 __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (&e)[kUnroll],
                                             const uint32_t (&q)[kUnroll],
                                             const bool (&act)[kUnroll], const ARelax& rx,
@@ -168,7 +165,7 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
     idx[u] = q[u] * a.n + pl.x;
     v[u] = (int32_t)pl.y;
   }
-  int32_t cur[kUnroll];
+  unsigned long long cur[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     const int32_t vhi = a.Q == 1 ? rx.vhi0 : __ldg(&a.qp[q[u]].vhi);
@@ -178,21 +175,39 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
       a.c->bad[3] = q[u];
 #endif
     if (!(act[u] && v[u] <= vhi)) v[u] = kInf;  // window containment (types.hpp:55-57)
-    cur[u] = v[u] != kInf ? ld_state(a.X + idx[u], rx.pol_keep) : kInf;
+    cur[u] = v[u] != kInf ? __ldcg(a.XQ + idx[u]) : xq_pack(kInf, 1u);
   }
-  int32_t old[kUnroll];
-#pragma unroll
-  for (int u = 0; u < kUnroll; ++u)
-    old[u] = v[u] < cur[u] ? atomicMin(a.X + idx[u], v[u]) : kInf;  // write_min
+  // write_min (parallel.hpp:91-99) + the queued bit in one CAS; all CASes of
+  // the batch are issued before any result is used
+  bool imp[kUnroll];
   uint32_t was[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
+    imp[u] = v[u] < xq_label(cur[u]);
     was[u] = 1u;
-    if (v[u] < old[u]) {
-      if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
-      was[u] = exch_release(a.flag + idx[u], 1u);  // the label update precedes the flag
+    if (imp[u]) {
+      const unsigned long long prev = atomicCAS(a.XQ + idx[u], cur[u], xq_pack(v[u], 1u));
+      if (prev == cur[u]) {
+        was[u] = (uint32_t)(prev & 1ull);
+      } else {
+        cur[u] = prev;
+        imp[u] = false;
+        // contended: retry until the label is no longer above v
+        while (v[u] < xq_label(cur[u])) {
+          const unsigned long long p2 = atomicCAS(a.XQ + idx[u], cur[u], xq_pack(v[u], 1u));
+          if (p2 == cur[u]) {
+            imp[u] = true;
+            was[u] = (uint32_t)(p2 & 1ull);
+            break;
+          }
+          cur[u] = p2;
+        }
+      }
     }
   }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (imp[u] && a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) vb_append(a, vb, was[u] == 0u, idx[u]);
 }
@@ -270,11 +285,9 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
   uint32_t q = 0, p0 = 0, p1 = 0;
   bool act = false;
   if (valid) {
-    // clear the queued flag before reading the label (acq_rel: the label
-    // load cannot move above it): an improvement after this point
-    // re-enqueues the slot, one before it is visible to the load below
-    exch_acq_rel(a.flag + item, 0u);
-    const int32_t x = __ldcg(a.X + item);
+    // clear the queued bit; the returned word holds the label to expand
+    // with (an improvement after this point re-enqueues the slot)
+    const int32_t x = xq_label(atomicAnd(a.XQ + item, ~1ull));
     const int2 ep = __ldcg(a.EP + item);
     q = a.Q == 1 ? 0u : item / a.n;
     const uint32_t v = item - q * a.n;
@@ -437,6 +450,13 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
       if (ld_volatile(&a.c->abort)) break;
     }
   }
+  grid.sync();  // every label is final: copy them out
+  {
+    const size_t slots = (size_t)a.Q * a.n;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
+         i += (size_t)gridDim.x * blockDim.x)
+      a.X[i] = xq_label(__ldcg(a.XQ + i));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     work += __shfl_xor_sync(0xffffffffu, work, o);
@@ -453,9 +473,9 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
 }
 
 // Query start: counters, and for EA / LD the roots as the first batch units.
-__global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_t* X,
-                                  uint32_t* flag, uint32_t* units, unsigned long long umask,
-                                  AsyncCtl* c, int fastest) {
+__global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n,
+                                  unsigned long long* XQ, uint32_t* units,
+                                  unsigned long long umask, AsyncCtl* c, int fastest) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   c->abort = 0;
   c->error = 0;
@@ -477,8 +497,7 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, 
     const uint32_t k = min(kBatch, Q - q0);
     for (uint32_t j = 0; j < k; ++j) {
       const uint32_t item = (q0 + j) * n + qp[q0 + j].root;
-      X[item] = qp[q0 + j].klo;
-      flag[item] = 1u;
+      XQ[item] = ((unsigned long long)(uint32_t)qp[q0 + j].klo << 32) | 1ull;
       u[1 + j] = item;
     }
     u[0] = k;
@@ -486,17 +505,19 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, 
   c->tail.v = t + nu;
 }
 
-// Fresh (or post-abort) queue state: flags clear, every unit free.
-__global__ void async_reset_kernel(uint32_t* flag, size_t slots, uint32_t* units, size_t nunits,
-                                   AsyncCtl* c) {
+// Fresh (or post-abort) queue state: every unit free.
+__global__ void async_reset_kernel(uint32_t* units, size_t nunits, AsyncCtl* c) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += stride)
-    flag[i] = 0;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nunits; i += stride)
     units[i * kUnitWords] = kEmpty;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c->head.v = c->tail.v = c->completed.v = 0;
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->head.v = c->tail.v = c->completed.v = 0;
+}
+
+// Per-query label words: INF, not queued.
+__global__ void async_init_kernel(unsigned long long* XQ, size_t slots) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const unsigned long long w = (unsigned long long)(uint32_t)kInf << 32;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += stride) XQ[i] = w;
 }
 
 }  // namespace tgxd

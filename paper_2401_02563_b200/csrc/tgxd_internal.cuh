@@ -65,7 +65,7 @@ struct Workspace {
   DeviceBuffer X, EP, R, fa, fb, chunks, smalls, ctl, params, seeds;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
   // asynchronous engine: queued flags, vertex / chunk rings, control block
-  DeviceBuffer aflag, aunits, actl;
+  DeviceBuffer axq, aunits, actl;
   uint64_t a_slots = 0, a_units = 0;
   bool last_async = false;
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
