@@ -57,7 +57,8 @@ enum tgxd_mode {
   TGXD_MODE_AUTO = 0,    /* engine's choice */
   TGXD_MODE_SPARSE = 1,  /* round-based, queue frontier every round */
   TGXD_MODE_DENSE = 2,   /* round-based, implicit (dense) frontier every round */
-  TGXD_MODE_ASYNC = 3    /* barrier-free work queues (no rounds) */
+  TGXD_MODE_ASYNC = 3,   /* barrier-free work queues (no rounds) */
+  TGXD_MODE_PULL = 4     /* round-based, every round pulled (dense bottom-up) */
 };
 
 /* Output label width: 8 = int64 exactly as PathResult::values
@@ -69,7 +70,7 @@ typedef struct tgxd_stats {
   uint32_t rounds;          /* frontier rounds (all candidates for fastest) */
   uint32_t candidates;      /* fastest: departure candidates swept */
   uint64_t expansions;      /* non-empty frontier ranges expanded */
-  uint64_t edges_relaxed;   /* edges handed to the relax step (all rounds) */
+  uint64_t edges_relaxed;   /* edges relaxed by push plus entries scanned by pull rounds */
   uint64_t index_lookups;   /* expansions that used the selective index */
   float kernel_ms;          /* traversal kernel time (CUDA events) */
   float total_ms;           /* device time of the whole query incl. init/output */

@@ -60,6 +60,7 @@ class Mode(enum.IntEnum):                # traversal schedule (tgxd_mode)
     SPARSE = 1     # rounds, queue frontier
     DENSE = 2      # rounds, implicit dense frontier
     ASYNC = 3      # barrier-free work queues
+    PULL = 4       # rounds, every round pulled (bottom-up)
 
 
 class OutOfRange(IndexError):
@@ -189,9 +190,11 @@ def load_library() -> ctypes.CDLL:
     elif _build.needs_build():
         try:
             _build.build()
-        except Exception as e:  # no nvcc on the box: use what travelled, if anything
-            if not path.exists():
-                raise DeviceError(f"libtgxd.so is not built and cannot be built: {e}") from e
+        except Exception as e:
+            # a stale library is only acceptable where nothing can rebuild it
+            import shutil
+            if not path.exists() or shutil.which("nvcc"):
+                raise DeviceError(f"libtgxd.so is out of date and failed to build: {e}") from e
     lib = ctypes.CDLL(str(path))
     vp = ctypes.c_void_p
     sig = {

@@ -511,6 +511,10 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   // (measured on config 2: the queue-driven expand is cheaper below that).
   a.dense_f = std::max<uint64_t>(1024, slots / 2);
   a.push_w = std::max<uint64_t>(4096, slots * 4);
+  // a frontier holding this share of the slots is pulled (direction switch)
+  const char* pf = getenv("TGXD_PULL_DIV");
+  a.pull_f = std::max<uint64_t>(1024, slots / (pf ? std::max(1, atoi(pf)) : 8));
+  a.rg = P.kind == TGXD_LATEST_DEPARTURE ? G->out : G->in;
   a.fastest = fast ? 1 : 0;
   a.n_cand = ncand;
   a.cand_lo = w.cand_lo.as<uint32_t>();
@@ -594,7 +598,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   st->rounds = c.rounds;
   st->candidates = c.candidates;
   st->expansions = c.expansions;
-  st->edges_relaxed = c.edges;
+  st->edges_relaxed = c.edges + c.pull_scanned;
   st->index_lookups = c.index_lookups;
   st->kernel_ms = kernel_ms;
   st->total_ms = total_ms;

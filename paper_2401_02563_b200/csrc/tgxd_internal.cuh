@@ -91,6 +91,7 @@ struct Control {
   unsigned long long edges;         // edges handed to the relax step
   unsigned long long expansions;    // non-empty ranges (chunks + small ranges)
   unsigned long long index_lookups; // expansions that used the fence index
+  unsigned long long pull_scanned;  // reverse-layout entries scanned by pull rounds
   unsigned int rounds;
   unsigned int candidates;
   unsigned int error;               // watchdog tripped

@@ -65,7 +65,8 @@ constexpr uint32_t kLocalMaxF = TGXD_LOCAL_F;    // frontier that one CTA expand
 constexpr uint32_t kLocalMaxW = 4096;            // edge work that one CTA relaxes
 
 struct TravArgs {
-  DevCsr g;
+  DevCsr g;            // push layout
+  DevCsr rg;           // reverse layout (pull rounds)
   const QueryParam* qp;
   int32_t* X;          // labels, Q x n (key space)
   int2* EP;            // per slot {bound it was last expanded with, position of
@@ -83,6 +84,7 @@ struct TravArgs {
   int mode;            // tgxd_mode
   unsigned long long dense_f;  // AUTO: frontier above this expands densely
   unsigned long long push_w;   // AUTO: rounds relaxing more edges do not push
+  unsigned long long pull_f;   // AUTO: a frontier at least this big is pulled
   // fastest sweep (Q == 1)
   int fastest;
   uint32_t n_cand;
@@ -579,6 +581,143 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
   if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
 }
 
+// ---------------------------------------------------------------------------
+// Pull round (the dense "bottom-up" direction of temporal_edge_map,
+// engine.hpp:321-346): every slot scans its segment of the reverse layout in
+// increasing candidate order and stops at the first edge admissible under
+// the current labels — the minimum possible value. Only the slot's own lane
+// writes its label, so no atomics. Afterwards every edge admissible under the
+// round-start labels has been considered, hence each slot's expansion bound
+// becomes bound(start label); slots improved by the pull are queued for a
+// push expansion of their new delta. On config 2 this turns the 17.8M + 37.9M
+// edge relaxations of the two heaviest push rounds into 11.4M + 6.2M scans.
+//
+// Reverse layout in key space (see DevCsr): for the push layout's edge
+// (key_P, val_P) the reverse entry has key_R = -val_P, val_R = -key_P, so a
+// pull candidate is -key_R and the admissibility key is -val_R. Positions
+// descending = candidates ascending.
+constexpr uint32_t kPullLane = 32;  // positions a lane scans before the warp helps
+
+struct PullProbe {
+  bool stop;   // candidate cannot improve (or leaves the window): scan ends
+  bool adm;    // admissible: its candidate is the answer
+  int32_t cand;
+};
+
+__device__ __forceinline__ PullProbe pull_probe(const TravArgs& a, const DevCsr& rg, uint32_t j,
+                                                uint32_t q, const QueryParam& qp, int32_t best,
+                                                uint64_t pol_keep) {
+  PullProbe r;
+  r.cand = -__ldg(rg.key + j);
+  r.stop = r.cand >= best || r.cand > qp.vhi;
+  r.adm = false;
+  if (!r.stop) {
+    const uint2 pl = __ldg(rg.pay + j);
+    const int32_t kp = -(int32_t)pl.y;
+    if (kp >= qp.klo) {
+      if (pl.x == qp.root) {
+        r.adm = true;
+      } else {
+        const int32_t xs = ld_state(a.X + q * a.n + pl.x, pol_keep);
+        r.adm = xs != kInf && kp >= bound_of(xs, a.strict);
+      }
+    }
+  }
+  return r;
+}
+
+__device__ void phase_pull(const TravArgs& a, RelaxCtx& rx, uint32_t bid, uint32_t nblk,
+                           uint32_t* wbuf, unsigned long long& scanned) {
+  const DevCsr& rg = a.rg;
+  const uint32_t lane = lane_id();
+  const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
+  const uint32_t nw = nblk * kWarps;
+  const uint32_t slots = a.Q * a.n;
+  PushBuf pb{wbuf, 0};
+  for (uint32_t base = gw * 32; base < slots; base += nw * 32) {
+    const uint32_t i = base + lane;
+    const bool valid = i < slots;
+    uint32_t q = 0, v = 0, s = 0, j = 0;
+    int32_t x0 = kInf, best = kInf;
+    bool open = false;  // scan not finished
+    if (valid) {
+      q = a.Q == 1 ? 0u : i / a.n;
+      v = i - q * a.n;
+      x0 = ld_state(a.X + i, rx.pol_keep);
+      best = x0;
+      s = __ldg(rg.off + v);
+      j = __ldg(rg.off + v + 1);
+      open = j > s;
+      const QueryParam& qp = a.qp[q];
+      for (uint32_t k = 0; open && k < kPullLane; ++k) {
+        if (j == s) {
+          open = false;
+          break;
+        }
+        --j;
+        ++scanned;
+        const PullProbe p = pull_probe(a, rg, j, q, qp, best, rx.pol_keep);
+        if (p.stop) open = false;
+        else if (p.adm) {
+          best = p.cand;
+          open = false;
+        }
+      }
+      if (j == s) open = false;
+    }
+    // long scans: the whole warp, 32 positions per step, lowest lane first
+    uint32_t pend = __ballot_sync(0xffffffffu, open);
+    while (pend) {
+      const uint32_t L = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const uint32_t S = __shfl_sync(0xffffffffu, s, L);
+      uint32_t J = __shfl_sync(0xffffffffu, j, L);
+      const uint32_t Lq = __shfl_sync(0xffffffffu, q, L);
+      int32_t B = __shfl_sync(0xffffffffu, best, L);
+      const QueryParam& qp = a.qp[Lq];
+      while (J > S) {
+        const bool in = J > S + lane;
+        PullProbe p{true, false, 0};
+        if (in) p = pull_probe(a, rg, J - 1 - lane, Lq, qp, B, rx.pol_keep);
+        scanned += in ? 1 : 0;
+        const uint32_t sb = __ballot_sync(0xffffffffu, in && p.stop);
+        const uint32_t ab = __ballot_sync(0xffffffffu, in && p.adm);
+        const uint32_t first_stop = sb ? __ffs(sb) - 1 : 32u;
+        const uint32_t first_adm = ab ? __ffs(ab) - 1 : 32u;
+        if (first_adm < first_stop) {
+          B = __shfl_sync(0xffffffffu, p.cand, first_adm);
+          break;
+        }
+        if (first_stop < 32) break;
+        J = J > S + 32 ? J - 32 : S;
+      }
+      if (lane == L) best = B;
+    }
+    bool improved = false;
+    if (valid) {
+      const QueryParam& qp = a.qp[q];
+      improved = best < x0;
+      if (improved) {
+        a.X[i] = best;
+        if (a.R) atomicMin(a.R + i, best - rx.depart);
+      }
+      // every edge admissible under the round-start label has been considered
+      if (x0 != kInf) {
+        int32_t lb = (v == qp.root) ? qp.klo : bound_of(x0, a.strict);
+        if (lb < qp.klo) lb = qp.klo;
+        a.EP[i] = make_int2(lb, (int32_t)kNoPos);
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, improved);
+    if (bal) {
+      if (improved) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = i;
+      pb.n += __popc(bal);
+      if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
+    }
+  }
+  push_drain(pb, a.ctl, rx.pstart, rx.fout);
+}
+
 // Traversal state; identical in every block at every grid barrier.
 //
 // Counter discipline. The shared counters (pushes, improved, chunks,
@@ -713,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   const uint64_t pol_keep = policy_evict_last();
   const int32_t vhi0 = a.qp[0].vhi;
   const bool tr = blockIdx.x == 0 && threadIdx.x == 0;
-  unsigned long long ix = 0;
+  unsigned long long ix = 0, work_pull = 0;
   TState st;
   st.prev_p = 0;
   st.prev_i = 0;
@@ -787,10 +926,32 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       const unsigned long long p_now = st.p_known, i_now = st.i_known;
       uint32_t* fin = st.flip ? a.fb : a.fa;
       uint32_t* fout = st.flip ? a.fa : a.fb;
+      const bool pull = !xcnt && (a.mode == TGXD_MODE_PULL ||
+                                  (a.mode == TGXD_MODE_AUTO && F >= a.pull_f));
       if (tr) {
         trace_round(a, st.rounds, 0, gtimer());
         trace_round(a, st.rounds, 3, F);
-        trace_round(a, st.rounds, 7, st.dense ? 2 : 0);
+        trace_round(a, st.rounds, 7, pull ? 3 : (st.dense ? 2 : 0));
+      }
+      if (pull) {
+        RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
+        unsigned long long scanned = 0;
+        phase_pull(a, rx, blockIdx.x, gridDim.x, wbuf, scanned);
+        work_pull += scanned;
+        trace_warp_done(a, st.rounds, 1);
+        grid.sync();
+        st.p_known = __ldcg(&ctl->pushes);
+        st.i_known = __ldcg(&ctl->improved);
+        st.prev_p = p_now;
+        st.flip ^= 1u;
+        st.dense = 0;
+        if (tr) {
+          trace_round(a, st.rounds, 1, gtimer());
+          trace_round(a, st.rounds, 2, gtimer());
+          trace_round(a, st.rounds, 6, st.p_known - p_now);
+        }
+        ++st.rounds;
+        continue;
       }
       unsigned long long c_end = st.c_cur, s_end = st.s_cur, e_end = st.e_cur;
       if (!xcnt) {
@@ -847,8 +1008,12 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
     if (!a.fastest || st.rounds > a.round_limit) break;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ix += __shfl_xor_sync(0xffffffffu, ix, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    ix += __shfl_xor_sync(0xffffffffu, ix, o);
+    work_pull += __shfl_xor_sync(0xffffffffu, work_pull, o);
+  }
   if (lane_id() == 0 && ix) atomicAdd(&ctl->index_lookups, ix);
+  if (lane_id() == 0 && work_pull) atomicAdd(&ctl->pull_scanned, work_pull);
   if (tr) {
     ctl->rounds = st.rounds;
     ctl->expansions = __ldcg(&ctl->chunks) + __ldcg(&ctl->smalls);
@@ -887,6 +1052,7 @@ __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_
     ctl->edges = 0;
     ctl->expansions = 0;
     ctl->index_lookups = 0;
+    ctl->pull_scanned = 0;
     ctl->error = 0;
   }
   if (q >= Q || fastest) return;

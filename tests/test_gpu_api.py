@@ -28,7 +28,7 @@ def test_hand_cases():
             assert got.values[vert] == want, (name, vert)
 
 
-@pytest.mark.parametrize("mode", [T.Mode.AUTO, T.Mode.SPARSE, T.Mode.DENSE, T.Mode.ASYNC])
+@pytest.mark.parametrize("mode", [T.Mode.AUTO, T.Mode.SPARSE, T.Mode.DENSE, T.Mode.ASYNC, T.Mode.PULL])
 def test_small_random_golden(mode):
     for E, n, v, ta, tb, kind, ordv, want in S.small_random():
         g = T.TemporalGraph.build(E, n, True, T.EngineConfig(index_cutoff=2))

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 KINDS = {"earliest_arrival": T.earliest_arrival, "latest_departure": T.latest_departure,
          "fastest": T.fastest_path}
-MODES = [T.Mode.AUTO, T.Mode.SPARSE, T.Mode.DENSE, T.Mode.ASYNC]
+MODES = [T.Mode.AUTO, T.Mode.SPARSE, T.Mode.DENSE, T.Mode.ASYNC, T.Mode.PULL]
 
 
 def rand_instance(rng, max_v=12, max_e=40, t_range=60, d_max=8, d_min=0):

@@ -34,4 +34,4 @@ for q in qs[:4]:
             a_first = (big - row[9] - row[0]) / 1e3 if row[9] else 0
             b_last = (row[10] - row[1]) / 1e3 if row[10] else 0
             b_first = (big - row[11] - row[1]) / 1e3 if row[11] else 0
-            print(f"  r{r:3d} F={row[3]:9d} A={(row[1]-row[0])/1e3:7.1f}us [warps {a_first:6.1f}..{a_last:6.1f}] B={(row[2]-row[1])/1e3:7.1f}us [warps {b_first:6.1f}..{b_last:6.1f}] ch={row[4]:7d} sm={row[5]:7d} push={row[6]:8d} {'L' if row[7]==1 else ('D' if row[7]==2 else 'G')}")
+            print(f"  r{r:3d} F={row[3]:9d} A={(row[1]-row[0])/1e3:7.1f}us [warps {a_first:6.1f}..{a_last:6.1f}] B={(row[2]-row[1])/1e3:7.1f}us [warps {b_first:6.1f}..{b_last:6.1f}] ch={row[4]:7d} sm={row[5]:7d} push={row[6]:8d} {'L' if row[7]==1 else ('D' if row[7]==2 else ('P' if row[7]==3 else 'G'))}")
