@@ -168,11 +168,13 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     DeviceBuffer& b_key = dir == 0 ? G->out_key : G->in_key;
     DeviceBuffer& b_pay = dir == 0 ? G->out_pay : G->in_pay;
     DeviceBuffer& b_fence = dir == 0 ? G->out_fence : G->in_fence;
+    DeviceBuffer& b_kmax = dir == 0 ? G->out_kmax : G->in_kmax;
+    int32_t* kmax = dalloc<int32_t>(b_kmax, (size_t)n + 1);
     uint32_t* off = dalloc<uint32_t>(b_off, (size_t)n + 1);
     int32_t* key = dalloc<int32_t>(b_key, m);
     uint2* pay = dalloc<uint2>(b_pay, m);
     int32_t* fence = dalloc<int32_t>(b_fence, nf);
-    if (!off || !key || !pay || !fence)
+    if (!off || !key || !pay || !fence || !kmax)
       return fail(TGXD_ERR_CUDA, "device allocation failed (T-CSR arrays)");
     if (m) {
       make_sort_keys<<<gb, 256, 0, s>>>(owner, kk, dir, m, ka, ia);
@@ -186,11 +188,13 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     size_t sb = scan_bytes;
     TGXD_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, sb, dc, off, (int64_t)n + 1, s));
     if (n) count_indexed<<<grid_for(n, G->sm_count), 256, 0, s>>>(off, n, G->index_cutoff, dctr + dir);
+    if (n) segment_kmax<<<grid_for(n, G->sm_count), 256, 0, s>>>(off, key, n, kmax);
     DevCsr& c = dir == 0 ? G->out : G->in;
     c.off = off;
     c.key = key;
     c.pay = pay;
     c.fence = fence;
+    c.kmax = kmax;
     c.n = n;
     c.m = (uint32_t)m;
   }
@@ -512,8 +516,11 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.dense_f = std::max<uint64_t>(1024, slots / 2);
   a.push_w = std::max<uint64_t>(4096, slots * 4);
   // a frontier holding this share of the slots is pulled (direction switch)
+  // (TGXD_PULL_DIV overrides the share's divisor; 0 turns AUTO's pulls off)
   const char* pf = getenv("TGXD_PULL_DIV");
-  a.pull_f = std::max<uint64_t>(1024, slots / (pf ? std::max(1, atoi(pf)) : 8));
+  const int pdiv = pf ? atoi(pf) : 8;
+  a.pull_f = pdiv <= 0 ? ~0ull : std::max<uint64_t>(1024, slots / pdiv);
+  if (const char* pfx = getenv("TGXD_PULL_F")) a.pull_f = strtoull(pfx, nullptr, 10);  // tests
   a.rg = P.kind == TGXD_LATEST_DEPARTURE ? G->out : G->in;
   a.fastest = fast ? 1 : 0;
   a.n_cand = ncand;

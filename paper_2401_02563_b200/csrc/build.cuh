@@ -106,6 +106,16 @@ __global__ void make_fences(const int32_t* key, uint64_t m, int32_t* fence) {
     fence[j] = key[j << kFenceShift];
 }
 
+// Last key of every segment (the pull side's "any candidate?" test and the
+// expansion's "anything at or above the bound?" test without a dependent load).
+__global__ void segment_kmax(const uint32_t* off, const int32_t* key, uint32_t n, int32_t* kmax) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const uint32_t s = off[v], t = off[v + 1];
+    kmax[v] = t > s ? key[t - 1] : INT32_MIN;
+  }
+}
+
 __global__ void count_indexed(const uint32_t* off, uint32_t n, uint64_t cutoff,
                               unsigned long long* out) {
   unsigned long long c = 0;

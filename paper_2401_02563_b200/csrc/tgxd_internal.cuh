@@ -36,6 +36,7 @@ struct DevCsr {
   const int32_t* key = nullptr;   // m: search keys (binary search / fences only)
   const uint2* pay = nullptr;     // m: relax payload {neighbor, val} (one 8-byte load)
   const int32_t* fence = nullptr; // ceil(m / 32): key[32 j]
+  const int32_t* kmax = nullptr;  // n: last (largest) key of each segment, INT32_MIN if empty
   uint32_t n = 0;
   uint32_t m = 0;
 };
@@ -92,6 +93,7 @@ struct Control {
   unsigned long long expansions;    // non-empty ranges (chunks + small ranges)
   unsigned long long index_lookups; // expansions that used the fence index
   unsigned long long pull_scanned;  // reverse-layout entries scanned by pull rounds
+  unsigned long long pchunks;       // pull chunks emitted
   unsigned int rounds;
   unsigned int candidates;
   unsigned int error;               // watchdog tripped
@@ -109,8 +111,8 @@ struct tgxd_graph {
   int directed = 1;
   uint64_t index_cutoff = 2048;
   uint64_t indexed[2] = {0, 0};
-  tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence;
-  tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence;
+  tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence, out_kmax;
+  tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax;
   tgxd::DevCsr out, in;
   cudaStream_t stream = nullptr;
   int sm_count = 0;

@@ -385,7 +385,8 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
       uint32_t pos = kNoPos;
       if (lb < hik) {
         const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-        if (t > s) {
+        const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
+        if (t > s && km >= lb) {
           act = true;
           const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
           ix += fence ? 1 : 0;
@@ -395,7 +396,7 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
           if (old <= qp.vhi + 1 && ep.y != (int32_t)kNoPos) {
             p1 = (uint32_t)ep.y;
           } else {
-            p1 = __ldg(a.g.key + t - 1) < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
+            p1 = km < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
           }
           p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
           pos = p0;
@@ -583,135 +584,197 @@ __device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned 
 
 // ---------------------------------------------------------------------------
 // Pull round (the dense "bottom-up" direction of temporal_edge_map,
-// engine.hpp:321-346): every slot scans its segment of the reverse layout in
-// increasing candidate order and stops at the first edge admissible under
-// the current labels — the minimum possible value. Only the slot's own lane
-// writes its label, so no atomics. Afterwards every edge admissible under the
-// round-start labels has been considered, hence each slot's expansion bound
-// becomes bound(start label); slots improved by the pull are queued for a
-// push expansion of their new delta. On config 2 this turns the 17.8M + 37.9M
-// edge relaxations of the two heaviest push rounds into 11.4M + 6.2M scans.
+// engine.hpp:321-346): every slot considers the in-edges (reverse layout)
+// that could lower its label — arrival below the current label and inside
+// the window, a suffix of its key-sorted segment found with the same index
+// search as the push side — and takes the smallest candidate admissible
+// under the current labels. Afterwards every edge admissible under the
+// round-start labels has been considered, so each slot's expansion bound
+// becomes bound(start label); slots the pull improved are queued for a push
+// expansion of their new delta. On config 2 the two heaviest push rounds
+// (17.8M + 37.9M edge relaxations) need 11.4M + 6.2M in-edge checks.
+//
+//   P1  one lane per slot finds its candidate window; short windows
+//       (<= kPullLane entries) are scanned in candidate order with batched
+//       loads, stopping at the first admissible entry. Long windows (a few
+//       thousand slots whose in-degree runs into the thousands) become
+//       kChunk-entry pull chunks {first position, slot}.
+//   P2  all warps take pull chunks; a chunk's smallest admissible candidate
+//       (warp min) goes in with one atomicMin, and the slot is queued on its
+//       first improvement (bound(old) == the EP bound P1 stored), the push
+//       rule of relax_steps.
 //
 // Reverse layout in key space (see DevCsr): for the push layout's edge
 // (key_P, val_P) the reverse entry has key_R = -val_P, val_R = -key_P, so a
-// pull candidate is -key_R and the admissibility key is -val_R. Positions
+// candidate is -key_R and the admissibility key is -val_R; positions
 // descending = candidates ascending.
-constexpr uint32_t kPullLane = 32;  // positions a lane scans before the warp helps
+#ifndef TGXD_PULL_LANE
+#define TGXD_PULL_LANE 16
+#endif
+#ifndef TGXD_PULL_BATCH
+#define TGXD_PULL_BATCH 8
+#endif
+constexpr uint32_t kPullLane = TGXD_PULL_LANE;    // longest window a lane scans by itself
+constexpr uint32_t kPullBatch = TGXD_PULL_BATCH;  // entries in flight per lane while scanning
 
-struct PullProbe {
-  bool stop;   // candidate cannot improve (or leaves the window): scan ends
-  bool adm;    // admissible: its candidate is the answer
-  int32_t cand;
-};
-
-__device__ __forceinline__ PullProbe pull_probe(const TravArgs& a, const DevCsr& rg, uint32_t j,
-                                                uint32_t q, const QueryParam& qp, int32_t best,
-                                                uint64_t pol_keep) {
-  PullProbe r;
-  r.cand = -__ldg(rg.key + j);
-  r.stop = r.cand >= best || r.cand > qp.vhi;
-  r.adm = false;
-  if (!r.stop) {
-    const uint2 pl = __ldg(rg.pay + j);
-    const int32_t kp = -(int32_t)pl.y;
-    if (kp >= qp.klo) {
-      if (pl.x == qp.root) {
-        r.adm = true;
-      } else {
-        const int32_t xs = ld_state(a.X + q * a.n + pl.x, pol_keep);
-        r.adm = xs != kInf && kp >= bound_of(xs, a.strict);
-      }
-    }
-  }
-  return r;
+// Is the reverse entry with payload pl admissible for query q under the
+// current labels? (the admissibility test of relax, path_algorithms.cpp:287-300)
+__device__ __forceinline__ bool pull_admissible(const TravArgs& a, uint2 pl, uint32_t q,
+                                                const QueryParam& qp, uint64_t pol_keep) {
+  const int32_t kp = -(int32_t)pl.y;
+  if (kp < qp.klo) return false;
+  if (pl.x == qp.root) return true;
+  const int32_t xs = ld_state(a.X + q * a.n + pl.x, pol_keep);
+  return xs != kInf && kp >= bound_of(xs, a.strict);
 }
 
-__device__ void phase_pull(const TravArgs& a, RelaxCtx& rx, uint32_t bid, uint32_t nblk,
-                           uint32_t* wbuf, unsigned long long& scanned) {
+__device__ void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned long long cstart,
+                            uint32_t bid, uint32_t nblk, uint32_t* wbuf, uint2* ebuf,
+                            unsigned long long& scanned) {
   const DevCsr& rg = a.rg;
   const uint32_t lane = lane_id();
   const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = nblk * kWarps;
   const uint32_t slots = a.Q * a.n;
   PushBuf pb{wbuf, 0};
+  WarpList chl{ebuf, 0};
   for (uint32_t base = gw * 32; base < slots; base += nw * 32) {
     const uint32_t i = base + lane;
     const bool valid = i < slots;
     uint32_t q = 0, v = 0, s = 0, j = 0;
-    int32_t x0 = kInf, best = kInf;
-    bool open = false;  // scan not finished
+    int32_t x0 = kInf, best = kInf, lim = kInf;
+    bool open = false;  // window not exhausted
     if (valid) {
       q = a.Q == 1 ? 0u : i / a.n;
       v = i - q * a.n;
+      const QueryParam& qp = a.qp[q];
+      // independent loads: label, last key of the segment, segment bounds
       x0 = ld_state(a.X + i, rx.pol_keep);
-      best = x0;
+      const int32_t km = __ldg(rg.kmax + v);
       s = __ldg(rg.off + v);
       j = __ldg(rg.off + v + 1);
-      open = j > s;
-      const QueryParam& qp = a.qp[q];
-      for (uint32_t k = 0; open && k < kPullLane; ++k) {
-        if (j == s) {
-          open = false;
-          break;
-        }
-        --j;
-        ++scanned;
-        const PullProbe p = pull_probe(a, rg, j, q, qp, best, rx.pol_keep);
-        if (p.stop) open = false;
-        else if (p.adm) {
-          best = p.cand;
-          open = false;
-        }
-      }
-      if (j == s) open = false;
-    }
-    // long scans: the whole warp, 32 positions per step, lowest lane first
-    uint32_t pend = __ballot_sync(0xffffffffu, open);
-    while (pend) {
-      const uint32_t L = __ffs(pend) - 1;
-      pend &= pend - 1;
-      const uint32_t S = __shfl_sync(0xffffffffu, s, L);
-      uint32_t J = __shfl_sync(0xffffffffu, j, L);
-      const uint32_t Lq = __shfl_sync(0xffffffffu, q, L);
-      int32_t B = __shfl_sync(0xffffffffu, best, L);
-      const QueryParam& qp = a.qp[Lq];
-      while (J > S) {
-        const bool in = J > S + lane;
-        PullProbe p{true, false, 0};
-        if (in) p = pull_probe(a, rg, J - 1 - lane, Lq, qp, B, rx.pol_keep);
-        scanned += in ? 1 : 0;
-        const uint32_t sb = __ballot_sync(0xffffffffu, in && p.stop);
-        const uint32_t ab = __ballot_sync(0xffffffffu, in && p.adm);
-        const uint32_t first_stop = sb ? __ffs(sb) - 1 : 32u;
-        const uint32_t first_adm = ab ? __ffs(ab) - 1 : 32u;
-        if (first_adm < first_stop) {
-          B = __shfl_sync(0xffffffffu, p.cand, first_adm);
-          break;
-        }
-        if (first_stop < 32) break;
-        J = J > S + 32 ? J - 32 : S;
-      }
-      if (lane == L) best = B;
-    }
-    bool improved = false;
-    if (valid) {
-      const QueryParam& qp = a.qp[q];
-      improved = best < x0;
-      if (improved) {
-        a.X[i] = best;
-        if (a.R) atomicMin(a.R + i, best - rx.depart);
-      }
-      // every edge admissible under the round-start label has been considered
+      best = x0;
+      // candidates below lim: key_R >= 1 - lim, a suffix of the segment
+      lim = min(x0, qp.vhi + 1);
+      open = km >= 1 - lim;
+      // every edge admissible under the round-start label is considered now
       if (x0 != kInf) {
         int32_t lb = (v == qp.root) ? qp.klo : bound_of(x0, a.strict);
         if (lb < qp.klo) lb = qp.klo;
         a.EP[i] = make_int2(lb, (int32_t)kNoPos);
       }
     }
+    // the smallest candidates first, kPullBatch entries in flight, until the
+    // first admissible one or the end of the window
+    for (uint32_t k = 0; open && k < kPullLane; k += kPullBatch) {
+      const QueryParam& qp = a.qp[q];
+      int32_t kr[kPullBatch];
+      uint2 pl[kPullBatch];
+#pragma unroll
+      for (uint32_t b = 0; b < kPullBatch; ++b) {
+        const bool in = j > s + b;
+        kr[b] = in ? __ldg(rg.key + j - 1 - b) : kInf;
+        pl[b] = in ? __ldg(rg.pay + j - 1 - b) : make_uint2(0u, 0x7fffffffu);
+      }
+      uint32_t stop = kPullBatch;  // first entry outside the window (keys ascend)
+#pragma unroll
+      for (int b = kPullBatch - 1; b >= 0; --b)
+        if (j <= s + b || -kr[b] >= lim) stop = b;
+      bool adm[kPullBatch];
+#pragma unroll
+      for (uint32_t b = 0; b < kPullBatch; ++b)
+        adm[b] = b < stop && pull_admissible(a, pl[b], q, qp, rx.pol_keep);
+      uint32_t hit = stop;
+#pragma unroll
+      for (int b = kPullBatch - 1; b >= 0; --b)
+        if (adm[b]) hit = b;
+#pragma unroll
+      for (uint32_t b = 0; b < kPullBatch; ++b)
+        if (b == hit && hit < stop) best = -kr[b];
+      scanned += min(hit + 1, stop);
+      if (hit < stop || stop < kPullBatch) open = false;
+      j -= kPullBatch;
+    }
+    uint32_t p = j;
+    if (open)  // a long window: the rest goes to pull chunks
+      p = lane_lower_bound(rg, s, j, 1 - lim, a.cutoff != 0 && j - s >= a.cutoff);
+    const bool improved = best < x0;
+    if (improved) {
+      a.X[i] = best;
+      if (a.R) atomicMin(a.R + i, best - rx.depart);
+    }
     const uint32_t bal = __ballot_sync(0xffffffffu, improved);
     if (bal) {
       if (improved) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = i;
       pb.n += __popc(bal);
+      if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
+    }
+    // chunks of [p, j), those nearest the smallest candidates first
+    const uint32_t nch = open ? (j - p + kChunk - 1) / kChunk : 0u;
+    uint32_t bigs = __ballot_sync(0xffffffffu, nch != 0);
+    while (bigs) {
+      const uint32_t L = __ffs(bigs) - 1;
+      bigs &= bigs - 1;
+      const uint32_t I = __shfl_sync(0xffffffffu, i, L);
+      const uint32_t bn = __shfl_sync(0xffffffffu, nch, L);
+      const uint32_t P = __shfl_sync(0xffffffffu, p, L);
+      for (uint32_t k0 = 0; k0 < bn; k0 += 32) {
+        // chunk k covers [P + k kChunk, min(P + (k+1) kChunk, window end))
+        const uint32_t k = bn - 1 - min(k0 + lane, bn - 1);
+        list_append(chl, k0 + lane < bn, make_uint2(P + k * kChunk, I), &a.ctl->pchunks, cstart,
+                    a.chunks);
+      }
+    }
+  }
+  push_drain(pb, a.ctl, rx.pstart, rx.fout);
+  list_drain(chl, &a.ctl->pchunks, cstart, a.chunks);
+}
+
+// P2: one warp per pull chunk, kUnroll entries per lane. A chunk's entries
+// run from its first position to min(first + kChunk, window end).
+__device__ void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned long long nch, uint32_t bid,
+                            uint32_t nblk, uint32_t* wbuf, unsigned long long& scanned) {
+  const DevCsr& rg = a.rg;
+  const uint32_t lane = lane_id();
+  const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
+  const uint32_t nw = nblk * kWarps;
+  PushBuf pb{wbuf, 0};
+  for (unsigned long long c = gw; c < nch; c += nw) {
+    const uint2 ch = __ldcg(a.chunks + c);
+    const uint32_t slot = ch.y;
+    const uint32_t q = a.Q == 1 ? 0u : slot / a.n;
+    const uint32_t v = slot - q * a.n;
+    const QueryParam& qp = a.qp[q];
+    // P1 already scanned the last kPullLane entries of the segment
+    const uint32_t hi = min(__ldg(rg.off + v + 1) - kPullLane, ch.x + kChunk);
+    int32_t kr[kUnroll];
+    uint2 pl[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t j = ch.x + u * 32 + lane;
+      const bool in = j < hi;
+      kr[u] = in ? ld_stream(rg.key + j, rx.pol_stream) : 0;
+      pl[u] = in ? ld_stream2(rg.pay + j, rx.pol_stream) : make_uint2(0u, 0x7fffffffu);
+    }
+    int32_t m = kInf;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (pull_admissible(a, pl[u], q, qp, rx.pol_keep)) m = min(m, -kr[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    scanned += lane == 0 ? hi - ch.x : 0u;
+    bool first = false;
+    if (lane == 0 && m != kInf && m < ld_state(a.X + slot, rx.pol_keep)) {
+      const int32_t old = atomicMin(a.X + slot, m);
+      if (m < old) {
+        if (a.R) atomicMin(a.R + slot, m - rx.depart);
+        first = bound_of(old, a.strict) == __ldcg(&a.EP[slot].x);
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, first);
+    if (bal) {
+      if (lane == 0) pb.buf[pb.n] = slot;
+      pb.n += 1;
       if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
     }
   }
@@ -731,6 +794,7 @@ struct TState {
   unsigned long long p_known;  // pushes counter as of the last barrier
   unsigned long long i_known;  // improved counter as of the last barrier
   unsigned long long c_cur, s_cur, e_cur;  // emission counters as of the last barrier
+  unsigned long long pc_cur;   // pull chunks counter as of the last barrier
   uint32_t rounds;
   uint32_t flip;               // fin/fout parity
   int dense;                   // the next expand scans densely
@@ -858,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   st.prev_i = 0;
   st.p_known = a.init_pushes;
   st.i_known = a.init_pushes;
-  st.c_cur = st.s_cur = st.e_cur = 0;
+  st.c_cur = st.s_cur = st.e_cur = st.pc_cur = 0;
   st.rounds = 0;
   st.flip = 0;
   st.dense = a.mode == TGXD_MODE_DENSE;
@@ -936,7 +1000,20 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       if (pull) {
         RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
         unsigned long long scanned = 0;
-        phase_pull(a, rx, blockIdx.x, gridDim.x, wbuf, scanned);
+        // P1 queues slots right away: every block's post-barrier read of the
+        // pushes counter must be over first (counter discipline)
+        grid.sync();
+        phase_pull1(a, rx, st.pc_cur, blockIdx.x, gridDim.x, wbuf, ebuf, scanned);
+        trace_warp_done(a, st.rounds, 0);
+        grid.sync();
+        const unsigned long long pc_end = __ldcg(&ctl->pchunks);
+        if (tr) {
+          trace_round(a, st.rounds, 1, gtimer());
+          trace_round(a, st.rounds, 4, pc_end - st.pc_cur);
+          trace_round(a, st.rounds, 5, 0);
+        }
+        phase_pull2(a, rx, pc_end - st.pc_cur, blockIdx.x, gridDim.x, wbuf, scanned);
+        st.pc_cur = pc_end;
         work_pull += scanned;
         trace_warp_done(a, st.rounds, 1);
         grid.sync();
@@ -946,7 +1023,6 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         st.flip ^= 1u;
         st.dense = 0;
         if (tr) {
-          trace_round(a, st.rounds, 1, gtimer());
           trace_round(a, st.rounds, 2, gtimer());
           trace_round(a, st.rounds, 6, st.p_known - p_now);
         }
@@ -1053,6 +1129,7 @@ __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_
     ctl->expansions = 0;
     ctl->index_lookups = 0;
     ctl->pull_scanned = 0;
+    ctl->pchunks = 0;
     ctl->error = 0;
   }
   if (q >= Q || fastest) return;

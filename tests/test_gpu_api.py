@@ -119,7 +119,8 @@ def test_stats_and_work_counters():
     g = T.TemporalGraph.generate(gen, True, T.EngineConfig(index_cutoff=64))
     st = T.EdgeMapStats()
     kind, v, ta, tb = qs[0]
-    T.earliest_arrival(g, v, T.QueryWindow(ta, tb), T.AlgoOptions(stats=st))
+    # push-only rounds relax every admissible edge at least once
+    T.earliest_arrival(g, v, T.QueryWindow(ta, tb), T.AlgoOptions(stats=st, mode=T.Mode.SPARSE))
     e_adm, v_reached = T.last_work(g, 0)
     E = T.generate_edges(gen)
     o = Oracle(E, n)
@@ -127,6 +128,10 @@ def test_stats_and_work_counters():
     assert (e_adm, v_reached) == o.work("earliest_arrival", v, ta, tb, lab)
     assert st.rounds > 0 and st.edges_relaxed >= e_adm
     assert st.index_decisions > 0  # the source is the hub: it used the index
+    # pull rounds may check fewer in-edges than there are admissible edges
+    st2 = T.EdgeMapStats()
+    r = T.earliest_arrival(g, v, T.QueryWindow(ta, tb), T.AlgoOptions(stats=st2, mode=T.Mode.PULL))
+    assert np.array_equal(r.values, lab) and st2.rounds > 0 and st2.edges_relaxed > 0
 
 
 def test_cpp_shim_runs():

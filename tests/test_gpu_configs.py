@@ -99,3 +99,17 @@ def test_full_c5_batch_properties():
     single = T.earliest_arrival(g, full[3].vertex, full[3].window).values
     s32 = np.where(single == (1 << 63) - 1, INT32_MAX, single).astype(np.int64)
     assert np.array_equal(s32, bf[3].astype(np.int64))
+
+
+@pytest.mark.parametrize("mode", [T.Mode.AUTO, T.Mode.PULL])
+def test_repeated_queries_are_stable(mode):
+    """Barrier/counter races show up as rare label differences between
+    identical runs: repeat the reduced config-4 source under push/pull mixes."""
+    wl, g, qs = setup("c4", -8)
+    o = Oracle(T.generate_edges(wl.gen), wl.gen.n_vertices)
+    src, w = qs[0].vertex, qs[0].window
+    for kind in ("fastest", "earliest_arrival"):
+        want = o.query(kind, src, w.t_a, w.t_b)
+        for _ in range(12):
+            got = FN[kind](g, src, w, T.AlgoOptions(mode=mode)).values
+            assert np.array_equal(got, want), (kind, mode)
