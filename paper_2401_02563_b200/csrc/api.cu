@@ -391,19 +391,20 @@ static uint64_t next_pow2(uint64_t x) {
 
 // The asynchronous engine: rings and flags persist across queries (every
 // query leaves them empty and clear); the kernel runs after init_kernel.
-static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint32_t ncand,
-                        cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+// Label words and the unit ring of the async engine (allocated on first use).
+static int ensure_async(tgxd_graph* G, uint32_t Q, bool required = true) {
   Workspace& w = G->ws;
   cudaStream_t s = G->stream;
-  const bool fast = P.kind == TGXD_FASTEST;
-  const uint64_t slots = (uint64_t)P.Q * G->n;
+  const uint64_t slots = (uint64_t)Q * G->n;
   // outstanding units <= batches (<= one per queued slot) + chunks (ranges of
   // >= kAInline edges and their 512-edge pieces) + staging slack
   const uint64_t nunits =
-      next_pow2(slots + (uint64_t)P.Q * (G->m / kAInline + G->m / kAChunk) +
+      next_pow2(slots + (uint64_t)Q * (G->m / kAInline + G->m / kAChunk) +
                 4ull * G->coop_blocks_async * kWarps + 64);
-  if (nunits > (1ull << 26))
+  if (nunits > (1ull << 26)) {
+    if (!required) return TGXD_ERR_UNSUPPORTED;
     return fail(TGXD_ERR_UNSUPPORTED, "async engine: batch too large (use a round-based mode)");
+  }
   if (w.a_slots < slots || w.a_units < nunits) {
     if (!dalloc<unsigned long long>(w.axq, slots) ||
         !dalloc<uint32_t>(w.aunits, nunits * kUnitWords) || !dalloc<AsyncCtl>(w.actl, 1))
@@ -414,6 +415,16 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
     w.a_slots = slots;
     w.a_units = nunits;
   }
+  return TGXD_OK;
+}
+
+static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint32_t ncand,
+                        cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  Workspace& w = G->ws;
+  cudaStream_t s = G->stream;
+  const bool fast = P.kind == TGXD_FASTEST;
+  const uint64_t slots = (uint64_t)P.Q * G->n;
+  if (const int rc = ensure_async(G, P.Q)) return rc;
   async_init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
       w.axq.as<unsigned long long>(), slots);
   async_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
@@ -439,6 +450,8 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
   a.time_limit_ns = 20ull * 1000 * 1000 * 1000;  // watchdog: 20 s
+  a.hctl = nullptr;
+  a.hfa = a.hfb = nullptr;
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
     void* args[] = {&a};
@@ -521,6 +534,15 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   const int pdiv = pf ? atoi(pf) : 8;
   a.pull_f = pdiv <= 0 ? ~0ull : std::max<uint64_t>(1024, slots / pdiv);
   if (const char* pfx = getenv("TGXD_PULL_F")) a.pull_f = strtoull(pfx, nullptr, 10);  // tests
+  // AUTO: a frontier past its peak and below 1/16 of the slots is finished by
+  // the async engine (TGXD_HANDOFF_F overrides the size; 0 turns it off)
+  a.handoff_f = 0;
+  if (mode == TGXD_MODE_AUTO && !fast) {
+    const char* hf = getenv("TGXD_HANDOFF_F");
+    const uint64_t want = hf ? strtoull(hf, nullptr, 10) : std::max<uint64_t>(4096, slots / 16);
+    if (want && ensure_async(G, P.Q, false) == TGXD_OK) a.handoff_f = want;
+  }
+  w.last_handoff = a.handoff_f != 0;
   a.rg = P.kind == TGXD_LATEST_DEPARTURE ? G->out : G->in;
   a.fastest = fast ? 1 : 0;
   a.n_cand = ncand;
@@ -544,6 +566,34 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     void* args[] = {&a};
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)traverse_kernel, dim3(G->coop_blocks),
                                           dim3(kThreads), args, 0, s));
+    if (a.handoff_f) {  // the continuation exits at once unless the round kernel handed off
+      AsyncArgs h;
+      h.g = g;
+      h.qp = a.qp;
+      h.X = a.X;
+      h.EP = a.EP;
+      h.R = nullptr;
+      h.XQ = w.axq.as<unsigned long long>();
+      h.units = w.aunits.as<uint32_t>();
+      h.umask = w.a_units - 1;
+      h.c = w.actl.as<AsyncCtl>();
+      h.n = G->n;
+      h.Q = P.Q;
+      h.strict = P.strict;
+      h.cutoff = a.cutoff;
+      h.fastest = 0;
+      h.n_cand = 0;
+      h.cand_lo = nullptr;
+      h.cand_cnt = nullptr;
+      h.cand_key = nullptr;
+      h.time_limit_ns = 20ull * 1000 * 1000 * 1000;
+      h.hctl = a.ctl;
+      h.hfa = a.fa;
+      h.hfb = a.fb;
+      void* hargs[] = {&h};
+      TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(G->coop_blocks_async),
+                                            dim3(kThreads), hargs, 0, s));
+    }
   } else {
     Control z;
     std::memset(&z, 0, sizeof z);
@@ -567,6 +617,25 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
 }
 
 static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float total_ms) {
+#ifdef TGXD_CHAIN_PROBE
+  {
+    unsigned long long pr[256][12];
+    unsigned int np = 0;
+    cudaStreamSynchronize(G->stream);
+    cudaMemcpyFromSymbol(pr, g_probe, sizeof pr);
+    cudaMemcpyFromSymbol(&np, g_probe_n, sizeof np);
+    for (unsigned i = 0; i < np && i < 256; ++i) {
+      fprintf(stderr, "probe %u:", i);
+      for (int k = 1; k <= 10; ++k)
+        fprintf(stderr, " %lld", pr[i][k] ? (long long)(pr[i][k] - pr[i][0]) : -1ll);
+      fprintf(stderr, " seg %llu cnt %llu\n", pr[i][11] >> 32, pr[i][11] & 0xffffffffull);
+    }
+    fprintf(stderr, "chase cycles: key %llu X %llu off %llu off(hot) %llu\n", pr[255][0], pr[255][1], pr[255][2], pr[255][3]);
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(g_probe_n, &z, sizeof z);
+    cudaMemset(pr, 0, 0);
+  }
+#endif
   if (G->ws.last_async) {
     AsyncCtl c;
     TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.actl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
@@ -601,12 +670,32 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ctl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
   if (c.error) return fail(TGXD_ERR_CUDA, "traversal watchdog: round limit exceeded");
+  AsyncCtl ac;
+  std::memset(&ac, 0, sizeof ac);
+  if (G->ws.last_handoff && c.handoff_n) {  // the async engine finished the tail
+    TGXD_CUDA(cudaMemcpyAsync(&ac, G->ws.actl.p, sizeof ac, cudaMemcpyDeviceToHost, G->stream));
+    TGXD_CUDA(cudaStreamSynchronize(G->stream));
+    if (ac.error) {
+      Workspace& w = G->ws;
+      async_reset_kernel<<<grid_for(w.a_units, G->sm_count), 256, 0, G->stream>>>(
+          w.aunits.as<uint32_t>(), w.a_units, w.actl.as<AsyncCtl>());
+      cudaStreamSynchronize(G->stream);
+      return fail(TGXD_ERR_CUDA, "async traversal watchdog expired");
+    }
+    if (getenv("TGXD_ASTATS"))
+      fprintf(stderr,
+              "handoff %llu: batches %llu chunks %llu edges %llu wait %.3f ms busy %.3f ms "
+              "gap %.1f us prep %.1f us loop %.1f us\n",
+              c.handoff_n, ac.batches, ac.chunks, ac.edges, ac.wait_ns / 1e6, ac.busy_ns / 1e6,
+              (ac.t_entry - c.t_end) / 1e3, (ac.t_loop - ac.t_entry) / 1e3,
+              (ac.t_last - ac.t_loop) / 1e3);
+  }
   if (!st) return TGXD_OK;
   st->rounds = c.rounds;
   st->candidates = c.candidates;
-  st->expansions = c.expansions;
-  st->edges_relaxed = c.edges + c.pull_scanned;
-  st->index_lookups = c.index_lookups;
+  st->expansions = c.expansions + ac.batches + ac.chunks;
+  st->edges_relaxed = c.edges + c.pull_scanned + ac.edges;
+  st->index_lookups = c.index_lookups + ac.index_lookups;
   st->kernel_ms = kernel_ms;
   st->total_ms = total_ms;
   return TGXD_OK;

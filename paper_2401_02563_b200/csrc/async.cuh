@@ -59,6 +59,7 @@ struct AsyncCtl {
   unsigned long long index_lookups;
   unsigned long long batches, chunks;
   unsigned long long wait_ns, busy_ns, t_first, t_last;  // time accounting
+  unsigned long long t_entry, t_loop;  // handoff: kernel entry, queue ready
   unsigned long long bad[4];  // TGXD_VALIDATE: first violation {kind, a, b, c}
 };
 
@@ -81,6 +82,10 @@ struct AsyncArgs {
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
   unsigned long long time_limit_ns;  // watchdog
+  // tail handoff from the round kernel: its frontier queue and labels
+  const Control* hctl;  // nullptr: a query of its own
+  const uint32_t* hfa;
+  const uint32_t* hfb;
 };
 
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
@@ -425,7 +430,40 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
   unsigned long long done = 0, work = 0, ix = 0, nb = 0, nc = 0, wait_ns = 0, busy_ns = 0;
   const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kWarps;
-  if (!a.fastest) {
+  if (a.hctl) {
+    // Continuation of a round-kernel query (traverse.cuh, tail handoff):
+    // labels become label words, the handed-over queue becomes batch units.
+    const unsigned long long nh = __ldcg(&a.hctl->handoff_n);
+    if (nh == 0) return;  // the round kernel finished the query itself
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.c->t_entry = gtimer();
+    const uint32_t* fin = __ldcg(&a.hctl->handoff_flip) ? a.hfb : a.hfa;
+    const unsigned long long t0 = __ldcg(&a.c->tail.v);
+    const size_t slots = (size_t)a.Q * a.n;
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t nthr = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = tid; i < slots; i += nthr) a.XQ[i] = xq_pack(a.X[i], 0u);
+    grid.sync();
+    for (size_t k = tid; k < nh; k += nthr) {
+      const uint32_t item = __ldcg(fin + k);
+      a.XQ[item] = xq_pack(a.X[item], 1u);
+      uint32_t* u = unit_ptr(a, t0 + k / kBatch);
+      u[1 + k % kBatch] = item;
+      if (k % kBatch == 0) u[0] = (uint32_t)min((unsigned long long)kBatch, nh - k);
+    }
+    if (tid == 0) {
+      a.c->abort = 0;
+      a.c->error = 0;
+      a.c->quiesce = 0;
+      a.c->edges = a.c->index_lookups = a.c->batches = a.c->chunks = 0;
+      a.c->wait_ns = a.c->busy_ns = 0;
+      a.c->head.v = a.c->completed.v = t0;
+      a.c->tail.v = t0 + (nh + kBatch - 1) / kBatch;
+      a.c->t_last = 0;
+    }
+    grid.sync();
+    if (tid == 0) a.c->t_loop = gtimer();
+    async_loop(a, rx, vb, 1, t_deadline, done, work, ix, nb, nc, wait_ns, busy_ns);
+  } else if (!a.fastest) {
     async_loop(a, rx, vb, 1, t_deadline, done, work, ix, nb, nc, wait_ns, busy_ns);
   } else {
     for (uint32_t cand = 0; cand < a.n_cand; ++cand) {
@@ -450,6 +488,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
       if (ld_volatile(&a.c->abort)) break;
     }
   }
+  if (lane_id() == 0) atomicMax(&a.c->t_last, gtimer());
   grid.sync();  // every label is final: copy them out
   {
     const size_t slots = (size_t)a.Q * a.n;

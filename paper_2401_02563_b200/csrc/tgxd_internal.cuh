@@ -69,6 +69,7 @@ struct Workspace {
   DeviceBuffer axq, aunits, actl;
   uint64_t a_slots = 0, a_units = 0;
   bool last_async = false;
+  bool last_handoff = false;  // round kernel may have handed its tail to the async engine
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
   unsigned long long* trace_dev = nullptr;
   DeviceBuffer wtrace;
@@ -97,8 +98,14 @@ struct Control {
   unsigned int rounds;
   unsigned int candidates;
   unsigned int error;               // watchdog tripped
-  unsigned int pad;
+  unsigned int handoff_flip;        // handoff: the queue holding the frontier (fb if 1)
+  unsigned long long handoff_n;     // handoff: frontier size left to the async engine
+  unsigned long long t_end;         // globaltimer when the round kernel finished
   unsigned long long state[12];     // CTA-local rounds hand their state over here
+  // grid barrier of the round kernel (traverse.cuh GridBarrier), own lines
+  alignas(128) unsigned int bar_count;
+  alignas(128) unsigned int bar_gen;
+  unsigned int bar_pad[31];
 };
 
 }  // namespace tgxd

@@ -51,6 +51,13 @@ namespace tgxd {
 #ifndef TGXD_MIN_BLOCKS
 #define TGXD_MIN_BLOCKS 4
 #endif
+// Phase functions are inlined (measured: out of line, the calls' stack
+// traffic costs ~25% on config 2); TGXD_NOINLINE_PHASES builds them as calls.
+#ifdef TGXD_NOINLINE_PHASES
+#define TGXD_PHASE __noinline__
+#else
+#define TGXD_PHASE
+#endif
 #ifndef TGXD_LOCAL_F
 #define TGXD_LOCAL_F 128
 #endif
@@ -85,6 +92,7 @@ struct TravArgs {
   unsigned long long dense_f;  // AUTO: frontier above this expands densely
   unsigned long long push_w;   // AUTO: rounds relaxing more edges do not push
   unsigned long long pull_f;   // AUTO: a frontier at least this big is pulled
+  unsigned long long handoff_f; // AUTO: a shrinking frontier this small goes to the async engine
   // fastest sweep (Q == 1)
   int fastest;
   uint32_t n_cand;
@@ -355,6 +363,17 @@ __device__ __forceinline__ uint32_t lane_lower_bound(const DevCsr& g, uint32_t l
   return line_count(g.key, lo, hi, x);
 }
 
+#ifdef TGXD_CHAIN_PROBE
+// Debug: cycle stamps of block 0 / warp 0 / lane 0 along one expansion chain.
+__device__ unsigned long long g_probe[256][12];
+__device__ unsigned int g_probe_n;
+__shared__ unsigned int s_probe_slot;
+#define PROBE_ON (blockIdx.x == 0 && threadIdx.x == 0)
+#define PROBE(slot, k) do { if (PROBE_ON && s_probe_slot < 256) g_probe[s_probe_slot][k] = clock64(); } while (0)
+#else
+#define PROBE(slot, k) do { } while (0)
+#endif
+
 struct ExpandBufs {
   WarpList sm, ch;
   unsigned long long cstart, sstart;
@@ -386,6 +405,10 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
       if (lb < hik) {
         const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
         const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
+#ifdef TGXD_CHAIN_PROBE
+        if (PROBE_ON && (s ^ t ^ (uint32_t)km) == 0x12345678u) asm volatile("trap;");
+        PROBE(g_probe_n, 3);
+#endif
         if (t > s && km >= lb) {
           act = true;
           const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
@@ -398,8 +421,17 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
           } else {
             p1 = km < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
           }
+#ifdef TGXD_CHAIN_PROBE
+          if (PROBE_ON && p1 == 0xfffffff0u) asm volatile("trap;");
+          PROBE(g_probe_n, 4);
+#endif
           p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
           pos = p0;
+#ifdef TGXD_CHAIN_PROBE
+          if (PROBE_ON && p0 == 0xfffffff0u) asm volatile("trap;");
+          PROBE(g_probe_n, 5);
+          if (PROBE_ON && s_probe_slot < 256) g_probe[s_probe_slot][11] = (unsigned long long)(p1 - s) << 32 | (p1 - p0);
+#endif
         }
       }
       a.EP[item] = make_int2(lb, (int32_t)pos);
@@ -461,7 +493,7 @@ __device__ __forceinline__ void flush_work(Control* ctl, unsigned long long work
 // Phase A over a sparse frontier queue (items [0, F) of fin) or, with
 // fin == nullptr, over the implicit dense frontier: every slot whose label
 // bound is below its expansion bound.
-__device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
+__device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
                         unsigned long long cstart, unsigned long long sstart, uint32_t bid,
                         uint32_t nblk, uint64_t pol_keep, uint2* ebuf, unsigned long long& ix) {
   const uint32_t lane = lane_id();
@@ -470,6 +502,26 @@ __device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
   const uint32_t total = fin ? F : a.Q * a.n;
   ExpandBufs eb{{ebuf, 0}, {ebuf + 64, 0}, cstart, sstart};
   unsigned long long work = 0;
+#ifdef TGXD_CHAIN_PROBE
+  const bool probing = fin && nblk == 1 && bid == 0;  // local rounds only
+  if (probing && PROBE_ON && g_probe_n == 0) {
+    // dependent-load latency in situ: 32 random keys, 32 random labels, 32 random offsets
+    uint32_t idx = 12345;
+    long long t0 = clock64();
+    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + (uint32_t)__ldg(a.g.key + idx % a.g.m)) ;
+    long long t1 = clock64();
+    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + (uint32_t)ld_state(a.X + idx % a.n, pol_keep));
+    long long t2 = clock64();
+    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + __ldg(a.g.off + idx % a.n));
+    long long t3 = clock64();
+    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + __ldg(a.g.off + (idx % 1024)));
+    long long t4 = clock64();
+    g_probe[255][0] = (t1 - t0) / 32; g_probe[255][1] = (t2 - t1) / 32; g_probe[255][2] = (t3 - t2) / 32;
+    g_probe[255][3] = (t4 - t3) / 32; g_probe[255][4] = idx;
+  }
+  if (PROBE_ON) s_probe_slot = g_probe_n;
+  if (probing) PROBE(g_probe_n, 0);
+#endif
   for (uint32_t base = gw * 32; base < total; base += nw * 32) {
     const uint32_t i = base + lane;
     bool valid = i < total;
@@ -478,20 +530,37 @@ __device__ void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
     int2 ep = make_int2(kInf, (int32_t)kNoPos);
     if (valid) {
       if (fin) item = __ldcg(fin + i);
+#ifdef TGXD_CHAIN_PROBE
+      if (PROBE_ON && item == 0xfffffff0u) asm volatile("trap;");
+      if (probing) PROBE(g_probe_n, 1);
+#endif
       x = ld_state(a.X + item, pol_keep);
       ep = __ldcg(a.EP + item);
       valid = x != kInf;
+#ifdef TGXD_CHAIN_PROBE
+      if (PROBE_ON && ep.y == 0x7ffffff0) asm volatile("trap;");
+      if (probing) PROBE(g_probe_n, 2);
+#endif
     }
     expand_warp(a, valid, item, x, ep, eb, work, ix);
+#ifdef TGXD_CHAIN_PROBE
+    if (probing) PROBE(g_probe_n, 6);
+#endif
   }
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
+#ifdef TGXD_CHAIN_PROBE
+  if (probing) PROBE(g_probe_n, 7);
+#endif
   flush_work(a.ctl, work);
+#ifdef TGXD_CHAIN_PROBE
+  if (probing) PROBE(g_probe_n, 8);
+#endif
 }
 
 // Phase B: relax the round's chunks and small ranges (plus, for a fastest
 // seed round, the virtual chunks of one explicit range).
-__device__ void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned long long nsmall,
+__device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned long long nsmall,
                         uint32_t xlo,
                         uint32_t xcnt, RelaxCtx& rx, uint32_t bid, uint32_t nblk,
                         uint32_t* wbuf) {
@@ -628,111 +697,188 @@ __device__ __forceinline__ bool pull_admissible(const TravArgs& a, uint2 pl, uin
   return xs != kInf && kp >= bound_of(xs, a.strict);
 }
 
-__device__ void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned long long cstart,
-                            uint32_t bid, uint32_t nblk, uint32_t* wbuf, uint2* ebuf,
+// Warp-shared list of 64 slots: append with a ballot, take 32 at a time.
+__device__ __forceinline__ void slot_list_push(uint2* buf, uint32_t& n, bool p, uint2 v) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, p);
+  if (p) buf[n + __popc(bal & ((1u << lane_id()) - 1))] = v;
+  n += __popc(bal);
+  __syncwarp();
+}
+__device__ __forceinline__ void slot_list_pop(uint2* buf, uint32_t& n, uint32_t taken) {
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  const uint2 t = taken + lane < 64 ? buf[taken + lane] : make_uint2(0u, 0u);
+  __syncwarp();
+  if (lane + taken < n) buf[lane] = t;
+  n -= taken;
+  __syncwarp();
+}
+
+struct PullBufs {
+  PushBuf pb;
+  WarpList chl;          // pull chunks
+  uint2* obuf;           // open slots {slot, lim}
+  uint2* rbuf;           // long windows {slot, lim}
+  uint32_t no, nr;
+  unsigned long long cstart;
+};
+
+// Long windows: the rest of the window below the lane-scanned entries,
+// [lower_bound(1 - lim), t - kPullLane), goes out as pull chunks, those
+// nearest the smallest candidates first. One window per lane.
+__device__ TGXD_PHASE void pull_search32(const TravArgs& a, PullBufs& b, uint32_t cnt) {
+  const DevCsr& rg = a.rg;
+  const uint32_t lane = lane_id();
+  const bool act = lane < cnt;
+  const uint2 r = act ? b.rbuf[lane] : make_uint2(0u, 0u);
+  uint32_t p = 0, j = 0;
+  if (act) {
+    const uint32_t q = a.Q == 1 ? 0u : r.x / a.n;
+    const uint32_t v = r.x - q * a.n;
+    const uint32_t s = __ldg(rg.off + v);
+    j = __ldg(rg.off + v + 1) - kPullLane;
+    p = lane_lower_bound(rg, s, j, 1 - (int32_t)r.y, a.cutoff != 0 && j - s >= a.cutoff);
+  }
+  slot_list_pop(b.rbuf, b.nr, cnt);
+  const uint32_t nch = act ? (j - p + kChunk - 1) / kChunk : 0u;
+  uint32_t bigs = __ballot_sync(0xffffffffu, nch != 0);
+  while (bigs) {
+    const uint32_t L = __ffs(bigs) - 1;
+    bigs &= bigs - 1;
+    const uint32_t I = __shfl_sync(0xffffffffu, r.x, L);
+    const uint32_t bn = __shfl_sync(0xffffffffu, nch, L);
+    const uint32_t P = __shfl_sync(0xffffffffu, p, L);
+    for (uint32_t k0 = 0; k0 < bn; k0 += 32) {
+      // chunk k covers [P + k kChunk, min(P + (k+1) kChunk, window end))
+      const uint32_t k = bn - 1 - min(k0 + lane, bn - 1);
+      list_append(b.chl, k0 + lane < bn, make_uint2(P + k * kChunk, I), &a.ctl->pchunks, b.cstart,
+                  a.chunks);
+    }
+  }
+}
+
+// Open slots (some in-edge below the label): one per lane, the smallest
+// candidates first, kPullBatch entries in flight, until the first admissible
+// one or the end of the window; windows longer than kPullLane entries go to
+// the long-window list.
+__device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs& b, uint32_t cnt,
                             unsigned long long& scanned) {
+  const DevCsr& rg = a.rg;
+  const uint32_t lane = lane_id();
+  const bool act = lane < cnt;
+  const uint2 o = act ? b.obuf[lane] : make_uint2(0u, 0u);
+  slot_list_pop(b.obuf, b.no, cnt);
+  const uint32_t i = o.x;
+  const int32_t lim = (int32_t)o.y;
+  int32_t best = kInf;
+  bool open = act;
+  if (act) {
+    const uint32_t q = a.Q == 1 ? 0u : i / a.n;
+    const uint32_t v = i - q * a.n;
+    const QueryParam& qp = a.qp[q];
+    const uint32_t s = __ldg(rg.off + v);
+    uint32_t j = __ldg(rg.off + v + 1);
+    for (uint32_t k = 0; open && k < kPullLane; k += kPullBatch) {
+      int32_t kr[kPullBatch];
+      uint2 pl[kPullBatch];
+#pragma unroll
+      for (uint32_t e = 0; e < kPullBatch; ++e) {
+        const bool in = j > s + e;
+        kr[e] = in ? __ldg(rg.key + j - 1 - e) : kInf;
+        pl[e] = in ? __ldg(rg.pay + j - 1 - e) : make_uint2(0u, 0x7fffffffu);
+      }
+      uint32_t stop = kPullBatch;  // first entry outside the window (keys ascend)
+#pragma unroll
+      for (int e = kPullBatch - 1; e >= 0; --e)
+        if (j <= s + e || -kr[e] >= lim) stop = e;
+      bool adm[kPullBatch];
+#pragma unroll
+      for (uint32_t e = 0; e < kPullBatch; ++e)
+        adm[e] = e < stop && pull_admissible(a, pl[e], q, qp, rx.pol_keep);
+      uint32_t hit = stop;
+#pragma unroll
+      for (int e = kPullBatch - 1; e >= 0; --e)
+        if (adm[e]) hit = e;
+#pragma unroll
+      for (uint32_t e = 0; e < kPullBatch; ++e)
+        if (e == hit && hit < stop) best = -kr[e];
+      scanned += min(hit + 1, stop);
+      if (hit < stop || stop < kPullBatch) open = false;
+      j -= kPullBatch;
+    }
+  }
+  // every candidate is below the label, so finding one improves it
+  const bool improved = best != kInf;
+  if (improved) {
+    a.X[i] = best;
+    if (a.R) atomicMin(a.R + i, best - rx.depart);
+  }
+  const uint32_t bal = __ballot_sync(0xffffffffu, improved);
+  if (bal) {
+    if (improved) b.pb.buf[b.pb.n + __popc(bal & ((1u << lane) - 1))] = i;
+    b.pb.n += __popc(bal);
+    if (b.pb.n >= 32) push_flush32(b.pb, a.ctl, rx.pstart, rx.fout);
+  }
+  slot_list_push(b.rbuf, b.nr, open, o);
+  if (b.nr >= 32) pull_search32(a, b, 32);
+}
+
+#ifndef TGXD_PULL_SLOTS
+#define TGXD_PULL_SLOTS 4
+#endif
+constexpr uint32_t kPullSlots = TGXD_PULL_SLOTS;  // slot groups per lane in flight in the sweep
+
+__device__ TGXD_PHASE void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned long long cstart,
+                            uint32_t bid, uint32_t nblk, uint32_t* wbuf, uint2* ebuf,
+                            uint2* rbuf, unsigned long long& scanned) {
   const DevCsr& rg = a.rg;
   const uint32_t lane = lane_id();
   const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = nblk * kWarps;
   const uint32_t slots = a.Q * a.n;
-  PushBuf pb{wbuf, 0};
-  WarpList chl{ebuf, 0};
-  for (uint32_t base = gw * 32; base < slots; base += nw * 32) {
-    const uint32_t i = base + lane;
-    const bool valid = i < slots;
-    uint32_t q = 0, v = 0, s = 0, j = 0;
-    int32_t x0 = kInf, best = kInf, lim = kInf;
-    bool open = false;  // window not exhausted
-    if (valid) {
-      q = a.Q == 1 ? 0u : i / a.n;
-      v = i - q * a.n;
-      const QueryParam& qp = a.qp[q];
-      // independent loads: label, last key of the segment, segment bounds
-      x0 = ld_state(a.X + i, rx.pol_keep);
-      const int32_t km = __ldg(rg.kmax + v);
-      s = __ldg(rg.off + v);
-      j = __ldg(rg.off + v + 1);
-      best = x0;
-      // candidates below lim: key_R >= 1 - lim, a suffix of the segment
-      lim = min(x0, qp.vhi + 1);
-      open = km >= 1 - lim;
-      // every edge admissible under the round-start label is considered now
-      if (x0 != kInf) {
-        int32_t lb = (v == qp.root) ? qp.klo : bound_of(x0, a.strict);
-        if (lb < qp.klo) lb = qp.klo;
-        a.EP[i] = make_int2(lb, (int32_t)kNoPos);
+  PullBufs b{{wbuf, 0}, {ebuf, 0}, ebuf + 64, rbuf, 0, 0, cstart};
+  // label sweep: coalesced labels and last keys; slots with an in-edge below
+  // their label are queued for the scan
+  for (uint32_t base = gw * 32 * kPullSlots; base < slots; base += nw * 32 * kPullSlots) {
+    int32_t x[kPullSlots], km[kPullSlots];
+#pragma unroll
+    for (uint32_t u = 0; u < kPullSlots; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      const uint32_t q = a.Q == 1 ? 0u : i / a.n;
+      x[u] = i < slots ? ld_state(a.X + i, rx.pol_keep) : kInf;
+      km[u] = i < slots ? __ldg(rg.kmax + (i - q * a.n)) : INT32_MIN;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kPullSlots; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      bool open = false;
+      int32_t lim = 0;
+      if (i < slots) {
+        const uint32_t q = a.Q == 1 ? 0u : i / a.n;
+        const QueryParam& qp = a.qp[q];
+        // candidates below lim: key_R >= 1 - lim, a suffix of the segment
+        lim = min(x[u], qp.vhi + 1);
+        open = km[u] >= 1 - lim;
+        // every edge admissible under the round-start label is considered now
+        if (x[u] != kInf) {
+          int32_t lb = (i - q * a.n == qp.root) ? qp.klo : bound_of(x[u], a.strict);
+          if (lb < qp.klo) lb = qp.klo;
+          a.EP[i] = make_int2(lb, (int32_t)kNoPos);
+        }
       }
-    }
-    // the smallest candidates first, kPullBatch entries in flight, until the
-    // first admissible one or the end of the window
-    for (uint32_t k = 0; open && k < kPullLane; k += kPullBatch) {
-      const QueryParam& qp = a.qp[q];
-      int32_t kr[kPullBatch];
-      uint2 pl[kPullBatch];
-#pragma unroll
-      for (uint32_t b = 0; b < kPullBatch; ++b) {
-        const bool in = j > s + b;
-        kr[b] = in ? __ldg(rg.key + j - 1 - b) : kInf;
-        pl[b] = in ? __ldg(rg.pay + j - 1 - b) : make_uint2(0u, 0x7fffffffu);
-      }
-      uint32_t stop = kPullBatch;  // first entry outside the window (keys ascend)
-#pragma unroll
-      for (int b = kPullBatch - 1; b >= 0; --b)
-        if (j <= s + b || -kr[b] >= lim) stop = b;
-      bool adm[kPullBatch];
-#pragma unroll
-      for (uint32_t b = 0; b < kPullBatch; ++b)
-        adm[b] = b < stop && pull_admissible(a, pl[b], q, qp, rx.pol_keep);
-      uint32_t hit = stop;
-#pragma unroll
-      for (int b = kPullBatch - 1; b >= 0; --b)
-        if (adm[b]) hit = b;
-#pragma unroll
-      for (uint32_t b = 0; b < kPullBatch; ++b)
-        if (b == hit && hit < stop) best = -kr[b];
-      scanned += min(hit + 1, stop);
-      if (hit < stop || stop < kPullBatch) open = false;
-      j -= kPullBatch;
-    }
-    uint32_t p = j;
-    if (open)  // a long window: the rest goes to pull chunks
-      p = lane_lower_bound(rg, s, j, 1 - lim, a.cutoff != 0 && j - s >= a.cutoff);
-    const bool improved = best < x0;
-    if (improved) {
-      a.X[i] = best;
-      if (a.R) atomicMin(a.R + i, best - rx.depart);
-    }
-    const uint32_t bal = __ballot_sync(0xffffffffu, improved);
-    if (bal) {
-      if (improved) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = i;
-      pb.n += __popc(bal);
-      if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
-    }
-    // chunks of [p, j), those nearest the smallest candidates first
-    const uint32_t nch = open ? (j - p + kChunk - 1) / kChunk : 0u;
-    uint32_t bigs = __ballot_sync(0xffffffffu, nch != 0);
-    while (bigs) {
-      const uint32_t L = __ffs(bigs) - 1;
-      bigs &= bigs - 1;
-      const uint32_t I = __shfl_sync(0xffffffffu, i, L);
-      const uint32_t bn = __shfl_sync(0xffffffffu, nch, L);
-      const uint32_t P = __shfl_sync(0xffffffffu, p, L);
-      for (uint32_t k0 = 0; k0 < bn; k0 += 32) {
-        // chunk k covers [P + k kChunk, min(P + (k+1) kChunk, window end))
-        const uint32_t k = bn - 1 - min(k0 + lane, bn - 1);
-        list_append(chl, k0 + lane < bn, make_uint2(P + k * kChunk, I), &a.ctl->pchunks, cstart,
-                    a.chunks);
-      }
+      slot_list_push(b.obuf, b.no, open, make_uint2(i, (uint32_t)lim));
+      if (b.no >= 32) pull_scan32(a, rx, b, 32, scanned);
     }
   }
-  push_drain(pb, a.ctl, rx.pstart, rx.fout);
-  list_drain(chl, &a.ctl->pchunks, cstart, a.chunks);
+  while (b.no) pull_scan32(a, rx, b, min(b.no, 32u), scanned);
+  while (b.nr) pull_search32(a, b, min(b.nr, 32u));
+  push_drain(b.pb, a.ctl, rx.pstart, rx.fout);
+  list_drain(b.chl, &a.ctl->pchunks, cstart, a.chunks);
 }
 
 // P2: one warp per pull chunk, kUnroll entries per lane. A chunk's entries
 // run from its first position to min(first + kChunk, window end).
-__device__ void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned long long nch, uint32_t bid,
+__device__ TGXD_PHASE void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned long long nch, uint32_t bid,
                             uint32_t nblk, uint32_t* wbuf, unsigned long long& scanned) {
   const DevCsr& rg = a.rg;
   const uint32_t lane = lane_id();
@@ -781,6 +927,43 @@ __device__ void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned long long 
   push_drain(pb, a.ctl, rx.pstart, rx.fout);
 }
 
+// Grid barrier for the persistent round kernel. One arrival atomic per
+// block; waiters poll the generation word with exponential __nanosleep
+// backoff, so ~600 blocks idling through a CTA-local round (or a slow phase)
+// do not keep one L2 slice saturated with polls — which stretches every
+// other memory access the working warps make (measured: ~1 us per
+// dependent load instead of ~0.4 us). Release/acquire as in cg's grid sync.
+struct GridBarrier {
+  unsigned int* count;
+  unsigned int* gen;
+  unsigned int nblocks;
+  unsigned int phase;  // generations passed (identical in every block)
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int g = phase;
+      __threadfence();
+      if (atomicAdd(count, 1u) + 1 == nblocks) {
+        *count = 0;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+      } else {
+        unsigned int ns = 32;
+        for (;;) {
+          unsigned int cur;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
+          if (cur != g) break;
+          __nanosleep(ns);
+          if (ns < 1024) ns <<= 1;
+        }
+      }
+      __threadfence();
+    }
+    ++phase;
+    __syncthreads();
+  }
+};
+
 // Traversal state; identical in every block at every grid barrier.
 //
 // Counter discipline. The shared counters (pushes, improved, chunks,
@@ -799,6 +982,7 @@ struct TState {
   uint32_t flip;               // fin/fout parity
   int dense;                   // the next expand scans densely
   int pending;                 // CTA expand done, grid relax of its work pending
+  uint32_t last_f;             // previous round's frontier size
 };
 
 __device__ __forceinline__ void save_state(Control* ctl, const TState& s) {
@@ -808,10 +992,36 @@ __device__ __forceinline__ void save_state(Control* ctl, const TState& s) {
 #pragma unroll
   for (int i = 0; i < (int)(sizeof(TState) / 8); ++i) dst[i] = src[i];
 }
+// Post-barrier reads of shared counters go through one thread per block and
+// shared memory: the same address read by every warp of the grid would
+// queue ~5k requests at one L2 slice (~10 us per read).
 __device__ __forceinline__ void load_state(const Control* ctl, TState& s) {
+  __shared__ unsigned long long s_st[sizeof(TState) / 8];
+  if (threadIdx.x < sizeof(TState) / 8) s_st[threadIdx.x] = __ldcg(ctl->state + threadIdx.x);
+  __syncthreads();
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
 #pragma unroll
-  for (int i = 0; i < (int)(sizeof(TState) / 8); ++i) dst[i] = __ldcg(ctl->state + i);
+  for (int i = 0; i < (int)(sizeof(TState) / 8); ++i) dst[i] = s_st[i];
+  __syncthreads();
+}
+
+struct Counters {
+  unsigned long long pushes, improved, chunks, smalls, edges, pchunks;
+};
+__device__ __forceinline__ Counters read_counters(const Control* ctl) {
+  __shared__ Counters s_c;
+  if (threadIdx.x == 0) {
+    s_c.pushes = __ldcg(&ctl->pushes);
+    s_c.improved = __ldcg(&ctl->improved);
+    s_c.chunks = __ldcg(&ctl->chunks);
+    s_c.smalls = __ldcg(&ctl->smalls);
+    s_c.edges = __ldcg(&ctl->edges);
+    s_c.pchunks = __ldcg(&ctl->pchunks);
+  }
+  __syncthreads();
+  const Counters c = s_c;
+  __syncthreads();
+  return c;
 }
 
 __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int slot,
@@ -846,7 +1056,7 @@ __device__ __forceinline__ unsigned long long block_read(const unsigned long lon
 // moving counters meanwhile). Returns with st updated and, if an expand
 // produced more edge work than one CTA should relax, st.pending set with the
 // relax left to the grid.
-__device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32_t xcnt,
+__device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32_t xcnt,
                              int32_t depart, int32_t vhi0, uint64_t pol_stream,
                              uint64_t pol_keep, uint32_t* wbuf, uint2* ebuf,
                              unsigned long long& ix) {
@@ -879,6 +1089,9 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
       const unsigned long long c_end = block_read(&ctl->chunks);
       const unsigned long long s_end = block_read(&ctl->smalls);
       const unsigned long long e_end = block_read(&ctl->edges);
+#ifdef TGXD_CHAIN_PROBE
+      PROBE(g_probe_n, 9);
+#endif
       if (tr) {
         trace_round(a, st.rounds, 1, gtimer());
         trace_round(a, st.rounds, 4, c_end - st.c_cur);
@@ -889,6 +1102,11 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
         return;
       }
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, 0, 1, wbuf);
+#ifdef TGXD_CHAIN_PROBE
+      PROBE(g_probe_n, 10);
+      __syncthreads();
+      if (PROBE_ON) ++g_probe_n;
+#endif
       st.c_cur = c_end;
       st.s_cur = s_end;
       st.e_cur = e_end;
@@ -908,7 +1126,8 @@ __device__ void local_rounds(const TravArgs& a, TState& st, uint32_t xlo, uint32
 __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
   __shared__ uint2 s_ebuf[kWarps][128];
-  cg::grid_group grid = cg::this_grid();
+  __shared__ uint2 s_rbuf[kWarps][64];
+  GridBarrier grid{&a.ctl->bar_count, &a.ctl->bar_gen, gridDim.x, 0};
   uint32_t* wbuf = s_buf[threadIdx.x >> 5];
   uint2* ebuf = s_ebuf[threadIdx.x >> 5];
   Control* ctl = a.ctl;
@@ -927,6 +1146,8 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   st.flip = 0;
   st.dense = a.mode == TGXD_MODE_DENSE;
   st.pending = 0;
+  st.last_f = 0;
+  bool handed = false;
   for (uint32_t cand = 0;; ++cand) {
     int32_t depart = 0;
     uint32_t xlo = 0, xcnt = 0;
@@ -949,6 +1170,20 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       const unsigned long long F =
           xcnt ? 0 : (st.dense ? st.i_known - st.prev_i : st.p_known - st.prev_p);
       if (!xcnt && F == 0) break;
+      // Tail handoff: once the frontier is past its peak and small, the
+      // barrier-free engine (async.cuh) finishes the query from this queue
+      // and these labels / expansion bounds — the same fixpoint, without a
+      // ~10 us latency floor per round.
+      if (!xcnt && !st.dense && !a.fastest && F <= a.handoff_f && F < st.last_f &&
+          st.rounds >= 2) {
+        if (tr) {
+          ctl->handoff_n = F;
+          ctl->handoff_flip = st.flip;
+        }
+        handed = true;
+        break;
+      }
+      if (!xcnt) st.last_f = (uint32_t)min(F, 0xffffffffull);
       const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
                             (xcnt ? xcnt <= kLocalMaxW : F <= kLocalMaxF);
       if (go_local) {
@@ -962,16 +1197,17 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         load_state(ctl, st);
         if (!st.pending) continue;
         // the grid relaxes what the CTA expanded
-        const unsigned long long c_end = __ldcg(&ctl->chunks), s_end = __ldcg(&ctl->smalls);
-        const unsigned long long e_end = __ldcg(&ctl->edges);
+        const Counters c0 = read_counters(ctl);
+        const unsigned long long c_end = c0.chunks, s_end = c0.smalls, e_end = c0.edges;
         const unsigned long long p_now = st.p_known;
         uint32_t* fout = st.flip ? a.fa : a.fb;
         RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
         phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
         trace_warp_done(a, st.rounds, 1);
         grid.sync();
-        st.p_known = __ldcg(&ctl->pushes);
-        st.i_known = __ldcg(&ctl->improved);
+        const Counters c1 = read_counters(ctl);
+        st.p_known = c1.pushes;
+        st.i_known = c1.improved;
         st.c_cur = c_end;
         st.s_cur = s_end;
         st.e_cur = e_end;
@@ -1003,10 +1239,10 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         // P1 queues slots right away: every block's post-barrier read of the
         // pushes counter must be over first (counter discipline)
         grid.sync();
-        phase_pull1(a, rx, st.pc_cur, blockIdx.x, gridDim.x, wbuf, ebuf, scanned);
+        phase_pull1(a, rx, st.pc_cur, blockIdx.x, gridDim.x, wbuf, ebuf, s_rbuf[threadIdx.x >> 5], scanned);
         trace_warp_done(a, st.rounds, 0);
         grid.sync();
-        const unsigned long long pc_end = __ldcg(&ctl->pchunks);
+        const unsigned long long pc_end = read_counters(ctl).pchunks;
         if (tr) {
           trace_round(a, st.rounds, 1, gtimer());
           trace_round(a, st.rounds, 4, pc_end - st.pc_cur);
@@ -1017,8 +1253,9 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         work_pull += scanned;
         trace_warp_done(a, st.rounds, 1);
         grid.sync();
-        st.p_known = __ldcg(&ctl->pushes);
-        st.i_known = __ldcg(&ctl->improved);
+        const Counters c1 = read_counters(ctl);
+        st.p_known = c1.pushes;
+        st.i_known = c1.improved;
         st.prev_p = p_now;
         st.flip ^= 1u;
         st.dense = 0;
@@ -1035,9 +1272,10 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
                 gridDim.x, pol_keep, ebuf, ix);
         trace_warp_done(a, st.rounds, 0);
         grid.sync();
-        c_end = __ldcg(&ctl->chunks);
-        s_end = __ldcg(&ctl->smalls);
-        e_end = __ldcg(&ctl->edges);
+        const Counters c0 = read_counters(ctl);
+        c_end = c0.chunks;
+        s_end = c0.smalls;
+        e_end = c0.edges;
       }
       if (tr) {
         trace_round(a, st.rounds, 1, gtimer());
@@ -1057,8 +1295,9 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       }
       trace_warp_done(a, st.rounds, 1);
       grid.sync();
-      st.p_known = __ldcg(&ctl->pushes);
-      st.i_known = __ldcg(&ctl->improved);
+      const Counters c1 = read_counters(ctl);
+      st.p_known = c1.pushes;
+      st.i_known = c1.improved;
       st.c_cur = c_end;
       st.s_cur = s_end;
       st.e_cur = e_end;
@@ -1081,7 +1320,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         if (st.dense) st.prev_i = st.i_known - pushed;
       }
     }
-    if (!a.fastest || st.rounds > a.round_limit) break;
+    if (!a.fastest || handed || st.rounds > a.round_limit) break;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1091,6 +1330,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   if (lane_id() == 0 && ix) atomicAdd(&ctl->index_lookups, ix);
   if (lane_id() == 0 && work_pull) atomicAdd(&ctl->pull_scanned, work_pull);
   if (tr) {
+    ctl->t_end = gtimer();
     ctl->rounds = st.rounds;
     ctl->expansions = __ldcg(&ctl->chunks) + __ldcg(&ctl->smalls);
     ctl->candidates = a.fastest ? a.n_cand : 0;
@@ -1130,7 +1370,10 @@ __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_
     ctl->index_lookups = 0;
     ctl->pull_scanned = 0;
     ctl->pchunks = 0;
+    ctl->handoff_n = 0;
     ctl->error = 0;
+    ctl->bar_count = 0;
+    ctl->bar_gen = 0;
   }
   if (q >= Q || fastest) return;
   const uint32_t item = q * n + qp[q].root;

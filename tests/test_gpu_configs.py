@@ -113,3 +113,19 @@ def test_repeated_queries_are_stable(mode):
         for _ in range(12):
             got = FN[kind](g, src, w, T.AlgoOptions(mode=mode)).values
             assert np.array_equal(got, want), (kind, mode)
+
+
+@pytest.mark.parametrize("handoff", ["0", "1000000000"])
+def test_tail_handoff_parity(monkeypatch, handoff):
+    """AUTO hands a shrinking frontier to the async engine; off (0) and
+    always-at-the-first-decline (huge threshold) give the same labels."""
+    monkeypatch.setenv("TGXD_HANDOFF_F", handoff)
+    for name in ("c2", "c4"):
+        wl, g, qs = setup(name, -8)
+        o = Oracle(T.generate_edges(wl.gen), wl.gen.n_vertices)
+        for q in qs:
+            for kind in ("earliest_arrival", "latest_departure"):
+                want = o.query(kind, q.vertex, q.window.t_a, q.window.t_b)
+                for _ in range(3):
+                    got = FN[kind](g, q.vertex, q.window).values
+                    assert np.array_equal(got, want), (name, kind, handoff)
