@@ -210,7 +210,30 @@ struct RelaxCtx {
 // Relax kUnroll 32-edge steps: e[u] edge ids, q[u] query slots, act[u] lane
 // validity. write_min (parallel.hpp:91-99) is a plain label probe followed by
 // atomicMin when the probe says the edge can improve.
+// Payload loads of kUnroll 32-edge steps (inactive lanes get a no-op edge).
+__device__ __forceinline__ void relax_load(const TravArgs& a, const uint32_t (&e)[kUnroll],
+                                           const bool (&act)[kUnroll], const RelaxCtx& rx,
+                                           uint2 (&pl)[kUnroll]) {
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    pl[u] = act[u] ? ld_stream2(a.g.pay + e[u], rx.pol_stream) : make_uint2(0u, kInf);
+}
+
+__device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)[kUnroll],
+                                            const uint32_t (&q)[kUnroll],
+                                            const bool (&act)[kUnroll], RelaxCtx& rx,
+                                            PushBuf& pb);
+
 __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&e)[kUnroll],
+                                            const uint32_t (&q)[kUnroll],
+                                            const bool (&act)[kUnroll], RelaxCtx& rx,
+                                            PushBuf& pb) {
+  uint2 pl[kUnroll];
+  relax_load(a, e, act, rx, pl);
+  relax_apply(a, pl, q, act, rx, pb);
+}
+
+__device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)[kUnroll],
                                             const uint32_t (&q)[kUnroll],
                                             const bool (&act)[kUnroll], RelaxCtx& rx,
                                             PushBuf& pb) {
@@ -218,9 +241,8 @@ __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&
   uint32_t idx[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    const uint2 pl = act[u] ? ld_stream2(a.g.pay + e[u], rx.pol_stream) : make_uint2(0u, kInf);
-    idx[u] = q[u] * a.n + pl.x;
-    v[u] = (int32_t)pl.y;
+    idx[u] = q[u] * a.n + pl[u].x;
+    v[u] = (int32_t)pl[u].y;
   }
   int32_t cur[kUnroll];
 #pragma unroll
@@ -334,11 +356,45 @@ __device__ __forceinline__ uint32_t line_count(const int32_t* key, uint32_t lo, 
   return lo + c;
 }
 
+#ifndef TGXD_SEARCH_W
+#define TGXD_SEARCH_W 8
+#endif
+constexpr int kSearchW = TGXD_SEARCH_W;  // probes per search step
+
+// W-ary narrowing of [a, b] (the first element >= x of the sorted A lies in
+// it): each step issues W independent probes — one memory latency instead
+// of log2(W + 1) dependent ones — and keeps the gap between the last probe
+// below x and the first one at or above it. A range of <= W + 1 elements is
+// resolved exactly in one step.
+__device__ __forceinline__ void wide_narrow(const int32_t* A, uint32_t& a, uint32_t& b, int32_t x,
+                                            uint32_t stop) {
+  while (b - a > stop) {
+    const uint32_t len = b - a;
+    int32_t v[kSearchW];
+#pragma unroll
+    for (int k = 0; k < kSearchW; ++k)
+      v[k] = __ldg(A + a + (uint32_t)(((unsigned long long)len * (k + 1)) / (kSearchW + 1)));
+    uint32_t na = a, nb = b;
+#pragma unroll
+    for (int k = 0; k < kSearchW; ++k) {
+      const uint32_t pk = a + (uint32_t)(((unsigned long long)len * (k + 1)) / (kSearchW + 1));
+      if (v[k] < x) na = pk + 1;
+    }
+#pragma unroll
+    for (int k = kSearchW - 1; k >= 0; --k) {
+      const uint32_t pk = a + (uint32_t)(((unsigned long long)len * (k + 1)) / (kSearchW + 1));
+      if (v[k] >= x) nb = pk;
+    }
+    a = na;
+    b = nb;
+  }
+}
+
 // lower_bound(x) over key[lo, hi) by one lane. With `fence` (the vertex is
 // at or above the index cutoff) the selective index first narrows the range
-// to one 32-key line by binary search over the fence array (every 32nd key
-// of the layout, a compact "bucketed timeline"); otherwise the keys
-// themselves are bisected down to 32. The last line is counted with vector
+// to one 32-key line through the fence array (every 32nd key of the layout,
+// a compact "bucketed timeline"); otherwise the keys themselves are narrowed
+// down to 32. Both with W-ary steps; the last line is counted with vector
 // loads. Results-neutral, like the reference's TGER-vs-scan choice
 // (test_algorithms.cpp:196-217).
 __device__ __forceinline__ uint32_t lane_lower_bound(const DevCsr& g, uint32_t lo, uint32_t hi,
@@ -347,19 +403,11 @@ __device__ __forceinline__ uint32_t lane_lower_bound(const DevCsr& g, uint32_t l
     const uint32_t jlo = (lo + kFenceStride - 1) >> kFenceShift;
     const uint32_t jhi = (hi - 1) >> kFenceShift;
     uint32_t a = jlo, b = jhi + 1;  // first fence >= x in [jlo, jhi], else jhi + 1
-    while (a < b) {
-      const uint32_t mid = (a + b) >> 1;
-      if (__ldg(g.fence + mid) < x) a = mid + 1;
-      else b = mid;
-    }
+    wide_narrow(g.fence, a, b, x, 0);
     if (a > jlo) lo = max(lo, ((a - 1) << kFenceShift) + 1);
     if (a <= jhi) hi = min(hi, a << kFenceShift);
   }
-  while (hi - lo > 32) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(g.key + mid) < x) lo = mid + 1;
-    else hi = mid;
-  }
+  if (hi - lo > 32) wide_narrow(g.key, lo, hi, x, 32);
   return line_count(g.key, lo, hi, x);
 }
 
@@ -584,7 +632,9 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
     relax_steps(a, e, q, act, rx, pb);
   }
 
-  // chunks of big ranges: coalesced kChunk-edge bursts
+  // chunks of big ranges: coalesced kChunk-edge bursts (software-pipelining
+  // the next chunk's payload loads measured no gain: the relax is bound by
+  // the L2 atomic rate, ~150 G/s when most edges improve)
   uint2 nxt = gw < nchunks ? __ldcg(a.chunks + gw) : make_uint2(0u, 0u);
   for (unsigned long long c = gw; c < nchunks; c += nw) {
     const uint2 ch = nxt;  // descriptor prefetched one iteration ahead
