@@ -26,7 +26,8 @@ _P = ctypes.POINTER
 _u32p = _P(ctypes.c_uint32)
 _u64p = _P(ctypes.c_uint64)
 _i64p = _P(ctypes.c_int64)
-KIND = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2}
+KIND = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2, "shortest_duration": 3,
+        "temporal_bfs": 4}
 
 
 class OracleError(Exception):

@@ -5,8 +5,8 @@
 // the Python tests, the golden-vector script and bench.py's reference arm call
 // the reference's own entry points through ctypes:
 //   TemporalGraph::build           /root/reference/proj/include/tgx/engine.hpp:32-33
-//   earliest_arrival / latest_departure / fastest_path
-//                                  /root/reference/proj/include/tgx/algorithms.hpp:46-58
+//   earliest_arrival / latest_departure / fastest_path / shortest_duration /
+//   temporal_bfs                   /root/reference/proj/include/tgx/algorithms.hpp:46-66
 //   oracle::enumerate_paths        /root/reference/proj/tests/support/oracle.hpp:27-29
 //   set_workers / num_workers      /root/reference/proj/include/tgx/parallel.hpp:19-21
 // Exceptions are mapped to integer codes (1 out_of_range, 2 invalid_argument,
@@ -88,7 +88,8 @@ int tgxref_build(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
 
 void tgxref_free(void* g) { delete static_cast<tgx::TemporalGraph*>(g); }
 
-// kind: 0 earliest arrival, 1 latest departure, 2 fastest.
+// kind: 0 earliest arrival, 1 latest departure, 2 fastest, 3 shortest duration
+// (unweighted), 4 temporal BFS.
 // force: -1 graph default, 0 auto, 1 index, 2 scan.
 int tgxref_query(void* gp, int kind, std::uint32_t vertex, std::uint64_t ta, std::uint64_t tb,
                  int ordering, int force, std::int64_t* out) {
@@ -107,13 +108,16 @@ int tgxref_query(void* gp, int kind, std::uint32_t vertex, std::uint64_t ta, std
       case 0: r = tgx::earliest_arrival(g, vertex, w, opts); break;
       case 1: r = tgx::latest_departure(g, vertex, w, opts); break;
       case 2: r = tgx::fastest_path(g, vertex, w, opts); break;
+      case 3: r = tgx::shortest_duration(g, vertex, w, opts); break;
+      case 4: r = tgx::temporal_bfs(g, vertex, w, opts); break;
       default: throw std::invalid_argument("unknown query kind");
     }
     std::memcpy(out, r.values.data(), r.values.size() * sizeof(std::int64_t));
   });
 }
 
-// metric: 0 EA, 1 LD, 2 fastest (oracle::PathMetric order).
+// metric: 0 EA, 1 LD, 2 fastest, 3 shortest duration, 4 hops (oracle::PathMetric
+// order, tests/support/oracle.hpp:19).
 int tgxref_enumerate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
                      const std::uint32_t* dst, const std::uint64_t* start,
                      const std::uint64_t* end, std::uint32_t vertex, std::uint64_t ta,

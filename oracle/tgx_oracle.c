@@ -26,6 +26,7 @@
 #define INF64 ((int64_t)0x7fffffffffffffffLL)    /* PathResult::kUnreachedMin, algorithms.hpp:17 */
 #define NEGINF64 ((int64_t)(-0x7fffffffffffffffLL - 1)) /* kUnreachedMax, algorithms.hpp:18 */
 #define TIME_LIMIT ((uint64_t)0x7fffffffffffffffULL)    /* internal.hpp:17-25, types.cpp:29 */
+#define TIME_MAX_U64 UINT64_MAX                          /* kMaxTimestamp, types.hpp */
 
 static _Thread_local char g_err[256];
 
@@ -502,18 +503,369 @@ static void fastest(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t 
   free(touched.v);
 }
 
+/* ---- Edge-state traversals ------------------------------------------------
+ * Growable edge-id list (flat positions of one layout). */
+typedef struct {
+  uint64_t* v;
+  uint64_t n, cap;
+} elist;
+
+static void epush(elist* l, uint64_t x) {
+  if (l->n == l->cap) {
+    l->cap = l->cap ? 2 * l->cap : 64;
+    l->v = realloc(l->v, l->cap * sizeof(uint64_t));
+  }
+  l->v[l->n++] = x;
+}
+
+static int u64_cmp(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* merge_edge_buffers: sort (path_algorithms.cpp:27-35; ids are unique by
+ * construction of the callers). */
+static void esort(elist* l) {
+  if (l->n > 1) qsort(l->v, l->n, sizeof(uint64_t), u64_cmp);
+}
+
+/* ordering_holds, types.hpp:72-82 (a precedes b). */
+static int holds(uint64_t as, uint64_t ae, uint64_t bs, uint64_t be, int ord) {
+  switch (ord) {
+    case TGXO_SUCCEEDS: return ae <= bs;
+    case TGXO_STRICTLY_SUCCEEDS: return ae < bs;
+    default: return as < bs && bs <= ae && ae < be;
+  }
+}
+
+/* forward_window / backward_window, internal.hpp:33-77: the retrieval
+ * window for edges that may follow (Out) or precede (In) interval [s, e];
+ * returns 0 when empty. */
+static int step_window(uint64_t s, uint64_t e, int ord, int out_dir, uint64_t* ta, uint64_t* tb) {
+  if (out_dir) {
+    uint64_t lo = *ta;
+    switch (ord) {
+      case TGXO_SUCCEEDS: lo = e; break;
+      case TGXO_STRICTLY_SUCCEEDS:
+        if (e == TIME_MAX_U64) return 0;
+        lo = e + 1;
+        break;
+      default:
+        if (s == TIME_MAX_U64) return 0;
+        lo = s + 1;
+        break;
+    }
+    if (lo > *ta) *ta = lo;
+  } else {
+    uint64_t hi = *tb;
+    switch (ord) {
+      case TGXO_SUCCEEDS: hi = s; break;
+      case TGXO_STRICTLY_SUCCEEDS:
+        if (s == 0) return 0;
+        hi = s - 1;
+        break;
+      default:
+        if (e == 0) return 0;
+        hi = e - 1;
+        break;
+    }
+    if (hi < *tb) *tb = hi;
+  }
+  return *ta <= *tb;
+}
+
+/* for_each_in_window over one segment (tcsr.hpp:60-69): start >= t_a and
+ * end <= t_b, scanning from the first start >= t_a up to start > t_b. The
+ * reference's index path yields the same set (test_algorithms.cpp:196-217). */
+#define FOR_WINDOW(c, v, ta_, tb_, e)                                              \
+  for (uint64_t e = lower_start((c), (c)->off[(v)], (c)->off[(v) + 1], (ta_));    \
+       e < (c)->off[(v) + 1] && (c)->st[e] <= (tb_); ++e)                          \
+    if ((c)->en[e] <= (tb_))
+
+/* edge_reachability, path_algorithms.cpp:40-87: breadth-first search over
+ * the edges of one layout under Overlaps; level[e] = the round an edge is
+ * first reached (seeds: round 1), 0 if never. */
+static uint32_t* edge_reachability(const tgxo_graph* g, uint64_t ta, uint64_t tb, int out_dir,
+                                   uint32_t anchor) {
+  const ocsr* c = out_dir ? &g->out : &g->in;
+  uint32_t* level = calloc(g->m ? g->m : 1, sizeof(uint32_t));
+  elist fr = {0}, nx = {0};
+  FOR_WINDOW(c, anchor, ta, tb, f) {
+    if (!level[f]) {
+      level[f] = 1;
+      epush(&fr, f);
+    }
+  }
+  esort(&fr);
+  uint32_t round = 1;
+  while (fr.n) {
+    ++round;
+    nx.n = 0;
+    for (uint64_t i = 0; i < fr.n; ++i) {
+      const uint64_t e = fr.v[i];
+      uint64_t wa = ta, wb = tb;
+      if (!step_window(c->st[e], c->en[e], TGXO_OVERLAPS, out_dir, &wa, &wb)) continue;
+      const uint32_t next = c->nbr[e];
+      FOR_WINDOW(c, next, wa, wb, f) {
+        const int ok = out_dir ? holds(c->st[e], c->en[e], c->st[f], c->en[f], TGXO_OVERLAPS)
+                               : holds(c->st[f], c->en[f], c->st[e], c->en[e], TGXO_OVERLAPS);
+        if (ok && !level[f]) {
+          level[f] = round;
+          epush(&nx, f);
+        }
+      }
+    }
+    esort(&nx);
+    elist t = fr;
+    fr = nx;
+    nx = t;
+  }
+  free(fr.v);
+  free(nx.v);
+  return level;
+}
+
+/* earliest_arrival_overlaps / latest_departure_overlaps /
+ * temporal_bfs_overlaps, path_algorithms.cpp:89-134. */
+static void overlaps_reach(const tgxo_graph* g, int kind, uint32_t v, uint64_t ta, uint64_t tb,
+                           int64_t* L) {
+  const int out_dir = kind != TGXO_LD;
+  const ocsr* c = out_dir ? &g->out : &g->in;
+  uint32_t* level = edge_reachability(g, ta, tb, out_dir, v);
+  for (uint32_t u = 0; u < g->n; ++u) L[u] = kind == TGXO_LD ? NEGINF64 : INF64;
+  for (uint64_t e = 0; e < g->m; ++e) {
+    if (!level[e]) continue;
+    const uint32_t u = c->nbr[e];
+    int64_t x;
+    if (kind == TGXO_EA) {
+      x = (int64_t)c->en[e];
+      if (x < L[u]) L[u] = x;
+    } else if (kind == TGXO_LD) {
+      x = (int64_t)c->st[e];
+      if (x > L[u]) L[u] = x;
+    } else {
+      x = (int64_t)level[e];
+      if (x < L[u]) L[u] = x;
+    }
+  }
+  L[v] = kind == TGXO_EA ? (int64_t)ta : kind == TGXO_LD ? (int64_t)tb : 0;
+  free(level);
+}
+
+/* fastest_overlaps, path_algorithms.cpp:136-191: per out-edge the latest
+ * first-edge start over valid paths ending with it (write_max + round stamp,
+ * base read at the round's start); r[v] = min(end - depart). */
+static void fastest_overlaps(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb,
+                             int64_t* R) {
+  const ocsr* c = &g->out;
+  const uint64_t m = g->m;
+  int64_t* dep = malloc((m ? m : 1) * sizeof(int64_t));
+  uint32_t* stamp = calloc(m ? m : 1, sizeof(uint32_t));
+  for (uint64_t e = 0; e < m; ++e) dep[e] = NEGINF64;
+  elist fr = {0}, nx = {0};
+  int64_t* base = NULL;
+  uint64_t bcap = 0;
+  FOR_WINDOW(c, source, ta, tb, f) {
+    if ((int64_t)c->st[f] > dep[f]) {
+      dep[f] = (int64_t)c->st[f];
+      epush(&fr, f);
+    }
+  }
+  esort(&fr);
+  uint32_t round = 0;
+  while (fr.n) {
+    ++round;
+    if (fr.n > bcap) {
+      bcap = fr.n;
+      base = realloc(base, bcap * sizeof(int64_t));
+    }
+    for (uint64_t i = 0; i < fr.n; ++i) base[i] = dep[fr.v[i]];
+    nx.n = 0;
+    for (uint64_t i = 0; i < fr.n; ++i) {
+      const uint64_t e = fr.v[i];
+      uint64_t wa = ta, wb = tb;
+      if (!step_window(c->st[e], c->en[e], TGXO_OVERLAPS, 1, &wa, &wb)) continue;
+      FOR_WINDOW(c, c->nbr[e], wa, wb, f) {
+        if (!holds(c->st[e], c->en[e], c->st[f], c->en[f], TGXO_OVERLAPS)) continue;
+        if (base[i] > dep[f]) { /* write_max */
+          dep[f] = base[i];
+          if (stamp[f] != round) { /* claim_stamp */
+            stamp[f] = round;
+            epush(&nx, f);
+          }
+        }
+      }
+    }
+    esort(&nx);
+    elist t = fr;
+    fr = nx;
+    nx = t;
+  }
+  for (uint32_t u = 0; u < g->n; ++u) R[u] = INF64;
+  for (uint64_t e = 0; e < m; ++e) {
+    if (dep[e] == NEGINF64) continue;
+    const int64_t d = (int64_t)c->en[e] - dep[e];
+    if (d < R[c->nbr[e]]) R[c->nbr[e]] = d;
+  }
+  R[source] = 0;
+  free(dep);
+  free(stamp);
+  free(base);
+  free(fr.v);
+  free(nx.v);
+}
+
+/* shortest_duration (unweighted), path_algorithms.cpp:205-258,410-434:
+ * out-edge states value[f] = min over valid paths ending with f of the sum of
+ * (end - start); frontier by write_min + round stamp with base read at the
+ * round's start; r[v] = min over reached in-edges, r[source] = 0. */
+static void shortest_duration(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb,
+                              int ord, int64_t* R) {
+  const ocsr* c = &g->out;
+  const uint64_t m = g->m;
+  int64_t* val = malloc((m ? m : 1) * sizeof(int64_t));
+  uint32_t* stamp = calloc(m ? m : 1, sizeof(uint32_t));
+  uint8_t* touched = calloc(m ? m : 1, 1);
+  for (uint64_t e = 0; e < m; ++e) val[e] = INF64;
+  elist fr = {0}, nx = {0};
+  int64_t* base = NULL;
+  uint64_t bcap = 0;
+  uint32_t round = 1;
+  FOR_WINDOW(c, source, ta, tb, f) {
+    const int64_t d = (int64_t)(c->en[f] - c->st[f]);
+    if (d < val[f]) {
+      val[f] = d;
+      touched[f] = 1;
+      if (stamp[f] != round) {
+        stamp[f] = round;
+        epush(&fr, f);
+      }
+    }
+  }
+  esort(&fr);
+  while (fr.n) {
+    ++round;
+    if (fr.n > bcap) {
+      bcap = fr.n;
+      base = realloc(base, bcap * sizeof(int64_t));
+    }
+    for (uint64_t i = 0; i < fr.n; ++i) base[i] = val[fr.v[i]];
+    nx.n = 0;
+    for (uint64_t i = 0; i < fr.n; ++i) {
+      const uint64_t e = fr.v[i];
+      uint64_t wa = ta, wb = tb;
+      if (!step_window(c->st[e], c->en[e], ord, 1, &wa, &wb)) continue;
+      FOR_WINDOW(c, c->nbr[e], wa, wb, f) {
+        if (!holds(c->st[e], c->en[e], c->st[f], c->en[f], ord)) continue;
+        const int64_t cand = base[i] + (int64_t)(c->en[f] - c->st[f]);
+        if (cand < val[f]) {
+          val[f] = cand;
+          touched[f] = 1;
+          if (stamp[f] != round) {
+            stamp[f] = round;
+            epush(&nx, f);
+          }
+        }
+      }
+    }
+    esort(&nx);
+    elist t = fr;
+    fr = nx;
+    nx = t;
+  }
+  for (uint32_t u = 0; u < g->n; ++u) R[u] = INF64;
+  for (uint64_t e = 0; e < m; ++e)
+    if (touched[e] && val[e] < R[c->nbr[e]]) R[c->nbr[e]] = val[e];
+  R[source] = 0;
+  free(val);
+  free(stamp);
+  free(touched);
+  free(base);
+  free(fr.v);
+  free(nx.v);
+}
+
+/* temporal_bfs, path_algorithms.cpp:359-408: round-synchronous earliest
+ * arrival (snapshot per round) recording the first round a vertex's arrival
+ * improves; r[source] = 0. */
+static void temporal_bfs(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb,
+                         int strict, int64_t* H) {
+  const uint32_t n = g->n;
+  const ocsr* c = &g->out;
+  int64_t* A = malloc((size_t)(n ? n : 1) * sizeof(int64_t));
+  int64_t* snap = malloc((size_t)(n ? n : 1) * sizeof(int64_t));
+  uint32_t* stamp = calloc(n ? n : 1, sizeof(uint32_t));
+  for (uint32_t v = 0; v < n; ++v) {
+    A[v] = INF64;
+    H[v] = INF64;
+  }
+  H[source] = 0;
+  uint32_t round = 0;
+  vlist fr = {0}, nx = {0};
+  vpush(&fr, source);
+  while (fr.n) {
+    ++round;
+    memcpy(snap, A, (size_t)n * sizeof(int64_t));
+    nx.n = 0;
+    for (uint64_t i = 0; i < fr.n; ++i) {
+      const uint32_t s = fr.v[i];
+      const int64_t ps = snap[s];
+      uint64_t lo_t = ta;
+      if (s != source) {
+        if (ps == INF64) continue;
+        lo_t = strict ? (uint64_t)ps + 1 : (uint64_t)ps;
+      }
+      if (lo_t < ta) lo_t = ta;
+      if (lo_t > tb) continue;
+      FOR_WINDOW(c, s, lo_t, tb, e) {
+        const uint64_t ts = c->st[e], te = c->en[e];
+        if (s != source && (strict ? (int64_t)ts <= ps : (int64_t)ts < ps)) continue;
+        const uint32_t d = c->nbr[e];
+        if ((int64_t)te < A[d]) {
+          A[d] = (int64_t)te;
+          if (H[d] == INF64) H[d] = round;
+          if (stamp[d] != round) {
+            stamp[d] = round;
+            vpush(&nx, d);
+          }
+        }
+      }
+    }
+    sort_unique(&nx);
+    vlist t = fr;
+    fr = nx;
+    nx = t;
+  }
+  H[source] = 0;
+  free(A);
+  free(snap);
+  free(stamp);
+  free(fr.v);
+  free(nx.v);
+}
+
 int tgxo_query(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint64_t tb,
                int ordering, int64_t* out) {
   if (vertex >= g->n) return fail(TGXO_OUT_OF_RANGE, "vertex outside vertex range");
   int rc = check_window(&ta, &tb);
   if (rc) return rc;
-  if (ordering == TGXO_OVERLAPS)
-    return fail(TGXO_UNSUPPORTED, "the Overlaps ordering is outside the restated path");
   const int strict = ordering == TGXO_STRICTLY_SUCCEEDS;
+  if (ordering == TGXO_OVERLAPS) { /* path_algorithms.cpp:267,315,366,443 */
+    switch (kind) {
+      case TGXO_EA:
+      case TGXO_LD:
+      case TGXO_BFS: overlaps_reach(g, kind, vertex, ta, tb, out); return TGXO_OK;
+      case TGXO_FASTEST: fastest_overlaps(g, vertex, ta, tb, out); return TGXO_OK;
+      case TGXO_SD: shortest_duration(g, vertex, ta, tb, ordering, out); return TGXO_OK;
+      default: return fail(TGXO_INVALID_ARGUMENT, "unknown query kind");
+    }
+  }
   switch (kind) {
     case TGXO_EA: earliest_arrival(g, vertex, ta, tb, strict, out); break;
     case TGXO_LD: latest_departure(g, vertex, ta, tb, strict, out); break;
     case TGXO_FASTEST: fastest(g, vertex, ta, tb, strict, out); break;
+    case TGXO_SD: shortest_duration(g, vertex, ta, tb, ordering, out); break;
+    case TGXO_BFS: temporal_bfs(g, vertex, ta, tb, strict, out); break;
     default: return fail(TGXO_INVALID_ARGUMENT, "unknown query kind");
   }
   return TGXO_OK;

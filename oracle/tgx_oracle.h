@@ -1,7 +1,8 @@
 /* TEST INFRASTRUCTURE ONLY — the checker, never the product.
  *
  * Plain-C restatement of the reference's temporal path algorithms
- * (earliest arrival, latest departure, fastest) over a host T-CSR, with the
+ * (earliest arrival, latest departure, fastest, shortest duration, temporal
+ * BFS; every ordering including Overlaps) over a host T-CSR, with the
  * reference's u64 timestamps, int64 labels and sentinels. Only tests/,
  * __graft_entry__.smoke() and bench.py's cpu_baseline leg may load it.
  * Pinned against the compiled reference (oracle/_ref/libtgxref.so) and the
@@ -17,7 +18,8 @@ extern "C" {
 #endif
 
 enum { TGXO_OK = 0, TGXO_OUT_OF_RANGE = 1, TGXO_INVALID_ARGUMENT = 2, TGXO_UNSUPPORTED = 3 };
-enum { TGXO_EA = 0, TGXO_LD = 1, TGXO_FASTEST = 2 };
+/* kinds: the reference's five path metrics (algorithms.hpp:46-66) */
+enum { TGXO_EA = 0, TGXO_LD = 1, TGXO_FASTEST = 2, TGXO_SD = 3, TGXO_BFS = 4 };
 /* Ordering values follow tgx::Ordering (types.hpp:64-68). */
 enum { TGXO_SUCCEEDS = 0, TGXO_STRICTLY_SUCCEEDS = 1, TGXO_OVERLAPS = 2 };
 

@@ -6,6 +6,8 @@ import numpy as np
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 KINDS = ["earliest_arrival", "latest_departure", "fastest"]
+# the reference's five path metrics (algorithms.hpp:46-66), fixture order
+KINDS5 = KINDS + ["shortest_duration", "temporal_bfs"]
 INF = (1 << 63) - 1
 NEG = -(1 << 63)
 
@@ -18,6 +20,23 @@ def small_random():
         a, b = eoff[it], eoff[it + 1]
         E = (z["src"][a:b], z["dst"][a:b], z["start"][a:b], z["end"][a:b])
         yield E, int(n), int(v), int(ta), int(tb), KINDS[ki], int(ordv), labels[lo:lo + n]
+
+
+def small_random_ext():
+    """All five metrics x all three orderings (small_random_ext.npz)."""
+    z = np.load(GOLDEN / "small_random_ext.npz")
+    eoff, meta, labels = z["eoff"], z["meta"], z["labels"]
+    for it, n, v, ta, tb, ki, ordv, lo in meta:
+        a, b = eoff[it], eoff[it + 1]
+        E = (z["src"][a:b], z["dst"][a:b], z["start"][a:b], z["end"][a:b])
+        yield E, int(n), int(v), int(ta), int(tb), KINDS5[ki], int(ordv), labels[lo:lo + n]
+
+
+def rmat12_ext():
+    """(edge_digest, [(kind, v, ta, tb, ordering)], labels) on the rmat12 graph."""
+    z = np.load(GOLDEN / "rmat12_ext.npz")
+    qs = [(KINDS5[k], int(v), int(ta), int(tb), int(o)) for k, v, ta, tb, o in z["meta"]]
+    return int(z["edge_digest"][0]), qs, z["labels"]
 
 
 def scaled(name):
@@ -64,6 +83,27 @@ HAND = [  # name, n, edges, kind, vertex, ta, tb, ordering
      (1 << 64) - 1, 0),
     ("fastest_no_edges", 3, [], "fastest", 2, 0, (1 << 64) - 1, 1),
 ]
+
+
+# test_algorithms.cpp:124-168 and test_engine.cpp:223-243 (as a path query)
+HAND_EXT = [  # name, n, edges, kind, vertex, ta, tb, ordering
+    ("sd_single_edge", 2, [(0, 1, 3, 5)], "shortest_duration", 0, 0, (1 << 64) - 1, 1),
+    ("sd_two_hop_sum_wins", 3, [(0, 1, 0, 4), (0, 2, 0, 1), (2, 1, 5, 7)], "shortest_duration",
+     0, 0, (1 << 64) - 1, 1),
+    ("bfs_chain", 4, [(0, 1, 1, 2), (1, 2, 3, 4), (2, 3, 5, 6)], "temporal_bfs", 0, 0,
+     (1 << 64) - 1, 1),
+    ("bfs_more_hops_unlock", 4, [(0, 1, 9, 10), (0, 2, 0, 1), (2, 1, 2, 3), (1, 3, 5, 6)],
+     "temporal_bfs", 0, 0, (1 << 64) - 1, 1),
+    ("overlaps_gate", 6, [(0, 1, 2, 6), (1, 2, 4, 9), (1, 3, 7, 9), (1, 4, 2, 8), (1, 5, 3, 5)],
+     "earliest_arrival", 0, 0, (1 << 64) - 1, 2),
+]
+HAND_EXT_EXPECT = {
+    "sd_single_edge": {1: 2},
+    "sd_two_hop_sum_wins": {1: 3},
+    "bfs_chain": {0: 0, 1: 1, 2: 2, 3: 3},
+    "bfs_more_hops_unlock": {1: 1, 3: 3},
+    "overlaps_gate": {1: 6, 2: 9, 3: INF, 4: INF, 5: INF},
+}
 
 
 def hand_edges(edges):

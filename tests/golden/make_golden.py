@@ -13,6 +13,14 @@ inputs + outputs as compressed npz files next to this script:
   rmat12.npz        RMAT scale 12 (config-2 distributions) with 12 queries,
                     full int64 label vectors + FNV-1a digests
   uniform14.npz     uniform n=2^14, m=2^18 (config-1 distributions), 6 queries
+  small_random_ext.npz  200 more random small instances x all five path
+                    metrics (+ shortest duration, temporal BFS) x all three
+                    orderings (+ Overlaps), checked against enumerate_paths
+  hand_ext.npz      shortest-duration / temporal-BFS hand cases
+                    (test_algorithms.cpp:124-168) and the Overlaps gate of
+                    test_engine.cpp:223-243 as a path query
+  rmat12_ext.npz    the rmat12 graph, 4 sources x 2 windows x 5 metrics x 3
+                    orderings
 
 Only this script touches the reference; tests read the npz files. Re-run
 with:  python tests/golden/make_golden.py
@@ -28,6 +36,7 @@ from oracle.pyoracle import Reference  # noqa: E402
 
 HERE = Path(__file__).resolve().parent
 KINDS = ["earliest_arrival", "latest_departure", "fastest"]
+KINDS5 = KINDS + ["shortest_duration", "temporal_bfs"]
 
 
 def small_random():
@@ -130,6 +139,94 @@ def edge_digest(E):
     return T.digest_of(np.frombuffer(buf, np.int64))
 
 
+def small_random_ext():
+    rng = np.random.default_rng(20240106)
+    eoff, loff = [0], [0]
+    src, dst, st, en, labels, meta = [], [], [], [], [], []
+    for it in range(200):
+        n = int(rng.integers(1, 10))
+        m = int(rng.integers(0, 29))
+        s = rng.integers(0, n, m)
+        d = rng.integers(0, n, m)
+        a = rng.integers(0, 61, m)
+        b = a + rng.integers(0, 9, m)
+        E = (s, d, a, b)
+        ref = Reference(E, n)
+        ta, tb = sorted(int(x) for x in rng.integers(0, 76, 2))
+        v = int(rng.integers(0, n))
+        for ki, kind in enumerate(KINDS5):
+            for ordv in (0, 1, 2):
+                out = ref.query(kind, v, ta, tb, ordv)
+                brute = Reference.enumerate(E, n, kind, v, ta, tb, ordv)
+                assert np.array_equal(out, brute), (it, kind, ordv)
+                meta.append((it, n, v, ta, tb, ki, ordv, loff[-1]))
+                labels.append(out)
+                loff.append(loff[-1] + n)
+        ref.close()
+        src.append(s); dst.append(d); st.append(a); en.append(b)
+        eoff.append(eoff[-1] + m)
+    np.savez_compressed(
+        HERE / "small_random_ext.npz",
+        eoff=np.array(eoff, np.int64), src=np.concatenate(src).astype(np.uint32),
+        dst=np.concatenate(dst).astype(np.uint32), start=np.concatenate(st).astype(np.uint64),
+        end=np.concatenate(en).astype(np.uint64), meta=np.array(meta, np.int64),
+        labels=np.concatenate(labels).astype(np.int64))
+
+
+# test_algorithms.cpp:124-168 (unweighted) and test_engine.cpp:223-243 as a
+# path query: 0 reaches 1 over [2, 6]; only 1's out-edge [4, 9] overlaps it.
+HAND_EXT = [
+    ("sd_single_edge", 2, [(0, 1, 3, 5)], "shortest_duration", 0, 0, (1 << 64) - 1, 1),
+    ("sd_two_hop_sum_wins", 3, [(0, 1, 0, 4), (0, 2, 0, 1), (2, 1, 5, 7)], "shortest_duration",
+     0, 0, (1 << 64) - 1, 1),
+    ("bfs_chain", 4, [(0, 1, 1, 2), (1, 2, 3, 4), (2, 3, 5, 6)], "temporal_bfs", 0, 0,
+     (1 << 64) - 1, 1),
+    ("bfs_more_hops_unlock", 4, [(0, 1, 9, 10), (0, 2, 0, 1), (2, 1, 2, 3), (1, 3, 5, 6)],
+     "temporal_bfs", 0, 0, (1 << 64) - 1, 1),
+    ("overlaps_gate", 6, [(0, 1, 2, 6), (1, 2, 4, 9), (1, 3, 7, 9), (1, 4, 2, 8), (1, 5, 3, 5)],
+     "earliest_arrival", 0, 0, (1 << 64) - 1, 2),
+]
+
+
+def hand_ext():
+    out = {}
+    for name, n, edges, kind, v, ta, tb, ordv in HAND_EXT:
+        e = np.array(edges, np.int64).reshape(-1, 4)
+        E = (e[:, 0], e[:, 1], e[:, 2], e[:, 3])
+        ref = Reference(E, n)
+        out[name] = ref.query(kind, v, ta, tb, ordv)
+        ref.close()
+    np.savez_compressed(HERE / "hand_ext.npz", **out)
+
+
+def rmat12_ext(gen):
+    import paper_2401_02563_b200 as T
+    E = T.generate_edges(gen)
+    n = gen.n_vertices
+    deg = np.bincount(E[0], minlength=n)
+    rng = np.random.default_rng(13)
+    srcs = [int(np.argmax(deg))] + [int(x) for x in rng.choice(np.flatnonzero(deg), 3)]
+    ref = Reference(E, n)
+    meta, labels = [], []
+    for s in srcs:
+        for w in ((0, 999_999), (200_000, 800_000)):
+            for ki, kind in enumerate(KINDS5):
+                for ordv in (0, 1, 2):
+                    meta.append((ki, s, w[0], w[1], ordv))
+                    labels.append(ref.query(kind, s, w[0], w[1], ordv))
+    ref.close()
+    np.savez_compressed(HERE / "rmat12_ext.npz", edge_digest=np.array([edge_digest(E)], np.uint64),
+                        meta=np.array(meta, np.int64), labels=np.array(labels, np.int64))
+
+
+def extended():
+    import paper_2401_02563_b200 as T
+    small_random_ext()
+    hand_ext()
+    rmat12_ext(T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 7,
+                                cube_root_starts=True))
+
+
 def main():
     import paper_2401_02563_b200 as T
     small_random()
@@ -148,6 +245,7 @@ def main():
     g2 = T.GenConfig.uniform(1 << 14, 1 << 18, 1_000_000, 0.01, 3)
     qs2 = [(k, 0, 0, 999_999) for k in KINDS] + [(k, 77, 100_000, 600_000) for k in KINDS]
     scaled("uniform14", g2, qs2)
+    extended()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
