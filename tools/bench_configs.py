@@ -1,0 +1,100 @@
+"""Per-config measurement: every BASELINE workload's
+queries, device-timed on one B200 (graph resident, outputs in HBM), next to
+the reference library (oracle/_ref, all host cores) on the same edge list.
+
+usage: python tools/bench_configs.py [--configs c1,c2,c3,c4,c5] [--steps 20]
+       [--ref-steps 3] [--ref-timeout-s 120]
+prints one JSON line per (config, query group)."""
+import argparse, json, os, sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import paper_2401_02563_b200 as T
+from paper_2401_02563_b200.configs import workload
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--warmup", type=int, default=3)
+ap.add_argument("--ref-steps", type=int, default=3)
+ap.add_argument("--no-ref", action="store_true")
+args = ap.parse_args()
+
+
+def ref_time(wl, edges, n, groups):
+    """Median seconds per reference call for each (kind, vertex, window)."""
+    from oracle.pyoracle import Reference
+    if not Reference.available():
+        return None, None
+    Reference.set_workers(os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    ref = Reference(edges, n, True, wl.index_cutoff)
+    build = time.perf_counter() - t0
+    out = []
+    for kind, v, w, steps in groups:
+        ts = []
+        for _ in range(steps):
+            t = time.perf_counter()
+            ref.query(kind, v, w.t_a, w.t_b)
+            ts.append(time.perf_counter() - t)
+        out.append(float(np.median(ts)))
+    ref.close()
+    return out, build
+
+
+for name in args.configs.split(","):
+    wl = workload(name)
+    t0 = time.perf_counter()
+    g = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
+    build_s = time.perf_counter() - t0
+    n = g.vertex_count()
+    qs = wl.queries(g.degrees(T.Direction.OUT), g.degrees(T.Direction.IN), n)
+    kinds = sorted({q.kind for q in qs})
+    edges = None if args.no_ref else T.generate_edges(wl.gen)
+    for kind in kinds:
+        sub = [q for q in qs if q.kind == kind]
+        verts = [q.vertex for q in sub]
+        wins = [q.window for q in sub]
+        # work per query from the final labels
+        e_adm = v_reached = 0
+        per_q = []
+        for q in sub:
+            T.query_batch(g, kind, [q.vertex], [q.window], width=4)
+            e, r = T.last_work(g, 0)
+            per_q.append((e, r))
+            e_adm += e
+            v_reached += r
+        # one query at a time, and (EA / LD) the whole group as one batch
+        single_ms = 0.0
+        for q in sub:
+            tot, ker = T.time_queries(g, kind, [q.vertex], [q.window], warmup=args.warmup,
+                                      steps=args.steps)
+            single_ms += tot / args.steps
+        batch_ms = None
+        if kind != "fastest" and len(sub) > 1:
+            tot, ker = T.time_queries(g, kind, verts, wins, warmup=args.warmup, steps=args.steps)
+            batch_ms = tot / args.steps
+        line = {"config": name, "workload": wl.describe, "kind": kind, "queries": len(sub),
+                "n": n, "m": g.edge_count(), "device_build_s": round(build_s, 3),
+                "e_adm_total": e_adm, "v_reached_total": v_reached,
+                "gpu_ms_sequential": single_ms,
+                "gpu_teps_sequential": e_adm / (single_ms * 1e-3) if single_ms else None,
+                "gpu_us_per_query": single_ms * 1e3 / len(sub)}
+        if batch_ms is not None:
+            line.update({"gpu_ms_batched": batch_ms,
+                         "gpu_teps_batched": e_adm / (batch_ms * 1e-3),
+                         "gpu_queries_per_s_batched": len(sub) / (batch_ms * 1e-3)})
+        if edges is not None:
+            steps = 1 if kind == "fastest" else args.ref_steps
+            # bounded sample: at most 8 queries of a group on the CPU
+            samp = sub[:8]
+            times, rbuild = ref_time(wl, edges, n, [(kind, q.vertex, q.window, steps) for q in samp])
+            if times is not None:
+                e_s = sum(per_q[i][0] for i in range(len(samp)))
+                line["ref"] = {"kind": "reference", "cores": os.cpu_count(), "queries": len(samp),
+                               "s_per_query": float(np.mean(times)),
+                               "teps": e_s / sum(times) if sum(times) else None,
+                               "build_s": round(rbuild, 2)}
+                line["speedup_sequential"] = (sum(times) / len(samp)) / (single_ms * 1e-3 / len(sub))
+        print(json.dumps(line), flush=True)
+    g.close()
