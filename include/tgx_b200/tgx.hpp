@@ -4,12 +4,14 @@
 // reference signatures and semantics (/root/reference/proj/include/tgx/):
 //   TemporalGraph::build(edges, n_v, directed, config)   engine.hpp:32-33
 //   earliest_arrival / latest_departure / fastest_path    algorithms.hpp:46-58
+//   shortest_duration / temporal_bfs                      algorithms.hpp:62-67
 //   PathResult (int64 values, INT64_MAX / INT64_MIN)       algorithms.hpp:16-21
 //   digest_of                                             digest.hpp:42-52
 // and re-throws the reference's exception types: std::out_of_range for a bad
-// vertex or edge, std::invalid_argument for a bad window. Ordering::Overlaps
-// and times outside [0, 2^31 - 2] raise std::domain_error (the device path
-// does not cover them; there is no CPU fallback). force_access is accepted
+// vertex or edge, std::invalid_argument for a bad window. Every ordering,
+// Overlaps included, runs on the device. Times outside [0, 2^31 - 2] and the
+// weighted shortest duration (edge weights are not stored on the device)
+// raise std::domain_error; there is no CPU fallback. force_access is accepted
 // and ignored: results are access-invariant (test_algorithms.cpp:196-217).
 //
 // A user of the reference switches by replacing `#include "tgx/..."` and
@@ -67,6 +69,7 @@ struct AlgoOptions {
   std::optional<Ordering> ordering;
   std::optional<ForceAccess> force_access;
   EdgeMapStats* stats = nullptr;
+  bool weighted = false;  // shortest_duration only
 };
 
 struct PathResult {
@@ -164,6 +167,18 @@ inline PathResult latest_departure(const TemporalGraph& g, VertexId target, cons
 inline PathResult fastest_path(const TemporalGraph& g, VertexId source, const QueryWindow& w,
                                const AlgoOptions& opts = {}) {
   return detail::run(TGXD_FASTEST, g, source, w, opts);
+}
+
+inline PathResult shortest_duration(const TemporalGraph& g, VertexId source, const QueryWindow& w,
+                                    const AlgoOptions& opts = {}) {
+  if (opts.weighted)
+    throw std::domain_error("weighted shortest duration: edge weights are not on the device");
+  return detail::run(TGXD_SHORTEST_DURATION, g, source, w, opts);
+}
+
+inline PathResult temporal_bfs(const TemporalGraph& g, VertexId source, const QueryWindow& w,
+                               const AlgoOptions& opts = {}) {
+  return detail::run(TGXD_TEMPORAL_BFS, g, source, w, opts);
 }
 
 template <class T>

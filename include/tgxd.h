@@ -12,7 +12,8 @@
  *   TGXD_ERR_TIME_RANGE    edge time outside the device's int32 time domain
  *                          [0, 2^31 - 2] (no reference equivalent: the
  *                          reference keeps u64 times)
- *   TGXD_ERR_UNSUPPORTED   Ordering::Overlaps (no CPU fallback by design)
+ *   TGXD_ERR_UNSUPPORTED   a request outside the device path (e.g. the unit of
+ *                          work of an edge-state query); no CPU fallback
  *   TGXD_ERR_CUDA          CUDA runtime failure, or no usable GPU
  *   TGXD_ERR_ARGUMENT      malformed call (null pointer, bad enum, ...)
  *
@@ -44,10 +45,18 @@ enum tgxd_status {
   TGXD_ERR_EDGE = 7
 };
 
-/* Path metrics on the hot path: algorithms.hpp:46-58. */
-enum tgxd_kind { TGXD_EARLIEST_ARRIVAL = 0, TGXD_LATEST_DEPARTURE = 1, TGXD_FASTEST = 2 };
+/* The reference's path metrics, algorithms.hpp:46-66 (EA / LD / fastest on
+ * the hot path; shortest duration (unweighted) and temporal BFS next to it). */
+enum tgxd_kind {
+  TGXD_EARLIEST_ARRIVAL = 0,
+  TGXD_LATEST_DEPARTURE = 1,
+  TGXD_FASTEST = 2,
+  TGXD_SHORTEST_DURATION = 3,
+  TGXD_TEMPORAL_BFS = 4
+};
 
-/* tgx::Ordering, types.hpp:64-68 (same numeric order). */
+/* tgx::Ordering, types.hpp:64-68 (same numeric order). Overlaps runs every
+ * metric on the edge-state engine (path_algorithms.cpp:40-191). */
 enum tgxd_ordering { TGXD_SUCCEEDS = 0, TGXD_STRICTLY_SUCCEEDS = 1, TGXD_OVERLAPS = 2 };
 
 /* Frontier representation policy (temporal_edge_map's representation switch,
@@ -137,6 +146,14 @@ int tgxd_latest_departure(tgxd_graph* g, uint32_t target, uint64_t t_a, uint64_t
                           int ordering, int64_t* out, tgxd_stats* stats);
 int tgxd_fastest(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int ordering,
                  int64_t* out, tgxd_stats* stats);
+/* shortest_duration (unweighted: sum of end - start; algorithms.hpp:62-63,
+ * path_algorithms.cpp:410-434) and temporal_bfs (hops; algorithms.hpp:66-67,
+ * path_algorithms.cpp:359-408). Same conventions: INT64_MAX unreached,
+ * out[source] = 0. */
+int tgxd_shortest_duration(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b,
+                           int ordering, int64_t* out, tgxd_stats* stats);
+int tgxd_temporal_bfs(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int ordering,
+                      int64_t* out, tgxd_stats* stats);
 
 /* General form: k queries of one kind run as one batched traversal
  * (configs 3 and 5). out holds k x n labels of `width` bytes (4 or 8),

@@ -72,7 +72,7 @@ class InvalidArgument(ValueError):
 
 
 class Unsupported(NotImplementedError):
-    """Ordering::Overlaps: not on the device path."""
+    """A request outside the device path (no CPU fallback)."""
 
 
 class TimeRangeError(ValueError):
@@ -129,6 +129,7 @@ class AlgoOptions:                       # algorithms.hpp:31-40
     force_access: Optional[ForceAccess] = None
     stats: Optional[EdgeMapStats] = None
     mode: Mode = Mode.AUTO
+    weighted: bool = False               # shortest_duration only (not on the device)
 
 
 @dataclass
@@ -217,6 +218,10 @@ def load_library() -> ctypes.CDLL:
                                    ctypes.c_int, _i64p, _P(_Stats)], ctypes.c_int),
         "tgxd_fastest": ([vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                           _i64p, _P(_Stats)], ctypes.c_int),
+        "tgxd_shortest_duration": ([vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                    ctypes.c_int, _i64p, _P(_Stats)], ctypes.c_int),
+        "tgxd_temporal_bfs": ([vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                               ctypes.c_int, _i64p, _P(_Stats)], ctypes.c_int),
         "tgxd_query": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p, ctypes.c_int,
                         ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, _P(_Stats)], ctypes.c_int),
         "tgxd_last_work": ([vp, ctypes.c_uint32, _u64p, _u64p], ctypes.c_int),
@@ -408,7 +413,23 @@ def fastest_path(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
     return _run(2, g, source, w, opts)
 
 
-KINDS = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2}
+def shortest_duration(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
+                      opts: Optional[AlgoOptions] = None) -> PathResult:
+    """algorithms.hpp:62-63 / path_algorithms.cpp:410-434 (unweighted: the sum
+    of end - start over the path's edges; edge-state engine)."""
+    if opts is not None and opts.weighted:
+        raise Unsupported("weighted shortest duration: edge weights are not stored on the device")
+    return _run(3, g, source, w, opts)
+
+
+def temporal_bfs(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
+                 opts: Optional[AlgoOptions] = None) -> PathResult:
+    """algorithms.hpp:66-67 / path_algorithms.cpp:359-408 (hop counts)."""
+    return _run(4, g, source, w, opts)
+
+
+KINDS = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2, "shortest_duration": 3,
+         "temporal_bfs": 4}
 
 
 def query_batch(g: TemporalGraph, kind: str, vertices: Sequence[int],

@@ -19,6 +19,7 @@
 #include "tgxd_internal.cuh"
 #include "traverse.cuh"
 #include "async.cuh"
+#include "edges.cuh"
 
 namespace tgxd {
 
@@ -233,6 +234,9 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
   int per_sm_a = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, async_kernel, kThreads, 0);
   G->coop_blocks_async = std::max(1, per_sm_a) * G->sm_count;
+  int per_sm_e = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_e, edge_kernel, kThreads, 0);
+  G->coop_blocks_edge = std::max(1, per_sm_e) * G->sm_count;
   *out = G;
   return TGXD_OK;
 }
@@ -243,6 +247,8 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
 struct Prepared {
   int kind;
   int strict;
+  int ordering;
+  bool edge;  // edge-state engine (edges.cuh): Overlaps, or shortest duration
   uint32_t Q;
   std::vector<QueryParam> qp;
   std::vector<Seed> seeds;
@@ -255,7 +261,7 @@ struct Prepared {
 // checked_window (invalid_argument), then the ordering.
 static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, const uint64_t* ta,
                    const uint64_t* tb, int ordering, Prepared& P) {
-  if (kind < 0 || kind > 2) return fail(TGXD_ERR_ARGUMENT, "unknown query kind");
+  if (kind < 0 || kind > 4) return fail(TGXD_ERR_ARGUMENT, "unknown query kind");
   if (k == 0 || !verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "empty or null query batch");
   if ((uint64_t)k * G->n >= 0xffffffffULL)
     return fail(TGXD_ERR_ARGUMENT, "batch too large: k * n must stay below 2^32");
@@ -263,6 +269,9 @@ static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, c
   P.kind = kind;
   P.Q = k;
   P.strict = ordering == TGXD_STRICTLY_SUCCEEDS ? 1 : 0;
+  P.ordering = ordering;
+  P.edge = ordering == TGXD_OVERLAPS || kind == TGXD_SHORTEST_DURATION;
+  if (P.edge && k != 1) return fail(TGXD_ERR_ARGUMENT, "edge-state queries run one at a time");
   P.qp.resize(k);
   P.seeds.resize(k);
   for (uint32_t q = 0; q < k; ++q) {
@@ -275,8 +284,6 @@ static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, c
     if (ta[q] > kTimeLimit63)
       return fail(TGXD_ERR_WINDOW, "window start beyond the supported time range (2^63 - 1)");
   }
-  if (ordering == TGXD_OVERLAPS)
-    return fail(TGXD_ERR_UNSUPPORTED, "the Overlaps ordering is not on the device path");
   for (uint32_t q = 0; q < k; ++q) {
     const uint64_t tb63 = std::min<uint64_t>(tb[q], kTimeLimit63);
     const int64_t ta_c = (int64_t)std::min<uint64_t>(ta[q], (uint64_t)kTimeMax + 1);
@@ -292,10 +299,13 @@ static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, c
       p.vhi = (int32_t)(-ta_c);
       sd.value = (long long)tb63;
     } else {
-      p.root = kind == TGXD_FASTEST ? kNoRoot : verts[q];
+      // fastest sweeps have no source exemption (path_algorithms.cpp:497-500);
+      // the edge engine seeds from the root's window edges
+      p.root = kind == TGXD_FASTEST && !P.edge ? kNoRoot : verts[q];
       p.klo = (int32_t)ta_c;  // == kInf when t_a lies beyond every edge time
       p.vhi = (int32_t)tb_c;
-      sd.value = kind == TGXD_FASTEST ? 0 : (long long)ta[q];
+      // r[source]: t_a (EA), 0 (fastest :526, shortest duration :432, BFS :406)
+      sd.value = kind == TGXD_EARLIEST_ARRIVAL ? (long long)ta[q] : 0;
     }
   }
   return TGXD_OK;
@@ -344,7 +354,7 @@ static int fastest_candidates(tgxd_graph* G, Prepared& P) {
   return TGXD_OK;
 }
 
-static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool fastest) {
+static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool need_r) {
   Workspace& w = G->ws;
   const uint64_t slots = (uint64_t)Q * G->n;
   // chunks per round <= frontier items + edges / kChunk (per query slot)
@@ -354,25 +364,30 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool fastest) {
             dalloc<uint32_t>(w.fb, slots) && dalloc<uint2>(w.chunks, max_chunks) &&
             dalloc<uint2>(w.smalls, slots) && dalloc<Control>(w.ctl, 1) &&
             dalloc<QueryParam>(w.params, Q) && dalloc<Seed>(w.seeds, Q);
-  if (ok && fastest) ok = dalloc<int32_t>(w.R, slots) != nullptr;
+  if (ok && need_r) ok = dalloc<int32_t>(w.R, slots) != nullptr;
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (traversal workspace)");
   w.slots = std::max(w.slots, slots);
   return TGXD_OK;
 }
 
-__global__ void convert_kernel(int kind, const int32_t* X, const int32_t* R, uint64_t total,
+// Device labels -> PathResult values. form 0: int32, INT32_MAX -> INT64_MAX
+// (EA, fastest durations, BFS hops); form 1: LD key space (negated,
+// INT32_MAX -> INT64_MIN); form 2: int64 as is (shortest duration). The
+// root's value is written exactly (Seed).
+enum ConvertForm : int { kFormMin = 0, kFormLd = 1, kFormI64 = 2 };
+
+__global__ void convert_kernel(int form, const int32_t* V, const long long* V64, uint64_t total,
                                uint32_t n, const Seed* seeds, void* out, int width) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
     const uint32_t q = (uint32_t)(i / n);
     const uint32_t v = (uint32_t)(i - (uint64_t)q * n);
     long long o;
-    if (kind == TGXD_FASTEST) {
-      const int32_t r = R[i];
-      o = r == kInf ? 0x7fffffffffffffffLL : (long long)r;
+    if (form == kFormI64) {
+      o = V64[i];
     } else {
-      const int32_t x = X[i];
-      if (kind == TGXD_LATEST_DEPARTURE) o = x == kInf ? (-0x7fffffffffffffffLL - 1) : -(long long)x;
+      const int32_t x = V[i];
+      if (form == kFormLd) o = x == kInf ? (-0x7fffffffffffffffLL - 1) : -(long long)x;
       else o = x == kInf ? 0x7fffffffffffffffLL : (long long)x;
     }
     if (v == seeds[q].root) o = seeds[q].value;
@@ -383,6 +398,24 @@ __global__ void convert_kernel(int kind, const int32_t* X, const int32_t* R, uin
       static_cast<int32_t*>(out)[i] = (int32_t)c;
     }
   }
+}
+
+// The form and source array of a query's result.
+static void convert_for(tgxd_graph* G, const Prepared& P, void* out_dev, int width) {
+  Workspace& w = G->ws;
+  const uint64_t slots = (uint64_t)P.Q * G->n;
+  int form = kFormMin;
+  const int32_t* V = w.X.as<int32_t>();
+  const long long* V64 = nullptr;
+  if (P.kind == TGXD_LATEST_DEPARTURE) form = kFormLd;
+  if (P.kind == TGXD_FASTEST) V = w.R.as<int32_t>();
+  if (P.kind == TGXD_TEMPORAL_BFS && !P.edge) V = w.R.as<int32_t>();
+  if (P.kind == TGXD_SHORTEST_DURATION) {
+    form = kFormI64;
+    V64 = w.ey.as<long long>();
+  }
+  convert_kernel<<<grid_for(slots, G->sm_count), 256, 0, G->stream>>>(
+      form, V, V64, slots, G->n, w.seeds.as<Seed>(), out_dev, width);
 }
 
 static uint64_t next_pow2(uint64_t x) {
@@ -465,13 +498,84 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   return TGXD_OK;
 }
 
+// Edge-state queries (edges.cuh): Overlaps for every metric, shortest
+// duration for every ordering. One query (Q == 1).
+static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int width,
+                        cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  Workspace& w = G->ws;
+  cudaStream_t s = G->stream;
+  const DevCsr& g = P.kind == TGXD_LATEST_DEPARTURE ? G->in : G->out;
+  const uint32_t m = g.m;
+  const int kind = P.kind == TGXD_SHORTEST_DURATION ? kEdgeShortest
+                   : P.kind == TGXD_FASTEST          ? kEdgeFastest
+                                                     : kEdgeReach;
+  bool ok = dalloc<uint32_t>(w.efa, (size_t)m + 1) && dalloc<uint32_t>(w.efb, (size_t)m + 1) &&
+            dalloc<EdgeCtl>(w.ectl, 1);
+  if (ok && kind == kEdgeReach) ok = dalloc<uint32_t>(w.ereached, (size_t)m / 32 + 1) != nullptr;
+  if (ok && kind != kEdgeReach) ok = dalloc<uint32_t>(w.estamp, (size_t)m + 1) != nullptr;
+  if (ok && kind == kEdgeFastest) ok = dalloc<int32_t>(w.edep, (size_t)m + 1) != nullptr;
+  if (ok && kind == kEdgeShortest)
+    ok = dalloc<long long>(w.eval, (size_t)m + 1) && dalloc<long long>(w.ey, G->n + 1);
+  if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (edge-state workspace)");
+  TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), sizeof(Seed), cudaMemcpyHostToDevice, s));
+  init_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
+      w.X.as<int32_t>(), w.EP.as<int2>(), kind == kEdgeFastest ? w.R.as<int32_t>() : nullptr,
+      G->n);
+  edge_init_kernel<<<grid_for(m, G->sm_count), 256, 0, s>>>(
+      kind, m, w.ereached.as<uint32_t>(), w.edep.as<int32_t>(), w.eval.as<long long>(),
+      w.estamp.as<uint32_t>(), kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n,
+      w.ectl.as<EdgeCtl>());
+  EdgeArgs a;
+  a.g = g;
+  a.qp = P.qp[0];
+  a.kind = kind;
+  a.ord = P.ordering;
+  a.bfs = P.kind == TGXD_TEMPORAL_BFS ? 1 : 0;
+  a.X = w.X.as<int32_t>();
+  a.reached = w.ereached.as<uint32_t>();
+  a.dep = w.edep.as<int32_t>();
+  a.val = w.eval.as<long long>();
+  a.stamp = w.estamp.as<uint32_t>();
+  a.fa = w.efa.as<uint32_t>();
+  a.fb = w.efb.as<uint32_t>();
+  a.ctl = w.ectl.as<EdgeCtl>();
+  a.n = G->n;
+  a.m = m;
+  a.round_limit = m + 16;  // every round queues an edge state that strictly improved
+  if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
+  void* args[] = {&a};
+  TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)edge_kernel, dim3(G->coop_blocks_edge),
+                                        dim3(kThreads), args, 0, s));
+  if (kind != kEdgeReach)
+    edge_fold_kernel<<<grid_for(m, G->sm_count), 256, 0, s>>>(
+        g, kind, a.dep, a.val, w.R.as<int32_t>(), w.ey.as<long long>());
+  if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
+  if (out_dev) convert_for(G, P, out_dev, width);
+  TGXD_CUDA(cudaGetLastError());
+  w.last_edge = true;
+  w.last_async = false;
+  w.last_handoff = false;
+  w.last_kind = P.kind;
+  w.last_q = P.Q;
+  w.last_strict = P.strict;
+  w.last_params = P.qp;
+  return TGXD_OK;
+}
+
 // Enqueues one traversal (init, seeds, the persistent kernel, widening into
 // out_dev). ev_k0/ev_k1 bracket the traversal kernel when non-null.
 static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int width,
                   cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  if (P.edge) return launch_edges(G, P, out_dev, width, ev_k0, ev_k1);
   Workspace& w = G->ws;
+  w.last_edge = false;
   cudaStream_t s = G->stream;
   const bool fast = P.kind == TGXD_FASTEST;
+  // temporal BFS is hop-minimal only with round-synchronous admission
+  // (path_algorithms.cpp:368-371): queue-driven or dense rounds, no pulls,
+  // no barrier-free engine
+  const bool bfs = P.kind == TGXD_TEMPORAL_BFS;
+  if (bfs && mode != TGXD_MODE_DENSE) mode = TGXD_MODE_SPARSE;
   const DevCsr& g = P.kind == TGXD_LATEST_DEPARTURE ? G->in : G->out;
   const uint64_t slots = (uint64_t)P.Q * G->n;
   TGXD_CUDA(cudaMemcpyAsync(w.params.p, P.qp.data(), P.Q * sizeof(QueryParam),
@@ -488,18 +592,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     TGXD_CUDA(cudaMemcpyAsync(w.cand_key.p, P.cand_key.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
   }
   init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
-      w.X.as<int32_t>(), w.EP.as<int2>(), fast ? w.R.as<int32_t>() : nullptr, slots);
+      w.X.as<int32_t>(), w.EP.as<int2>(), fast || bfs ? w.R.as<int32_t>() : nullptr, slots);
   seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
                                                  w.X.as<int32_t>(), w.fa.as<uint32_t>(),
                                                  w.ctl.as<Control>(), fast);
   if (mode == TGXD_MODE_ASYNC) {
     const int rc = launch_async(G, P, g, ncand, ev_k0, ev_k1);
     if (rc) return rc;
-    if (out_dev) {
-      convert_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
-          P.kind, w.X.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr, slots, G->n,
-          w.seeds.as<Seed>(), out_dev, width);
-    }
+    if (out_dev) convert_for(G, P, out_dev, width);
     TGXD_CUDA(cudaGetLastError());
     w.last_kind = P.kind;
     w.last_q = P.Q;
@@ -514,7 +614,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.qp = w.params.as<QueryParam>();
   a.X = w.X.as<int32_t>();
   a.EP = w.EP.as<int2>();
-  a.R = fast ? w.R.as<int32_t>() : nullptr;
+  a.R = fast || bfs ? w.R.as<int32_t>() : nullptr;
+  a.hops = bfs ? 1 : 0;
   a.fa = w.fa.as<uint32_t>();
   a.fb = w.fb.as<uint32_t>();
   a.chunks = w.chunks.as<uint2>();
@@ -603,11 +704,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     TGXD_CUDA(cudaMemcpyAsync(w.ctl.p, &z, sizeof z, cudaMemcpyHostToDevice, s));
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
-  if (out_dev) {
-    convert_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
-        P.kind, w.X.as<int32_t>(), fast ? w.R.as<int32_t>() : nullptr, slots, G->n,
-        w.seeds.as<Seed>(), out_dev, width);
-  }
+  if (out_dev) convert_for(G, P, out_dev, width);
   TGXD_CUDA(cudaGetLastError());
   w.last_kind = P.kind;
   w.last_q = P.Q;
@@ -620,6 +717,21 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
 }
 
 static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float total_ms) {
+  if (G->ws.last_edge) {
+    EdgeCtl c;
+    TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ectl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
+    TGXD_CUDA(cudaStreamSynchronize(G->stream));
+    if (c.error) return fail(TGXD_ERR_CUDA, "edge traversal watchdog: round limit exceeded");
+    if (!st) return TGXD_OK;
+    st->rounds = c.rounds;
+    st->candidates = 0;
+    st->expansions = c.expanded;
+    st->edges_relaxed = c.checked;
+    st->index_lookups = 0;
+    st->kernel_ms = kernel_ms;
+    st->total_ms = total_ms;
+    return TGXD_OK;
+  }
 #ifdef TGXD_CHAIN_PROBE
   {
     unsigned long long pr[256][12];
@@ -710,7 +822,8 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   if (!G) return fail(TGXD_ERR_ARGUMENT, "null graph");
   if (!out) return fail(TGXD_ERR_ARGUMENT, "null output");
   if (width != 4 && width != 8) return fail(TGXD_ERR_ARGUMENT, "width must be 4 or 8");
-  if (kind == TGXD_FASTEST && k > 1) {  // one sweep per source
+  const bool edge_kind = ordering == TGXD_OVERLAPS || kind == TGXD_SHORTEST_DURATION;
+  if ((kind == TGXD_FASTEST || edge_kind) && k > 1) {  // one sweep / edge traversal per source
     if (!verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "null query arrays");
     tgxd_stats acc;
     std::memset(&acc, 0, sizeof acc);
@@ -736,11 +849,11 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   Prepared P;
   int rc = prepare(G, kind, k, verts, ta, tb, ordering, P);
   if (rc) return rc;
-  if (kind == TGXD_FASTEST) {
+  if (kind == TGXD_FASTEST && !P.edge) {
     rc = fastest_candidates(G, P);
     if (rc) return rc;
   }
-  rc = ensure_workspace(G, P.Q, kind == TGXD_FASTEST);
+  rc = ensure_workspace(G, P.Q, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS);
   if (rc) return rc;
   Workspace& w = G->ws;
   const uint64_t slots = (uint64_t)P.Q * G->n;
@@ -1117,11 +1230,25 @@ int tgxd_fastest(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int
                     stats);
 }
 
+int tgxd_shortest_duration(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b,
+                           int ordering, int64_t* out, tgxd_stats* stats) {
+  return query_impl(g, TGXD_SHORTEST_DURATION, 1, &source, &t_a, &t_b, ordering, TGXD_MODE_AUTO,
+                    out, 8, 0, stats);
+}
+
+int tgxd_temporal_bfs(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int ordering,
+                      int64_t* out, tgxd_stats* stats) {
+  return query_impl(g, TGXD_TEMPORAL_BFS, 1, &source, &t_a, &t_b, ordering, TGXD_MODE_AUTO, out,
+                    8, 0, stats);
+}
+
 int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reached) {
   if (!g || !e_adm || !v_reached) return fail(TGXD_ERR_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lock(g->mu);
   Workspace& w = g->ws;
   if (w.last_kind < 0 || q >= w.last_q) return fail(TGXD_ERR_ARGUMENT, "no such query slot");
+  if (w.last_edge)
+    return fail(TGXD_ERR_UNSUPPORTED, "the unit of work is defined for vertex-label traversals");
   TGXD_CUDA(cudaSetDevice(g->device));
   const DevCsr& c = w.last_kind == TGXD_LATEST_DEPARTURE ? g->in : g->out;
   DeviceBuffer acc;
@@ -1149,8 +1276,9 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
   Prepared P;
   int rc = prepare(g, kind, k, vertices, t_a, t_b, ordering, P);
   if (rc) return rc;
-  if (kind == TGXD_FASTEST && (rc = fastest_candidates(g, P))) return rc;
-  if ((rc = ensure_workspace(g, P.Q, kind == TGXD_FASTEST))) return rc;
+  if (kind == TGXD_FASTEST && !P.edge && (rc = fastest_candidates(g, P))) return rc;
+  if ((rc = ensure_workspace(g, P.Q, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS)))
+    return rc;
   Workspace& w = g->ws;
   const uint64_t slots = (uint64_t)P.Q * g->n;
   if (!dalloc<int32_t>(w.timing_out, slots)) return fail(TGXD_ERR_CUDA, "allocation (output)");

@@ -68,6 +68,9 @@ struct Workspace {
   // asynchronous engine: queued flags, vertex / chunk rings, control block
   DeviceBuffer axq, aunits, actl;
   uint64_t a_slots = 0, a_units = 0;
+  // edge-state engine (edges.cuh): per-edge states, edge queues, results
+  DeviceBuffer ereached, edep, eval, estamp, efa, efb, ectl, ey;
+  bool last_edge = false;
   bool last_async = false;
   bool last_handoff = false;  // round kernel may have handed its tail to the async engine
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
@@ -125,6 +128,7 @@ struct tgxd_graph {
   int sm_count = 0;
   int coop_blocks = 0;
   int coop_blocks_async = 0;
+  int coop_blocks_edge = 0;
   std::mutex mu;
   tgxd::Workspace ws;
 };

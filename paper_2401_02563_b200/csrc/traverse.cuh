@@ -78,7 +78,8 @@ struct TravArgs {
   int32_t* X;          // labels, Q x n (key space)
   int2* EP;            // per slot {bound it was last expanded with, position of
                        // that bound in its segment (kNoPos: unknown)}
-  int32_t* R;          // fastest durations (nullptr otherwise)
+  int32_t* R;          // fastest durations / BFS hop counts (nullptr otherwise)
+  int hops;            // temporal BFS: R[v] = the round v's arrival first improved
   uint32_t* fa;        // frontier queues (items = q * n + v)
   uint32_t* fb;
   uint2* chunks;       // {lo, q << 9 | len}
@@ -205,6 +206,7 @@ struct RelaxCtx {
   uint32_t* fout;
   uint64_t pol_stream, pol_keep;
   uint32_t improved;         // per-lane improvement count (no-push rounds)
+  int32_t hop;               // temporal BFS: this round's number (1-based)
 };
 
 // Relax kUnroll 32-edge steps: e[u] edge ids, q[u] query slots, act[u] lane
@@ -256,7 +258,7 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
   int32_t old[kUnroll], ex[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
-    old[u] = kInf;
+    old[u] = v[u];  // no atomic issued: not an improvement
     ex[u] = 0;
     if (v[u] < cur[u]) {
       if (rx.push) ex[u] = ld_state(reinterpret_cast<const int32_t*>(a.EP + idx[u]), rx.pol_keep);
@@ -268,7 +270,13 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
   for (int u = 0; u < kUnroll; ++u) {
     p[u] = false;
     if (v[u] < old[u]) {
-      if (a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
+      // fastest: r = min(arrival - departure); BFS: the first improving round
+      // (compare_and_swap(r[d], inf, round), path_algorithms.cpp:395-397)
+      if (a.hops) {
+        if (old[u] == kInf) a.R[idx[u]] = rx.hop;
+      } else if (a.R) {
+        atomicMin(a.R + idx[u], v[u] - rx.depart);
+      }
       if (rx.push) p[u] = bound_of(old[u], a.strict) == ex[u];
       else ++rx.improved;
     }
@@ -1118,7 +1126,7 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
     const unsigned long long p_now = st.p_known;
     uint32_t* fin = st.flip ? a.fb : a.fa;
     uint32_t* fout = st.flip ? a.fa : a.fb;
-    RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
+    RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
     if (seed) {
       if (tr) {
         trace_round(a, st.rounds, 0, gtimer());
@@ -1251,7 +1259,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         const unsigned long long c_end = c0.chunks, s_end = c0.smalls, e_end = c0.edges;
         const unsigned long long p_now = st.p_known;
         uint32_t* fout = st.flip ? a.fa : a.fb;
-        RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
+        RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
         phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
         trace_warp_done(a, st.rounds, 1);
         grid.sync();
@@ -1284,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         trace_round(a, st.rounds, 7, pull ? 3 : (st.dense ? 2 : 0));
       }
       if (pull) {
-        RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0};
+        RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
         unsigned long long scanned = 0;
         // P1 queues slots right away: every block's post-barrier read of the
         // pushes counter must be over first (counter discipline)
@@ -1335,7 +1343,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       const unsigned long long w = (e_end - st.e_cur) + xcnt;
       const bool push = a.mode == TGXD_MODE_SPARSE ||
                         (a.mode == TGXD_MODE_AUTO && w <= a.push_w);
-      RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0};
+      RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, xlo, xcnt, rx, blockIdx.x, gridDim.x, wbuf);
       if (!push) {  // improvements only feed the dense frontier's size
         uint32_t imp = rx.improved;

@@ -78,6 +78,46 @@ int main() {
     CHECK(r.values[2] == 0);
     CHECK(r.values[0] == kInf);
   }
+  {  // shortest duration (test_algorithms.cpp:124-146)
+    const auto g1 = TemporalGraph::build({{0, 1, 3, 5, 1.0}}, 2, true);
+    CHECK(shortest_duration(g1, 0, QueryWindow{}).values[1] == 2);
+    const auto g =
+        TemporalGraph::build({{0, 1, 0, 4, 1.0}, {0, 2, 0, 1, 1.0}, {2, 1, 5, 7, 1.0}}, 3, true);
+    CHECK(shortest_duration(g, 0, QueryWindow{}).values[1] == 3);
+    bool thrown = false;
+    AlgoOptions w;
+    w.weighted = true;
+    try {
+      shortest_duration(g, 0, QueryWindow{}, w);
+    } catch (const std::domain_error&) {
+      thrown = true;
+    }
+    CHECK(thrown);
+  }
+  {  // temporal BFS (test_algorithms.cpp:149-168)
+    const auto g = TemporalGraph::build(
+        {{0, 1, 1, 2, 1.0}, {1, 2, 3, 4, 1.0}, {2, 3, 5, 6, 1.0}}, 4, true);
+    const auto r = temporal_bfs(g, 0, QueryWindow{});
+    CHECK(r.values == (std::vector<std::int64_t>{0, 1, 2, 3}));
+    const auto g2 = TemporalGraph::build(
+        {{0, 1, 9, 10, 1.0}, {0, 2, 0, 1, 1.0}, {2, 1, 2, 3, 1.0}, {1, 3, 5, 6, 1.0}}, 4, true);
+    const auto r2 = temporal_bfs(g2, 0, QueryWindow{});
+    CHECK(r2.values[1] == 1);
+    CHECK(r2.values[3] == 3);
+  }
+  {  // Overlaps gate (test_engine.cpp:223-243 as a path query)
+    const auto g = TemporalGraph::build({{0, 1, 2, 6, 1.0},
+                                         {1, 2, 4, 9, 1.0},
+                                         {1, 3, 7, 9, 1.0},
+                                         {1, 4, 2, 8, 1.0},
+                                         {1, 5, 3, 5, 1.0}},
+                                        6, true);
+    AlgoOptions ov;
+    ov.ordering = Ordering::Overlaps;
+    const auto r = earliest_arrival(g, 0, QueryWindow{}, ov);
+    CHECK(r.values[2] == 9);
+    CHECK(r.values[3] == kInf && r.values[4] == kInf && r.values[5] == kInf);
+  }
   {  // edge validation (types.cpp:41-54)
     bool thrown = false;
     try {

@@ -92,8 +92,14 @@ def test_error_semantics():
         T.fastest_path(g, 0, T.QueryWindow(9, 3))
     with pytest.raises(T.InvalidArgument):     # internal.hpp:19-21
         T.earliest_arrival(g, 0, T.QueryWindow(1 << 63, (1 << 64) - 1))
-    with pytest.raises(T.Unsupported):         # no device path for Overlaps
-        T.earliest_arrival(g, 0, T.QueryWindow(), T.AlgoOptions(ordering=T.Ordering.OVERLAPS))
+    with pytest.raises(T.Unsupported):         # weights are not stored on the device
+        T.shortest_duration(g, 0, T.QueryWindow(), T.AlgoOptions(weighted=True))
+    with pytest.raises(T.OutOfRange):
+        T.shortest_duration(g, 2)
+    with pytest.raises(T.InvalidArgument):
+        T.temporal_bfs(g, 0, T.QueryWindow(9, 3))
+    with pytest.raises(T.InvalidArgument):
+        T.earliest_arrival(g, 0, T.QueryWindow(9, 3), T.AlgoOptions(ordering=T.Ordering.OVERLAPS))
     with pytest.raises(T.OutOfRange, match="edge 1: endpoint"):   # types.cpp:43-47
         T.TemporalGraph.build(S.hand_edges([(0, 1, 3, 5), (0, 2, 3, 5)]), 2)
     with pytest.raises(T.OutOfRange, match="edge 0: end 4 precedes start 5"):  # :48-51
