@@ -18,7 +18,65 @@ ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--ref-steps", type=int, default=3)
 ap.add_argument("--no-ref", action="store_true")
+ap.add_argument("--extras", action="store_true",
+                help="8(f) rows: temporal BFS, shortest duration and the Overlaps ordering "
+                     "(config 2 graph; shortest duration on the 2^16-vertex reduction)")
 args = ap.parse_args()
+FN = {"earliest_arrival": T.earliest_arrival, "latest_departure": T.latest_departure,
+      "fastest": T.fastest_path, "shortest_duration": T.shortest_duration,
+      "temporal_bfs": T.temporal_bfs}
+
+
+def extras():
+    """One query per (kind, ordering): GPU wall / kernel time next to the
+    reference library on the same edge list."""
+    from oracle.pyoracle import Reference
+    plan = [("c2", 0, [("temporal_bfs", 1), ("earliest_arrival", 2), ("latest_departure", 2),
+                       ("fastest", 2), ("temporal_bfs", 2)]),
+            ("c2", -6, [("shortest_duration", 1), ("shortest_duration", 0),
+                        ("shortest_duration", 2)])]
+    for name, delta, qs in plan:
+        wl = workload(name, delta)
+        g = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
+        n = g.vertex_count()
+        q = wl.queries(g.degrees(T.Direction.OUT), g.degrees(T.Direction.IN), n)[0]
+        ref = None
+        if not args.no_ref and Reference.available():
+            Reference.set_workers(os.cpu_count() or 1)
+            ref = Reference(T.generate_edges(wl.gen), n, True, wl.index_cutoff)
+        for kind, ordv in qs:
+            opts = T.AlgoOptions(ordering=T.Ordering(ordv))
+            FN[kind](g, q.vertex, q.window, opts)  # warm
+            times = []
+            st = T.EdgeMapStats()
+            for _ in range(args.ref_steps):
+                t = time.perf_counter()
+                st = T.EdgeMapStats()
+                got = FN[kind](g, q.vertex, q.window, T.AlgoOptions(ordering=T.Ordering(ordv),
+                                                                     stats=st)).values
+                times.append(time.perf_counter() - t)
+            line = {"config": name, "delta": delta, "kind": kind, "ordering": ordv, "n": n,
+                    "m": g.edge_count(), "gpu_wall_ms": 1e3 * float(np.median(times)),
+                    "gpu_kernel_ms": st.kernel_ms, "rounds": st.rounds,
+                    "edge_checks": st.edges_relaxed,
+                    "reached": int((got != (got.min() if kind == "latest_departure"
+                                            else got.max())).sum())}
+            if ref is not None:
+                t = time.perf_counter()
+                want = ref.query(kind, q.vertex, q.window.t_a, q.window.t_b, ordv)
+                rs = time.perf_counter() - t
+                line["ref"] = {"kind": "reference", "cores": os.cpu_count(), "s": rs}
+                line["identical"] = bool(np.array_equal(got, want))
+                line["speedup_wall"] = rs / (line["gpu_wall_ms"] * 1e-3)
+            print(json.dumps(line), flush=True)
+        if ref is not None:
+            ref.close()
+        g.close()
+
+
+if args.extras:
+    extras()
+    sys.exit(0)
 
 
 def ref_time(wl, edges, n, groups):
