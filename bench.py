@@ -245,7 +245,15 @@ def run_ours(args):
 
     # end to end through the reference-facing C-ABI call with a host output
     # (int64 PathResult values): H2D of the query, D2H of the labels per step
-    out = np.empty(n, np.int64)
+    # the caller's result buffer is pinned host memory (page-locked: the D2H of
+    # the 33.5 MB int64 vector runs at PCIe speed instead of through staging)
+    pinned_ptr = None
+    try:
+        pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        out = pinned.numpy()
+        pinned_ptr = out.ctypes.data
+    except Exception:
+        out = np.empty(n, np.int64)
     import ctypes
     for _ in range(args.warmup):
         T._check(lib.tgxd_earliest_arrival(g.handle, q.vertex, q.window.t_a, q.window.t_b, 1,
@@ -280,6 +288,7 @@ def run_ours(args):
                      "kernel": "traverse_kernel", "kernel_ms": kernel_ms,
                      "algorithmic_bytes": b_alg, "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
+                "host_buffer": "pinned" if out.ctypes.data == pinned_ptr else "pageable",
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3},
         "gpu_launches": 4 * args.steps,
         "clocks": sampler.summary(),

@@ -104,10 +104,16 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Label word: (label with its sign bit flipped) << 32 | queued bit, so the
+// unsigned order of words is the signed order of labels (LD labels are
+// negative in key space) and one 64-bit atomicMin both lowers the label and
+// sets the bit.
 __device__ __forceinline__ unsigned long long xq_pack(int32_t label, uint32_t queued) {
-  return ((unsigned long long)(uint32_t)label << 32) | queued;
+  return ((unsigned long long)((uint32_t)label ^ 0x80000000u) << 32) | queued;
 }
-__device__ __forceinline__ int32_t xq_label(unsigned long long w) { return (int32_t)(w >> 32); }
+__device__ __forceinline__ int32_t xq_label(unsigned long long w) {
+  return (int32_t)((uint32_t)(w >> 32) ^ 0x80000000u);
+}
 
 __device__ __forceinline__ uint32_t* unit_ptr(const AsyncArgs& a, unsigned long long pos) {
   return a.units + (pos & a.umask) * kUnitWords;
@@ -182,8 +188,9 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
     if (!(act[u] && v[u] <= vhi)) v[u] = kInf;  // window containment (types.hpp:55-57)
     cur[u] = v[u] != kInf ? __ldcg(a.XQ + idx[u]) : xq_pack(kInf, 1u);
   }
-  // write_min (parallel.hpp:91-99) + the queued bit in one CAS; all CASes of
-  // the batch are issued before any result is used
+  // write_min (parallel.hpp:91-99) and the queued bit in one 64-bit
+  // atomicMin: a lower label wins whatever the bit, and the new word carries
+  // the bit set; all atomics of the batch are issued before any result is used
   bool imp[kUnroll];
   uint32_t was[kUnroll];
 #pragma unroll
@@ -191,23 +198,9 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
     imp[u] = v[u] < xq_label(cur[u]);
     was[u] = 1u;
     if (imp[u]) {
-      const unsigned long long prev = atomicCAS(a.XQ + idx[u], cur[u], xq_pack(v[u], 1u));
-      if (prev == cur[u]) {
-        was[u] = (uint32_t)(prev & 1ull);
-      } else {
-        cur[u] = prev;
-        imp[u] = false;
-        // contended: retry until the label is no longer above v
-        while (v[u] < xq_label(cur[u])) {
-          const unsigned long long p2 = atomicCAS(a.XQ + idx[u], cur[u], xq_pack(v[u], 1u));
-          if (p2 == cur[u]) {
-            imp[u] = true;
-            was[u] = (uint32_t)(p2 & 1ull);
-            break;
-          }
-          cur[u] = p2;
-        }
-      }
+      const unsigned long long prev = atomicMin(a.XQ + idx[u], xq_pack(v[u], 1u));
+      imp[u] = v[u] < xq_label(prev);
+      if (imp[u]) was[u] = (uint32_t)(prev & 1ull);
     }
   }
 #pragma unroll
@@ -306,14 +299,15 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
       uint32_t pos = kNoPos;
       if (lb < hik) {
         const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-        if (t > s) {
+        const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
+        if (t > s && km >= lb) {
           act = true;
           const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
           ix += fence ? 1 : 0;
           if (old <= qp.vhi + 1 && ep.y != (int32_t)kNoPos) {
             p1 = (uint32_t)ep.y;
           } else {
-            p1 = __ldg(a.g.key + t - 1) < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
+            p1 = km < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
           }
           p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
           pos = p0;
@@ -536,7 +530,7 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n,
     const uint32_t k = min(kBatch, Q - q0);
     for (uint32_t j = 0; j < k; ++j) {
       const uint32_t item = (q0 + j) * n + qp[q0 + j].root;
-      XQ[item] = ((unsigned long long)(uint32_t)qp[q0 + j].klo << 32) | 1ull;
+      XQ[item] = ((unsigned long long)((uint32_t)qp[q0 + j].klo ^ 0x80000000u) << 32) | 1ull;
       u[1 + j] = item;
     }
     u[0] = k;
@@ -555,7 +549,7 @@ __global__ void async_reset_kernel(uint32_t* units, size_t nunits, AsyncCtl* c) 
 // Per-query label words: INF, not queued.
 __global__ void async_init_kernel(unsigned long long* XQ, size_t slots) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  const unsigned long long w = (unsigned long long)(uint32_t)kInf << 32;
+  const unsigned long long w = (unsigned long long)((uint32_t)kInf ^ 0x80000000u) << 32;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += stride) XQ[i] = w;
 }
 
