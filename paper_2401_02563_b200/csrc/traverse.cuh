@@ -772,10 +772,26 @@ __device__ __forceinline__ void slot_list_pop(uint2* buf, uint32_t& n, uint32_t 
   __syncwarp();
 }
 
+__device__ __forceinline__ void slot_list_push4(uint4* buf, uint32_t& n, bool p, uint4 v) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, p);
+  if (p) buf[n + __popc(bal & ((1u << lane_id()) - 1))] = v;
+  n += __popc(bal);
+  __syncwarp();
+}
+__device__ __forceinline__ void slot_list_pop4(uint4* buf, uint32_t& n, uint32_t taken) {
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  const uint4 t = taken + lane < 64 ? buf[taken + lane] : make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+  if (lane + taken < n) buf[lane] = t;
+  n -= taken;
+  __syncwarp();
+}
+
 struct PullBufs {
   PushBuf pb;
   WarpList chl;          // pull chunks
-  uint2* obuf;           // open slots {slot, lim}
+  uint4* obuf;           // open slots {slot, lim, segment start, segment end}
   uint2* rbuf;           // long windows {slot, lim}
   uint32_t no, nr;
   unsigned long long cstart;
@@ -824,18 +840,17 @@ __device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs
   const DevCsr& rg = a.rg;
   const uint32_t lane = lane_id();
   const bool act = lane < cnt;
-  const uint2 o = act ? b.obuf[lane] : make_uint2(0u, 0u);
-  slot_list_pop(b.obuf, b.no, cnt);
+  const uint4 o = act ? b.obuf[lane] : make_uint4(0u, 0u, 0u, 0u);
+  slot_list_pop4(b.obuf, b.no, cnt);
   const uint32_t i = o.x;
   const int32_t lim = (int32_t)o.y;
   int32_t best = kInf;
   bool open = act;
   if (act) {
     const uint32_t q = a.Q == 1 ? 0u : i / a.n;
-    const uint32_t v = i - q * a.n;
     const QueryParam& qp = a.qp[q];
-    const uint32_t s = __ldg(rg.off + v);
-    uint32_t j = __ldg(rg.off + v + 1);
+    const uint32_t s = o.z;  // segment bounds came with the sweep's coalesced loads
+    uint32_t j = o.w;
     for (uint32_t k = 0; open && k < kPullLane; k += kPullBatch) {
       int32_t kr[kPullBatch];
       uint2 pl[kPullBatch];
@@ -877,34 +892,39 @@ __device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs
     b.pb.n += __popc(bal);
     if (b.pb.n >= 32) push_flush32(b.pb, a.ctl, rx.pstart, rx.fout);
   }
-  slot_list_push(b.rbuf, b.nr, open, o);
+  slot_list_push(b.rbuf, b.nr, open, make_uint2(o.x, o.y));
   if (b.nr >= 32) pull_search32(a, b, 32);
 }
 
 #ifndef TGXD_PULL_SLOTS
-#define TGXD_PULL_SLOTS 4
+#define TGXD_PULL_SLOTS 1
 #endif
 constexpr uint32_t kPullSlots = TGXD_PULL_SLOTS;  // slot groups per lane in flight in the sweep
 
 __device__ TGXD_PHASE void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned long long cstart,
                             uint32_t bid, uint32_t nblk, uint32_t* wbuf, uint2* ebuf,
-                            uint2* rbuf, unsigned long long& scanned) {
+                            uint2* rbuf, uint4* obuf, unsigned long long& scanned) {
   const DevCsr& rg = a.rg;
   const uint32_t lane = lane_id();
   const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = nblk * kWarps;
   const uint32_t slots = a.Q * a.n;
-  PullBufs b{{wbuf, 0}, {ebuf, 0}, ebuf + 64, rbuf, 0, 0, cstart};
+  PullBufs b{{wbuf, 0}, {ebuf, 0}, obuf, rbuf, 0, 0, cstart};
   // label sweep: coalesced labels and last keys; slots with an in-edge below
   // their label are queued for the scan
   for (uint32_t base = gw * 32 * kPullSlots; base < slots; base += nw * 32 * kPullSlots) {
     int32_t x[kPullSlots], km[kPullSlots];
+    uint32_t sg[kPullSlots], tg[kPullSlots];
 #pragma unroll
     for (uint32_t u = 0; u < kPullSlots; ++u) {
       const uint32_t i = base + u * 32 + lane;
       const uint32_t q = a.Q == 1 ? 0u : i / a.n;
+      const uint32_t v = i - q * a.n;
       x[u] = i < slots ? ld_state(a.X + i, rx.pol_keep) : kInf;
-      km[u] = i < slots ? __ldg(rg.kmax + (i - q * a.n)) : INT32_MIN;
+      km[u] = i < slots ? __ldg(rg.kmax + v) : INT32_MIN;
+      // segment bounds ride along (coalesced): the scan starts at the keys
+      sg[u] = i < slots ? __ldg(rg.off + v) : 0u;
+      tg[u] = i < slots ? __ldg(rg.off + v + 1) : 0u;
     }
 #pragma unroll
     for (uint32_t u = 0; u < kPullSlots; ++u) {
@@ -924,7 +944,7 @@ __device__ TGXD_PHASE void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned
           a.EP[i] = make_int2(lb, (int32_t)kNoPos);
         }
       }
-      slot_list_push(b.obuf, b.no, open, make_uint2(i, (uint32_t)lim));
+      slot_list_push4(b.obuf, b.no, open, make_uint4(i, (uint32_t)lim, sg[u], tg[u]));
       if (b.no >= 32) pull_scan32(a, rx, b, 32, scanned);
     }
   }
@@ -1185,6 +1205,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   __shared__ uint32_t s_buf[kWarps][64];
   __shared__ uint2 s_ebuf[kWarps][128];
   __shared__ uint2 s_rbuf[kWarps][64];
+  __shared__ uint4 s_obuf[kWarps][64];
   GridBarrier grid{&a.ctl->bar_count, &a.ctl->bar_gen, gridDim.x, 0};
   uint32_t* wbuf = s_buf[threadIdx.x >> 5];
   uint2* ebuf = s_ebuf[threadIdx.x >> 5];
@@ -1297,7 +1318,8 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         // P1 queues slots right away: every block's post-barrier read of the
         // pushes counter must be over first (counter discipline)
         grid.sync();
-        phase_pull1(a, rx, st.pc_cur, blockIdx.x, gridDim.x, wbuf, ebuf, s_rbuf[threadIdx.x >> 5], scanned);
+        phase_pull1(a, rx, st.pc_cur, blockIdx.x, gridDim.x, wbuf, ebuf, s_rbuf[threadIdx.x >> 5],
+                    s_obuf[threadIdx.x >> 5], scanned);
         trace_warp_done(a, st.rounds, 0);
         grid.sync();
         const unsigned long long pc_end = read_counters(ctl).pchunks;
