@@ -440,7 +440,8 @@ struct ExpandBufs {
 // warp's lists. All lanes must call it; no lane ever waits on another's
 // search.
 __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint32_t item, int32_t x,
-                                            int2 ep, ExpandBufs& eb, unsigned long long& work,
+                                            int2 ep, uint32_t s, uint32_t t, int32_t km,
+                                            ExpandBufs& eb, unsigned long long& work,
                                             unsigned long long& ix) {
   const uint32_t lane = lane_id();
   uint32_t q = 0, p0 = 0, p1 = 0;
@@ -459,8 +460,7 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
       const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
       uint32_t pos = kNoPos;
       if (lb < hik) {
-        const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-        const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
+        // (s, t, km: segment bounds and last key, loaded with the label)
 #ifdef TGXD_CHAIN_PROBE
         if (PROBE_ON && (s ^ t ^ (uint32_t)km) == 0x12345678u) asm volatile("trap;");
         PROBE(g_probe_n, 3);
@@ -584,6 +584,8 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
     uint32_t item = i;
     int32_t x = kInf;
     int2 ep = make_int2(kInf, (int32_t)kNoPos);
+    uint32_t s0 = 0, t0 = 0;
+    int32_t km0 = INT32_MIN;
     if (valid) {
       if (fin) item = __ldcg(fin + i);
 #ifdef TGXD_CHAIN_PROBE
@@ -592,13 +594,19 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
 #endif
       x = ld_state(a.X + item, pol_keep);
       ep = __ldcg(a.EP + item);
+      // the segment's bounds and last key do not depend on the label: issue
+      // them with it (one dependent load less per expansion)
+      const uint32_t v = a.Q == 1 ? item : item % a.n;
+      s0 = __ldg(a.g.off + v);
+      t0 = __ldg(a.g.off + v + 1);
+      km0 = __ldg(a.g.kmax + v);
       valid = x != kInf;
 #ifdef TGXD_CHAIN_PROBE
       if (PROBE_ON && ep.y == 0x7ffffff0) asm volatile("trap;");
       if (probing) PROBE(g_probe_n, 2);
 #endif
     }
-    expand_warp(a, valid, item, x, ep, eb, work, ix);
+    expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix);
 #ifdef TGXD_CHAIN_PROBE
     if (probing) PROBE(g_probe_n, 6);
 #endif

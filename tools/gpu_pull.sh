@@ -1,4 +1,4 @@
-mkdir -p gpurun_out/p19
-timeout 300 python tools/hunt.py 4 79 > gpurun_out/p19/h4.log 2>&1; echo "h4 mism $(grep -c MISMATCH gpurun_out/p19/h4.log) $(tail -n 1 gpurun_out/p19/h4.log)"
-timeout 300 python tools/race_loop.py c4 4 0,4 > gpurun_out/p19/rl.log 2>&1; tail -n 1 gpurun_out/p19/rl.log
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/p19/pytest.log 2>&1; tail -n 3 gpurun_out/p19/pytest.log
+mkdir -p gpurun_out/p20
+for m in 0 1; do timeout 600 python tools/diag.py --mode $m --trace --reps 3 > gpurun_out/p20/d$m.log 2>&1; done
+timeout 300 python tools/hunt.py 0 80 > gpurun_out/p20/h0.log 2>&1; echo "h0 mism $(grep -c MISMATCH gpurun_out/p20/h0.log) $(tail -n 1 gpurun_out/p20/h0.log)"
+timeout 300 python tools/hunt.py 2 81 > gpurun_out/p20/h2.log 2>&1; echo "h2 mism $(grep -c MISMATCH gpurun_out/p20/h2.log) $(tail -n 1 gpurun_out/p20/h2.log)"
