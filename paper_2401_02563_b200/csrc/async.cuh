@@ -285,10 +285,13 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
   if (valid) {
     // clear the queued bit; the returned word holds the label to expand
     // with (an improvement after this point re-enqueues the slot)
-    const int32_t x = xq_label(atomicAnd(a.XQ + item, ~1ull));
-    const int2 ep = __ldcg(a.EP + item);
     q = a.Q == 1 ? 0u : item / a.n;
     const uint32_t v = item - q * a.n;
+    // label, bounds and the segment's extent all issued together
+    const int32_t x = xq_label(atomicAnd(a.XQ + item, ~1ull));
+    const int2 ep = __ldcg(a.EP + item);
+    const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
+    const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
     const QueryParam& qp = a.qp[q];
     // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342)
     int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
@@ -298,8 +301,6 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
       const int32_t hik = min(old, qp.vhi + 1);
       uint32_t pos = kNoPos;
       if (lb < hik) {
-        const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
-        const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
         if (t > s && km >= lb) {
           act = true;
           const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
