@@ -306,9 +306,16 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
 // Emission is buffered per warp in shared memory (no block barriers).
 
 
-// Per-warp staging of emitted work: appended 32 entries at a time.
+// Per-warp staging of emitted work, appended to the global list kListFlush
+// entries per atomic (the list counters are shared by every warp).
+#ifndef TGXD_LIST_FLUSH
+#define TGXD_LIST_FLUSH 32
+#endif
+constexpr uint32_t kListFlush = TGXD_LIST_FLUSH;
+constexpr uint32_t kListCap = kListFlush + 32;  // entries of one warp buffer
+
 struct WarpList {
-  uint2* buf;       // 64 entries of this warp
+  uint2* buf;       // kListCap entries of this warp
   uint32_t n;       // staged entries (warp-uniform)
 };
 
@@ -316,15 +323,15 @@ __device__ __forceinline__ void list_flush(WarpList& wl, uint32_t count, unsigne
                                            unsigned long long start, uint2* list) {
   const uint32_t lane = lane_id();
   __syncwarp();
-  const uint2 v = wl.buf[lane];
-  const uint2 tail = wl.buf[32 + lane];
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(ctr, (unsigned long long)count);
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (lane < count) list[base - start + lane] = v;
+  for (uint32_t k = lane; k < count; k += 32) list[base - start + k] = wl.buf[k];
+  const uint32_t rem = wl.n - count;  // < 32
+  const uint2 t = lane < rem ? wl.buf[count + lane] : make_uint2(0u, 0u);
   __syncwarp();
-  if (lane + count < wl.n && lane < 32) wl.buf[lane] = tail;
-  wl.n -= count;
+  if (lane < rem) wl.buf[lane] = t;
+  wl.n = rem;
   __syncwarp();
 }
 
@@ -334,12 +341,12 @@ __device__ __forceinline__ void list_append(WarpList& wl, bool p, uint2 v, unsig
   if (bal == 0) return;
   if (p) wl.buf[wl.n + __popc(bal & ((1u << lane_id()) - 1))] = v;
   wl.n += __popc(bal);
-  if (wl.n >= 32) list_flush(wl, 32, ctr, start, list);
+  if (wl.n >= kListFlush) list_flush(wl, kListFlush, ctr, start, list);
 }
 
 __device__ __forceinline__ void list_drain(WarpList& wl, unsigned long long* ctr,
                                            unsigned long long start, uint2* list) {
-  if (wl.n) list_flush(wl, wl.n, ctr, start, list);
+  while (wl.n) list_flush(wl, min(wl.n, kListFlush), ctr, start, list);
 }
 
 constexpr uint32_t kNoPos = 0xffffffffu;
@@ -556,7 +563,7 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
   const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = nblk * kWarps;
   const uint32_t total = fin ? F : a.Q * a.n;
-  ExpandBufs eb{{ebuf, 0}, {ebuf + 64, 0}, cstart, sstart};
+  ExpandBufs eb{{ebuf, 0}, {ebuf + kListCap, 0}, cstart, sstart};
   unsigned long long work = 0;
 #ifdef TGXD_CHAIN_PROBE
   const bool probing = fin && nblk == 1 && bid == 0;  // local rounds only
@@ -1211,7 +1218,7 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
 
 __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
-  __shared__ uint2 s_ebuf[kWarps][128];
+  __shared__ uint2 s_ebuf[kWarps][2 * kListCap];
   __shared__ uint2 s_rbuf[kWarps][64];
   __shared__ uint4 s_obuf[kWarps][64];
   GridBarrier grid{&a.ctl->bar_count, &a.ctl->bar_gen, gridDim.x, 0};
