@@ -1041,13 +1041,16 @@ struct GridBarrier {
         __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
       } else {
+#ifndef TGXD_BAR_MAX_NS
+#define TGXD_BAR_MAX_NS 256
+#endif
         unsigned int ns = 32;
         for (;;) {
           unsigned int cur;
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
           if (cur != g) break;
           __nanosleep(ns);
-          if (ns < 1024) ns <<= 1;
+          if (ns < TGXD_BAR_MAX_NS) ns <<= 1;
         }
       }
       __threadfence();
