@@ -37,6 +37,9 @@
 
 namespace tgxd {
 
+#ifndef TGXD_ASYNC_SLEEP
+#define TGXD_ASYNC_SLEEP 256  // ns between polls of a long-waiting ticket
+#endif
 constexpr uint32_t kAChunk = 512;        // edges per chunk unit (4 x 128-edge bursts)
 constexpr uint32_t kAInline = 64;        // shorter ranges are relaxed by the expanding warp
 constexpr uint32_t kUnitWords = 16;      // 64-byte units
@@ -393,7 +396,7 @@ __device__ void async_loop(const AsyncArgs& a, const ARelax& rx, VBuf& vb, uint3
         wait_ns += gtimer() - t0;
         return;
       }
-      __nanosleep(polls < 64 ? 64 : 512);
+      __nanosleep(polls < 64 ? 64 : TGXD_ASYNC_SLEEP);
     }
     const unsigned long long t1 = gtimer();
     wait_ns += t1 - t0;

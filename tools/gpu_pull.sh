@@ -1,3 +1,4 @@
-mkdir -p gpurun_out/p25
-for v in default b128 b256 b4096; do L=build/variants/lib_$v.so; [ $v = default ] && L=paper_2401_02563_b200/libtgxd.so
- for h in 262144 0; do TGXD_HANDOFF_F=$h TGXD_LIB=$L timeout 600 python tools/diag.py --mode 0 --trace --reps 3 > gpurun_out/p25/${v}_$h.log 2>&1; done; done
+mkdir -p gpurun_out/p27
+timeout 300 python tools/hunt.py 3 87 > gpurun_out/p27/h3.log 2>&1; echo "h3 mism $(grep -c MISMATCH gpurun_out/p27/h3.log) $(tail -n 1 gpurun_out/p27/h3.log)"
+timeout 300 python tools/race_loop.py c4 4 0,3 > gpurun_out/p27/rl.log 2>&1; tail -n 1 gpurun_out/p27/rl.log
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/p27/pytest.log 2>&1; tail -n 3 gpurun_out/p27/pytest.log
