@@ -290,7 +290,12 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
                 "host_buffer": "pinned" if out.ctypes.data == pinned_ptr else "pageable",
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3},
-        "gpu_launches": 4 * args.steps,
+        # per step: init_kernel, seed_kernel, traverse_kernel, async_kernel (the
+        # tail continuation, exits at once when the rounds finished the query),
+        # convert_kernel
+        "gpu_launches": 5 * args.steps,
+        "kernels_per_step": ["init_kernel", "seed_kernel", "traverse_kernel", "async_kernel",
+                             "convert_kernel"],
         "clocks": sampler.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
