@@ -20,6 +20,7 @@
 #include "traverse.cuh"
 #include "async.cuh"
 #include "edges.cuh"
+#include "sd.cuh"
 
 namespace tgxd {
 
@@ -237,6 +238,9 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
   int per_sm_e = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_e, edge_kernel, kThreads, 0);
   G->coop_blocks_edge = std::max(1, per_sm_e) * G->sm_count;
+  int per_sm_s = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, sd_kernel, kThreads, 0);
+  G->coop_blocks_sd = std::max(1, per_sm_s) * G->sm_count;
   *out = G;
   return TGXD_OK;
 }
@@ -509,22 +513,67 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   const int kind = P.kind == TGXD_SHORTEST_DURATION ? kEdgeShortest
                    : P.kind == TGXD_FASTEST          ? kEdgeFastest
                                                      : kEdgeReach;
-  bool ok = dalloc<uint32_t>(w.efa, (size_t)m + 1) && dalloc<uint32_t>(w.efb, (size_t)m + 1) &&
+  // shortest duration under the succeeds orderings: vertex-driven (sd.cuh)
+  const bool sd = kind == kEdgeShortest && P.ordering != TGXD_OVERLAPS;
+  const size_t qcap = (size_t)std::max<uint64_t>(m, G->n) + 1;  // edge or vertex queues
+  bool ok = dalloc<uint32_t>(w.efa, qcap) && dalloc<uint32_t>(w.efb, qcap) &&
             dalloc<EdgeCtl>(w.ectl, 1);
   if (ok && kind == kEdgeReach) ok = dalloc<uint32_t>(w.ereached, (size_t)m / 32 + 1) != nullptr;
-  if (ok && kind != kEdgeReach) ok = dalloc<uint32_t>(w.estamp, (size_t)m + 1) != nullptr;
+  if (ok && kind != kEdgeReach) ok = dalloc<uint32_t>(w.estamp, qcap) != nullptr;
+  if (ok && sd) ok = dalloc<long long>(w.esm, (size_t)G->in.m + 1) != nullptr;
+  if (ok && sd && !G->in2out_ready) {
+    ok = dalloc<uint32_t>(G->in2out, (size_t)G->in.m + 1) != nullptr;
+    if (ok && G->in.m) {
+      in2out_kernel<<<grid_for(G->in.m, G->sm_count), 256, 0, s>>>(G->out, G->in,
+                                                                   G->in2out.as<uint32_t>());
+      G->in2out_ready = true;
+    }
+  }
   if (ok && kind == kEdgeFastest) ok = dalloc<int32_t>(w.edep, (size_t)m + 1) != nullptr;
   if (ok && kind == kEdgeShortest)
-    ok = dalloc<long long>(w.eval, (size_t)m + 1) && dalloc<long long>(w.ey, G->n + 1);
+    ok = dalloc<long long>(w.eval, qcap) && dalloc<long long>(w.ey, G->n + 1);
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (edge-state workspace)");
   TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), sizeof(Seed), cudaMemcpyHostToDevice, s));
   init_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
       w.X.as<int32_t>(), w.EP.as<int2>(), kind == kEdgeFastest ? w.R.as<int32_t>() : nullptr,
       G->n);
-  edge_init_kernel<<<grid_for(m, G->sm_count), 256, 0, s>>>(
-      kind, m, w.ereached.as<uint32_t>(), w.edep.as<int32_t>(), w.eval.as<long long>(),
-      w.estamp.as<uint32_t>(), kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n,
-      w.ectl.as<EdgeCtl>());
+  edge_init_kernel<<<grid_for(qcap, G->sm_count), 256, 0, s>>>(
+      kind, sd ? (uint32_t)(qcap - 1) : m, w.ereached.as<uint32_t>(), w.edep.as<int32_t>(),
+      w.eval.as<long long>(), w.estamp.as<uint32_t>(),
+      kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n, w.ectl.as<EdgeCtl>());
+  if (sd) {
+    SdArgs d;
+    d.out = G->out;
+    d.in = G->in;
+    d.in2out = G->in2out.as<uint32_t>();
+    d.qp = P.qp[0];
+    d.strict = P.strict;
+    d.val = w.eval.as<long long>();
+    d.sm = w.esm.as<long long>();
+    d.stamp = w.estamp.as<uint32_t>();
+    d.fa = w.efa.as<uint32_t>();
+    d.fb = w.efb.as<uint32_t>();
+    d.ctl = w.ectl.as<EdgeCtl>();
+    d.n = G->n;
+    d.round_limit = m + 16;
+    if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
+    void* sargs[] = {&d};
+    TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)sd_kernel, dim3(G->coop_blocks_sd),
+                                          dim3(kThreads), sargs, 0, s));
+    edge_fold_kernel<<<grid_for(m, G->sm_count), 256, 0, s>>>(
+        g, kEdgeShortest, nullptr, d.val, w.R.as<int32_t>(), w.ey.as<long long>());
+    if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
+    if (out_dev) convert_for(G, P, out_dev, width);
+    TGXD_CUDA(cudaGetLastError());
+    w.last_edge = true;
+    w.last_async = false;
+    w.last_handoff = false;
+    w.last_kind = P.kind;
+    w.last_q = P.Q;
+    w.last_strict = P.strict;
+    w.last_params = P.qp;
+    return TGXD_OK;
+  }
   EdgeArgs a;
   a.g = g;
   a.qp = P.qp[0];

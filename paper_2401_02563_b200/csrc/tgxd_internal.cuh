@@ -69,7 +69,7 @@ struct Workspace {
   DeviceBuffer axq, aunits, actl;
   uint64_t a_slots = 0, a_units = 0;
   // edge-state engine (edges.cuh): per-edge states, edge queues, results
-  DeviceBuffer ereached, edep, eval, estamp, efa, efb, ectl, ey;
+  DeviceBuffer ereached, edep, eval, estamp, efa, efb, ectl, ey, esm;
   bool last_edge = false;
   bool last_async = false;
   bool last_handoff = false;  // round kernel may have handed its tail to the async engine
@@ -123,12 +123,15 @@ struct tgxd_graph {
   uint64_t indexed[2] = {0, 0};
   tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence, out_kmax;
   tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax;
+  tgxd::DeviceBuffer in2out;  // In -> Out position of each edge (shortest duration; lazy)
+  bool in2out_ready = false;
   tgxd::DevCsr out, in;
   cudaStream_t stream = nullptr;
   int sm_count = 0;
   int coop_blocks = 0;
   int coop_blocks_async = 0;
   int coop_blocks_edge = 0;
+  int coop_blocks_sd = 0;
   std::mutex mu;
   tgxd::Workspace ws;
 };
