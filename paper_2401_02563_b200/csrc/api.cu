@@ -521,12 +521,12 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   if (ok && kind == kEdgeReach) ok = dalloc<uint32_t>(w.ereached, (size_t)m / 32 + 1) != nullptr;
   if (ok && kind != kEdgeReach) ok = dalloc<uint32_t>(w.estamp, qcap) != nullptr;
   if (ok && sd) ok = dalloc<long long>(w.esm, (size_t)G->in.m + 1) != nullptr;
-  if (ok && sd && !G->in2out_ready) {
-    ok = dalloc<uint32_t>(G->in2out, (size_t)G->in.m + 1) != nullptr;
-    if (ok && G->in.m) {
-      in2out_kernel<<<grid_for(G->in.m, G->sm_count), 256, 0, s>>>(G->out, G->in,
-                                                                   G->in2out.as<uint32_t>());
-      G->in2out_ready = true;
+  if (ok && sd && !G->out2in_ready) {
+    ok = dalloc<uint32_t>(G->out2in, (size_t)G->out.m + 1) != nullptr;
+    if (ok && G->out.m) {
+      out2in_kernel<<<grid_for(G->out.m, G->sm_count), 256, 0, s>>>(G->out, G->in,
+                                                                    G->out2in.as<uint32_t>());
+      G->out2in_ready = true;
     }
   }
   if (ok && kind == kEdgeFastest) ok = dalloc<int32_t>(w.edep, (size_t)m + 1) != nullptr;
@@ -540,20 +540,23 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   edge_init_kernel<<<grid_for(qcap, G->sm_count), 256, 0, s>>>(
       kind, sd ? (uint32_t)(qcap - 1) : m, w.ereached.as<uint32_t>(), w.edep.as<int32_t>(),
       w.eval.as<long long>(), w.estamp.as<uint32_t>(),
-      kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n, w.ectl.as<EdgeCtl>());
+      kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n, w.ectl.as<EdgeCtl>(),
+      sd ? w.esm.as<long long>() : nullptr, sd ? G->in.m : 0u);
   if (sd) {
     SdArgs d;
     d.out = G->out;
     d.in = G->in;
-    d.in2out = G->in2out.as<uint32_t>();
+    d.out2in = G->out2in.as<uint32_t>();
     d.qp = P.qp[0];
     d.strict = P.strict;
     d.val = w.eval.as<long long>();
-    d.sm = w.esm.as<long long>();
+    d.tree = w.esm.as<long long>();
     d.stamp = w.estamp.as<uint32_t>();
     d.fa = w.efa.as<uint32_t>();
     d.fb = w.efb.as<uint32_t>();
+    d.chunks = w.chunks.as<uint2>();
     d.ctl = w.ectl.as<EdgeCtl>();
+    d.nchunks = &w.ectl.as<EdgeCtl>()->nchunks;
     d.n = G->n;
     d.round_limit = m + 16;
     if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));

@@ -43,6 +43,7 @@ struct EdgeCtl {
   unsigned long long pushes;   // frontier appends (queue position)
   unsigned long long expanded; // frontier edges expanded
   unsigned long long checked;  // candidate edges examined
+  unsigned long long nchunks;  // shortest duration: out-edge chunks emitted
   unsigned int rounds;
   unsigned int error;
   alignas(128) unsigned int bar_count;
@@ -325,7 +326,7 @@ __global__ void edge_fold_kernel(DevCsr g, int kind, const int32_t* dep, const l
 // Per-query reset of the edge states and the control block.
 __global__ void edge_init_kernel(int kind, uint32_t m, uint32_t* reached, int32_t* dep,
                                  long long* val, uint32_t* stamp, long long* Y, uint32_t n,
-                                 EdgeCtl* ctl) {
+                                 EdgeCtl* ctl, long long* tree = nullptr, uint32_t tree_n = 0) {
   const uint32_t stride = gridDim.x * blockDim.x;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (kind == kEdgeReach) {
@@ -338,11 +339,14 @@ __global__ void edge_init_kernel(int kind, uint32_t m, uint32_t* reached, int32_
     }
     if (Y)
       for (uint32_t i = tid; i < n; i += stride) Y[i] = kInf64;
+    if (tree)
+      for (uint32_t i = tid; i < tree_n; i += stride) tree[i] = kInf64;
   }
   if (tid == 0) {
     ctl->pushes = 0;
     ctl->expanded = 0;
     ctl->checked = 0;
+    ctl->nchunks = 0;
     ctl->rounds = 0;
     ctl->error = 0;
     ctl->bar_count = 0;

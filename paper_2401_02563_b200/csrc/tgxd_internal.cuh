@@ -123,8 +123,8 @@ struct tgxd_graph {
   uint64_t indexed[2] = {0, 0};
   tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence, out_kmax;
   tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax;
-  tgxd::DeviceBuffer in2out;  // In -> Out position of each edge (shortest duration; lazy)
-  bool in2out_ready = false;
+  tgxd::DeviceBuffer out2in;  // Out -> In position of each edge (shortest duration; lazy)
+  bool out2in_ready = false;
   tgxd::DevCsr out, in;
   cudaStream_t stream = nullptr;
   int sm_count = 0;
