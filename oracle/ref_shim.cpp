@@ -23,6 +23,7 @@
 #include "tgx/algorithms.hpp"
 #include "tgx/digest.hpp"
 #include "tgx/engine.hpp"
+#include "tgx/ingest.hpp"
 #include "tgx/parallel.hpp"
 
 namespace {
@@ -129,6 +130,63 @@ int tgxref_enumerate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
         tgx::oracle::enumerate_paths(edges, n, vertex, tgx::QueryWindow{ta, tb},
                                      ordering_of(ordering), pm);
     std::memcpy(out, r.values.data(), r.values.size() * sizeof(std::int64_t));
+  });
+}
+
+// Edge-list IO (ingest.hpp): load into caller arrays of capacity `cap`
+// (m and n_v are always reported; arrays are filled only when m <= cap).
+int tgxref_load_edge_list(const char* path, int map_ids, std::uint64_t seed, std::uint64_t dmax,
+                          std::uint64_t cap, std::uint64_t* m, std::uint32_t* n_v,
+                          std::uint32_t* src, std::uint32_t* dst, std::uint64_t* start,
+                          std::uint64_t* end, double* weight) {
+  return guarded([&] {
+    tgx::LoadOptions opt;
+    opt.map_ids = map_ids != 0;
+    opt.seed = seed;
+    opt.end_sample_max = dmax;
+    const tgx::LoadResult r = tgx::load_edge_list(path, opt);
+    *m = r.edges.size();
+    *n_v = r.meta.n_v;
+    if (r.edges.size() > cap) return;
+    for (std::size_t i = 0; i < r.edges.size(); ++i) {
+      src[i] = r.edges[i].source;
+      dst[i] = r.edges[i].destination;
+      start[i] = r.edges[i].start;
+      end[i] = r.edges[i].end;
+      weight[i] = r.edges[i].weight;
+    }
+  });
+}
+
+int tgxref_write_edge_list(const char* path, std::uint64_t m, const std::uint32_t* src,
+                           const std::uint32_t* dst, const std::uint64_t* start,
+                           const std::uint64_t* end, const double* weight) {
+  return guarded([&] {
+    std::vector<tgx::TemporalEdge> e(m);
+    for (std::uint64_t i = 0; i < m; ++i) e[i] = {src[i], dst[i], start[i], end[i], weight[i]};
+    tgx::write_edge_list(path, e);
+  });
+}
+
+int tgxref_sample_end_times(std::uint64_t m, const std::uint64_t* start, std::uint64_t seed,
+                            std::uint64_t dmax, std::uint64_t* end) {
+  return guarded([&] {
+    std::vector<tgx::TemporalEdge> e(m);
+    for (std::uint64_t i = 0; i < m; ++i) e[i] = {0, 0, start[i], start[i], 1.0};
+    tgx::sample_end_times(e, seed, dmax);
+    for (std::uint64_t i = 0; i < m; ++i) end[i] = e[i].end;
+  });
+}
+
+int tgxref_window_for_recent_fraction(std::uint64_t m, const std::uint64_t* start,
+                                      const std::uint64_t* end, double fraction,
+                                      std::uint64_t* ta, std::uint64_t* tb) {
+  return guarded([&] {
+    std::vector<tgx::TemporalEdge> e(m);
+    for (std::uint64_t i = 0; i < m; ++i) e[i] = {0, 0, start[i], end[i], 1.0};
+    const tgx::QueryWindow w = tgx::window_for_recent_fraction(e, fraction);
+    *ta = w.t_a;
+    *tb = w.t_b;
   });
 }
 

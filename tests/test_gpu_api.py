@@ -151,3 +151,18 @@ def test_cpp_shim_runs():
     run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
     assert "shim ok" in run.stdout
+
+
+def test_edge_list_file_to_device_graph(tmp_path):
+    """ingest.cpp's on-disk format (edgelist.py) feeding the device build."""
+    from paper_2401_02563_b200 import edgelist as EL
+    rng = np.random.default_rng(11)
+    E, n = S.rand_instance(rng, max_v=50, max_e=400, t_range=300, d_max=20)
+    p = str(tmp_path / "g.txt.gz")
+    EL.write_edge_list(p, *E)
+    L = EL.load_edge_list(p)
+    g = T.TemporalGraph.build(L.edges, max(L.n_vertices, n))
+    o = Oracle(E, max(L.n_vertices, n))
+    for v in range(0, min(n, 10)):
+        assert np.array_equal(T.earliest_arrival(g, v, T.QueryWindow(0, 400)).values,
+                              o.query("earliest_arrival", v, 0, 400))
