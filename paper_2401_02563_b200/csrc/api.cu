@@ -699,6 +699,10 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     if (want && ensure_async(G, P.Q, false) == TGXD_OK) a.handoff_f = want;
   }
   w.last_handoff = a.handoff_f != 0;
+  {
+    const char* hg = getenv("TGXD_HANDOFF_GROWTH");
+    a.handoff_growth = hg ? (unsigned)std::max(1, atoi(hg)) : 8u;
+  }
   a.rg = P.kind == TGXD_LATEST_DEPARTURE ? G->out : G->in;
   a.fastest = fast ? 1 : 0;
   a.n_cand = ncand;

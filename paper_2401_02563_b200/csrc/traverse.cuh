@@ -94,6 +94,7 @@ struct TravArgs {
   unsigned long long push_w;   // AUTO: rounds relaxing more edges do not push
   unsigned long long pull_f;   // AUTO: a frontier at least this big is pulled
   unsigned long long handoff_f; // AUTO: a shrinking frontier this small goes to the async engine
+  unsigned int handoff_growth;  // ... or one growing by less than this factor per round
   // fastest sweep (Q == 1)
   int fastest;
   uint32_t n_cand;
@@ -1271,8 +1272,10 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       // barrier-free engine (async.cuh) finishes the query from this queue
       // and these labels / expansion bounds — the same fixpoint, without a
       // ~10 us latency floor per round.
-      if (!xcnt && !st.dense && !a.fastest && F <= a.handoff_f && F < st.last_f &&
-          st.rounds >= 2) {
+      // (past its peak, or growing by less than handoff_growth per round: a
+      // frontier that stays small for many rounds is latency-bound in rounds)
+      if (!xcnt && !st.dense && !a.fastest && F <= a.handoff_f && st.rounds >= 2 &&
+          F < (unsigned long long)st.last_f * a.handoff_growth) {
         if (tr) {
           ctl->handoff_n = F;
           ctl->handoff_flip = st.flip;
