@@ -788,25 +788,6 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     st->total_ms = total_ms;
     return TGXD_OK;
   }
-#ifdef TGXD_CHAIN_PROBE
-  {
-    unsigned long long pr[256][12];
-    unsigned int np = 0;
-    cudaStreamSynchronize(G->stream);
-    cudaMemcpyFromSymbol(pr, g_probe, sizeof pr);
-    cudaMemcpyFromSymbol(&np, g_probe_n, sizeof np);
-    for (unsigned i = 0; i < np && i < 256; ++i) {
-      fprintf(stderr, "probe %u:", i);
-      for (int k = 1; k <= 10; ++k)
-        fprintf(stderr, " %lld", pr[i][k] ? (long long)(pr[i][k] - pr[i][0]) : -1ll);
-      fprintf(stderr, " seg %llu cnt %llu\n", pr[i][11] >> 32, pr[i][11] & 0xffffffffull);
-    }
-    fprintf(stderr, "chase cycles: key %llu X %llu off %llu off(hot) %llu\n", pr[255][0], pr[255][1], pr[255][2], pr[255][3]);
-    unsigned int z = 0;
-    cudaMemcpyToSymbol(g_probe_n, &z, sizeof z);
-    cudaMemset(pr, 0, 0);
-  }
-#endif
   if (G->ws.last_async) {
     AsyncCtl c;
     TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.actl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));

@@ -427,16 +427,6 @@ __device__ __forceinline__ uint32_t lane_lower_bound(const DevCsr& g, uint32_t l
   return line_count(g.key, lo, hi, x);
 }
 
-#ifdef TGXD_CHAIN_PROBE
-// Debug: cycle stamps of block 0 / warp 0 / lane 0 along one expansion chain.
-__device__ unsigned long long g_probe[256][12];
-__device__ unsigned int g_probe_n;
-__shared__ unsigned int s_probe_slot;
-#define PROBE_ON (blockIdx.x == 0 && threadIdx.x == 0)
-#define PROBE(slot, k) do { if (PROBE_ON && s_probe_slot < 256) g_probe[s_probe_slot][k] = clock64(); } while (0)
-#else
-#define PROBE(slot, k) do { } while (0)
-#endif
 
 struct ExpandBufs {
   WarpList sm, ch;
@@ -469,10 +459,6 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
       uint32_t pos = kNoPos;
       if (lb < hik) {
         // (s, t, km: segment bounds and last key, loaded with the label)
-#ifdef TGXD_CHAIN_PROBE
-        if (PROBE_ON && (s ^ t ^ (uint32_t)km) == 0x12345678u) asm volatile("trap;");
-        PROBE(g_probe_n, 3);
-#endif
         if (t > s && km >= lb) {
           act = true;
           const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
@@ -485,17 +471,8 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
           } else {
             p1 = km < hik ? t : lane_lower_bound(a.g, s, t, hik, fence);
           }
-#ifdef TGXD_CHAIN_PROBE
-          if (PROBE_ON && p1 == 0xfffffff0u) asm volatile("trap;");
-          PROBE(g_probe_n, 4);
-#endif
           p0 = p1 > s ? lane_lower_bound(a.g, s, p1, lb, fence) : s;
           pos = p0;
-#ifdef TGXD_CHAIN_PROBE
-          if (PROBE_ON && p0 == 0xfffffff0u) asm volatile("trap;");
-          PROBE(g_probe_n, 5);
-          if (PROBE_ON && s_probe_slot < 256) g_probe[s_probe_slot][11] = (unsigned long long)(p1 - s) << 32 | (p1 - p0);
-#endif
         }
       }
       a.EP[item] = make_int2(lb, (int32_t)pos);
@@ -566,26 +543,6 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
   const uint32_t total = fin ? F : a.Q * a.n;
   ExpandBufs eb{{ebuf, 0}, {ebuf + kListCap, 0}, cstart, sstart};
   unsigned long long work = 0;
-#ifdef TGXD_CHAIN_PROBE
-  const bool probing = fin && nblk == 1 && bid == 0;  // local rounds only
-  if (probing && PROBE_ON && g_probe_n == 0) {
-    // dependent-load latency in situ: 32 random keys, 32 random labels, 32 random offsets
-    uint32_t idx = 12345;
-    long long t0 = clock64();
-    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + (uint32_t)__ldg(a.g.key + idx % a.g.m)) ;
-    long long t1 = clock64();
-    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + (uint32_t)ld_state(a.X + idx % a.n, pol_keep));
-    long long t2 = clock64();
-    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + __ldg(a.g.off + idx % a.n));
-    long long t3 = clock64();
-    for (int k = 0; k < 32; ++k) idx = (idx * 2654435761u + __ldg(a.g.off + (idx % 1024)));
-    long long t4 = clock64();
-    g_probe[255][0] = (t1 - t0) / 32; g_probe[255][1] = (t2 - t1) / 32; g_probe[255][2] = (t3 - t2) / 32;
-    g_probe[255][3] = (t4 - t3) / 32; g_probe[255][4] = idx;
-  }
-  if (PROBE_ON) s_probe_slot = g_probe_n;
-  if (probing) PROBE(g_probe_n, 0);
-#endif
   for (uint32_t base = gw * 32; base < total; base += nw * 32) {
     const uint32_t i = base + lane;
     bool valid = i < total;
@@ -596,10 +553,6 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
     int32_t km0 = INT32_MIN;
     if (valid) {
       if (fin) item = __ldcg(fin + i);
-#ifdef TGXD_CHAIN_PROBE
-      if (PROBE_ON && item == 0xfffffff0u) asm volatile("trap;");
-      if (probing) PROBE(g_probe_n, 1);
-#endif
       x = ld_state(a.X + item, pol_keep);
       ep = __ldcg(a.EP + item);
       // the segment's bounds and last key do not depend on the label: issue
@@ -609,25 +562,12 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
       t0 = __ldg(a.g.off + v + 1);
       km0 = __ldg(a.g.kmax + v);
       valid = x != kInf;
-#ifdef TGXD_CHAIN_PROBE
-      if (PROBE_ON && ep.y == 0x7ffffff0) asm volatile("trap;");
-      if (probing) PROBE(g_probe_n, 2);
-#endif
     }
     expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix);
-#ifdef TGXD_CHAIN_PROBE
-    if (probing) PROBE(g_probe_n, 6);
-#endif
   }
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
-#ifdef TGXD_CHAIN_PROBE
-  if (probing) PROBE(g_probe_n, 7);
-#endif
   flush_work(a.ctl, work);
-#ifdef TGXD_CHAIN_PROBE
-  if (probing) PROBE(g_probe_n, 8);
-#endif
 }
 
 // Phase B: relax the round's chunks and small ranges (plus, for a fastest
@@ -1186,9 +1126,6 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
       const unsigned long long c_end = block_read(&ctl->chunks);
       const unsigned long long s_end = block_read(&ctl->smalls);
       const unsigned long long e_end = block_read(&ctl->edges);
-#ifdef TGXD_CHAIN_PROBE
-      PROBE(g_probe_n, 9);
-#endif
       if (tr) {
         trace_round(a, st.rounds, 1, gtimer());
         trace_round(a, st.rounds, 4, c_end - st.c_cur);
@@ -1199,11 +1136,6 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
         return;
       }
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, 0, 1, wbuf);
-#ifdef TGXD_CHAIN_PROBE
-      PROBE(g_probe_n, 10);
-      __syncthreads();
-      if (PROBE_ON) ++g_probe_n;
-#endif
       st.c_cur = c_end;
       st.s_cur = s_end;
       st.e_cur = e_end;
