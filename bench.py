@@ -285,7 +285,8 @@ def run_ours(args):
                    "parallelism": f"replicas x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "traverse_kernel", "kernel_ms": kernel_ms,
+                     "kernel": "traverse_kernel (+ async_kernel tail)", "kernel_ms": kernel_ms,
+                     "timed": "CUDA events on the graph stream around the traversal kernels",
                      "algorithmic_bytes": b_alg, "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
                 "host_buffer": "pinned" if out.ctypes.data == pinned_ptr else "pageable",
