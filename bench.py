@@ -248,11 +248,11 @@ def run_ours(args):
     # the caller's result buffer is pinned host memory (page-locked: the D2H of
     # the 33.5 MB int64 vector runs at PCIe speed instead of through staging)
     pinned_ptr = None
-    try:
+    if os.environ.get("BENCH_PINNED_OUT"):
         pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
         out = pinned.numpy()
         pinned_ptr = out.ctypes.data
-    except Exception:
+    else:  # an ordinary (pageable) result array, as a reference caller has
         out = np.empty(n, np.int64)
     import ctypes
     for _ in range(args.warmup):
@@ -290,7 +290,9 @@ def run_ours(args):
                      "algorithmic_bytes": b_alg, "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
                 "host_buffer": "pinned" if out.ctypes.data == pinned_ptr else "pageable",
-                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3},
+                # the library moves int32 labels over PCIe in chunks and widens
+                # them into the caller's int64 array on the host meanwhile
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_s * 1e3},
         # per step: init_kernel, seed_kernel, traverse_kernel, async_kernel (the
         # tail continuation, exits at once when the rounds finished the query),
         # convert_kernel

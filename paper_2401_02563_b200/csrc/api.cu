@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -894,18 +895,83 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   if (rc) return rc;
   Workspace& w = G->ws;
   const uint64_t slots = (uint64_t)P.Q * G->n;
+  // Large int64 results for the host travel as int32 (every label but the
+  // root's fits; the root's exact value is written on the host) in chunks,
+  // widened by the handle's host threads while later chunks are still
+  // crossing PCIe: half the bytes on the link, the widening hidden behind it.
+  const bool staged = !out_on_device && width == 8 && slots >= (1u << 20) &&
+                      kind != TGXD_SHORTEST_DURATION;
   void* dout = out;
   if (!out_on_device) {
     if (!dalloc<char>(w.timing_out, slots * width))
       return fail(TGXD_ERR_CUDA, "device allocation failed (output staging)");
     dout = w.timing_out.p;
   }
+  if (staged && G->pinned_n < slots) {
+    if (G->pinned) cudaFreeHost(G->pinned);
+    G->pinned = nullptr;
+    G->pinned_n = 0;
+    TGXD_CUDA(cudaHostAlloc(&G->pinned, slots * 4, cudaHostAllocDefault));
+    G->pinned_n = slots;
+  }
+  static const int kChunks = [] {
+    const char* e = getenv("TGXD_HOST_CHUNKS");
+    return e ? std::max(1, std::min(16, atoi(e))) : 8;
+  }();
+  if (staged && !G->chunk_ev[kChunks - 1])
+    for (int c = 0; c < kChunks; ++c)
+      if (!G->chunk_ev[c])
+      TGXD_CUDA(cudaEventCreateWithFlags(&G->chunk_ev[c], cudaEventDisableTiming));
   TGXD_CUDA(cudaEventRecord(w.ev[2], G->stream));
-  rc = launch(G, P, mode, dout, width, w.ev[0], w.ev[1]);
+  rc = launch(G, P, mode, dout, staged ? 4 : width, w.ev[0], w.ev[1]);
   if (rc) return rc;
-  if (!out_on_device)
+  const uint64_t chunk = (slots + kChunks - 1) / kChunks;
+  if (staged) {
+    for (int c = 0; c < kChunks; ++c) {
+      const uint64_t lo = std::min<uint64_t>(slots, c * chunk);
+      const uint64_t len = std::min<uint64_t>(slots, lo + chunk) - lo;
+      if (len)
+        TGXD_CUDA(cudaMemcpyAsync(G->pinned + lo, static_cast<int32_t*>(dout) + lo, len * 4,
+                                  cudaMemcpyDeviceToHost, G->stream));
+      TGXD_CUDA(cudaEventRecord(G->chunk_ev[c], G->stream));
+    }
+  } else if (!out_on_device) {
     TGXD_CUDA(cudaMemcpyAsync(out, dout, slots * width, cudaMemcpyDeviceToHost, G->stream));
+  }
   TGXD_CUDA(cudaEventRecord(w.ev[3], G->stream));
+  if (staged) {
+    if (G->pool.size() == 0)
+      G->pool.start([] {
+        const char* e = getenv("TGXD_HOST_THREADS");
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        return e ? std::max(1, atoi(e)) : (int)std::min(8u, hw);
+      }());
+    const int T = G->pool.size();
+    int64_t* o64 = static_cast<int64_t*>(out);
+    const int32_t* src = G->pinned;
+    std::atomic<int> bad{0};
+    G->pool.run([&](int wi) {
+      for (int c = 0; c < kChunks; ++c) {
+        const uint64_t lo = std::min<uint64_t>(slots, c * chunk);
+        const uint64_t hi = std::min<uint64_t>(slots, lo + chunk);
+        const uint64_t per = (hi - lo + T - 1) / T;
+        const uint64_t a = std::min(hi, lo + wi * per), b = std::min(hi, a + per);
+        if (cudaEventSynchronize(G->chunk_ev[c]) != cudaSuccess) {
+          bad = 1;
+          return;
+        }
+        for (uint64_t i = a; i < b; ++i) {
+          const int32_t v = src[i];
+          o64[i] = v == INT32_MAX   ? INT64_MAX
+                   : v == INT32_MIN ? INT64_MIN
+                                    : (int64_t)v;
+        }
+      }
+    });
+    if (bad) return fail(TGXD_ERR_CUDA, "result copy failed");
+    for (uint32_t q = 0; q < P.Q; ++q)  // the roots' exact values (t_a, t_b, 0)
+      o64[(uint64_t)q * G->n + P.seeds[q].root] = P.seeds[q].value;
+  }
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
   float km = 0, tm = 0;
   TGXD_CUDA(cudaEventElapsedTime(&km, w.ev[0], w.ev[1]));
@@ -1174,6 +1240,9 @@ void tgxd_graph_destroy(tgxd_graph* g) {
   for (auto& e : g->ws.ev)
     if (e) cudaEventDestroy(e);
   if (g->ws.trace_host) cudaFreeHost(g->ws.trace_host);
+  if (g->pinned) cudaFreeHost(g->pinned);
+  for (auto& e : g->chunk_ev)
+    if (e) cudaEventDestroy(e);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }

@@ -4,7 +4,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <vector>
 #include <string>
 #include <vector>
 
@@ -113,6 +117,55 @@ struct Control {
 
 }  // namespace tgxd
 
+// Host-side widening pool: a few threads per graph handle that turn the
+// int32 result chunks arriving in pinned staging into the caller's int64
+// PathResult values while later chunks are still on the PCIe link.
+struct WidenPool {
+  std::vector<std::thread> threads;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::function<void(int)> job;  // called with the worker index
+  uint64_t generation = 0;
+  int pending = 0;
+  bool stop = false;
+  int size() const { return (int)threads.size(); }
+  void start(int n) {
+    for (int i = 0; i < n; ++i)
+      threads.emplace_back([this, i] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::function<void(int)> f;
+          {
+            std::unique_lock<std::mutex> l(mu);
+            cv.wait(l, [&] { return stop || generation != seen; });
+            if (stop) return;
+            seen = generation;
+            f = job;
+          }
+          f(i);
+          std::lock_guard<std::mutex> l(mu);
+          if (--pending == 0) done_cv.notify_all();
+        }
+      });
+  }
+  void run(std::function<void(int)> f) {  // blocks until every worker ran f
+    std::unique_lock<std::mutex> l(mu);
+    job = std::move(f);
+    pending = (int)threads.size();
+    ++generation;
+    cv.notify_all();
+    done_cv.wait(l, [&] { return pending == 0; });
+  }
+  ~WidenPool() {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : threads) t.join();
+  }
+};
+
 struct tgxd_graph {
   int device = 0;
   uint32_t n = 0;
@@ -134,4 +187,9 @@ struct tgxd_graph {
   int coop_blocks_sd = 0;
   std::mutex mu;
   tgxd::Workspace ws;
+  // pipelined host results (int32 chunks -> int64 on the host)
+  int32_t* pinned = nullptr;  // cudaHostAlloc'd staging
+  size_t pinned_n = 0;
+  cudaEvent_t chunk_ev[16] = {};
+  WidenPool pool;
 };
