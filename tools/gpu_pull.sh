@@ -1,3 +1,3 @@
-mkdir -p gpurun_out/p36
-for c in 4 8 16; do for t in 4 8 16; do TGXD_HOST_CHUNKS=$c TGXD_HOST_THREADS=$t timeout 600 python bench.py --steps 50 --warmup 3 --no-cpu-baseline > gpurun_out/p36/c${c}_t$t.json 2>/dev/null; echo "c$c t$t $(python -c "import json; d=json.load(open('gpurun_out/p36/c${c}_t$t.json')); print(d['e2e']['ms_per_step'], d['e2e']['host_buffer'])")"; done; done
-BENCH_PINNED_OUT=1 timeout 600 python bench.py --steps 50 --warmup 3 --no-cpu-baseline > gpurun_out/p36/pinned.json 2>/dev/null; echo "pinned $(python -c "import json; d=json.load(open('gpurun_out/p36/pinned.json')); print(d['e2e']['ms_per_step'], d['e2e']['host_buffer'])")"
+mkdir -p gpurun_out/p38
+for v in default l8 l24 l32 b4l16; do L=build/variants/lib_$v.so; [ $v = default ] && L=paper_2401_02563_b200/libtgxd.so
+TGXD_LIB=$L timeout 600 python tools/diag.py --mode 0 --trace --reps 5 > gpurun_out/p38/$v.log 2>&1; done
