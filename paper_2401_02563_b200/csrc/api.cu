@@ -684,11 +684,12 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   // (measured on config 2: the queue-driven expand is cheaper below that).
   a.dense_f = std::max<uint64_t>(1024, slots / 2);
   a.push_w = std::max<uint64_t>(4096, slots * 4);
-  // a frontier holding half the slots is pulled (direction switch; measured on
-  // config 2: below that the pull's sweep over every slot costs more than it saves)
+  // a frontier holding a quarter of the slots is pulled (direction switch;
+  // measured on configs 2 and 4: below that the pull's sweep over every slot
+  // costs more than it saves)
   // (TGXD_PULL_DIV overrides the share's divisor; 0 turns AUTO's pulls off)
   const char* pf = getenv("TGXD_PULL_DIV");
-  const int pdiv = pf ? atoi(pf) : 2;
+  const int pdiv = pf ? atoi(pf) : 4;
   a.pull_f = pdiv <= 0 ? ~0ull : std::max<uint64_t>(1024, slots / pdiv);
   if (const char* pfx = getenv("TGXD_PULL_F")) a.pull_f = strtoull(pfx, nullptr, 10);  // tests
   // AUTO: a frontier past its peak and below 1/16 of the slots is finished by

@@ -1,3 +1,2 @@
-mkdir -p gpurun_out/p38
-for v in default l8 l24 l32 b4l16; do L=build/variants/lib_$v.so; [ $v = default ] && L=paper_2401_02563_b200/libtgxd.so
-TGXD_LIB=$L timeout 600 python tools/diag.py --mode 0 --trace --reps 5 > gpurun_out/p38/$v.log 2>&1; done
+mkdir -p gpurun_out/p39
+for d in 2 4 8; do TGXD_PULL_DIV=$d timeout 1500 python tools/bench_configs.py --no-ref --steps 5 --configs c1,c2,c4 > gpurun_out/p39/d$d.jsonl 2>/dev/null; done
