@@ -753,7 +753,15 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       h.hfa = a.fa;
       h.hfb = a.fb;
       void* hargs[] = {&h};
-      TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(G->coop_blocks_async),
+      // the tail runs on fewer CTAs: its frontier is small, and every idle
+      // warp polls a queue ticket (TGXD_TAIL_BLOCKS_PER_SM overrides)
+      // (measured on config 2: 3 CTAs per SM 0.91 ms, all 4 1.02 ms, 1 1.01 ms)
+      static const int tail_per_sm = [] {
+        const char* e = getenv("TGXD_TAIL_BLOCKS_PER_SM");
+        return e ? std::max(1, atoi(e)) : 3;
+      }();
+      const int tail_blocks = std::min(G->coop_blocks_async, tail_per_sm * G->sm_count);
+      TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(tail_blocks),
                                             dim3(kThreads), hargs, 0, s));
     }
   } else {
