@@ -495,8 +495,15 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
     void* args[] = {&a};
-    TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel,
-                                          dim3(G->coop_blocks_async), dim3(kThreads), args, 0, s));
+    // 3 CTAs per SM: every idle warp polls a queue ticket, and with all 4
+    // resident the polls slow the working warps (config 2: 1.7 vs 3.4 ms)
+    static const int per_sm = [] {
+      const char* e = getenv("TGXD_ASYNC_BLOCKS_PER_SM");
+      return e ? std::max(1, atoi(e)) : 3;
+    }();
+    const int blocks = std::min(G->coop_blocks_async, per_sm * G->sm_count);
+    TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(blocks), dim3(kThreads),
+                                          args, 0, s));
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   w.last_async = true;
