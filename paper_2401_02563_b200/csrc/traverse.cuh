@@ -961,6 +961,12 @@ __device__ TGXD_PHASE void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned
   push_drain(pb, a.ctl, rx.pstart, rx.fout);
 }
 
+#ifndef TGXD_BAR_MAX_NS
+#define TGXD_BAR_MAX_NS 256
+#endif
+#ifndef TGXD_BAR_LOCAL_NS
+#define TGXD_BAR_LOCAL_NS 2048
+#endif
 // Grid barrier for the persistent round kernel. One arrival atomic per
 // block; waiters poll the generation word with exponential __nanosleep
 // backoff, so ~600 blocks idling through a CTA-local round (or a slow phase)
@@ -972,7 +978,8 @@ struct GridBarrier {
   unsigned int* gen;
   unsigned int nblocks;
   unsigned int phase;  // generations passed (identical in every block)
-  __device__ __forceinline__ void sync() {
+  // max_ns: backoff cap of the waiters (longer while one CTA works alone)
+  __device__ __forceinline__ void sync(unsigned int max_ns = TGXD_BAR_MAX_NS) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned int g = phase;
@@ -982,16 +989,13 @@ struct GridBarrier {
         __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
       } else {
-#ifndef TGXD_BAR_MAX_NS
-#define TGXD_BAR_MAX_NS 256
-#endif
         unsigned int ns = 32;
         for (;;) {
           unsigned int cur;
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
           if (cur != g) break;
           __nanosleep(ns);
-          if (ns < TGXD_BAR_MAX_NS) ns <<= 1;
+          if (ns < max_ns) ns <<= 1;
         }
       }
       __threadfence();
@@ -1225,7 +1229,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
           if (threadIdx.x == 0) save_state(ctl, st);
         }
         xcnt = 0;
-        grid.sync();
+        grid.sync(TGXD_BAR_LOCAL_NS);  // the other CTAs idle through block 0's rounds
         load_state(ctl, st);
         if (!st.pending) continue;
         // the grid relaxes what the CTA expanded
