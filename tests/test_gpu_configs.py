@@ -129,3 +129,18 @@ def test_tail_handoff_parity(monkeypatch, handoff):
                 for _ in range(3):
                     got = FN[kind](g, q.vertex, q.window).values
                     assert np.array_equal(got, want), (name, kind, handoff)
+
+
+@pytest.mark.slow
+def test_full_c3_queries_bit_exact():
+    """Config 3 at full size: narrow-window EA and LD queries (index cutoff
+    256, so hubs go through the selective index) label for label."""
+    wl, g, qs = setup("c3", 0)
+    o = Oracle(T.generate_edges(wl.gen), wl.gen.n_vertices)
+    for kind in ("earliest_arrival", "latest_departure"):
+        sub = [q for q in qs if q.kind == kind][:4]
+        batch = T.query_batch(g, kind, [q.vertex for q in sub], [q.window for q in sub])
+        for i, q in enumerate(sub):
+            want = o.query(kind, q.vertex, q.window.t_a, q.window.t_b)
+            assert np.array_equal(FN[kind](g, q.vertex, q.window).values, want), (kind, i)
+            assert np.array_equal(batch[i], want), (kind, i)
