@@ -915,8 +915,9 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   // root's fits; the root's exact value is written on the host) in chunks,
   // widened by the handle's host threads while later chunks are still
   // crossing PCIe: half the bytes on the link, the widening hidden behind it.
+  // (up to 2^26 slots: the pinned staging stays <= 256 MB per handle)
   const bool staged = !out_on_device && width == 8 && slots >= (1u << 20) &&
-                      kind != TGXD_SHORTEST_DURATION;
+                      slots <= (1ull << 26) && kind != TGXD_SHORTEST_DURATION;
   void* dout = out;
   if (!out_on_device) {
     if (!dalloc<char>(w.timing_out, slots * width))
