@@ -550,6 +550,14 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
       w.eval.as<long long>(), w.estamp.as<uint32_t>(),
       kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n, w.ectl.as<EdgeCtl>(),
       sd ? w.esm.as<long long>() : nullptr, sd ? G->in.m : 0u);
+#ifdef TGXD_CHECK
+  {
+    const unsigned long long caps[2] = {qcap, (uint64_t)G->n + (uint64_t)(G->m / kChunk + 1)};
+    const unsigned int zero = 0;
+    TGXD_CUDA(cudaMemcpyToSymbolAsync(g_cap, caps, sizeof caps, 0, cudaMemcpyHostToDevice, s));
+    TGXD_CUDA(cudaMemcpyToSymbolAsync(g_check_fail, &zero, 4, 0, cudaMemcpyHostToDevice, s));
+  }
+#endif
   if (sd) {
     SdArgs d;
     d.out = G->out;
@@ -669,6 +677,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     return TGXD_OK;
   }
   w.last_async = false;
+#ifdef TGXD_CHECK
+  {
+    const unsigned long long caps[2] = {slots, slots + (uint64_t)P.Q * (G->m / kChunk + 1)};
+    const unsigned int zero = 0;
+    TGXD_CUDA(cudaMemcpyToSymbolAsync(g_cap, caps, sizeof caps, 0, cudaMemcpyHostToDevice, s));
+    TGXD_CUDA(cudaMemcpyToSymbolAsync(g_check_fail, &zero, 4, 0, cudaMemcpyHostToDevice, s));
+  }
+#endif
   TravArgs a;
   a.g = g;
   a.qp = w.params.as<QueryParam>();
@@ -790,6 +806,15 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
 }
 
 static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float total_ms) {
+#ifdef TGXD_CHECK
+  {
+    unsigned int bad = 0;
+    TGXD_CUDA(cudaMemcpyFromSymbol(&bad, g_check_fail, 4));
+    if (bad)
+      return fail(TGXD_ERR_CUDA, bad == 1 ? "check: frontier queue overflow"
+                                          : "check: work list overflow");
+  }
+#endif
   if (G->ws.last_edge) {
     EdgeCtl c;
     TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ectl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));

@@ -113,7 +113,7 @@ __device__ __forceinline__ void edge_push(uint32_t* buf, uint32_t& nb, bool p, u
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&ctl->pushes, 32ull);
     base = __shfl_sync(0xffffffffu, base, 0);
-    fout[base - pstart + lane] = buf[lane];
+    if (TGXD_IN_CAP(base - pstart + lane, 0)) fout[base - pstart + lane] = buf[lane];
     __syncwarp();
     const uint32_t t = buf[32 + lane];
     __syncwarp();
@@ -131,7 +131,7 @@ __device__ __forceinline__ void edge_push_drain(uint32_t* buf, uint32_t& nb, Edg
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(&ctl->pushes, (unsigned long long)nb);
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (lane < nb) fout[base - pstart + lane] = buf[lane];
+  if (lane < nb && TGXD_IN_CAP(base - pstart + lane, 0)) fout[base - pstart + lane] = buf[lane];
   nb = 0;
   __syncwarp();
 }

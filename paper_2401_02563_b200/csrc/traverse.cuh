@@ -157,6 +157,18 @@ __device__ __forceinline__ int32_t ld_state(const int32_t* p, uint64_t pol) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Debug builds (-DTGXD_CHECK): every queue / work-list store is checked
+// against its allocation; a violation is recorded (and the store skipped)
+// and reported by the host as an internal error.
+#ifdef TGXD_CHECK
+__device__ unsigned long long g_cap[2];  // [0] frontier queue entries, [1] work-list entries
+__device__ unsigned int g_check_fail;
+#define TGXD_IN_CAP(idx, which) \
+  ((unsigned long long)(idx) < g_cap[which] || (atomicExch(&g_check_fail, 1u + (which)), false))
+#else
+#define TGXD_IN_CAP(idx, which) true
+#endif
+
 // The bound a label implies for its vertex's next expansion (min_start /
 // max_end hooks, path_algorithms.cpp:287-291, :337-342).
 __device__ __forceinline__ int32_t bound_of(int32_t x, int strict) {
@@ -179,7 +191,7 @@ __device__ __forceinline__ void push_flush32(PushBuf& pb, Control* ctl,
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(&ctl->pushes, 32ull);
   base = __shfl_sync(0xffffffffu, base, 0);
-  fout[base - pstart + lane] = v;
+  if (TGXD_IN_CAP(base - pstart + lane, 0)) fout[base - pstart + lane] = v;
   __syncwarp();
   if (lane + 32 < pb.n) pb.buf[lane] = tail;
   pb.n -= 32;
@@ -194,7 +206,7 @@ __device__ __forceinline__ void push_drain(PushBuf& pb, Control* ctl, unsigned l
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(&ctl->pushes, (unsigned long long)pb.n);
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (lane < pb.n) fout[base - pstart + lane] = pb.buf[lane];
+  if (lane < pb.n && TGXD_IN_CAP(base - pstart + lane, 0)) fout[base - pstart + lane] = pb.buf[lane];
   pb.n = 0;
   __syncwarp();
 }
@@ -327,7 +339,8 @@ __device__ __forceinline__ void list_flush(WarpList& wl, uint32_t count, unsigne
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(ctr, (unsigned long long)count);
   base = __shfl_sync(0xffffffffu, base, 0);
-  for (uint32_t k = lane; k < count; k += 32) list[base - start + k] = wl.buf[k];
+  for (uint32_t k = lane; k < count; k += 32)
+    if (TGXD_IN_CAP(base - start + k, 1)) list[base - start + k] = wl.buf[k];
   const uint32_t rem = wl.n - count;  // < 32
   const uint2 t = lane < rem ? wl.buf[count + lane] : make_uint2(0u, 0u);
   __syncwarp();
@@ -510,7 +523,8 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
     base = __shfl_sync(0xffffffffu, base, 0) - eb.cstart;
     for (uint32_t j = lane; j < bn; j += 32) {
       const uint32_t off = j * kChunk;
-      a.chunks[base + j] = make_uint2(B0 + off, (BQ << kChunkLenBits) | min(kChunk, BC - off));
+      if (TGXD_IN_CAP(base + j, 1))
+        a.chunks[base + j] = make_uint2(B0 + off, (BQ << kChunkLenBits) | min(kChunk, BC - off));
     }
   }
 }
