@@ -67,7 +67,9 @@ enum tgxd_mode {
   TGXD_MODE_SPARSE = 1,  /* round-based, queue frontier every round */
   TGXD_MODE_DENSE = 2,   /* round-based, implicit (dense) frontier every round */
   TGXD_MODE_ASYNC = 3,   /* barrier-free work queues (no rounds) */
-  TGXD_MODE_PULL = 4     /* round-based, every round pulled (dense bottom-up) */
+  TGXD_MODE_PULL = 4,    /* round-based, every round pulled (dense bottom-up) */
+  TGXD_MODE_LANES = 5    /* batches of 2..32 EA / LD queries: one warp lane per query,
+                            vertex-major labels (AUTO's choice when they share one source) */
 };
 
 /* Output label width: 8 = int64 exactly as PathResult::values

@@ -61,6 +61,7 @@ class Mode(enum.IntEnum):                # traversal schedule (tgxd_mode)
     DENSE = 2      # rounds, implicit dense frontier
     ASYNC = 3      # barrier-free work queues
     PULL = 4       # rounds, every round pulled (bottom-up)
+    LANES = 5      # batches of 2..32 EA / LD queries, one warp lane per query
 
 
 class OutOfRange(IndexError):

@@ -22,6 +22,7 @@
 #include "async.cuh"
 #include "edges.cuh"
 #include "sd.cuh"
+#include "lanes.cuh"
 
 namespace tgxd {
 
@@ -242,6 +243,9 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
   int per_sm_s = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, sd_kernel, kThreads, 0);
   G->coop_blocks_sd = std::max(1, per_sm_s) * G->sm_count;
+  int per_sm_l = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, lanes_kernel, kThreads, 0);
+  G->coop_blocks_lanes = std::max(1, per_sm_l) * G->sm_count;
   *out = G;
   return TGXD_OK;
 }
@@ -630,6 +634,55 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   return TGXD_OK;
 }
 
+// A batch on the lane-per-query engine (lanes.cuh); params already uploaded.
+static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void* out_dev,
+                        int width, cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  Workspace& w = G->ws;
+  cudaStream_t s = G->stream;
+  const size_t n = G->n;
+  if (!dalloc<int32_t>(w.lxm, n * 32) || !dalloc<int2>(w.leb, n * 32) ||
+      !dalloc<uint32_t>(w.ldirty, n))
+    return fail(TGXD_ERR_CUDA, "device allocation failed (lane-per-query labels)");
+  lanes_init_kernel<<<grid_for(n * 8, G->sm_count), 256, 0, s>>>(
+      w.lxm.as<int32_t>(), w.leb.as<int2>(), w.ldirty.as<uint32_t>(), n);
+  lanes_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, w.lxm.as<int32_t>(),
+                                     w.ldirty.as<uint32_t>(), w.fa.as<uint32_t>(),
+                                     w.ctl.as<Control>());
+  LanesArgs a;
+  a.g = g;
+  a.qp = w.params.as<QueryParam>();
+  a.Q = P.Q;
+  a.n = G->n;
+  a.strict = P.strict;
+  a.cutoff = (uint32_t)std::min<uint64_t>(G->index_cutoff, 0xffffffffULL);
+  a.XM = w.lxm.as<int32_t>();
+  a.EB = w.leb.as<int2>();
+  a.dirty = w.ldirty.as<uint32_t>();
+  a.fa = w.fa.as<uint32_t>();
+  a.fb = w.fb.as<uint32_t>();
+  a.chunks = w.chunks.as<uint2>();
+  a.ctl = w.ctl.as<Control>();
+  // every round lowers some (vertex, query) label
+  a.round_limit = (uint32_t)std::min<uint64_t>(0xfffffff0ULL, (uint64_t)P.Q * G->n + 16);
+  if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
+  void* args[] = {&a};
+  TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)lanes_kernel, dim3(G->coop_blocks_lanes),
+                                        dim3(kThreads), args, 0, s));
+  if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
+  lanes_transpose_kernel<<<std::min<uint64_t>((n + 31) / 32, 8ull * G->sm_count), 256, 0, s>>>(
+      w.lxm.as<int32_t>(), w.X.as<int32_t>(), G->n, P.Q);
+  if (out_dev) convert_for(G, P, out_dev, width);
+  TGXD_CUDA(cudaGetLastError());
+  w.last_edge = false;
+  w.last_async = false;
+  w.last_handoff = false;
+  w.last_kind = P.kind;
+  w.last_q = P.Q;
+  w.last_strict = P.strict;
+  w.last_params = P.qp;
+  return TGXD_OK;
+}
+
 // Enqueues one traversal (init, seeds, the persistent kernel, widening into
 // out_dev). ev_k0/ev_k1 bracket the traversal kernel when non-null.
 static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int width,
@@ -659,6 +712,25 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     TGXD_CUDA(cudaMemcpyAsync(w.cand_cnt.p, P.cand_cnt.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
     TGXD_CUDA(cudaMemcpyAsync(w.cand_key.p, P.cand_key.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
   }
+  // batches of EA / LD queries: one warp lane per query (AUTO's choice)
+  const bool lanes_ok = P.Q >= 2 && P.Q <= 32 && G->n <= kLanesMaxN && !fast && !bfs &&
+                        (P.kind == TGXD_EARLIEST_ARRIVAL || P.kind == TGXD_LATEST_DEPARTURE);
+  if (mode == TGXD_MODE_LANES && !lanes_ok)
+    return fail(TGXD_ERR_UNSUPPORTED,
+                "lane-per-query mode: 2..32 earliest-arrival or latest-departure queries, "
+                "n <= 2^24");
+  // AUTO takes it for window sweeps from one source: their rounds advance
+  // together, so a vertex's ranges for all queries are scanned at once
+  // (config-2 graph, 32 nested / shifted full windows: 9.3 ms vs 25 ms
+  // slot-major). Independent sources reach a vertex in different rounds and
+  // its union range is rescanned per query (32 random sources: 43 vs 36 ms;
+  // config 5: 94 vs 55 ms), so those stay slot-major.
+  bool one_root = true;
+  for (uint32_t q = 1; q < P.Q; ++q) one_root = one_root && P.qp[q].root == P.qp[0].root;
+  if (lanes_ok && (mode == TGXD_MODE_LANES ||
+                   (mode == TGXD_MODE_AUTO && one_root && !getenv("TGXD_NO_LANES"))))
+    return launch_lanes(G, P, g, out_dev, width, ev_k0, ev_k1);
+  if (mode == TGXD_MODE_LANES) mode = TGXD_MODE_AUTO;
   init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
       w.X.as<int32_t>(), w.EP.as<int2>(), fast || bfs ? w.R.as<int32_t>() : nullptr, slots);
   seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,

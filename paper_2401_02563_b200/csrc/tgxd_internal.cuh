@@ -68,6 +68,8 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
   DeviceBuffer X, EP, R, fa, fb, chunks, smalls, ctl, params, seeds;
+  // lane-per-query batches (lanes.cuh): vertex-major labels, ranges, dirty masks
+  DeviceBuffer lxm, leb, ldirty;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
   // asynchronous engine: queued flags, vertex / chunk rings, control block
   DeviceBuffer axq, aunits, actl;
@@ -185,6 +187,7 @@ struct tgxd_graph {
   int coop_blocks_async = 0;
   int coop_blocks_edge = 0;
   int coop_blocks_sd = 0;
+  int coop_blocks_lanes = 0;
   std::mutex mu;
   tgxd::Workspace ws;
   // pipelined host results (int32 chunks -> int64 on the host)
