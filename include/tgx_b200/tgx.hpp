@@ -18,6 +18,7 @@
 // `tgx::` with this header and `tgx_b200::`, and linking libtgxd.so.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <limits>
 #include <memory>
@@ -179,6 +180,75 @@ inline PathResult shortest_duration(const TemporalGraph& g, VertexId source, con
 inline PathResult temporal_bfs(const TemporalGraph& g, VertexId source, const QueryWindow& w,
                                const AlgoOptions& opts = {}) {
   return detail::run(TGXD_TEMPORAL_BFS, g, source, w, opts);
+}
+
+// Selective-index cost model (selective_index.hpp:45-130). The registry is
+// the graph's own (its index cutoff); histograms live on the device.
+enum class AccessMethod { IndexLookup, Scan };
+struct CostModelParams {
+  double c = 1.0;
+  double c_prime = 1.0;
+  double theta_sel = 0.2;
+};
+struct AccessDecision {
+  AccessMethod method = AccessMethod::Scan;
+  double beta_hat = -1.0;
+  double k_hat = -1.0;
+};
+struct CalibrationPoint {
+  std::uint64_t degree = 0;
+  std::uint64_t matches = 0;
+  double index_seconds = 0.0;
+  double scan_seconds = 0.0;
+};
+
+inline AccessDecision choose_access_method(VertexId v, const TemporalGraph& g, Direction d,
+                                           const QueryWindow& w,
+                                           const CostModelParams& params = {}) {
+  std::int32_t m = 1;
+  double beta = -1.0, kh = -1.0;
+  std::uint64_t matches = 0;
+  const std::uint64_t ta = w.t_a, tb = w.t_b;
+  detail::check(tgxd_access_decisions(g.handle(), d == Direction::Out ? 0 : 1, 1, &v, &ta, &tb,
+                                      params.theta_sel, &m, &beta, &kh, &matches));
+  return AccessDecision{m == 0 ? AccessMethod::IndexLookup : AccessMethod::Scan, beta, kh};
+}
+
+inline std::uint64_t count_in_window(const TemporalGraph& g, VertexId v, Direction d,
+                                     const QueryWindow& w) {
+  std::int32_t m = 1;
+  double beta = -1.0, kh = -1.0;
+  std::uint64_t matches = 0;
+  const std::uint64_t ta = w.t_a, tb = w.t_b;
+  detail::check(tgxd_access_decisions(g.handle(), d == Direction::Out ? 0 : 1, 1, &v, &ta, &tb,
+                                      0.2, &m, &beta, &kh, &matches));
+  return matches;
+}
+
+inline CostModelParams fit_cost_constants(const std::vector<CalibrationPoint>& points,
+                                          double theta_sel = 0.2) {
+  std::vector<std::uint64_t> deg, mat;
+  std::vector<double> ix, sc;
+  for (const CalibrationPoint& p : points) {
+    deg.push_back(p.degree);
+    mat.push_back(p.matches);
+    ix.push_back(p.index_seconds);
+    sc.push_back(p.scan_seconds);
+  }
+  CostModelParams out;
+  out.theta_sel = theta_sel;
+  detail::check(tgxd_fit_cost_constants(points.size(), deg.data(), mat.data(), ix.data(),
+                                        sc.data(), &out.c, &out.c_prime));
+  return out;
+}
+
+inline double cost_index_lookup(std::uint64_t degree, double k, double c) {
+  if (degree == 0) throw std::domain_error("cost_index_lookup: degree must be >= 1");
+  return c * (std::log2(static_cast<double>(degree)) + k);
+}
+
+inline double cost_scan(std::uint64_t degree, double c_prime) {
+  return c_prime * static_cast<double>(degree);
 }
 
 template <class T>

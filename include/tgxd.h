@@ -185,6 +185,26 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
 int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds);
 int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds, int with_device);
 
+/* Selective-index cost model (replaces choose_access_method,
+ * selective_index.hpp:63-106 / selective_index.cpp:98-209, and
+ * TemporalCsr::count_in_window, tcsr.hpp:72): for k (vertex, window) pairs of
+ * one direction (0 out, 1 in), the access decision (0 index lookup, 1 scan),
+ * beta_hat and k_hat from the vertex's 100x100 (start, duration) density
+ * histogram (-1 and -1 for vertices below the index cutoff: no histogram),
+ * and the exact number of window-contained edges. Bit-identical to the
+ * reference's doubles. The histograms are built on the device on first use. */
+int tgxd_access_decisions(tgxd_graph* g, int direction, uint32_t k, const uint32_t* vertices,
+                          const uint64_t* t_a, const uint64_t* t_b, double theta_sel,
+                          int32_t* method, double* beta_hat, double* k_hat, uint64_t* matches);
+
+/* fit_cost_constants (selective_index.cpp:211-235): least-squares c (index:
+ * seconds ~ c (log2 degree + matches)) and c' (scan: seconds ~ c' degree)
+ * over k calibration points; INVALID_ARGUMENT for an empty sample or one
+ * without degree >= 1 (TGXD_ERR_WINDOW: the reference throws std::invalid_argument). */
+int tgxd_fit_cost_constants(uint64_t k, const uint64_t* degree, const uint64_t* matches,
+                            const double* index_seconds, const double* scan_seconds,
+                            double* c, double* c_prime);
+
 /* FNV-1a digest of int64 labels (digest.hpp:12-52). */
 uint64_t tgxd_digest(const int64_t* values, uint64_t n);
 

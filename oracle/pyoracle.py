@@ -82,9 +82,12 @@ class Oracle:
                                          b.ctypes.data_as(_u64p), 1 if directed else 0,
                                          ctypes.byref(self._h)))
 
-    def _check(self, rc):
+    @classmethod
+    def _check(cls, rc):
         if rc:
-            raise OracleError(rc, self.lib().tgxo_last_error().decode())
+            lib = cls.lib()
+            lib.tgxo_last_error.restype = ctypes.c_char_p
+            raise OracleError(rc, lib.tgxo_last_error().decode())
 
     def query(self, kind: str, vertex: int, t_a: int, t_b: int, ordering: int = 1) -> np.ndarray:
         out = np.empty(self.n, np.int64)
@@ -101,6 +104,22 @@ class Oracle:
                                          lab.ctypes.data_as(_i64p), ctypes.byref(e),
                                          ctypes.byref(r)))
         return e.value, r.value
+
+    def access_decisions(self, direction: int, cutoff: int, verts, t_a, t_b, theta: float = 0.2):
+        """(method, beta_hat, k_hat, matches) per (vertex, window): selective_index.cpp:98-209."""
+        return _decisions(self.lib().tgxo_access_decisions, self._check,
+                          (self._h, ctypes.c_int(direction), ctypes.c_uint64(cutoff)), verts, t_a, t_b,
+                          theta)
+
+    @classmethod
+    def fit_cost_constants(cls, degree, matches, index_s, scan_s):
+        out = (ctypes.c_double * 2)()
+        deg, mat, ix, sc = _fit_arrays(degree, matches, index_s, scan_s)
+        cls._check(cls.lib().tgxo_fit_cost_constants(
+            ctypes.c_uint64(len(deg)), deg.ctypes.data_as(_u64p), mat.ctypes.data_as(_u64p),
+            ix.ctypes.data_as(_f64p), sc.ctypes.data_as(_f64p), ctypes.byref(out, 0),
+            ctypes.byref(out, 8)))
+        return out[0], out[1]
 
     def close(self):
         if self._h:
@@ -198,6 +217,20 @@ class Reference:
                                               ordering, KIND[kind], out.ctypes.data_as(_i64p)))
         return out
 
+    def access_decisions(self, direction: int, verts, t_a, t_b, theta: float = 0.2):
+        """choose_access_method + count_in_window of the reference (its registry)."""
+        return _decisions(self.lib().tgxref_access_decisions, self._check,
+                          (self._h, ctypes.c_int(direction)), verts, t_a, t_b, theta)
+
+    @classmethod
+    def fit_cost_constants(cls, degree, matches, index_s, scan_s, theta: float = 0.2):
+        out = (ctypes.c_double * 3)()
+        deg, mat, ix, sc = _fit_arrays(degree, matches, index_s, scan_s)
+        cls._check(cls.lib().tgxref_fit_cost_constants(
+            ctypes.c_uint64(len(deg)), deg.ctypes.data_as(_u64p), mat.ctypes.data_as(_u64p),
+            ix.ctypes.data_as(_f64p), sc.ctypes.data_as(_f64p), ctypes.c_double(theta), out))
+        return out[0], out[1]
+
     def close(self):
         if self._h:
             self.lib().tgxref_free(self._h)
@@ -208,3 +241,29 @@ class Reference:
             self.close()
         except Exception:
             pass
+
+
+_f64p = ctypes.POINTER(ctypes.c_double)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+def _decisions(fn, check, head, verts, t_a, t_b, theta):
+    v = np.ascontiguousarray(verts, np.uint32)
+    ta = np.ascontiguousarray(t_a, np.uint64)
+    tb = np.ascontiguousarray(t_b, np.uint64)
+    k = len(v)
+    method = np.empty(k, np.int32)
+    beta = np.empty(k, np.float64)
+    khat = np.empty(k, np.float64)
+    matches = np.empty(k, np.uint64)
+    fn.restype = ctypes.c_int
+    check(fn(*head, ctypes.c_uint64(k), v.ctypes.data_as(_u32p), ta.ctypes.data_as(_u64p),
+             tb.ctypes.data_as(_u64p), ctypes.c_double(theta), method.ctypes.data_as(_i32p),
+             beta.ctypes.data_as(_f64p), khat.ctypes.data_as(_f64p),
+             matches.ctypes.data_as(_u64p)))
+    return method, beta, khat, matches
+
+
+def _fit_arrays(degree, matches, index_s, scan_s):
+    return (np.ascontiguousarray(degree, np.uint64), np.ascontiguousarray(matches, np.uint64),
+            np.ascontiguousarray(index_s, np.float64), np.ascontiguousarray(scan_s, np.float64))

@@ -9,6 +9,9 @@
 //   temporal_bfs                   /root/reference/proj/include/tgx/algorithms.hpp:46-66
 //   oracle::enumerate_paths        /root/reference/proj/tests/support/oracle.hpp:27-29
 //   set_workers / num_workers      /root/reference/proj/include/tgx/parallel.hpp:19-21
+//   choose_access_method / fit_cost_constants / count_in_window
+//                                  /root/reference/proj/include/tgx/selective_index.hpp:63-120,
+//                                  /root/reference/proj/include/tgx/tcsr.hpp:72
 // Exceptions are mapped to integer codes (1 out_of_range, 2 invalid_argument,
 // 3 anything else) and the message is kept for tgxref_last_error().
 
@@ -25,6 +28,7 @@
 #include "tgx/engine.hpp"
 #include "tgx/ingest.hpp"
 #include "tgx/parallel.hpp"
+#include "tgx/selective_index.hpp"
 
 namespace {
 
@@ -194,4 +198,39 @@ std::uint64_t tgxref_digest(const std::int64_t* values, std::uint64_t n) {
   return tgx::digest_of(std::span<const std::int64_t>(values, n));
 }
 
+
+// Selective-index cost model: decision (0 index lookup, 1 scan), beta_hat,
+// k_hat and count_in_window for k (vertex, window) pairs of one direction.
+int tgxref_access_decisions(void* gp, int dir, std::uint64_t k, const std::uint32_t* verts,
+                            const std::uint64_t* ta, const std::uint64_t* tb, double theta,
+                            std::int32_t* method, double* beta, double* khat,
+                            std::uint64_t* matches) {
+  return guarded([&] {
+    const auto& g = *static_cast<const tgx::TemporalGraph*>(gp);
+    const tgx::Direction d = dir == 0 ? tgx::Direction::Out : tgx::Direction::In;
+    tgx::CostModelParams p;
+    p.theta_sel = theta;
+    for (std::uint64_t i = 0; i < k; ++i) {
+      const tgx::QueryWindow w{ta[i], tb[i]};
+      const tgx::AccessDecision a = tgx::choose_access_method(verts[i], g.registry(), d, w, p);
+      method[i] = a.method == tgx::AccessMethod::IndexLookup ? 0 : 1;
+      beta[i] = a.beta_hat;
+      khat[i] = a.k_hat;
+      matches[i] = g.csr(d).count_in_window(verts[i], w);
+    }
+  });
+}
+
+int tgxref_fit_cost_constants(std::uint64_t k, const std::uint64_t* degree,
+                              const std::uint64_t* matches, const double* index_s,
+                              const double* scan_s, double theta, double* out) {
+  return guarded([&] {
+    std::vector<tgx::CalibrationPoint> pts(k);
+    for (std::uint64_t i = 0; i < k; ++i) pts[i] = {degree[i], matches[i], index_s[i], scan_s[i]};
+    const tgx::CostModelParams p = tgx::fit_cost_constants(pts, theta);
+    out[0] = p.c;
+    out[1] = p.c_prime;
+    out[2] = p.theta_sel;
+  });
+}
 }  // extern "C"

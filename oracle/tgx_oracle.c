@@ -19,6 +19,7 @@
  */
 #include "tgx_oracle.h"
 
+#include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -917,4 +918,166 @@ uint64_t tgxo_digest(const int64_t* values, uint64_t n) {
     h *= 0x100000001b3ULL;
   }
   return h;
+}
+
+/* ------------------------------------------------------------------------
+ * Selective-index cost model, selective_index.cpp:67-209 (DensityHistogram
+ * build / estimate, choose_access_method) and :211-235 (fit_cost_constants).
+ * Same double operations in the same order (x86-64 baseline: no FMA
+ * contraction), so results are bit-identical to the reference's. */
+
+#define HB 100 /* DensityHistogram::kBucketsPerDim, selective_index.hpp:21 */
+
+static int bucket_of(uint64_t x, uint64_t lo, uint64_t hi, int buckets) {
+  if (buckets == 1 || hi == lo) return 0;
+  const unsigned __int128 num = (unsigned __int128)(x - lo) * (unsigned)buckets;
+  int b = (int)(num / (hi - lo));
+  if (b >= buckets) b = buckets - 1;
+  return b;
+}
+
+static double dmin2(double a, double b) { return b < a ? b : a; } /* std::min */
+static double dmax2(double a, double b) { return a < b ? b : a; } /* std::max */
+
+static double region_fraction(double s0, double s1, double d0, double d1, double ta, double tb) {
+  const int s_point = s1 <= s0;
+  const int d_point = d1 <= d0;
+  if (s_point && d_point) return (s0 >= ta && s0 + d0 <= tb) ? 1.0 : 0.0;
+  if (s_point) {
+    if (s0 < ta) return 0.0;
+    const double dmax = dmin2(d1, tb - s0);
+    if (dmax <= d0) return 0.0;
+    return (dmax - d0) / (d1 - d0);
+  }
+  if (d_point) {
+    const double a = dmax2(s0, ta);
+    const double b = dmin2(s1, tb - d0);
+    if (b <= a) return 0.0;
+    return (b - a) / (s1 - s0);
+  }
+  const double a = dmax2(s0, ta);
+  if (a >= s1) return 0.0;
+  const double height = d1 - d0;
+  const double full_hi = dmin2(s1, tb - d1);
+  double area = 0.0;
+  if (full_hi > a) area += (full_hi - a) * height;
+  const double lin_lo = dmax2(a, tb - d1);
+  const double lin_hi = dmin2(s1, tb - d0);
+  if (lin_hi > lin_lo) {
+    const double h_lo = tb - d0 - lin_lo;
+    const double h_hi = tb - d0 - lin_hi;
+    area += 0.5 * (h_lo + h_hi) * (lin_hi - lin_lo);
+  }
+  return area / ((s1 - s0) * height);
+}
+
+/* DensityHistogram::build + estimate over one segment [lo, hi). */
+static double hist_estimate(const ocsr* c, uint64_t lo, uint64_t hi, uint64_t wta, uint64_t wtb) {
+  const uint64_t total = hi - lo;
+  if (total == 0) return 0.0;
+  uint64_t smin = UINT64_MAX, smax = 0, dmin = UINT64_MAX, dmax = 0;
+  for (uint64_t e = lo; e < hi; ++e) {
+    const uint64_t d = c->en[e] - c->st[e];
+    if (c->st[e] < smin) smin = c->st[e];
+    if (c->st[e] > smax) smax = c->st[e];
+    if (d < dmin) dmin = d;
+    if (d > dmax) dmax = d;
+  }
+  const int sb = smin == smax ? 1 : HB;
+  const int db = dmin == dmax ? 1 : HB;
+  static _Thread_local uint32_t counts[HB * HB];
+  static _Thread_local uint64_t rows[HB];
+  memset(counts, 0, sizeof counts);
+  memset(rows, 0, sizeof rows);
+  for (uint64_t e = lo; e < hi; ++e) {
+    const int i = bucket_of(c->st[e], smin, smax, sb);
+    const int j = bucket_of(c->en[e] - c->st[e], dmin, dmax, db);
+    ++counts[i * db + j];
+    ++rows[i];
+  }
+  const double ta = (double)wta;
+  const double tb = (double)wtb;
+  const double s_lo = (double)smin;
+  const double s_span = (double)(smax - smin);
+  const double d_lo = (double)dmin;
+  const double d_span = (double)(dmax - dmin);
+  const double s_width = sb == 1 ? 0.0 : s_span / sb;
+  const double d_width = db == 1 ? 0.0 : d_span / db;
+  const double d_top = db == 1 ? d_lo : d_lo + d_span;
+  double acc = 0.0;
+  for (int i = 0; i < sb; ++i) {
+    if (rows[i] == 0) continue;
+    const double s0 = s_lo + i * s_width;
+    const double s1 = sb == 1 ? s0 : s_lo + (i + 1) * s_width;
+    double s_frac;
+    if (s1 <= s0) {
+      s_frac = s0 >= ta ? 1.0 : 0.0;
+    } else {
+      s_frac = (s1 - dmax2(s0, ta)) / (s1 - s0);
+      s_frac = s_frac < 0.0 ? 0.0 : (1.0 < s_frac ? 1.0 : s_frac); /* std::clamp */
+    }
+    if (s_frac == 0.0) continue;
+    if (s1 + d_top <= tb) {
+      acc += (double)rows[i] * s_frac;
+      continue;
+    }
+    for (int j = 0; j < db; ++j) {
+      const uint32_t count = counts[i * db + j];
+      if (count == 0) continue;
+      const double d0 = d_lo + j * d_width;
+      const double d1 = db == 1 ? d0 : d_lo + (j + 1) * d_width;
+      acc += count * region_fraction(s0, s1, d0, d1, ta, tb);
+    }
+  }
+  const double tot = (double)total;
+  return acc < 0.0 ? 0.0 : (tot < acc ? tot : acc);
+}
+
+int tgxo_access_decisions(const tgxo_graph* g, int dir, uint64_t cutoff, uint64_t k,
+                          const uint32_t* verts, const uint64_t* ta, const uint64_t* tb,
+                          double theta_sel, int32_t* method, double* beta_hat, double* k_hat,
+                          uint64_t* matches) {
+  if (cutoff < 1) return fail(TGXO_INVALID_ARGUMENT, "index cutoff must be >= 1");
+  const ocsr* c = dir == 0 ? &g->out : &g->in;
+  for (uint64_t i = 0; i < k; ++i) {
+    const uint32_t v = verts[i];
+    if (v >= g->n) return fail(TGXO_OUT_OF_RANGE, "vertex outside vertex range");
+    const uint64_t lo = c->off[v], hi = c->off[v + 1];
+    uint64_t cnt = 0; /* count_in_window: window_contains, types.hpp:55-57 */
+    for (uint64_t e = lo; e < hi; ++e) cnt += c->st[e] >= ta[i] && c->en[e] <= tb[i];
+    matches[i] = cnt;
+    if (hi - lo < cutoff) { /* no histogram: Scan, -1, -1 (selective_index.cpp:202) */
+      method[i] = 1;
+      beta_hat[i] = -1.0;
+      k_hat[i] = -1.0;
+      continue;
+    }
+    const double kh = hist_estimate(c, lo, hi, ta[i], tb[i]);
+    const double beta = kh / (double)(hi - lo);
+    method[i] = beta <= theta_sel ? 0 : 1;
+    beta_hat[i] = beta;
+    k_hat[i] = kh;
+  }
+  return TGXO_OK;
+}
+
+int tgxo_fit_cost_constants(uint64_t k, const uint64_t* degree, const uint64_t* matches,
+                            const double* index_s, const double* scan_s, double* c,
+                            double* c_prime) {
+  if (k == 0) return fail(TGXO_INVALID_ARGUMENT, "cost calibration needs a nonempty sample");
+  double num_c = 0.0, den_c = 0.0, num_cp = 0.0, den_cp = 0.0;
+  for (uint64_t i = 0; i < k; ++i) {
+    if (degree[i] == 0) continue;
+    const double x = log2((double)degree[i]) + (double)matches[i];
+    num_c += index_s[i] * x;
+    den_c += x * x;
+    const double y = (double)degree[i];
+    num_cp += scan_s[i] * y;
+    den_cp += y * y;
+  }
+  if (den_c == 0.0 || den_cp == 0.0)
+    return fail(TGXO_INVALID_ARGUMENT, "cost calibration needs samples with degree >= 1");
+  *c = num_c / den_c;
+  *c_prime = num_cp / den_cp;
+  return TGXO_OK;
 }

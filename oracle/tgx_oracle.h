@@ -39,6 +39,20 @@ int tgxo_work(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint6
               int ordering, const int64_t* labels, uint64_t* e_adm, uint64_t* v_reached);
 
 uint64_t tgxo_digest(const int64_t* values, uint64_t n);
+
+/* Selective-index cost model (selective_index.cpp:67-209): for k (vertex,
+ * window) pairs of one direction (0 out, 1 in) of a graph indexed at
+ * `cutoff`, choose_access_method's decision (0 index lookup, 1 scan),
+ * beta_hat and k_hat (-1 / -1 below the cutoff), and count_in_window
+ * (tcsr.cpp:124-128). */
+int tgxo_access_decisions(const tgxo_graph* g, int dir, uint64_t cutoff, uint64_t k,
+                          const uint32_t* verts, const uint64_t* ta, const uint64_t* tb,
+                          double theta_sel, int32_t* method, double* beta_hat, double* k_hat,
+                          uint64_t* matches);
+/* fit_cost_constants (selective_index.cpp:211-235): least-squares c, c'. */
+int tgxo_fit_cost_constants(uint64_t k, const uint64_t* degree, const uint64_t* matches,
+                            const double* index_s, const double* scan_s, double* c,
+                            double* c_prime);
 const char* tgxo_last_error(void);
 
 #ifdef __cplusplus

@@ -18,6 +18,7 @@ the library or a GPU is missing, calls raise.
 from __future__ import annotations
 
 import ctypes
+import math
 import enum
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -30,7 +31,9 @@ __all__ = [
     "AlgoOptions", "EdgeMapStats", "PathResult", "TemporalGraph", "GenConfig",
     "earliest_arrival", "latest_departure", "fastest_path", "query_batch", "digest_of",
     "generate_edges", "OutOfRange", "InvalidArgument", "Unsupported", "DeviceError",
-    "TimeRangeError", "load_library", "K_MAX_TIMESTAMP",
+    "TimeRangeError", "load_library", "K_MAX_TIMESTAMP", "AccessMethod", "AccessDecision",
+    "CostModelParams", "CalibrationPoint", "choose_access_method", "access_decisions",
+    "count_in_window", "fit_cost_constants", "cost_index_lookup", "cost_scan",
 ]
 
 K_MAX_TIMESTAMP = (1 << 64) - 1          # types.hpp:18
@@ -230,6 +233,12 @@ def load_library() -> ctypes.CDLL:
                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
         "tgxd_digest": ([_i64p, ctypes.c_uint64], ctypes.c_uint64),
+        "tgxd_access_decisions": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p,
+                                   ctypes.c_double, _P(ctypes.c_int32), _P(ctypes.c_double),
+                                   _P(ctypes.c_double), _u64p], ctypes.c_int),
+        "tgxd_fit_cost_constants": ([ctypes.c_uint64, _u64p, _u64p, _P(ctypes.c_double),
+                                     _P(ctypes.c_double), _P(ctypes.c_double),
+                                     _P(ctypes.c_double)], ctypes.c_int),
         "tgxd_set_trace": ([vp, ctypes.c_uint32], ctypes.c_int),
         "tgxd_get_trace": ([vp, _u64p, ctypes.c_uint32, ctypes.c_int], ctypes.c_int),
     }
@@ -519,3 +528,96 @@ def digest_of(values: np.ndarray) -> int:
     """FNV-1a over the int64 label bytes (digest.hpp:12-52)."""
     v = np.ascontiguousarray(values, dtype=np.int64)
     return int(load_library().tgxd_digest(_ptr(v, ctypes.c_int64), len(v)))
+
+
+# ---------------------------------------------------------------------------
+# Selective-index cost model (selective_index.hpp:45-130): results-neutral
+# for the traversals; the device builds each indexed vertex's density
+# histogram on first use and answers estimates bit-identically.
+
+class AccessMethod(enum.IntEnum):        # selective_index.hpp:51
+    INDEX_LOOKUP = 0
+    SCAN = 1
+
+
+@dataclass
+class AccessDecision:                    # selective_index.hpp:53-59
+    method: AccessMethod = AccessMethod.SCAN
+    beta_hat: float = -1.0
+    k_hat: float = -1.0
+
+
+@dataclass
+class CostModelParams:                   # selective_index.hpp:45-49
+    c: float = 1.0
+    c_prime: float = 1.0
+    theta_sel: float = 0.2
+
+
+@dataclass
+class CalibrationPoint:                  # selective_index.hpp:110-115
+    degree: int = 0
+    matches: int = 0
+    index_seconds: float = 0.0
+    scan_seconds: float = 0.0
+
+
+def access_decisions(g: TemporalGraph, d: Direction, vertices: Sequence[int],
+                     windows: Sequence[QueryWindow], theta_sel: float = 0.2):
+    """choose_access_method (selective_index.cpp:200-209) and count_in_window
+    (tcsr.cpp:124-128) for k (vertex, window) pairs: (method int32, beta_hat,
+    k_hat, matches) arrays; beta_hat = k_hat = -1 below the index cutoff."""
+    k = len(vertices)
+    if len(windows) != k:
+        raise InvalidArgument("one window per vertex")
+    v = np.ascontiguousarray(vertices, np.uint32)
+    ta = np.array([w.t_a for w in windows], np.uint64)
+    tb = np.array([w.t_b for w in windows], np.uint64)
+    method = np.empty(k, np.int32)
+    beta = np.empty(k, np.float64)
+    khat = np.empty(k, np.float64)
+    matches = np.empty(k, np.uint64)
+    _check(load_library().tgxd_access_decisions(
+        g.handle, int(d), k, _ptr(v, ctypes.c_uint32), _ptr(ta, ctypes.c_uint64),
+        _ptr(tb, ctypes.c_uint64), float(theta_sel), _ptr(method, ctypes.c_int32),
+        _ptr(beta, ctypes.c_double), _ptr(khat, ctypes.c_double), _ptr(matches, ctypes.c_uint64)))
+    return method, beta, khat, matches
+
+
+def choose_access_method(v: int, g: TemporalGraph, d: Direction, w: QueryWindow,
+                         params: CostModelParams = CostModelParams()) -> AccessDecision:
+    """selective_index.hpp:105-106 (the registry is the graph's)."""
+    m, b, k, _ = access_decisions(g, d, [v], [w], params.theta_sel)
+    return AccessDecision(AccessMethod(int(m[0])), float(b[0]), float(k[0]))
+
+
+def count_in_window(g: TemporalGraph, v: int, d: Direction, w: QueryWindow) -> int:
+    """TemporalCsr::count_in_window (tcsr.hpp:72)."""
+    return int(access_decisions(g, d, [v], [w])[3][0])
+
+
+def fit_cost_constants(points: Sequence[CalibrationPoint],
+                       theta_sel: float = 0.2) -> CostModelParams:
+    """selective_index.cpp:211-235 (least squares through the origin)."""
+    deg = np.array([p.degree for p in points], np.uint64)
+    mat = np.array([p.matches for p in points], np.uint64)
+    ix = np.array([p.index_seconds for p in points], np.float64)
+    sc = np.array([p.scan_seconds for p in points], np.float64)
+    c = ctypes.c_double()
+    cp = ctypes.c_double()
+    _check(load_library().tgxd_fit_cost_constants(
+        len(deg), _ptr(deg, ctypes.c_uint64), _ptr(mat, ctypes.c_uint64),
+        _ptr(ix, ctypes.c_double), _ptr(sc, ctypes.c_double), ctypes.byref(c), ctypes.byref(cp)))
+    return CostModelParams(c.value, cp.value, theta_sel)
+
+
+def cost_index_lookup(degree: int, k: float, c: float) -> float:
+    """selective_index.cpp:144-147: c (log2 degree + k)."""
+    if degree == 0:
+        raise ValueError("cost_index_lookup: degree must be >= 1")  # std::domain_error
+    return c * (math.log2(float(degree)) + k)
+
+
+def cost_scan(degree: int, c_prime: float) -> float:
+    """selective_index.cpp:149-151: c' degree."""
+    return c_prime * float(degree)

@@ -23,6 +23,7 @@
 #include "edges.cuh"
 #include "sd.cuh"
 #include "lanes.cuh"
+#include "costmodel.cuh"
 
 namespace tgxd {
 
@@ -1382,6 +1383,117 @@ int tgxd_graph_degrees(tgxd_graph* g, int direction, uint32_t* out) {
   if (g->n) degrees_kernel<<<grid_for(g->n, g->sm_count), 256, 0, g->stream>>>(c.off, g->n, d);
   TGXD_CUDA(cudaMemcpyAsync(out, d, g->n * 4ull, cudaMemcpyDeviceToHost, g->stream));
   TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  return TGXD_OK;
+}
+
+// Histograms of the indexed vertices of one direction (costmodel.cuh).
+static int ensure_hist(tgxd_graph* g, int dir) {
+  tgxd_graph::Hist& H = g->hist[dir];
+  if (H.built) return TGXD_OK;
+  const DevCsr& c = dir == 0 ? g->out : g->in;
+  std::vector<uint32_t> off((size_t)g->n + 1);
+  TGXD_CUDA(cudaMemcpyAsync(off.data(), c.off, off.size() * 4, cudaMemcpyDeviceToHost, g->stream));
+  TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  // VertexIndexRegistry::build (selective_index.cpp:153-186): degree >= cutoff, ascending ids
+  std::vector<uint32_t> ids, slot(g->n, kNoSlot);
+  for (uint32_t v = 0; v < g->n; ++v)
+    if ((uint64_t)(off[v + 1] - off[v]) >= g->index_cutoff) {
+      slot[v] = (uint32_t)ids.size();
+      ids.push_back(v);
+    }
+  const size_t K = ids.size();
+  if (!dalloc<uint32_t>(H.ids, std::max<size_t>(K, 1)) || !dalloc<uint32_t>(H.slot, g->n) ||
+      !dalloc<HistHdr>(H.hdr, std::max<size_t>(K, 1)) ||
+      !dalloc<uint32_t>(H.counts, std::max<size_t>(K, 1) * kHistB * kHistB) ||
+      !dalloc<unsigned long long>(H.rows, std::max<size_t>(K, 1) * kHistB))
+    return fail(TGXD_ERR_CUDA, "device allocation failed (density histograms)");
+  if (K)
+    TGXD_CUDA(cudaMemcpyAsync(H.ids.p, ids.data(), K * 4, cudaMemcpyHostToDevice, g->stream));
+  if (g->n)
+    TGXD_CUDA(cudaMemcpyAsync(H.slot.p, slot.data(), (size_t)g->n * 4, cudaMemcpyHostToDevice,
+                              g->stream));
+  const int smem = kHistB * kHistB * 4;
+  TGXD_CUDA(cudaFuncSetAttribute(hist_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+  if (K)
+    hist_build_kernel<<<(unsigned)K, 256, smem, g->stream>>>(
+        c, dir, H.ids.as<uint32_t>(), H.hdr.as<HistHdr>(), H.counts.as<uint32_t>(),
+        H.rows.as<unsigned long long>());
+  TGXD_CUDA(cudaGetLastError());
+  TGXD_CUDA(cudaStreamSynchronize(g->stream));
+  H.count = (uint32_t)K;
+  H.built = true;
+  return TGXD_OK;
+}
+
+int tgxd_access_decisions(tgxd_graph* g, int direction, uint32_t k, const uint32_t* vertices,
+                          const uint64_t* t_a, const uint64_t* t_b, double theta_sel,
+                          int32_t* method, double* beta_hat, double* k_hat, uint64_t* matches) {
+  if (!g) return fail(TGXD_ERR_ARGUMENT, "null graph");
+  if (direction != 0 && direction != 1) return fail(TGXD_ERR_ARGUMENT, "direction must be 0 or 1");
+  if (k == 0) return TGXD_OK;
+  if (!vertices || !t_a || !t_b || !method || !beta_hat || !k_hat || !matches)
+    return fail(TGXD_ERR_ARGUMENT, "null argument");
+  for (uint32_t i = 0; i < k; ++i)
+    if (vertices[i] >= g->n) {
+      char msg[128];
+      snprintf(msg, sizeof msg, "vertex %u outside vertex range [0, %u)", vertices[i], g->n);
+      return fail(TGXD_ERR_VERTEX_RANGE, msg);
+    }
+  std::lock_guard<std::mutex> lock(g->mu);
+  TGXD_CUDA(cudaSetDevice(g->device));
+  int rc = ensure_hist(g, direction);
+  if (rc) return rc;
+  const tgxd_graph::Hist& H = g->hist[direction];
+  const DevCsr& c = direction == 0 ? g->out : g->in;
+  // vertices (padded to 8), windows, beta, k_hat, matches, method: 56 bytes per query
+  DeviceBuffer b;
+  char* d = dalloc<char>(b, (size_t)k * 56 + 64);
+  if (!d) return fail(TGXD_ERR_CUDA, "allocation");
+  uint32_t* dv = reinterpret_cast<uint32_t*>(d);
+  unsigned long long* dta = reinterpret_cast<unsigned long long*>(d + (size_t)k * 8);
+  unsigned long long* dtb = dta + k;
+  double* dbeta = reinterpret_cast<double*>(dtb + k);
+  double* dkh = dbeta + k;
+  unsigned long long* dm = reinterpret_cast<unsigned long long*>(dkh + k);
+  int32_t* dmeth = reinterpret_cast<int32_t*>(dm + k);
+  cudaStream_t s = g->stream;
+  TGXD_CUDA(cudaMemcpyAsync(dv, vertices, (size_t)k * 4, cudaMemcpyHostToDevice, s));
+  TGXD_CUDA(cudaMemcpyAsync(dta, t_a, (size_t)k * 8, cudaMemcpyHostToDevice, s));
+  TGXD_CUDA(cudaMemcpyAsync(dtb, t_b, (size_t)k * 8, cudaMemcpyHostToDevice, s));
+  access_decision_kernel<<<grid_for((uint64_t)k * 32, g->sm_count), 256, 0, s>>>(
+      c, direction, k, dv, dta, dtb, theta_sel, H.slot.as<uint32_t>(), H.hdr.as<HistHdr>(),
+      H.counts.as<uint32_t>(), H.rows.as<unsigned long long>(), dmeth, dbeta, dkh, dm);
+  TGXD_CUDA(cudaGetLastError());
+  TGXD_CUDA(cudaMemcpyAsync(method, dmeth, (size_t)k * 4, cudaMemcpyDeviceToHost, s));
+  TGXD_CUDA(cudaMemcpyAsync(beta_hat, dbeta, (size_t)k * 8, cudaMemcpyDeviceToHost, s));
+  TGXD_CUDA(cudaMemcpyAsync(k_hat, dkh, (size_t)k * 8, cudaMemcpyDeviceToHost, s));
+  TGXD_CUDA(cudaMemcpyAsync(matches, dm, (size_t)k * 8, cudaMemcpyDeviceToHost, s));
+  TGXD_CUDA(cudaStreamSynchronize(s));
+  return TGXD_OK;
+}
+
+// fit_cost_constants (selective_index.cpp:211-235), the same host arithmetic.
+int tgxd_fit_cost_constants(uint64_t k, const uint64_t* degree, const uint64_t* matches,
+                            const double* index_seconds, const double* scan_seconds, double* c,
+                            double* c_prime) {
+  if (k == 0) return fail(TGXD_ERR_WINDOW, "cost calibration needs a nonempty sample");
+  if (!degree || !matches || !index_seconds || !scan_seconds || !c || !c_prime)
+    return fail(TGXD_ERR_ARGUMENT, "null argument");
+  double num_c = 0.0, den_c = 0.0, num_cp = 0.0, den_cp = 0.0;
+  for (uint64_t i = 0; i < k; ++i) {
+    if (degree[i] == 0) continue;
+    const double x = std::log2(static_cast<double>(degree[i])) + static_cast<double>(matches[i]);
+    num_c += index_seconds[i] * x;
+    den_c += x * x;
+    const double y = static_cast<double>(degree[i]);
+    num_cp += scan_seconds[i] * y;
+    den_cp += y * y;
+  }
+  if (den_c == 0.0 || den_cp == 0.0)
+    return fail(TGXD_ERR_WINDOW, "cost calibration needs samples with degree >= 1");
+  *c = num_c / den_c;
+  *c_prime = num_cp / den_cp;
   return TGXD_OK;
 }
 

@@ -181,6 +181,12 @@ struct tgxd_graph {
   tgxd::DeviceBuffer out2in;  // Out -> In position of each edge (shortest duration; lazy)
   bool out2in_ready = false;
   tgxd::DevCsr out, in;
+  // selective-index cost model (costmodel.cuh), per direction, built on first use
+  struct Hist {
+    bool built = false;
+    uint32_t count = 0;  // indexed vertices
+    tgxd::DeviceBuffer ids, slot, hdr, counts, rows;
+  } hist[2];
   cudaStream_t stream = nullptr;
   int sm_count = 0;
   int coop_blocks = 0;

@@ -120,3 +120,34 @@ def rand_instance(rng, max_v=12, max_e=40, t_range=60, d_max=8, d_min=0):
     a = rng.integers(0, t_range + 1, m)
     b = a + rng.integers(d_min, d_max + 1, m)
     return (s, d, a, b), n
+
+
+def cost_model():
+    """The cost-model fixture: (npz, {name: (edges, n, cutoff)}) with the rmat
+    graph regenerated from its generator fields and the hand graph stored."""
+    import paper_2401_02563_b200 as T
+    z = np.load(GOLDEN / "cost_model.npz")
+    kind, scale, n, m, sd, tr, seed = (int(x) for x in z["gen_fields"])
+    a, b, c, p = (float(x) for x in z["gen_probs"])
+    gen = T.GenConfig(kind, scale, n, m, a, b, c, sd, tr, p, seed)
+    E = T.generate_edges(gen)
+    de = z["degen_edges"]
+    DE = (de[0].astype(np.uint32), de[1].astype(np.uint32), de[2], de[3])
+    dn, dcut = (int(x) for x in z["degen_n_cutoff"])
+    return z, {"rmat": (E, gen.n_vertices, 64), "degen": (DE, dn, dcut)}
+
+
+def cost_cases(z, name, d):
+    """verts, t_a, t_b, theta and the reference's (method, beta, k_hat, matches)."""
+    k = f"{name}_d{d}_"
+    return (z[k + "verts"], z[k + "ta"], z[k + "tb"], float(z[k + "theta"][0]),
+            (z[k + "method"], z[k + "beta"], z[k + "khat"], z[k + "matches"]))
+
+
+def fit_cases(z):
+    o = 0
+    for i, k in enumerate(z["fit_k"]):
+        k = int(k)
+        yield (z["fit_degree"][o:o + k], z["fit_matches"][o:o + k], z["fit_index_s"][o:o + k],
+               z["fit_scan_s"][o:o + k], float(z["fit_c"][i]), float(z["fit_c_prime"][i]))
+        o += k

@@ -127,6 +127,28 @@ int main() {
     }
     CHECK(thrown);
   }
+  {  // selective-index cost model (selective_index.cpp:98-235)
+    std::vector<TemporalEdge> es;
+    for (std::uint64_t i = 0; i < 20; ++i) es.push_back({0, 1 + i % 3, 10 * i, 10 * i + 5, 1.0});
+    EngineConfig cfg;
+    cfg.index_cutoff = 8;
+    const auto g = TemporalGraph::build(es, 4, true, cfg);
+    const QueryWindow w{0, 1000};
+    const AccessDecision a = choose_access_method(0, g, Direction::Out, w);
+    CHECK(a.method == AccessMethod::Scan && a.k_hat == 20.0 && a.beta_hat == 1.0);
+    CHECK(count_in_window(g, 0, Direction::Out, QueryWindow{10, 34}) == 2);
+    const AccessDecision b = choose_access_method(1, g, Direction::Out, w);
+    CHECK(b.beta_hat == -1.0 && b.k_hat == -1.0);
+    const CostModelParams p = fit_cost_constants({{16, 0, 4.0, 16.0}});
+    CHECK(p.c == 1.0 && p.c_prime == 1.0);
+    bool thrown = false;
+    try {
+      fit_cost_constants({});
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    CHECK(thrown);
+  }
   if (failures) return 1;
   std::printf("shim ok\n");
   return 0;

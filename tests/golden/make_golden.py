@@ -21,6 +21,12 @@ inputs + outputs as compressed npz files next to this script:
                     test_engine.cpp:223-243 as a path query
   rmat12_ext.npz    the rmat12 graph, 4 sources x 2 windows x 5 metrics x 3
                     orderings
+  cost_model.npz    the selective-index cost model (choose_access_method:
+                    decision, beta_hat, k_hat; count_in_window) on the rmat12
+                    graph indexed at 64 (both directions, every indexed vertex
+                    and 100 others, seeded windows incl. unbounded / empty /
+                    inverted ones) and on a hand graph with degenerate
+                    histograms; fit_cost_constants on seeded samples
 
 Only this script touches the reference; tests read the npz files. Re-run
 with:  python tests/golden/make_golden.py
@@ -227,6 +233,71 @@ def extended():
                                 cube_root_starts=True))
 
 
+def degenerate_graph():
+    """Hubs whose histograms collapse: one start (vertex 0), one duration
+    (vertex 1), both (vertex 2), and a spread hub (vertex 3)."""
+    s, d, a, b = [], [], [], []
+    for i in range(40):
+        s += [0, 1, 2, 3]
+        d += [10 + i % 7, 20 + i % 5, 30 + i % 3, 40 + i % 9]
+        a += [500, 100 + 37 * i, 700, 13 * i * i % 997]
+        b += [500 + 1 + (i * 31) % 90, 100 + 37 * i + 25, 750, 13 * i * i % 997 + 1 + i % 11]
+    return (np.array(s, np.uint32), np.array(d, np.uint32), np.array(a, np.uint64),
+            np.array(b, np.uint64)), 64
+
+
+def cost_model():
+    import paper_2401_02563_b200 as T
+    gen = T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 7, cube_root_starts=True)
+    E = T.generate_edges(gen)
+    n = gen.n_vertices
+    rng = np.random.default_rng(2024)
+    out = {"gen_fields": np.array([gen.kind, gen.scale, gen.n, gen.m, gen.start_dist,
+                                   gen.t_range, gen.seed], np.uint64),
+           "gen_probs": np.array([gen.a, gen.b, gen.c, gen.geo_p], np.float64)}
+    ref = Reference(E, n, True, 64)
+    DE, dn = degenerate_graph()
+    dref = Reference(DE, dn, True, 4)
+    for name, r, edges, nn, cutoff in (("rmat", ref, E, n, 64), ("degen", dref, DE, dn, 4)):
+        for d in (0, 1):
+            deg = np.bincount(edges[d], minlength=nn)
+            idx = np.flatnonzero(deg >= cutoff)
+            other = rng.integers(0, nn, 100)
+            verts = np.concatenate([idx, idx, other]).astype(np.uint32)
+            k = len(verts)
+            ta = rng.integers(0, 1_000_000, k).astype(np.uint64)
+            tb = ta + rng.integers(0, 300_000, k).astype(np.uint64)
+            ta[::9] = 0
+            tb[::5] = (1 << 63) - 1
+            tb[3::17] = ta[3::17]                      # one-instant windows
+            tb[5::23] = np.maximum(ta[5::23], 1) - 1   # inverted (t_b < t_a)
+            theta = 0.2 if d == 0 else 0.05
+            m, beta, khat, matches = r.access_decisions(d, verts, ta, tb, theta)
+            key = f"{name}_d{d}_"
+            out.update({key + "verts": verts, key + "ta": ta, key + "tb": tb,
+                        key + "theta": np.array([theta]), key + "method": m, key + "beta": beta,
+                        key + "khat": khat, key + "matches": matches})
+    out["degen_edges"] = np.stack([x.astype(np.uint64) for x in DE])
+    out["degen_n_cutoff"] = np.array([dn, 4], np.uint64)
+    fits = []
+    for t in range(5):
+        kk = int(rng.integers(1, 40))
+        degree = rng.integers(0 if t == 4 else 1, 5000, kk).astype(np.uint64)
+        matches = rng.integers(0, 300, kk).astype(np.uint64)
+        ix = rng.random(kk) * 1e-5
+        sc = rng.random(kk) * 1e-4
+        c, cp = Reference.fit_cost_constants(degree, matches, ix, sc)
+        fits.append((degree, matches, ix, sc, c, cp))
+    out["fit_k"] = np.array([len(f[0]) for f in fits], np.uint64)
+    out["fit_degree"] = np.concatenate([f[0] for f in fits])
+    out["fit_matches"] = np.concatenate([f[1] for f in fits])
+    out["fit_index_s"] = np.concatenate([f[2] for f in fits])
+    out["fit_scan_s"] = np.concatenate([f[3] for f in fits])
+    out["fit_c"] = np.array([f[4] for f in fits])
+    out["fit_c_prime"] = np.array([f[5] for f in fits])
+    np.savez_compressed(HERE / "cost_model.npz", **out)
+
+
 def main():
     import paper_2401_02563_b200 as T
     small_random()
@@ -246,9 +317,13 @@ def main():
     qs2 = [(k, 0, 0, 999_999) for k in KINDS] + [(k, 77, 100_000, 600_000) for k in KINDS]
     scaled("uniform14", g2, qs2)
     extended()
+    cost_model()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["cost_model"]:
+        cost_model()
+    else:
+        main()
