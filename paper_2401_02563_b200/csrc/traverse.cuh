@@ -584,8 +584,59 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
   flush_work(a.ctl, work);
 }
 
+#ifdef TGXD_TMA_RELAX
+// Chunk payloads staged through shared memory by the TMA engine (1-D bulk
+// copies, cp.async.bulk + mbarrier complete_tx): the copy of the next chunk
+// is in flight while the current one is relaxed. Per warp two buffers of
+// kChunk + 2 entries (the copy starts at the 16-byte-aligned entry at or
+// below the chunk's first) and two mbarriers.
+constexpr uint32_t kTmaEntries = kChunk + 2;
+struct TmaBufs {
+  uint2* buf;                // 2 x kTmaEntries
+  unsigned long long* bar;   // 2 mbarriers
+  uint32_t* parity;          // per-buffer phase bits (bit b)
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_issue(const TmaBufs& t, int b, const uint2* pay, uint32_t first,
+                                          uint32_t len, uint64_t pol) {
+  if (lane_id() == 0) {
+    const uint32_t a0 = first & ~1u;
+    const uint32_t bytes = (((first + len + 1) & ~1u) - a0) * 8u;
+    const uint32_t bar = smem_u32(t.bar + b);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(t.buf + b * kTmaEntries)),
+        "l"(pay + a0), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_wait(const TmaBufs& t, int b) {
+  const uint32_t bar = smem_u32(t.bar + b);
+  const uint32_t ph = (*t.parity >> b) & 1u;
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(ph)
+        : "memory");
+  }
+  __syncwarp();
+  if (lane_id() == 0) *t.parity ^= 1u << b;
+  __syncwarp();
+}
+#endif
+
 // Phase B: relax the round's chunks and small ranges (plus, for a fastest
 // seed round, the virtual chunks of one explicit range).
+#ifdef TGXD_TMA_RELAX
+__device__ TmaBufs tma_bufs_of_warp();
+#endif
 __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks, unsigned long long nsmall,
                         uint32_t xlo,
                         uint32_t xcnt, RelaxCtx& rx, uint32_t bid, uint32_t nblk,
@@ -613,10 +664,50 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
   // chunks of big ranges: coalesced kChunk-edge bursts (software-pipelining
   // the next chunk's payload loads measured no gain: the relax is bound by
   // the L2 atomic rate, ~150 G/s when most edges improve)
+#ifdef TGXD_TMA_RELAX
+  if (gw < nchunks) {
+    const TmaBufs tb = tma_bufs_of_warp();
+    // descriptor of chunk c in `cur`, of c + nw in `nxt`; the copy of c is
+    // in buffer cb, issued one iteration ahead
+    uint2 cur = __ldcg(a.chunks + gw);
+    uint2 nxt = gw + nw < nchunks ? __ldcg(a.chunks + gw + nw) : make_uint2(0u, 0u);
+    int cb = 0;
+    tma_issue(tb, cb, a.g.pay, cur.x, cur.y & ((1u << kChunkLenBits) - 1), rx.pol_stream);
+    for (unsigned long long c = gw; c < nchunks; c += nw) {
+      const uint2 ch = cur;
+      const bool more = c + nw < nchunks;
+      if (more) {
+        tma_issue(tb, cb ^ 1, a.g.pay, nxt.x, nxt.y & ((1u << kChunkLenBits) - 1), rx.pol_stream);
+        cur = nxt;
+        if (c + 2ull * nw < nchunks) nxt = __ldcg(a.chunks + c + 2ull * nw);
+      }
+      const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
+      const uint32_t cq = ch.y >> kChunkLenBits;
+      tma_wait(tb, cb);
+      const uint2* sb = tb.buf + cb * kTmaEntries + (ch.x - (ch.x & ~1u));
+      uint2 pl[kUnroll];
+      uint32_t q[kUnroll];
+      bool act[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t off = u * 32 + lane;
+        act[u] = off < len;
+        q[u] = cq;
+        pl[u] = act[u] ? sb[off] : make_uint2(0u, kInf);
+      }
+      __syncwarp();
+      relax_apply(a, pl, q, act, rx, pb);
+      cb ^= 1;
+    }
+  }
+  for (unsigned long long c = nchunks; false;) {
+    const uint2 ch = make_uint2(0u, 0u);
+#else
   uint2 nxt = gw < nchunks ? __ldcg(a.chunks + gw) : make_uint2(0u, 0u);
   for (unsigned long long c = gw; c < nchunks; c += nw) {
     const uint2 ch = nxt;  // descriptor prefetched one iteration ahead
     if (c + nw < nchunks) nxt = __ldcg(a.chunks + c + nw);
+#endif
     const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
     const uint32_t cq = ch.y >> kChunkLenBits;
     uint32_t e[kUnroll], q[kUnroll];
@@ -1170,11 +1261,30 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
   }
 }
 
+#ifdef TGXD_TMA_RELAX
+__shared__ __align__(128) uint2 s_tma_buf[kWarps][2 * kTmaEntries];
+__shared__ __align__(8) unsigned long long s_tma_bar[kWarps][2];
+__shared__ uint32_t s_tma_par[kWarps];
+__device__ TmaBufs tma_bufs_of_warp() {
+  const uint32_t w = threadIdx.x >> 5;
+  return TmaBufs{s_tma_buf[w], s_tma_bar[w], &s_tma_par[w]};
+}
+#endif
 __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(TravArgs a) {
   __shared__ uint32_t s_buf[kWarps][64];
   __shared__ uint2 s_ebuf[kWarps][2 * kListCap];
   __shared__ uint2 s_rbuf[kWarps][64];
   __shared__ uint4 s_obuf[kWarps][64];
+#ifdef TGXD_TMA_RELAX
+  if (threadIdx.x < kWarps) {
+    const uint32_t b0 = smem_u32(&s_tma_bar[threadIdx.x][0]);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0 + 8) : "memory");
+    s_tma_par[threadIdx.x] = 0;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+#endif
   GridBarrier grid{&a.ctl->bar_count, &a.ctl->bar_gen, gridDim.x, 0};
   uint32_t* wbuf = s_buf[threadIdx.x >> 5];
   uint2* ebuf = s_ebuf[threadIdx.x >> 5];
