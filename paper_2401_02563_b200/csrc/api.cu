@@ -495,6 +495,9 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
   a.time_limit_ns = 20ull * 1000 * 1000 * 1000;  // watchdog: 20 s
+  a.chg = nullptr;
+  a.chg_n = nullptr;
+  a.chg_cap = 0;
   a.hctl = nullptr;
   a.hfa = a.hfb = nullptr;
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
@@ -822,8 +825,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   if (!fast || ncand) {
     void* args[] = {&a};
+    const bool early = w.early_req && !fast && !bfs;
+    if (early && a.handoff_f) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)traverse_kernel, dim3(G->coop_blocks),
                                           dim3(kThreads), args, 0, s));
+    if (early) {  // the caller's copy of the labels may start now
+      TGXD_CUDA(cudaEventRecord(G->early_ev, s));
+      w.early_done = true;
+    }
     if (a.handoff_f) {  // the continuation exits at once unless the round kernel handed off
       AsyncArgs h;
       h.g = g;
@@ -845,6 +854,9 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       h.cand_cnt = nullptr;
       h.cand_key = nullptr;
       h.time_limit_ns = 20ull * 1000 * 1000 * 1000;
+      h.chg = early ? w.chg.as<uint32_t>() : nullptr;
+      h.chg_n = early ? w.chg_n.as<unsigned long long>() : nullptr;
+      h.chg_cap = early ? w.chg_cap : 0;
       h.hctl = a.ctl;
       h.hfa = a.fa;
       h.hfb = a.fb;
@@ -859,6 +871,10 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       const int tail_blocks = std::min(G->coop_blocks_async, tail_per_sm * G->sm_count);
       TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(tail_blocks),
                                             dim3(kThreads), hargs, 0, s));
+      if (early)
+        tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
+            w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X,
+            G->patch_dev);
     }
   } else {
     Control z;
@@ -866,7 +882,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     TGXD_CUDA(cudaMemcpyAsync(w.ctl.p, &z, sizeof z, cudaMemcpyHostToDevice, s));
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
-  if (out_dev) convert_for(G, P, out_dev, width);
+  if (out_dev && !w.early_done) convert_for(G, P, out_dev, width);
   TGXD_CUDA(cudaGetLastError());
   w.last_kind = P.kind;
   w.last_q = P.Q;
@@ -1037,19 +1053,55 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     for (int c = 0; c < kChunks; ++c)
       if (!G->chunk_ev[c])
       TGXD_CUDA(cudaEventCreateWithFlags(&G->chunk_ev[c], cudaEventDisableTiming));
+  // Early copy (EA / LD through the round kernel): the labels leave for the
+  // host on a second stream as soon as the round kernel is done, while the
+  // async engine finishes the tail; the few labels the tail changes come
+  // back afterwards as a patch list in mapped memory.
+  const bool early_ok = staged && !P.edge && !getenv("TGXD_NO_EARLY_COPY") &&
+                        (kind == TGXD_EARLIEST_ARRIVAL || kind == TGXD_LATEST_DEPARTURE);
+  if (early_ok) {
+    size_t cap = std::min<size_t>(1ull << 24, std::max<size_t>(1ull << 16, slots / 4));
+    if (const char* e = getenv("TGXD_PATCH_CAP")) cap = std::max(1, atoi(e));  // tests: the re-copy
+    if (!G->copy_stream)
+      TGXD_CUDA(cudaStreamCreateWithFlags(&G->copy_stream, cudaStreamNonBlocking));
+    if (!G->early_ev) TGXD_CUDA(cudaEventCreateWithFlags(&G->early_ev, cudaEventDisableTiming));
+    if (G->patch_cap < cap) {
+      if (G->patch_host) cudaFreeHost(G->patch_host);
+      G->patch_host = nullptr;
+      G->patch_cap = 0;
+      void* hp = nullptr;
+      TGXD_CUDA(cudaHostAlloc(&hp, (cap + 1) * 8, cudaHostAllocMapped));
+      G->patch_host = static_cast<unsigned long long*>(hp);
+      void* dp = nullptr;
+      TGXD_CUDA(cudaHostGetDevicePointer(&dp, hp, 0));
+      G->patch_dev = static_cast<unsigned long long*>(dp);
+      G->patch_cap = cap;
+    }
+    if (!dalloc<uint32_t>(w.chg, cap) || !dalloc<unsigned long long>(w.chg_n, 1))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (tail patch list)");
+    w.chg_cap = cap;
+    G->patch_host[0] = 0;  // no tail: nothing to patch
+  }
+  w.early_req = early_ok;
+  w.early_done = false;
   TGXD_CUDA(cudaEventRecord(w.ev[2], G->stream));
   rc = launch(G, P, mode, dout, staged ? 4 : width, w.ev[0], w.ev[1]);
+  w.early_req = false;
   if (rc) return rc;
+  const bool early = w.early_done;  // the traversal took the round kernel
   const uint64_t chunk = (slots + kChunks - 1) / kChunks;
+  cudaStream_t cs = early ? G->copy_stream : G->stream;
+  const int32_t* csrc = early ? w.X.as<int32_t>() : static_cast<int32_t*>(dout);
+  if (early) TGXD_CUDA(cudaStreamWaitEvent(cs, G->early_ev, 0));
   if (staged) {
     for (int c = 0; c < kChunks; ++c) {
       const uint64_t lo = std::min<uint64_t>(slots, c * chunk);
       const uint64_t len = std::min<uint64_t>(slots, lo + chunk) - lo;
       if (len)
-        TGXD_CUDA(cudaMemcpyAsync(G->pinned + lo, static_cast<int32_t*>(dout) + lo, len * 4,
-                                  cudaMemcpyDeviceToHost, G->stream));
-      TGXD_CUDA(cudaEventRecord(G->chunk_ev[c], G->stream));
+        TGXD_CUDA(cudaMemcpyAsync(G->pinned + lo, csrc + lo, len * 4, cudaMemcpyDeviceToHost, cs));
+      TGXD_CUDA(cudaEventRecord(G->chunk_ev[c], cs));
     }
+    if (early) TGXD_CUDA(cudaStreamWaitEvent(G->stream, G->chunk_ev[kChunks - 1], 0));
   } else if (!out_on_device) {
     TGXD_CUDA(cudaMemcpyAsync(out, dout, slots * width, cudaMemcpyDeviceToHost, G->stream));
   }
@@ -1064,6 +1116,12 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     const int T = G->pool.size();
     int64_t* o64 = static_cast<int64_t*>(out);
     const int32_t* src = G->pinned;
+    // early copies carry key-space labels: LD's are negated (DevCsr In layout)
+    const bool neg = early && kind == TGXD_LATEST_DEPARTURE;
+    auto widen = [neg](int32_t v) -> int64_t {
+      if (neg) return v == INT32_MAX ? INT64_MIN : -(int64_t)v;
+      return v == INT32_MAX ? INT64_MAX : v == INT32_MIN ? INT64_MIN : (int64_t)v;
+    };
     std::atomic<int> bad{0};
     G->pool.run([&](int wi) {
       for (int c = 0; c < kChunks; ++c) {
@@ -1075,15 +1133,42 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
           bad = 1;
           return;
         }
-        for (uint64_t i = a; i < b; ++i) {
-          const int32_t v = src[i];
-          o64[i] = v == INT32_MAX   ? INT64_MAX
-                   : v == INT32_MIN ? INT64_MIN
-                                    : (int64_t)v;
+        if (neg) {
+          for (uint64_t i = a; i < b; ++i) o64[i] = widen(src[i]);
+        } else {
+          for (uint64_t i = a; i < b; ++i) {
+            const int32_t v = src[i];
+            o64[i] = v == INT32_MAX   ? INT64_MAX
+                     : v == INT32_MIN ? INT64_MIN
+                                      : (int64_t)v;
+          }
         }
       }
     });
     if (bad) return fail(TGXD_ERR_CUDA, "result copy failed");
+    if (early) {
+      TGXD_CUDA(cudaStreamSynchronize(G->stream));  // the tail and its patch list
+      const volatile unsigned long long* ph = G->patch_host;
+      const unsigned long long np = ph[0];
+      if (np > w.chg_cap) {  // too many changes to list: copy the labels again
+        TGXD_CUDA(cudaMemcpyAsync(G->pinned, w.X.p, slots * 4, cudaMemcpyDeviceToHost, G->stream));
+        TGXD_CUDA(cudaStreamSynchronize(G->stream));
+        G->pool.run([&](int wi) {
+          const uint64_t per = (slots + T - 1) / T;
+          const uint64_t a = std::min<uint64_t>(slots, wi * per), b = std::min(slots, a + per);
+          for (uint64_t i = a; i < b; ++i) o64[i] = widen(src[i]);
+        });
+      } else if (np) {
+        G->pool.run([&](int wi) {
+          const uint64_t per = (np + T - 1) / T;
+          const uint64_t a = std::min<uint64_t>(np, wi * per), b = std::min<uint64_t>(np, a + per);
+          for (uint64_t i = a; i < b; ++i) {
+            const unsigned long long e = ph[1 + i];
+            o64[(uint32_t)e] = widen((int32_t)(uint32_t)(e >> 32));
+          }
+        });
+      }
+    }
     for (uint32_t q = 0; q < P.Q; ++q)  // the roots' exact values (t_a, t_b, 0)
       o64[(uint64_t)q * G->n + P.seeds[q].root] = P.seeds[q].value;
   }
@@ -1356,6 +1441,9 @@ void tgxd_graph_destroy(tgxd_graph* g) {
     if (e) cudaEventDestroy(e);
   if (g->ws.trace_host) cudaFreeHost(g->ws.trace_host);
   if (g->pinned) cudaFreeHost(g->pinned);
+  if (g->patch_host) cudaFreeHost(g->patch_host);
+  if (g->early_ev) cudaEventDestroy(g->early_ev);
+  if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
   for (auto& e : g->chunk_ev)
     if (e) cudaEventDestroy(e);
   if (g->stream) cudaStreamDestroy(g->stream);

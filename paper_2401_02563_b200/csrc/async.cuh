@@ -85,6 +85,11 @@ struct AsyncArgs {
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
   unsigned long long time_limit_ns;  // watchdog
+  // host results copied early (api.cu): every label the tail lowers is
+  // listed here (slot ids, repeats allowed) so the host can patch its copy
+  uint32_t* chg;
+  unsigned long long* chg_n;
+  unsigned long long chg_cap;
   // tail handoff from the round kernel: its frontier queue and labels
   const Control* hctl;  // nullptr: a query of its own
   const uint32_t* hfa;
@@ -204,6 +209,17 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
       const unsigned long long prev = atomicMin(a.XQ + idx[u], xq_pack(v[u], 1u));
       imp[u] = v[u] < xq_label(prev);
       if (imp[u]) was[u] = (uint32_t)(prev & 1ull);
+    }
+  }
+  if (a.chg) {  // every label the tail lowers, for the early host copy's patch
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t m = __ballot_sync(0xffffffffu, imp[u]);
+      if (m == 0) continue;
+      unsigned long long cb = 0;
+      if (lane_id() == 0) cb = atomicAdd(a.chg_n, (unsigned long long)__popc(m));
+      cb = __shfl_sync(0xffffffffu, cb, 0) + __popc(m & ((1u << lane_id()) - 1));
+      if (imp[u] && cb < a.chg_cap) a.chg[cb] = idx[u];
     }
   }
 #pragma unroll
@@ -540,6 +556,22 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n,
     u[0] = k;
   }
   c->tail.v = t + nu;
+}
+
+// The tail's changed labels for the host (mapped memory): out[0] = count,
+// then {slot, label} pairs (count <= cap; a larger count means the host
+// copies the labels again).
+__global__ void tail_patch_kernel(const uint32_t* chg, const unsigned long long* chg_n,
+                                  unsigned long long cap, const int32_t* X,
+                                  unsigned long long* out) {
+  const unsigned long long n = *chg_n;
+  const unsigned long long k = n < cap ? n : cap;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+    const uint32_t v = chg[i];
+    out[1 + i] = (unsigned long long)v | ((unsigned long long)(uint32_t)X[v] << 32);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = n;
 }
 
 // Fresh (or post-abort) queue state: every unit free.

@@ -79,6 +79,12 @@ struct Workspace {
   bool last_edge = false;
   bool last_async = false;
   bool last_handoff = false;  // round kernel may have handed its tail to the async engine
+  // early host copy (api.cu query_impl): the labels leave for the host while
+  // the async tail runs; the tail's changed labels are patched afterwards
+  bool early_req = false;   // set by the caller for one launch
+  bool early_done = false;  // launch recorded early_ev (and the patch list)
+  DeviceBuffer chg, chg_n;
+  unsigned long long chg_cap = 0;
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
   unsigned long long* trace_dev = nullptr;
   DeviceBuffer wtrace;
@@ -200,5 +206,10 @@ struct tgxd_graph {
   int32_t* pinned = nullptr;  // cudaHostAlloc'd staging
   size_t pinned_n = 0;
   cudaEvent_t chunk_ev[16] = {};
+  cudaStream_t copy_stream = nullptr;  // early host copies
+  cudaEvent_t early_ev = nullptr;      // the round kernel is done
+  unsigned long long* patch_host = nullptr;  // mapped: count, {slot, label} pairs
+  unsigned long long* patch_dev = nullptr;
+  size_t patch_cap = 0;
   WidenPool pool;
 };
