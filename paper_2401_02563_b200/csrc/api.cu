@@ -1123,6 +1123,9 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
       return v == INT32_MAX ? INT64_MAX : v == INT32_MIN ? INT64_MIN : (int64_t)v;
     };
     std::atomic<int> bad{0};
+    std::atomic<int> widened{0};
+    std::atomic<int> recopy{0};
+    const volatile unsigned long long* ph = G->patch_host;
     G->pool.run([&](int wi) {
       for (int c = 0; c < kChunks; ++c) {
         const uint64_t lo = std::min<uint64_t>(slots, c * chunk);
@@ -1131,7 +1134,7 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
         const uint64_t a = std::min(hi, lo + wi * per), b = std::min(hi, a + per);
         if (cudaEventSynchronize(G->chunk_ev[c]) != cudaSuccess) {
           bad = 1;
-          return;
+          break;
         }
         if (neg) {
           for (uint64_t i = a; i < b; ++i) o64[i] = widen(src[i]);
@@ -1144,30 +1147,35 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
           }
         }
       }
+      if (!early) return;
+      // the tail's patch list, in the same dispatch: once every worker has
+      // widened (a patched slot may lie in another worker's share) and the
+      // tail and its list are done
+      widened.fetch_add(1);
+      if (cudaEventSynchronize(w.ev[3]) != cudaSuccess) bad = 1;
+      while (widened.load() < T) std::this_thread::yield();
+      if (bad) return;
+      const unsigned long long np = ph[0];
+      if (np > w.chg_cap) {  // too many changes to list: the caller copies the labels again
+        recopy = 1;
+        return;
+      }
+      const uint64_t per = (np + T - 1) / T;
+      const uint64_t a = std::min<uint64_t>(np, wi * per), b = std::min<uint64_t>(np, a + per);
+      for (uint64_t i = a; i < b; ++i) {
+        const unsigned long long e = ph[1 + i];
+        o64[(uint32_t)e] = widen((int32_t)(uint32_t)(e >> 32));
+      }
     });
     if (bad) return fail(TGXD_ERR_CUDA, "result copy failed");
-    if (early) {
-      TGXD_CUDA(cudaStreamSynchronize(G->stream));  // the tail and its patch list
-      const volatile unsigned long long* ph = G->patch_host;
-      const unsigned long long np = ph[0];
-      if (np > w.chg_cap) {  // too many changes to list: copy the labels again
-        TGXD_CUDA(cudaMemcpyAsync(G->pinned, w.X.p, slots * 4, cudaMemcpyDeviceToHost, G->stream));
-        TGXD_CUDA(cudaStreamSynchronize(G->stream));
-        G->pool.run([&](int wi) {
-          const uint64_t per = (slots + T - 1) / T;
-          const uint64_t a = std::min<uint64_t>(slots, wi * per), b = std::min(slots, a + per);
-          for (uint64_t i = a; i < b; ++i) o64[i] = widen(src[i]);
-        });
-      } else if (np) {
-        G->pool.run([&](int wi) {
-          const uint64_t per = (np + T - 1) / T;
-          const uint64_t a = std::min<uint64_t>(np, wi * per), b = std::min<uint64_t>(np, a + per);
-          for (uint64_t i = a; i < b; ++i) {
-            const unsigned long long e = ph[1 + i];
-            o64[(uint32_t)e] = widen((int32_t)(uint32_t)(e >> 32));
-          }
-        });
-      }
+    if (recopy) {
+      TGXD_CUDA(cudaMemcpyAsync(G->pinned, w.X.p, slots * 4, cudaMemcpyDeviceToHost, G->stream));
+      TGXD_CUDA(cudaStreamSynchronize(G->stream));
+      G->pool.run([&](int wi) {
+        const uint64_t per = (slots + T - 1) / T;
+        const uint64_t a = std::min<uint64_t>(slots, wi * per), b = std::min(slots, a + per);
+        for (uint64_t i = a; i < b; ++i) o64[i] = widen(src[i]);
+      });
     }
     for (uint32_t q = 0; q < P.Q; ++q)  // the roots' exact values (t_a, t_b, 0)
       o64[(uint64_t)q * G->n + P.seeds[q].root] = P.seeds[q].value;
