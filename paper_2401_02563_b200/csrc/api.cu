@@ -652,6 +652,15 @@ static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void*
   lanes_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, w.lxm.as<int32_t>(),
                                      w.ldirty.as<uint32_t>(), w.fa.as<uint32_t>(),
                                      w.ctl.as<Control>());
+#ifdef TGXD_CHECK
+  {  // frontier: distinct vertices; chunks: segments / 128 + one per vertex
+    const unsigned long long caps[2] = {(uint64_t)P.Q * G->n,
+                                        (uint64_t)P.Q * G->n + (uint64_t)P.Q * (G->m / kChunk + 1)};
+    const unsigned int zero = 0;
+    TGXD_CUDA(cudaMemcpyToSymbolAsync(g_cap, caps, sizeof caps, 0, cudaMemcpyHostToDevice, s));
+    TGXD_CUDA(cudaMemcpyToSymbolAsync(g_check_fail, &zero, 4, 0, cudaMemcpyHostToDevice, s));
+  }
+#endif
   LanesArgs a;
   a.g = g;
   a.qp = w.params.as<QueryParam>();
