@@ -376,6 +376,7 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool need_r) {
             dalloc<QueryParam>(w.params, Q) && dalloc<Seed>(w.seeds, Q);
   if (ok && need_r) ok = dalloc<int32_t>(w.R, slots) != nullptr;
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (traversal workspace)");
+  if (slots > w.slots) w.xinv = false;  // X / EP may have been reallocated
   w.slots = std::max(w.slots, slots);
   return TGXD_OK;
 }
@@ -642,6 +643,7 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
 static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void* out_dev,
                         int width, cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
   Workspace& w = G->ws;
+  w.xinv = false;  // X is rewritten by the transpose
   cudaStream_t s = G->stream;
   const size_t n = G->n;
   if (!dalloc<int32_t>(w.lxm, n * 32) || !dalloc<int2>(w.leb, n * 32) ||
@@ -700,7 +702,10 @@ static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void*
 // out_dev). ev_k0/ev_k1 bracket the traversal kernel when non-null.
 static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int width,
                   cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
-  if (P.edge) return launch_edges(G, P, out_dev, width, ev_k0, ev_k1);
+  if (P.edge) {
+    G->ws.xinv = false;
+    return launch_edges(G, P, out_dev, width, ev_k0, ev_k1);
+  }
   Workspace& w = G->ws;
   w.last_edge = false;
   cudaStream_t s = G->stream;
@@ -744,8 +749,25 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
                    (mode == TGXD_MODE_AUTO && one_root && !getenv("TGXD_NO_LANES"))))
     return launch_lanes(G, P, g, out_dev, width, ev_k0, ev_k1);
   if (mode == TGXD_MODE_LANES) mode = TGXD_MODE_AUTO;
-  init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
-      w.X.as<int32_t>(), w.EP.as<int2>(), fast || bfs ? w.R.as<int32_t>() : nullptr, slots);
+  // EA / LD on the round kernel: reset only what the previous such query
+  // touched (X finite) instead of initializing every slot (config 3's batch:
+  // 134M slots, 1.6 GB of writes); everything else initializes in full
+  const bool lazy = !fast && !bfs && mode != TGXD_MODE_ASYNC && !getenv("TGXD_FULL_INIT");
+  if (lazy) {
+    if (!w.xinv) {
+      init_kernel<<<grid_for(w.slots, G->sm_count), 256, 0, s>>>(w.X.as<int32_t>(),
+                                                                  w.EP.as<int2>(), nullptr, w.slots);
+      w.xinv = true;
+    } else if (w.xdirty) {
+      reset_kernel<<<grid_for(w.xdirty, G->sm_count), 256, 0, s>>>(w.X.as<int32_t>(),
+                                                                    w.EP.as<int2>(), w.xdirty);
+    }
+    w.xdirty = slots;
+  } else {
+    init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
+        w.X.as<int32_t>(), w.EP.as<int2>(), fast || bfs ? w.R.as<int32_t>() : nullptr, slots);
+    w.xinv = false;
+  }
   seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
                                                  w.X.as<int32_t>(), w.fa.as<uint32_t>(),
                                                  w.ctl.as<Control>(), fast);

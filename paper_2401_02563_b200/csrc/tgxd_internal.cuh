@@ -68,6 +68,12 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
   DeviceBuffer X, EP, R, fa, fb, chunks, smalls, ctl, params, seeds;
+  // lazy label reset (api.cu launch): while `xinv` holds, every slot whose
+  // expansion state is not the initial one has a finite label, and slots at
+  // or above `xdirty` are untouched — so the next round-kernel query resets
+  // only [0, xdirty) where X is finite instead of writing every slot
+  bool xinv = false;
+  uint64_t xdirty = 0;
   // lane-per-query batches (lanes.cuh): vertex-major labels, ranges, dirty masks
   DeviceBuffer lxm, leb, ldirty;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;

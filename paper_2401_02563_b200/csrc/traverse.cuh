@@ -1517,6 +1517,31 @@ __global__ void init_kernel(int32_t* X, int2* EP, int32_t* R, size_t nl) {
   }
 }
 
+// Lazy reset (api.cu launch): slots the previous query reached (finite
+// label) back to INF / the initial expansion state; untouched slots are only
+// read.
+__global__ void reset_kernel(int32_t* X, int2* EP, size_t nl) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t n4 = nl / 4;
+  const int2 ep0 = make_int2(kInf, (int32_t)kNoPos);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int4 x = reinterpret_cast<const int4*>(X)[i];
+    if (x.x != kInf || x.y != kInf || x.z != kInf || x.w != kInf) {
+      reinterpret_cast<int4*>(X)[i] = make_int4(kInf, kInf, kInf, kInf);
+      if (x.x != kInf) EP[4 * i] = ep0;
+      if (x.y != kInf) EP[4 * i + 1] = ep0;
+      if (x.z != kInf) EP[4 * i + 2] = ep0;
+      if (x.w != kInf) EP[4 * i + 3] = ep0;
+    }
+  }
+  for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+    if (X[i] != kInf) {
+      X[i] = kInf;
+      EP[i] = ep0;
+    }
+  }
+}
+
 // Seeds: X[root] = klo (EA: t_a, LD: -t_b), root queued as round-0 frontier.
 __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_t* X,
                             uint32_t* fa, Control* ctl, int fastest) {

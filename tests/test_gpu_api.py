@@ -166,3 +166,33 @@ def test_edge_list_file_to_device_graph(tmp_path):
     for v in range(0, min(n, 10)):
         assert np.array_equal(T.earliest_arrival(g, v, T.QueryWindow(0, 400)).values,
                               o.query("earliest_arrival", v, 0, 400))
+
+
+def test_lazy_label_reset_across_query_kinds():
+    # api.cu launch: round-kernel EA / LD queries reset only the slots the
+    # previous such query reached; every other route re-initializes. Mixed
+    # sequences on one handle must keep every answer exact.
+    gen = T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 31, cube_root_starts=True)
+    E = T.generate_edges(gen)
+    n = gen.n_vertices
+    g = T.TemporalGraph.build(E, n, True, T.EngineConfig(index_cutoff=64))
+    o = Oracle(E, n)
+    deg = np.bincount(E[0], minlength=n)
+    srcs = [int(x) for x in np.argsort(-deg)[:6]]
+    w_full, w_part = T.QueryWindow(0, 999_999), T.QueryWindow(300_000, 800_000)
+    seq = [("earliest_arrival", srcs[:4], [w_full, w_part, w_full, w_part], T.Mode.AUTO),
+           ("earliest_arrival", srcs[:1], [w_part], T.Mode.AUTO),
+           ("latest_departure", srcs[1:3], [w_full, w_part], T.Mode.SPARSE),
+           ("fastest", srcs[2:3], [w_full], T.Mode.AUTO),
+           ("earliest_arrival", srcs[:2], [w_full, w_full], T.Mode.AUTO),
+           ("earliest_arrival", [srcs[0]] * 3, [w_full, w_part, w_full], T.Mode.AUTO),  # lanes
+           ("latest_departure", srcs[3:4], [w_full], T.Mode.ASYNC),
+           ("earliest_arrival", srcs, [w_part] * 6, T.Mode.PULL),
+           ("temporal_bfs", srcs[4:5], [w_full], T.Mode.AUTO),
+           ("earliest_arrival", srcs[5:6], [w_full], T.Mode.DENSE),
+           ("earliest_arrival", srcs[:3], [w_part] * 3, T.Mode.AUTO)]
+    for kind, vs, ws, mode in seq:
+        out = T.query_batch(g, kind, vs, ws, mode=mode)
+        for q, (v, w) in enumerate(zip(vs, ws)):
+            assert np.array_equal(out[q], o.query(kind, v, w.t_a, w.t_b)), (kind, mode, q)
+    g.close()
