@@ -455,7 +455,15 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
     const size_t slots = (size_t)a.Q * a.n;
     const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t nthr = (size_t)gridDim.x * blockDim.x;
-    for (size_t i = tid; i < slots; i += nthr) a.XQ[i] = xq_pack(a.X[i], 0u);
+    // label words from the labels, 4 slots per thread and step (16-byte
+    // accesses; X and XQ are 256-byte aligned allocations)
+    for (size_t i = tid; i < slots / 4; i += nthr) {
+      const int4 x = reinterpret_cast<const int4*>(a.X)[i];
+      ulonglong2* d = reinterpret_cast<ulonglong2*>(a.XQ) + 2 * i;
+      d[0] = make_ulonglong2(xq_pack(x.x, 0u), xq_pack(x.y, 0u));
+      d[1] = make_ulonglong2(xq_pack(x.z, 0u), xq_pack(x.w, 0u));
+    }
+    for (size_t i = slots / 4 * 4 + tid; i < slots; i += nthr) a.XQ[i] = xq_pack(a.X[i], 0u);
     grid.sync();
     for (size_t k = tid; k < nh; k += nthr) {
       const uint32_t item = __ldcg(fin + k);
@@ -503,12 +511,18 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
     }
   }
   if (lane_id() == 0) atomicMax(&a.c->t_last, gtimer());
-  grid.sync();  // every label is final: copy them out
+  grid.sync();  // every label is final: copy them out (4 slots per thread and step)
   {
     const size_t slots = (size_t)a.Q * a.n;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
-         i += (size_t)gridDim.x * blockDim.x)
-      a.X[i] = xq_label(__ldcg(a.XQ + i));
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t nthr = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = tid; i < slots / 4; i += nthr) {
+      const ulonglong2* q = reinterpret_cast<const ulonglong2*>(a.XQ) + 2 * i;
+      const ulonglong2 w0 = __ldcg(q), w1 = __ldcg(q + 1);
+      reinterpret_cast<int4*>(a.X)[i] =
+          make_int4(xq_label(w0.x), xq_label(w0.y), xq_label(w1.x), xq_label(w1.y));
+    }
+    for (size_t i = slots / 4 * 4 + tid; i < slots; i += nthr) a.X[i] = xq_label(__ldcg(a.XQ + i));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
