@@ -387,26 +387,60 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool need_r) {
 // root's value is written exactly (Seed).
 enum ConvertForm : int { kFormMin = 0, kFormLd = 1, kFormI64 = 2 };
 
+__device__ __forceinline__ long long convert_one(int form, int32_t x) {
+  if (form == kFormLd) return x == kInf ? (-0x7fffffffffffffffLL - 1) : -(long long)x;
+  return x == kInf ? 0x7fffffffffffffffLL : (long long)x;
+}
+__device__ __forceinline__ int32_t clamp32(long long o) {
+  return (int32_t)(o > 0x7fffffffLL ? 0x7fffffffLL : (o < -0x80000000LL ? -0x80000000LL : o));
+}
+
 __global__ void convert_kernel(int form, const int32_t* V, const long long* V64, uint64_t total,
                                uint32_t n, const Seed* seeds, void* out, int width) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+  uint64_t done = 0;
+  // int32 labels, 4 slots per thread and step with 16-byte accesses (the
+  // output must be 16-byte aligned; a step crosses at most one query)
+  if (form != kFormI64 && n >= 4 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    const uint64_t n4 = total / 4;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += stride) {
+      const int4 x4 = reinterpret_cast<const int4*>(V)[j];
+      const int32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
+      const uint64_t i0 = 4 * j;
+      const uint32_t q0 = (uint32_t)(i0 / n);
+      const uint32_t v0 = (uint32_t)(i0 - (uint64_t)q0 * n);
+      long long o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t q = q0, v = v0 + k;
+        if (v >= n) {
+          ++q;
+          v -= n;
+        }
+        o[k] = convert_one(form, xs[k]);
+        const Seed sd = seeds[q];
+        if (v == sd.root) o[k] = sd.value;
+      }
+      if (width == 8) {
+        longlong2* d = reinterpret_cast<longlong2*>(out) + 2 * j;
+        d[0] = make_longlong2(o[0], o[1]);
+        d[1] = make_longlong2(o[2], o[3]);
+      } else {
+        reinterpret_cast<int4*>(out)[j] = make_int4(clamp32(o[0]), clamp32(o[1]), clamp32(o[2]),
+                                                    clamp32(o[3]));
+      }
+    }
+    done = n4 * 4;
+  }
+  for (uint64_t i = done + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
     const uint32_t q = (uint32_t)(i / n);
     const uint32_t v = (uint32_t)(i - (uint64_t)q * n);
-    long long o;
-    if (form == kFormI64) {
-      o = V64[i];
-    } else {
-      const int32_t x = V[i];
-      if (form == kFormLd) o = x == kInf ? (-0x7fffffffffffffffLL - 1) : -(long long)x;
-      else o = x == kInf ? 0x7fffffffffffffffLL : (long long)x;
-    }
+    long long o = form == kFormI64 ? V64[i] : convert_one(form, V[i]);
     if (v == seeds[q].root) o = seeds[q].value;
     if (width == 8) {
       static_cast<long long*>(out)[i] = o;
     } else {
-      const long long c = o > 0x7fffffffLL ? 0x7fffffffLL : (o < -0x80000000LL ? -0x80000000LL : o);
-      static_cast<int32_t*>(out)[i] = (int32_t)c;
+      static_cast<int32_t*>(out)[i] = clamp32(o);
     }
   }
 }

@@ -1527,11 +1527,11 @@ __global__ void reset_kernel(int32_t* X, int2* EP, size_t nl) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     const int4 x = reinterpret_cast<const int4*>(X)[i];
     if (x.x != kInf || x.y != kInf || x.z != kInf || x.w != kInf) {
+      // whole 16-byte groups (slots already initial are rewritten unchanged)
       reinterpret_cast<int4*>(X)[i] = make_int4(kInf, kInf, kInf, kInf);
-      if (x.x != kInf) EP[4 * i] = ep0;
-      if (x.y != kInf) EP[4 * i + 1] = ep0;
-      if (x.z != kInf) EP[4 * i + 2] = ep0;
-      if (x.w != kInf) EP[4 * i + 3] = ep0;
+      const int4 e2 = make_int4(kInf, (int32_t)kNoPos, kInf, (int32_t)kNoPos);
+      reinterpret_cast<int4*>(EP)[2 * i] = e2;
+      reinterpret_cast<int4*>(EP)[2 * i + 1] = e2;
     }
   }
   for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
