@@ -42,4 +42,29 @@ for scale, kind_gen in ((14, "rmat"), (16, "rmat"), (15, "uniform"), (17, "rmat"
                                   int(np.sum(got != want)), flush=True)
         g.close()
     print(kind_gen, scale, "done", f"{time.time() - t0:.1f}s", flush=True)
+# 2^20 slots and more: the host results take the staged / early-copy path
+# (int32 over PCIe while the async tail runs, patched afterwards)
+for scale in (20, 21):
+    gen = T.GenConfig.rmat(scale, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, seed=scale,
+                           cube_root_starts=True)
+    E = T.generate_edges(gen)
+    n = gen.n_vertices
+    t0 = time.time()
+    o = Oracle(E, n)
+    g = T.TemporalGraph.build(E, n, True, T.EngineConfig(index_cutoff=256))
+    deg = g.degrees(T.Direction.OUT)
+    srcs = [int(np.argmax(deg))] + [int(x) for x in rng.choice(np.flatnonzero(deg), 3)]
+    for s in srcs:
+        for w in ((0, 999_999), (300_000, 900_000)):
+            for kind in ("earliest_arrival", "latest_departure"):
+                for ordv in (0, 1):
+                    got = FN[kind](g, s, T.QueryWindow(*w), T.AlgoOptions(ordering=T.Ordering(ordv))).values
+                    want = o.query(kind, s, w[0], w[1], ordv)
+                    total += 1
+                    if not np.array_equal(got, want):
+                        bad += 1
+                        print("MISMATCH rmat", scale, s, w, kind, ordv, int(np.sum(got != want)),
+                              flush=True)
+    g.close()
+    print("rmat", scale, "(staged host results) done", f"{time.time() - t0:.1f}s", flush=True)
 print("checked", total, "mismatches", bad)
