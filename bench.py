@@ -290,14 +290,16 @@ def run_ours(args):
                      "algorithmic_bytes": b_alg, "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
                 "host_buffer": "pinned" if out.ctypes.data == pinned_ptr else "pageable",
-                # the library moves int32 labels over PCIe in chunks and widens
-                # them into the caller's int64 array on the host meanwhile
+                # the library moves int32 labels over PCIe in chunks (starting
+                # while the async tail still runs; the tail's changes follow as
+                # a patch list) and widens them into the caller's int64 array
                 "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_s * 1e3},
-        # per step: init_kernel, seed_kernel, traverse_kernel, async_kernel (the
-        # tail continuation, exits at once when the rounds finished the query),
+        # per timed step: reset_kernel (the previous query's reached slots back
+        # to INF), seed_kernel, traverse_kernel, async_kernel (the tail
+        # continuation, exits at once when the rounds finished the query),
         # convert_kernel
         "gpu_launches": 5 * args.steps,
-        "kernels_per_step": ["init_kernel", "seed_kernel", "traverse_kernel", "async_kernel",
+        "kernels_per_step": ["reset_kernel", "seed_kernel", "traverse_kernel", "async_kernel",
                              "convert_kernel"],
         "clocks": sampler.summary(),
     }
