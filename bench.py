@@ -267,6 +267,7 @@ def run_ours(args):
                                            None))
     barrier()
     e2e_s = max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, "cuda")[0]
+    d2h_bytes = T.last_d2h_bytes(g)  # int32 labels + the tail's patch pairs
     e2e_value = whole_job_teps(world, e_adm, e2e_s * 1e3)
 
     peak, peak_kind = measured_peak()
@@ -293,7 +294,7 @@ def run_ours(args):
                 # the library moves int32 labels over PCIe in chunks (starting
                 # while the async tail still runs; the tail's changes follow as
                 # a patch list) and widens them into the caller's int64 array
-                "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_s * 1e3},
+                "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_s * 1e3},
         # per timed step: reset_kernel (the previous query's reached slots back
         # to INF), seed_kernel, traverse_kernel, async_kernel (the tail
         # continuation, exits at once when the rounds finished the query),

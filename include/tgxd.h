@@ -169,6 +169,11 @@ int tgxd_query(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
  * from the final labels. For fastest, the arrival fixpoint is counted. */
 int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reached);
 
+/* Bytes the LAST host-result query moved device -> host: the int32 (or int64)
+ * result copies plus, for the early copy of EA / LD results, the tail's
+ * {slot, label} patch pairs (8 B each) written through mapped memory. */
+int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes);
+
 /* Device time of `steps` back-to-back queries with device-resident output,
  * after `warmup` untimed ones: total ms (CUDA events on the handle's stream)
  * and the mean traversal-kernel ms per query. */

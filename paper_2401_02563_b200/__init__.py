@@ -229,6 +229,7 @@ def load_library() -> ctypes.CDLL:
         "tgxd_query": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p, ctypes.c_int,
                         ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, _P(_Stats)], ctypes.c_int),
         "tgxd_last_work": ([vp, ctypes.c_uint32, _u64p, _u64p], ctypes.c_int),
+        "tgxd_last_d2h_bytes": ([vp, _u64p], ctypes.c_int),
         "tgxd_time_queries": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p,
                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
@@ -465,6 +466,13 @@ def query_batch(g: TemporalGraph, kind: str, vertices: Sequence[int],
     if stats is not None:
         _fill_stats(AlgoOptions(stats=stats), st)
     return out
+
+
+def last_d2h_bytes(g: TemporalGraph) -> int:
+    """Bytes the last host-result query moved device -> host (copies + patch pairs)."""
+    b = ctypes.c_uint64()
+    _check(load_library().tgxd_last_d2h_bytes(g.handle, ctypes.byref(b)))
+    return b.value
 
 
 def last_work(g: TemporalGraph, q: int = 0) -> tuple[int, int]:

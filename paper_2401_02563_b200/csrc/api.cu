@@ -1248,6 +1248,13 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     }
     for (uint32_t q = 0; q < P.Q; ++q)  // the roots' exact values (t_a, t_b, 0)
       o64[(uint64_t)q * G->n + P.seeds[q].root] = P.seeds[q].value;
+    w.last_d2h = slots * 4;
+    if (early) {
+      const unsigned long long np = G->patch_host[0];
+      w.last_d2h += np > w.chg_cap ? slots * 4 : 8 * (np + 1);
+    }
+  } else {
+    w.last_d2h = out_on_device ? 0 : slots * (uint64_t)width;
   }
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
   float km = 0, tm = 0;
@@ -1737,6 +1744,13 @@ int tgxd_temporal_bfs(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b
                       int64_t* out, tgxd_stats* stats) {
   return query_impl(g, TGXD_TEMPORAL_BFS, 1, &source, &t_a, &t_b, ordering, TGXD_MODE_AUTO, out,
                     8, 0, stats);
+}
+
+int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes) {
+  if (!g || !bytes) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  *bytes = g->ws.last_d2h;
+  return TGXD_OK;
 }
 
 int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reached) {

@@ -89,6 +89,7 @@ struct Workspace {
   // the async tail runs; the tail's changed labels are patched afterwards
   bool early_req = false;   // set by the caller for one launch
   bool early_done = false;  // launch recorded early_ev (and the patch list)
+  uint64_t last_d2h = 0;    // bytes the last host-result query moved to the host
   DeviceBuffer chg, chg_n;
   unsigned long long chg_cap = 0;
   unsigned long long* trace_host = nullptr;  // mapped pinned trace (diagnostics)
