@@ -40,8 +40,14 @@ namespace tgxd {
 #ifndef TGXD_ASYNC_SLEEP
 #define TGXD_ASYNC_SLEEP 256  // ns between polls of a long-waiting ticket
 #endif
-constexpr uint32_t kAChunk = 512;        // edges per chunk unit (4 x 128-edge bursts)
-constexpr uint32_t kAInline = 64;        // shorter ranges are relaxed by the expanding warp
+#ifndef TGXD_A_CHUNK
+#define TGXD_A_CHUNK 512
+#endif
+#ifndef TGXD_A_INLINE
+#define TGXD_A_INLINE 64
+#endif
+constexpr uint32_t kAChunk = TGXD_A_CHUNK;    // edges per chunk unit (4 x 128-edge bursts)
+constexpr uint32_t kAInline = TGXD_A_INLINE;  // shorter ranges are relaxed by the expanding warp
 constexpr uint32_t kUnitWords = 16;      // 64-byte units
 constexpr uint32_t kBatch = kUnitWords - 1;  // vertices per batch unit
 constexpr uint32_t kEmpty = 0xffffffffu;
