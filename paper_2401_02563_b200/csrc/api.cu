@@ -235,6 +235,13 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
   if (const char* b = getenv("TGXD_BLOCKS_PER_SM"))  // experiments: fewer resident CTAs
     per_sm = std::min(per_sm, std::max(1, atoi(b)));
   G->coop_blocks = std::max(1, per_sm) * G->sm_count;
+  // the tail runs on fewer CTAs: its frontier is small, and every idle warp
+  // polls a queue ticket (measured on config 2: 3 CTAs per SM 0.91 ms, all 4
+  // 1.02 ms, 1 1.01 ms; TGXD_TAIL_BLOCKS_PER_SM overrides)
+  {
+    const char* t = getenv("TGXD_TAIL_BLOCKS_PER_SM");
+    G->tail_per_sm = t ? std::max(1, atoi(t)) : 3;
+  }
   int per_sm_a = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, async_kernel, kThreads, 0);
   G->coop_blocks_async = std::max(1, per_sm_a) * G->sm_count;
@@ -926,14 +933,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       h.hfa = a.fa;
       h.hfb = a.fb;
       void* hargs[] = {&h};
-      // the tail runs on fewer CTAs: its frontier is small, and every idle
-      // warp polls a queue ticket (TGXD_TAIL_BLOCKS_PER_SM overrides)
-      // (measured on config 2: 3 CTAs per SM 0.91 ms, all 4 1.02 ms, 1 1.01 ms)
-      static const int tail_per_sm = [] {
-        const char* e = getenv("TGXD_TAIL_BLOCKS_PER_SM");
-        return e ? std::max(1, atoi(e)) : 3;
-      }();
-      const int tail_blocks = std::min(G->coop_blocks_async, tail_per_sm * G->sm_count);
+      // the tail on fewer CTAs per SM (new_graph: G->tail_per_sm)
+      const int tail_blocks = std::min(G->coop_blocks_async, G->tail_per_sm * G->sm_count);
       TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(tail_blocks),
                                             dim3(kThreads), hargs, 0, s));
       if (early)
@@ -1173,13 +1174,16 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   TGXD_CUDA(cudaEventRecord(w.ev[3], G->stream));
   if (staged) {
     if (G->pool.size() == 0)
-      G->pool.start([] {
+      G->pool.start([&] {
         const char* e = getenv("TGXD_HOST_THREADS");
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         // the widening is the e2e limit once the copies overlap the tail:
         // config 2 on a 16-core host, 12 threads 1.28-1.33 ms vs 8 threads
-        // 1.43-1.53 (non-temporal stores measured 2.9-3.6 ms)
-        return e ? std::max(1, atoi(e)) : (int)std::max(1u, std::min(12u, hw > 4 ? hw - 4 : hw));
+        // 1.43-1.53 (non-temporal stores measured 2.9-3.6 ms); views that
+        // run side by side split the host threads
+        if (e) return std::max(1, atoi(e));
+        const int t = (int)std::max(1u, std::min(12u, hw > 4 ? hw - 4 : hw));
+        return std::max(1, t / std::max(1, G->share));
       }());
     const int T = G->pool.size();
     int64_t* o64 = static_cast<int64_t*>(out);
@@ -1532,6 +1536,35 @@ void tgxd_graph_destroy(tgxd_graph* g) {
     if (e) cudaEventDestroy(e);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
+}
+
+int tgxd_graph_view(tgxd_graph* g, int share, tgxd_graph** out) {
+  if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  if (share < 1 || share > 16) return fail(TGXD_ERR_ARGUMENT, "share must lie in [1, 16]");
+  if (g->parent) return fail(TGXD_ERR_ARGUMENT, "a view of a view: use the owning handle");
+  *out = nullptr;
+  TGXD_CUDA(cudaSetDevice(g->device));
+  tgxd_graph* v = nullptr;
+  int rc = new_graph(g->n, g->index_cutoff, g->directed, &v);
+  if (rc) return rc;
+  v->m_logical = g->m_logical;
+  v->m = g->m;
+  v->indexed[0] = g->indexed[0];
+  v->indexed[1] = g->indexed[1];
+  v->out = g->out;  // the device graph is the parent's: no buffers owned here
+  v->in = g->in;
+  v->parent = g;
+  v->share = share;
+  // grids sized so `share` views fit on the GPU side by side
+  auto div = [&](int blocks) { return std::max(1, blocks / v->sm_count / share) * v->sm_count; };
+  v->coop_blocks = div(v->coop_blocks);
+  v->coop_blocks_async = div(v->coop_blocks_async);
+  v->coop_blocks_edge = div(v->coop_blocks_edge);
+  v->coop_blocks_sd = div(v->coop_blocks_sd);
+  v->coop_blocks_lanes = div(v->coop_blocks_lanes);
+  v->tail_per_sm = std::max(1, std::min(v->tail_per_sm, v->coop_blocks / v->sm_count));
+  *out = v;
+  return TGXD_OK;
 }
 
 int tgxd_graph_info(const tgxd_graph* g, uint32_t* n, uint64_t* m, uint64_t* indexed_out,

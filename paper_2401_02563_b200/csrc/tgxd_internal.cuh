@@ -207,6 +207,9 @@ struct tgxd_graph {
   int coop_blocks_edge = 0;
   int coop_blocks_sd = 0;
   int coop_blocks_lanes = 0;
+  int tail_per_sm = 3;       // CTAs per SM of the async tail continuation
+  int share = 1;             // views: handles meant to run side by side (grids divided)
+  const tgxd_graph* parent = nullptr;  // views: the handle whose device graph is shared
   std::mutex mu;
   tgxd::Workspace ws;
   // pipelined host results (int32 chunks -> int64 on the host)

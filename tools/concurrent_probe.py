@@ -1,8 +1,7 @@
 """Throughput probe for serving: the same set of EA queries run one by one on
-one handle (full grid) versus split across S handles (one stream and one
-workspace each, every grid limited so all fit on the GPU together: set
-TGXD_BLOCKS_PER_SM / TGXD_TAIL_BLOCKS_PER_SM before the library loads)
-driven from S host threads. Wall time of the whole set.
+one handle (full grid) versus split across S views of the graph
+(tgxd_graph_view: one stream and workspace each, grids sized so all fit on
+the GPU together) driven from S host threads. Wall time of the whole set.
 
 usage: python tools/concurrent_probe.py --config c5 --streams 2"""
 import argparse, os, sys, threading, time
@@ -19,8 +18,9 @@ from paper_2401_02563_b200.configs import workload
 
 wl = workload(args.config)
 S = args.streams
-gs = [T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
-      for _ in range(S)]
+base = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
+# S views of one device graph (tgxd_graph_view: own stream / workspace, grids / S)
+gs = [base] if S == 1 else [base.view(S) for _ in range(S)]
 qs = [q for q in wl.queries(gs[0].degrees(T.Direction.OUT), gs[0].degrees(T.Direction.IN),
                             gs[0].vertex_count()) if q.kind == "earliest_arrival"]
 qs = (qs * (args.queries // max(1, len(qs)) + 1))[:args.queries]
@@ -42,6 +42,5 @@ for t in th:
 for t in th:
     t.join()
 wall = time.perf_counter() - t0
-print(f"{args.config} streams={S} blocks/SM={os.environ.get('TGXD_BLOCKS_PER_SM', 'all')} "
-      f"tail/SM={os.environ.get('TGXD_TAIL_BLOCKS_PER_SM', 3)}: {len(qs)} EA queries in "
+print(f"{args.config} streams={S} (views): {len(qs)} EA queries in "
       f"{wall * 1e3:.1f} ms ({wall * 1e3 / len(qs):.3f} ms per query)", flush=True)
