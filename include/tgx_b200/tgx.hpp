@@ -126,6 +126,18 @@ class TemporalGraph {
     return g;
   }
 
+  // A handle on the same device graph with its own stream and workspace
+  // (tgxd_graph_view): give each serving thread one; `share` of them run
+  // side by side. Keeps this graph alive.
+  TemporalGraph view(int share) const {
+    tgxd_graph* v = nullptr;
+    detail::check(tgxd_graph_view(h_.get(), share, &v));
+    TemporalGraph g = *this;
+    std::shared_ptr<tgxd_graph> parent = h_;
+    g.h_ = std::shared_ptr<tgxd_graph>(v, [parent](tgxd_graph* p) { tgxd_graph_destroy(p); });
+    return g;
+  }
+
   VertexId vertex_count() const { return n_; }
   const EngineConfig& config() const { return config_; }
   Ordering ordering() const { return config_.ordering; }

@@ -127,6 +127,12 @@ int main() {
     }
     CHECK(thrown);
   }
+  {  // views share the device graph (tgxd_graph_view)
+    std::vector<TemporalEdge> es{{0, 1, 1, 2, 1.0}, {1, 2, 3, 4, 1.0}};
+    const auto g = TemporalGraph::build(es, 3, true);
+    const auto v = g.view(2);
+    CHECK(earliest_arrival(v, 0, QueryWindow{}).values == earliest_arrival(g, 0, QueryWindow{}).values);
+  }
   {  // selective-index cost model (selective_index.cpp:98-235)
     std::vector<TemporalEdge> es;
     for (std::uint64_t i = 0; i < 20; ++i) es.push_back({0, 1 + i % 3, 10 * i, 10 * i + 5, 1.0});
