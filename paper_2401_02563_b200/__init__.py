@@ -338,11 +338,15 @@ class TemporalGraph:
         _check(load_library().tgxd_graph_view(self._h, int(share), ctypes.byref(h)))
         v = TemporalGraph(h.value, self.config, self.directed)
         v._parent = self
+        if not hasattr(self, "_views"):
+            self._views = []
+        self._views.append(v)  # closed before this graph's own handle
         return v
 
     def close(self) -> None:
         for v in getattr(self, "_views", []):
             v.close()
+        self._views = []
         if self._h and self._h.value:
             load_library().tgxd_graph_destroy(self._h)
             self._h = ctypes.c_void_p()
@@ -656,12 +660,12 @@ def concurrent_queries(g: TemporalGraph, kind: str, vertices: Sequence[int],
     k = len(vertices)
     if len(windows) != k:
         raise InvalidArgument("one window per query")
-    views = getattr(g, "_views", None)
+    views = getattr(g, "_serve_views", None)
     if not views or len(views) != streams:
         for v in views or []:
             v.close()
         views = [g.view(streams) for _ in range(streams)]
-        g._views = views
+        g._serve_views = views
     fn = {"earliest_arrival": earliest_arrival, "latest_departure": latest_departure,
           "fastest": fastest_path, "shortest_duration": shortest_duration,
           "temporal_bfs": temporal_bfs}[kind]
