@@ -4,6 +4,7 @@
 // semantics, workspace management, kernel launches on the handle's stream,
 // output widening. All per-edge work is in build.cuh / traverse.cuh.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1050,6 +1051,51 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   return TGXD_OK;
 }
 
+// Host widening of int32 labels into the caller's int64 PathResult values
+// (INT32_MAX -> INT64_MAX / INT32_MIN -> INT64_MIN; LD key space: negated,
+// INT32_MAX -> INT64_MIN), 8 labels per AVX2 step when the host has it (the
+// widening is the e2e limit once the copies overlap the tail). Returns the
+// first index left to the scalar loop.
+__attribute__((target("avx2"))) static uint64_t widen_avx2(const int32_t* src, int64_t* dst,
+                                                         uint64_t a, uint64_t b, bool neg) {
+  const __m256i imax32 = _mm256_set1_epi32(INT32_MAX);
+  const __m256i imin32 = _mm256_set1_epi32(INT32_MIN);
+  const __m256i imax64 = _mm256_set1_epi64x(INT64_MAX);
+  const __m256i imin64 = _mm256_set1_epi64x(INT64_MIN);
+  const __m256i zero = _mm256_setzero_si256();
+  uint64_t i = a;
+  for (; i + 8 <= b; i += 8) {
+    const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i is_max = _mm256_cmpeq_epi32(x, imax32);
+    __m256i lo = _mm256_cvtepi32_epi64(_mm256_castsi256_si128(x));
+    __m256i hi = _mm256_cvtepi32_epi64(_mm256_extracti128_si256(x, 1));
+    const __m256i mlo = _mm256_cvtepi32_epi64(_mm256_castsi256_si128(is_max));
+    const __m256i mhi = _mm256_cvtepi32_epi64(_mm256_extracti128_si256(is_max, 1));
+    if (neg) {
+      lo = _mm256_blendv_epi8(_mm256_sub_epi64(zero, lo), imin64, mlo);
+      hi = _mm256_blendv_epi8(_mm256_sub_epi64(zero, hi), imin64, mhi);
+    } else {
+      const __m256i is_min = _mm256_cmpeq_epi32(x, imin32);
+      const __m256i nlo = _mm256_cvtepi32_epi64(_mm256_castsi256_si128(is_min));
+      const __m256i nhi = _mm256_cvtepi32_epi64(_mm256_extracti128_si256(is_min, 1));
+      lo = _mm256_blendv_epi8(_mm256_blendv_epi8(lo, imax64, mlo), imin64, nlo);
+      hi = _mm256_blendv_epi8(_mm256_blendv_epi8(hi, imax64, mhi), imin64, nhi);
+    }
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), lo);
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i + 4), hi);
+  }
+  return i;
+}
+
+static bool host_avx2() {
+  static const bool has = [] {
+    if (const char* e = getenv("TGXD_HOST_AVX2")) return atoi(e) != 0;
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx2") != 0;
+  }();
+  return has;
+}
+
 static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts,
                       const uint64_t* ta, const uint64_t* tb, int ordering, int mode, void* out,
                       int width, int out_on_device, tgxd_stats* stats) {
@@ -1209,6 +1255,7 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
           break;
         }
         uint64_t i = a;
+        if (host_avx2()) i = widen_avx2(src, o64, a, b, neg);  // 8 labels per step
         if (neg) {
           for (; i < b; ++i) o64[i] = widen(src[i]);
         } else {
