@@ -65,7 +65,10 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = TGXD_UNROLL;             // 32-edge steps in flight per warp
 constexpr uint32_t kChunk = 32u * kUnroll;       // edges per chunk of a big range
-constexpr uint32_t kSmall = 32;                  // ranges below this go to the small list
+#ifndef TGXD_SMALL
+#define TGXD_SMALL 32
+#endif
+constexpr uint32_t kSmall = TGXD_SMALL;          // ranges below this go to the small list
 constexpr uint32_t kChunkLenBits = 10;           // kChunk <= 512
 constexpr uint32_t kSmallCntBits = 6;
 constexpr uint32_t kLocalMaxF = TGXD_LOCAL_F;    // frontier that one CTA expands
