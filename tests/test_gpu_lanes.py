@@ -119,3 +119,19 @@ def test_lanes_auto_window_sweep(rmat):
         for q in (0, 13, 31):
             assert np.array_equal(auto[q], o.query(kind, src, wins[q].t_a, wins[q].t_b, 1))
     g.close()
+
+
+def test_lanes_window_sweep_at_scale():
+    # a one-source sweep of 24 windows on a 2^20-vertex graph (AUTO: lane engine,
+    # host results through the staged path) equals the queries one by one
+    gen = T.GenConfig.rmat(20, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 5, cube_root_starts=True)
+    g = T.TemporalGraph.generate(gen, True, T.EngineConfig(index_cutoff=256))
+    src = int(np.argmax(g.degrees(T.Direction.OUT)))
+    wins = [T.QueryWindow(20_000 * i, 999_999 - 10_000 * i) for i in range(24)]
+    for kind in ("earliest_arrival", "latest_departure"):
+        v = src if kind == "earliest_arrival" else int(np.argmax(g.degrees(T.Direction.IN)))
+        batch = T.query_batch(g, kind, [v] * 24, wins)
+        for q in (0, 7, 23):
+            fn = T.earliest_arrival if kind == "earliest_arrival" else T.latest_departure
+            assert np.array_equal(batch[q], fn(g, v, wins[q]).values), (kind, q)
+    g.close()
