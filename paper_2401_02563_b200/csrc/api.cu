@@ -384,7 +384,10 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool need_r) {
             dalloc<QueryParam>(w.params, Q) && dalloc<Seed>(w.seeds, Q);
   if (ok && need_r) ok = dalloc<int32_t>(w.R, slots) != nullptr;
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (traversal workspace)");
-  if (slots > w.slots) w.xinv = false;  // X / EP may have been reallocated
+  if (slots > w.slots) {  // X / EP / params / seeds may have been reallocated
+    w.xinv = false;
+    w.up_cache.clear();
+  }
   w.slots = std::max(w.slots, slots);
   return TGXD_OK;
 }
@@ -593,6 +596,7 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
     ok = dalloc<long long>(w.eval, qcap) && dalloc<long long>(w.ey, G->n + 1);
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (edge-state workspace)");
   TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), sizeof(Seed), cudaMemcpyHostToDevice, s));
+  w.up_cache.clear();  // seeds rewritten here
   init_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
       w.X.as<int32_t>(), w.EP.as<int2>(), kind == kEdgeFastest ? w.R.as<int32_t>() : nullptr,
       G->n);
@@ -759,10 +763,28 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   if (bfs && mode != TGXD_MODE_DENSE) mode = TGXD_MODE_SPARSE;
   const DevCsr& g = P.kind == TGXD_LATEST_DEPARTURE ? G->in : G->out;
   const uint64_t slots = (uint64_t)P.Q * G->n;
-  TGXD_CUDA(cudaMemcpyAsync(w.params.p, P.qp.data(), P.Q * sizeof(QueryParam),
-                            cudaMemcpyHostToDevice, s));
-  TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), P.Q * sizeof(Seed), cudaMemcpyHostToDevice,
-                            s));
+  {  // the query's parameters and seeds, unless the device already holds them
+    std::vector<int64_t> key;
+    key.reserve(6 * P.Q + 3);
+    key.push_back((int64_t)P.Q);
+    key.push_back((int64_t)(uintptr_t)w.params.p);
+    key.push_back((int64_t)(uintptr_t)w.seeds.p);
+    for (uint32_t q = 0; q < P.Q; ++q) {
+      key.push_back(P.qp[q].root);
+      key.push_back(P.qp[q].klo);
+      key.push_back(P.qp[q].vhi);
+      key.push_back(P.qp[q].depart);
+      key.push_back(P.seeds[q].root);
+      key.push_back(P.seeds[q].value);
+    }
+    if (key != w.up_cache) {
+      TGXD_CUDA(cudaMemcpyAsync(w.params.p, P.qp.data(), P.Q * sizeof(QueryParam),
+                                cudaMemcpyHostToDevice, s));
+      TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), P.Q * sizeof(Seed),
+                                cudaMemcpyHostToDevice, s));
+      w.up_cache.swap(key);
+    }
+  }
   const uint32_t ncand = (uint32_t)P.cand_key.size();
   if (fast && ncand) {
     if (!dalloc<uint32_t>(w.cand_lo, ncand) || !dalloc<uint32_t>(w.cand_cnt, ncand) ||

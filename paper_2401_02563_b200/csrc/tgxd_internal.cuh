@@ -74,6 +74,9 @@ struct Workspace {
   // only [0, xdirty) where X is finite instead of writing every slot
   bool xinv = false;
   uint64_t xdirty = 0;
+  // query parameters / seeds last uploaded to params / seeds (api.cu launch:
+  // a repeated query skips its two small host-to-device copies)
+  std::vector<int64_t> up_cache;
   // lane-per-query batches (lanes.cuh): vertex-major labels, ranges, dirty masks
   DeviceBuffer lxm, leb, ldirty;
   DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
