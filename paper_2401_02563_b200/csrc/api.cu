@@ -817,11 +817,17 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   // touched (X finite) instead of initializing every slot (config 3's batch:
   // 134M slots, 1.6 GB of writes); everything else initializes in full
   const bool lazy = !fast && !bfs && mode != TGXD_MODE_ASYNC && !getenv("TGXD_FULL_INIT");
+  bool seeded = false;
   if (lazy) {
     if (!w.xinv) {
       init_kernel<<<grid_for(w.slots, G->sm_count), 256, 0, s>>>(w.X.as<int32_t>(),
                                                                   w.EP.as<int2>(), nullptr, w.slots);
       w.xinv = true;
+    } else if (P.Q == 1) {  // reset + seed in one launch
+      reset_seed_kernel<<<grid_for(std::max<uint64_t>(w.xdirty / 4, 1), G->sm_count), 256, 0, s>>>(
+          w.X.as<int32_t>(), w.EP.as<int2>(), w.xdirty, P.qp[0].root, P.qp[0].klo,
+          w.fa.as<uint32_t>(), w.ctl.as<Control>());
+      seeded = true;
     } else if (w.xdirty) {
       reset_kernel<<<grid_for(w.xdirty, G->sm_count), 256, 0, s>>>(w.X.as<int32_t>(),
                                                                     w.EP.as<int2>(), w.xdirty);
@@ -832,9 +838,10 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
         w.X.as<int32_t>(), w.EP.as<int2>(), fast || bfs ? w.R.as<int32_t>() : nullptr, slots);
     w.xinv = false;
   }
-  seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
-                                                 w.X.as<int32_t>(), w.fa.as<uint32_t>(),
-                                                 w.ctl.as<Control>(), fast);
+  if (!seeded)
+    seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
+                                                   w.X.as<int32_t>(), w.fa.as<uint32_t>(),
+                                                   w.ctl.as<Control>(), fast);
   if (mode == TGXD_MODE_ASYNC) {
     const int rc = launch_async(G, P, g, ncand, ev_k0, ev_k1);
     if (rc) return rc;

@@ -1545,6 +1545,51 @@ __global__ void reset_kernel(int32_t* X, int2* EP, size_t nl) {
   }
 }
 
+// One query (Q == 1) on the lazy path: reset_kernel and seed_kernel in one
+// launch. The thread that resets the root's slot group writes the seed after
+// it (a root beyond the dirty range is written by thread 0: that slot is
+// clean); thread 0 also resets the counters and queues the root.
+__global__ void reset_seed_kernel(int32_t* X, int2* EP, size_t nl, uint32_t root, int32_t klo,
+                                  uint32_t* fa, Control* ctl) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t n4 = nl / 4;
+  for (size_t i = tid; i < n4; i += stride) {
+    const int4 x = reinterpret_cast<const int4*>(X)[i];
+    if (x.x != kInf || x.y != kInf || x.z != kInf || x.w != kInf) {
+      reinterpret_cast<int4*>(X)[i] = make_int4(kInf, kInf, kInf, kInf);
+      const int4 e2 = make_int4(kInf, (int32_t)kNoPos, kInf, (int32_t)kNoPos);
+      reinterpret_cast<int4*>(EP)[2 * i] = e2;
+      reinterpret_cast<int4*>(EP)[2 * i + 1] = e2;
+    }
+    if (root / 4 == i) X[root] = klo;
+  }
+  for (size_t i = n4 * 4 + tid; i < nl; i += stride) {
+    if (X[i] != kInf) {
+      X[i] = kInf;
+      EP[i] = make_int2(kInf, (int32_t)kNoPos);
+    }
+    if (i == root) X[root] = klo;
+  }
+  if (tid == 0) {
+    if (root >= nl) X[root] = klo;
+    fa[0] = root;
+    ctl->pushes = 1;
+    ctl->improved = 1;
+    ctl->chunks = 0;
+    ctl->smalls = 0;
+    ctl->edges = 0;
+    ctl->expansions = 0;
+    ctl->index_lookups = 0;
+    ctl->pull_scanned = 0;
+    ctl->pchunks = 0;
+    ctl->handoff_n = 0;
+    ctl->error = 0;
+    ctl->bar_count = 0;
+    ctl->bar_gen = 0;
+  }
+}
+
 // Seeds: X[root] = klo (EA: t_a, LD: -t_b), root queued as round-0 frontier.
 __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_t* X,
                             uint32_t* fa, Control* ctl, int fastest) {
