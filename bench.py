@@ -7,7 +7,9 @@ Metric (BASELINE.json): temporal edges traversed per second (TEPS) on one
 B200, TEPS = E_adm / t with E_adm the admissible window edges of the reached
 vertices, plus the roofline of the traversal kernel against
 the measured HBM copy bandwidth. A step is one EA query over the whole
-device-resident graph (labels re-initialised every step).
+device-resident graph; the steps rotate over 8 seeded non-isolated sources
+(the first is config 2's own), so every step is a distinct query: its
+parameters are uploaded and the previous query's labels reset.
 
 N > 1 runs N independent replicas (one process per GPU, no data-path
 collective: the path does not shard); value = all ranks'
@@ -130,104 +132,144 @@ def profile_traffic():
     return None
 
 
-def pick_queries(T, g, wl):
-    out_deg = g.degrees(T.Direction.OUT)
-    in_deg = g.degrees(T.Direction.IN)
-    return wl.queries(out_deg, in_deg, g.vertex_count())
+def bench_config(wl, queries, n, m, work):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": f"{CONFIG}: {wl.describe}",
+            "stream": f"{len(queries)} seeded non-isolated sources (the first is config 2's "
+                      "own), one EA query per step in turn",
+            "sources": [q.vertex for q in queries],
+            "window": [queries[0].window.t_a, queries[0].window.t_b], "n": n, "m": m,
+            "e_adm": [e for e, _ in work], "v_reached": [r for _, r in work],
+            "l2": "inputs larger than L2 (edge arrays 12 B/edge x 67M = 805 MB)"}
 
 
-def cpu_reference_run(wl, edges, n, q, threads, steps, warmup):
+def stream_edges(work, steps):
+    """Edges traversed by `steps` steps of the rotation (step i: query i mod k)."""
+    k = len(work)
+    return sum(work[i % k][0] for i in range(steps))
+
+
+def cpu_reference_run(wl, edges, n, queries, threads, steps, warmup):
     """Times the reference library (oracle/_ref, compiled unmodified from the
-    reference sources) on the same edge list and query: returns per-query s."""
+    reference sources) on the same edge list over the query rotation: returns
+    per-step seconds and the labels of the rotation's queries."""
     from oracle.pyoracle import Reference
 
     Reference.set_workers(threads)
     t0 = time.perf_counter()
     ref = Reference(edges, n, True, wl.index_cutoff)
     build_s = time.perf_counter() - t0
-    labels = None
-    for _ in range(warmup):
-        labels = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+    k = len(queries)
+    labels = {}
+    for i in range(warmup):
+        q = queries[i % k]
+        labels[i % k] = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
     times = []
-    for _ in range(steps):
+    for i in range(steps):
+        q = queries[i % k]
         t = time.perf_counter()
-        labels = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+        labels[i % k] = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
         times.append(time.perf_counter() - t)
+    for i, q in enumerate(queries):  # untimed: labels of queries the steps did not reach
+        if i not in labels:
+            labels[i] = ref.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
     ref.close()
     return times, build_s, labels
 
 
+def reference_work(edges, n, queries, labels):
+    """(E_adm, V_reached) per rotation query from the reference's labels
+    (the C restatement's tgxo_work)."""
+    from oracle.pyoracle import Oracle
+    o = Oracle(edges, n)
+    out = [o.work(q.kind, q.vertex, q.window.t_a, q.window.t_b, labels[i])
+           for i, q in enumerate(queries)]
+    o.close()
+    return out
+
+
 def run_reference(args):
+    """The reference arm: the reference library's CPU path on the host cores.
+    Only oracle/ is loaded (the edge list comes from the checker's own
+    generator, oracle/tgx_gen.c): libtgxd.so never enters this process."""
     rank, world, _ = _dist()
     if rank != 0:
         return 0
-    import paper_2401_02563_b200 as T
-    from paper_2401_02563_b200.configs import workload
-    from oracle.pyoracle import Oracle, Reference
+    from paper_2401_02563_b200.configs import c2_rotation, workload  # pure Python
+    from oracle.pyoracle import Reference, generate
 
     if not Reference.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtgxref.so missing"}))
         return 0
     wl = workload(CONFIG)
-    edges = T.generate_edges(wl.gen)
+    edges = generate(wl.gen)
     n = wl.gen.n_vertices
-    out_deg = np.bincount(edges[0], minlength=n)
-    in_deg = np.bincount(edges[1], minlength=n)
-    q = wl.queries(out_deg, in_deg, n)[0]
+    queries = c2_rotation(np.bincount(edges[0], minlength=n))
     threads = os.cpu_count() or 1
-    times, build_s, labels = cpu_reference_run(wl, edges, n, q, threads, args.steps, args.warmup)
-    o = Oracle(edges, n)
-    e_adm, v_reached = o.work(q.kind, q.vertex, q.window.t_a, q.window.t_b, labels)
-    o.close()
-    t = sum(times) / len(times)
-    value = e_adm / t
+    warm = args.warmup
+    times, build_s, labels = cpu_reference_run(wl, edges, n, queries, threads, args.steps, warm)
+    work = reference_work(edges, n, queries, labels)
+    t = sum(times)
+    value = stream_edges(work, args.steps) / t
     line = {
         "impl": "reference",
         "metric": "temporal edges traversed/sec (TEPS)",
         "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "warmup": warm, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{CONFIG}: {wl.describe}", "source": q.vertex,
-                   "window": [q.window.t_a, q.window.t_b], "n": n, "m": int(len(edges[0])),
-                   "e_adm": e_adm, "v_reached": v_reached, "graph_build_s": build_s},
+        "config": bench_config(wl, queries, n, int(len(edges[0])), work),
+        "graph_build_s": build_s,
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} full {CONFIG} EA queries"},
+                         "sample": f"{args.steps} EA queries of the {len(queries)}-source "
+                                   f"{CONFIG} rotation"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_libs": loaded_native_libs(),
     }
     print(json.dumps(line))
     return 0
 
 
+def loaded_native_libs():
+    """The repo's shared libraries mapped into this process."""
+    libs = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            path = ln.split()[-1] if ln.strip() else ""
+            if path.endswith(".so") and str(ROOT) in path:
+                libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_ours(args):
     rank, world, local = _dist()
     import paper_2401_02563_b200 as T
-    from paper_2401_02563_b200.configs import workload
+    from paper_2401_02563_b200.configs import c2_rotation, workload
 
+    import torch
+    torch.cuda.set_device(local)
     dist = None
     if world > 1:
-        import torch
         import torch.distributed as dist_mod
-        torch.cuda.set_device(local)
         dist_mod.init_process_group("nccl")
         dist = dist_mod
-    else:
-        try:
-            import torch
-            torch.cuda.set_device(local)
-        except Exception:
-            torch = None
-    import torch  # noqa: F811
 
     lib = T.load_library()
     wl = workload(CONFIG)
     g = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
-    q = pick_queries(T, g, wl)[0]
     n = g.vertex_count()
+    queries = c2_rotation(g.degrees(T.Direction.OUT))
+    srcs = [q.vertex for q in queries]
+    wins = [q.window for q in queries]
+    k = len(queries)
 
-    # unit of work from the final labels (untimed)
-    T.query_batch(g, q.kind, [q.vertex], [q.window], width=4)
-    e_adm, v_reached = T.last_work(g, 0)
+    # unit of work of every rotation query from its final labels (untimed)
+    work = []
+    for q in queries:
+        T.query_batch(g, q.kind, [q.vertex], [q.window], width=4)
+        work.append(T.last_work(g, 0))
 
     def barrier():
         if dist:
@@ -237,75 +279,72 @@ def run_ours(args):
     sampler = ClockSampler(local)
     barrier()
     with sampler:
-        total_ms, kernel_ms = T.time_queries(g, q.kind, [q.vertex], [q.window],
-                                             warmup=args.warmup, steps=args.steps)
+        total_ms, kernel_ms = T.time_rotation(g, "earliest_arrival", srcs, wins,
+                                              warmup=args.warmup, steps=args.steps)
     barrier()
     ms_step, kernel_ms = max_over_ranks([total_ms / args.steps, kernel_ms], dist, "cuda")
-    value = whole_job_teps(world, e_adm, ms_step)
+    edges_per_rank = stream_edges(work, args.steps)
+    value = world * edges_per_rank / (ms_step * args.steps * 1e-3)
 
-    # end to end through the reference-facing C-ABI call with a host output
-    # (int64 PathResult values): H2D of the query, D2H of the labels per step
-    # the caller's result buffer is pinned host memory (page-locked: the D2H of
-    # the 33.5 MB int64 vector runs at PCIe speed instead of through staging)
-    pinned_ptr = None
-    if os.environ.get("BENCH_PINNED_OUT"):
-        pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
-        out = pinned.numpy()
-        pinned_ptr = out.ctypes.data
-    else:  # an ordinary (pageable) result array, as a reference caller has
-        out = np.empty(n, np.int64)
+    # end to end through the reference-facing C-ABI call (earliest_arrival
+    # with an int64 PathResult in an ordinary host array): every step uploads
+    # its query and reads its labels back, the rotation's sources in turn
+    out = np.empty(n, np.int64)
     import ctypes
-    for _ in range(args.warmup):
+    optr = out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+    def ea(i):
+        q = queries[i % k]
         T._check(lib.tgxd_earliest_arrival(g.handle, q.vertex, q.window.t_a, q.window.t_b, 1,
-                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                                           None))
+                                           optr, None))
+
+    for i in range(args.warmup):
+        ea(i)
+    h2d = d2h = 0
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        T._check(lib.tgxd_earliest_arrival(g.handle, q.vertex, q.window.t_a, q.window.t_b, 1,
-                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                                           None))
+    for i in range(args.steps):
+        ea(i)
+        h2d += T.last_h2d_bytes(g)
+        d2h += T.last_d2h_bytes(g)
     barrier()
     e2e_s = max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, "cuda")[0]
-    d2h_bytes = T.last_d2h_bytes(g)  # int32 labels + the tail's patch pairs
-    e2e_value = whole_job_teps(world, e_adm, e2e_s * 1e3)
+    e2e_value = world * edges_per_rank / (e2e_s * args.steps)
+
+    # continuity with earlier rounds: config 2's own source repeated
+    tot1, ker1 = T.time_queries(g, "earliest_arrival", [srcs[0]], [wins[0]], warmup=3,
+                                steps=args.steps)
 
     peak, peak_kind = measured_peak()
-    b_alg = 16 * e_adm + 12 * v_reached + 4 * n
-    achieved = b_alg / (kernel_ms * 1e-3) / 1e9
-    traffic = profile_traffic()
+    b_alg = [16 * e + 12 * r + 4 * n for e, r in work]  # SURVEY.md 8(d), per query
+    b_steps = sum(b_alg[i % k] for i in range(args.steps))
+    achieved = b_steps / (kernel_ms * args.steps * 1e-3) / 1e9
+    kernels = ["reset_seed_kernel", "traverse_kernel", "async_kernel", "convert_kernel"]
     line = {
         "metric": "temporal edges traversed/sec (TEPS)",
         "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{CONFIG}: {wl.describe}", "source": q.vertex,
-                   "window": [q.window.t_a, q.window.t_b], "n": n, "m": g.edge_count(),
-                   "e_adm": e_adm, "v_reached": v_reached,
-                   "l2": "inputs larger than L2 (edge arrays 12 B/edge x 67M = 805 MB)",
-                   "parallelism": f"replicas x{world}"},
+        "config": bench_config(wl, queries, n, g.edge_count(), work),
+        "parallelism": f"replicas x{world}",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": profile_traffic(),
                      "kernel": "traverse_kernel (+ async_kernel tail)", "kernel_ms": kernel_ms,
                      "timed": "CUDA events on the graph stream around the traversal kernels",
-                     "algorithmic_bytes": b_alg, "peak_kind": peak_kind},
-        "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 56,
-                "host_buffer": "pinned" if out.ctypes.data == pinned_ptr else "pageable",
-                # the library moves int32 labels over PCIe in chunks (starting
-                # while the async tail still runs; the tail's changes follow as
-                # a patch list) and widens them into the caller's int64 array
-                "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_s * 1e3},
-        # per timed step: reset_kernel (the previous query's reached slots back
-        # to INF), seed_kernel, traverse_kernel, async_kernel (the tail
-        # continuation, exits at once when the rounds finished the query),
-        # convert_kernel
-        "gpu_launches": 5 * args.steps,
-        "kernels_per_step": ["reset_kernel", "seed_kernel", "traverse_kernel", "async_kernel",
-                             "convert_kernel"],
+                     "algorithmic_bytes_per_step": b_steps / args.steps,
+                     "algorithmic_bytes_per_query": b_alg, "peak_kind": peak_kind},
+        "e2e": {"value": e2e_value, "unit": "edges/s",
+                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                "host_buffer": "pageable", "ms_per_step": e2e_s * 1e3,
+                "call": "tgxd_earliest_arrival (int64 PathResult values in host memory)"},
+        "single_source": {"source": srcs[0], "ms_per_step": tot1 / args.steps,
+                          "kernel_ms": ker1, "value": work[0][0] / (tot1 / args.steps * 1e-3)},
+        "gpu_launches": len(kernels) * args.steps,
+        "kernels_per_step": kernels,
         "clocks": sampler.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(wl, q, n)
+        line["cpu_baseline"] = cpu_baseline(wl, queries, n, work)
     if rank == 0:
         print(json.dumps(line))
     g.close()
@@ -314,30 +353,32 @@ def run_ours(args):
     return 0
 
 
-def cpu_baseline(wl, q, n):
-    """The reference CPU path on the box's host cores, one full C2 query
-    (graph generation and build untimed), or the C oracle if the reference
-    library did not travel."""
-    import paper_2401_02563_b200 as T
-    from oracle.pyoracle import Oracle, Reference
+def cpu_baseline(wl, queries, n, work):
+    """The reference CPU path on the box's host cores over one pass of the
+    rotation after one warm-up query (graph generation and build untimed, as
+    `tgx run` does, tools/tgx.cpp:341-376), or the C oracle (one thread) if
+    the reference library did not travel."""
+    from oracle.pyoracle import Oracle, Reference, generate
 
-    edges = T.generate_edges(wl.gen)
+    edges = generate(wl.gen)
     threads = os.cpu_count() or 1
+    k = len(queries)
     if Reference.available():
-        times, _, labels = cpu_reference_run(wl, edges, n, q, threads, 1, 0)
+        times, _, _ = cpu_reference_run(wl, edges, n, queries, threads, k, 1)
         kind = "reference"
     else:
         o = Oracle(edges, n)
-        t = time.perf_counter()
-        labels = o.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
-        times = [time.perf_counter() - t]
+        times = []
+        for q in queries:
+            t = time.perf_counter()
+            o.query(q.kind, q.vertex, q.window.t_a, q.window.t_b)
+            times.append(time.perf_counter() - t)
         o.close()
         kind, threads = "port", 1
-    o = Oracle(edges, n)
-    e_adm, _ = o.work(q.kind, q.vertex, q.window.t_a, q.window.t_b, labels)
-    o.close()
-    return {"value": e_adm / times[0], "unit": "edges/s", "cores": threads, "kind": kind,
-            "sample": f"1 full {CONFIG} EA query ({times[0]:.3f} s)"}
+    return {"value": stream_edges(work, k) / sum(times), "unit": "edges/s", "cores": threads,
+            "kind": kind,
+            "sample": f"one pass of the {k}-query {CONFIG} rotation after 1 warm-up "
+                      f"({sum(times):.2f} s, median query {statistics.median(times):.3f} s)"}
 
 
 def main():

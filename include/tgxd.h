@@ -174,12 +174,24 @@ int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reach
  * {slot, label} patch pairs (8 B each) written through mapped memory. */
 int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes);
 
+/* Bytes the LAST query moved host -> device: its parameters and seeds (only
+ * when they differ from what the device already holds) and fastest's
+ * candidate lists. */
+int tgxd_last_h2d_bytes(tgxd_graph* g, uint64_t* bytes);
+
 /* Device time of `steps` back-to-back queries with device-resident output,
  * after `warmup` untimed ones: total ms (CUDA events on the handle's stream)
  * and the mean traversal-kernel ms per query. */
 int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
                       const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode,
                       int warmup, int steps, float* total_ms, float* kernel_ms);
+
+/* Same, but step i answers the single query i mod k (a rotation over k
+ * sources / windows: every step uploads its own parameters and resets the
+ * previous query's labels, as a stream of distinct queries does). */
+int tgxd_time_rotation(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
+                       const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode,
+                       int warmup, int steps, float* total_ms, float* kernel_ms);
 
 /* Diagnostics: record a per-round trace of the next queries, max_rounds = 0
  * disables. tgxd_get_trace writes 12 u64 per round: globaltimer (ns) at round

@@ -133,6 +133,37 @@ class Oracle:
             pass
 
 
+class _GenConfig(ctypes.Structure):      # tgxo_gen_config (= tgxd_gen_config's layout)
+    _fields_ = [("kind", ctypes.c_int), ("scale", ctypes.c_uint32), ("n", ctypes.c_uint32),
+                ("m", ctypes.c_uint64), ("a", ctypes.c_double), ("b", ctypes.c_double),
+                ("c", ctypes.c_double), ("start_dist", ctypes.c_int),
+                ("t_range", ctypes.c_uint32), ("geo_p", ctypes.c_double),
+                ("seed", ctypes.c_uint64)]
+
+
+def generate(gen):
+    """The BASELINE workload edge list from the checker's own generator
+    (tgx_gen.c): (src u32, dst u32, start u64, end u64). `gen` is any object
+    with the generator fields (e.g. the package's GenConfig)."""
+    lib = Oracle.lib()
+    c = _GenConfig(*(getattr(gen, f) for f, _ in _GenConfig._fields_))
+    fn = lib.tgxo_generate
+    fn.argtypes = [_P(_GenConfig), ctypes.c_uint64, _u64p, _u32p, _u32p, _u64p, _u64p]
+    fn.restype = ctypes.c_int
+    m = ctypes.c_uint64()
+    Oracle._check(fn(ctypes.byref(c), 0, ctypes.byref(m), None, None, None, None)
+                  if c.kind == 0 else 0)
+    cap = int(m.value) if c.kind == 0 else int(c.m)
+    s = np.empty(cap, np.uint32)
+    d = np.empty(cap, np.uint32)
+    a = np.empty(cap, np.uint64)
+    b = np.empty(cap, np.uint64)
+    Oracle._check(fn(ctypes.byref(c), cap, ctypes.byref(m), s.ctypes.data_as(_u32p),
+                     d.ctypes.data_as(_u32p), a.ctypes.data_as(_u64p), b.ctypes.data_as(_u64p)))
+    k = int(m.value)
+    return s[:k], d[:k], a[:k], b[:k]
+
+
 def digest(values: np.ndarray) -> int:
     v = np.ascontiguousarray(values, np.int64)
     return int(Oracle.lib().tgxo_digest(v.ctypes.data_as(_i64p), len(v)))

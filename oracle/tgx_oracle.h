@@ -55,6 +55,22 @@ int tgxo_fit_cost_constants(uint64_t k, const uint64_t* degree, const uint64_t* 
                             double* c_prime);
 const char* tgxo_last_error(void);
 
+/* The BASELINE workload generator (tgx_gen.c); same field layout as the
+ * product's tgxd_gen_config so one ctypes structure serves both. */
+typedef struct tgxo_gen_config {
+  int kind; /* 0 uniform, 1 RMAT */
+  uint32_t scale;
+  uint32_t n;
+  uint64_t m;
+  double a, b, c;
+  int start_dist; /* 0 uniform, 1 cube root */
+  uint32_t t_range;
+  double geo_p;
+  uint64_t seed;
+} tgxo_gen_config;
+int tgxo_generate(const tgxo_gen_config* c, uint64_t capacity, uint64_t* m_out, uint32_t* src,
+                  uint32_t* dst, uint64_t* start, uint64_t* end);
+
 #ifdef __cplusplus
 }
 #endif

@@ -232,6 +232,10 @@ def load_library() -> ctypes.CDLL:
                         ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, _P(_Stats)], ctypes.c_int),
         "tgxd_last_work": ([vp, ctypes.c_uint32, _u64p, _u64p], ctypes.c_int),
         "tgxd_last_d2h_bytes": ([vp, _u64p], ctypes.c_int),
+        "tgxd_last_h2d_bytes": ([vp, _u64p], ctypes.c_int),
+        "tgxd_time_rotation": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
         "tgxd_time_queries": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p,
                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
@@ -344,9 +348,15 @@ class TemporalGraph:
         return v
 
     def close(self) -> None:
-        for v in getattr(self, "_views", []):
+        for v in list(getattr(self, "_views", [])):
             v.close()
         self._views = []
+        parent = getattr(self, "_parent", None)
+        if parent is not None:  # a closed view leaves its parent's list
+            pv = getattr(parent, "_views", [])
+            if self in pv:
+                pv.remove(self)
+            self._parent = None
         if self._h and self._h.value:
             load_library().tgxd_graph_destroy(self._h)
             self._h = ctypes.c_void_p()
@@ -493,6 +503,13 @@ def last_d2h_bytes(g: TemporalGraph) -> int:
     return b.value
 
 
+def last_h2d_bytes(g: TemporalGraph) -> int:
+    """Bytes the last query moved host -> device (parameters, seeds, candidates)."""
+    b = ctypes.c_uint64()
+    _check(load_library().tgxd_last_h2d_bytes(g.handle, ctypes.byref(b)))
+    return b.value
+
+
 def last_work(g: TemporalGraph, q: int = 0) -> tuple[int, int]:
     """(E_adm, V_reached) of slot q of the last query on g."""
     e = ctypes.c_uint64()
@@ -517,6 +534,26 @@ def time_queries(g: TemporalGraph, kind: str, vertices: Sequence[int],
                                             _ptr(tb, ctypes.c_uint64), int(ordering), int(mode),
                                             warmup, steps, ctypes.byref(tot),
                                             ctypes.byref(ker)))
+    return tot.value, ker.value
+
+
+def time_rotation(g: TemporalGraph, kind: str, vertices: Sequence[int],
+                  windows: Sequence[QueryWindow], ordering: Optional[Ordering] = None,
+                  mode: Mode = Mode.AUTO, warmup: int = 3,
+                  steps: int = 10) -> tuple[float, float]:
+    """Like time_queries, but step i is the single query i mod k (a stream of
+    distinct queries): (total ms, mean traversal-kernel ms per step)."""
+    v = np.ascontiguousarray(vertices, np.uint32)
+    ta = np.array([w.t_a for w in windows], np.uint64)
+    tb = np.array([w.t_b for w in windows], np.uint64)
+    tot = ctypes.c_float()
+    ker = ctypes.c_float()
+    ordering = g.ordering() if ordering is None else ordering
+    _check(load_library().tgxd_time_rotation(g.handle, KINDS[kind], len(v),
+                                             _ptr(v, ctypes.c_uint32), _ptr(ta, ctypes.c_uint64),
+                                             _ptr(tb, ctypes.c_uint64), int(ordering), int(mode),
+                                             warmup, steps, ctypes.byref(tot),
+                                             ctypes.byref(ker)))
     return tot.value, ker.value
 
 

@@ -79,6 +79,14 @@ def _c5(out_deg, in_deg, n):
     return qs
 
 
+def c2_rotation(out_deg: np.ndarray, k: int = 8) -> List[Query]:
+    """The bench's query stream on config 2: k seeded non-isolated sources
+    (the first is config 2's own source), EA over [0, 999999], one query per
+    step in turn — distinct queries, as a serving stream has."""
+    srcs = _pick(_rng(2), out_deg > 0, k)
+    return [Query("earliest_arrival", int(s), QueryWindow(0, 999_999)) for s in srcs]
+
+
 def workload(name: str, scale_delta: int = 0) -> Workload:
     """A BASELINE workload; scale_delta < 0 shrinks the graph (parity tests at
     oracle-friendly sizes) while keeping its distributions."""

@@ -24,6 +24,7 @@
 #include "edges.cuh"
 #include "sd.cuh"
 #include "lanes.cuh"
+#include "candidates.cuh"
 #include "costmodel.cuh"
 
 namespace tgxd {
@@ -270,9 +271,6 @@ struct Prepared {
   uint32_t Q;
   std::vector<QueryParam> qp;
   std::vector<Seed> seeds;
-  // fastest
-  std::vector<uint32_t> cand_lo, cand_cnt;
-  std::vector<int32_t> cand_key;
 };
 
 // Validation in the reference's order: require_vertex (out_of_range), then
@@ -329,46 +327,29 @@ static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, c
   return TGXD_OK;
 }
 
-// Candidate departures of a fastest query (path_algorithms.cpp:449-458):
-// distinct starts of the source's window out-edges, descending. Each
-// candidate's seed range is its whole key group; the relax step applies the
-// end <= t_b filter, so a group whose edges all end too late seeds nothing.
-static int fastest_candidates(tgxd_graph* G, Prepared& P) {
-  const QueryParam& p = P.qp[0];
-  const uint32_t src = P.seeds[0].root;
-  uint32_t se[2];
-  TGXD_CUDA(cudaMemcpyAsync(se, G->out.off + src, 8, cudaMemcpyDeviceToHost, G->stream));
+__global__ void max_degree_kernel(const uint32_t* off, uint32_t n, unsigned int* out) {
+  unsigned int m = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    m = max(m, off[v + 1] - off[v]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// Largest out-degree (once per graph): sizes the device candidate lists of
+// fastest queries (candidates.cuh) and bounds their watchdog.
+static int ensure_max_out_degree(tgxd_graph* G) {
+  if (G->max_out_deg_known) return TGXD_OK;
+  DeviceBuffer tmp;
+  unsigned int* d = dalloc<unsigned int>(tmp, 1);
+  if (!d) return fail(TGXD_ERR_CUDA, "allocation (max degree)");
+  TGXD_CUDA(cudaMemsetAsync(d, 0, 4, G->stream));
+  if (G->n)
+    max_degree_kernel<<<grid_for(G->n, G->sm_count), 256, 0, G->stream>>>(G->out.off, G->n, d);
+  unsigned int h = 0;
+  TGXD_CUDA(cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, G->stream));
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
-  const uint32_t deg = se[1] - se[0];
-  std::vector<int32_t> key(deg), val(deg);
-  std::vector<uint2> pay(deg);
-  if (deg) {
-    TGXD_CUDA(cudaMemcpyAsync(key.data(), G->out.key + se[0], deg * 4ull, cudaMemcpyDeviceToHost,
-                              G->stream));
-    TGXD_CUDA(cudaMemcpyAsync(pay.data(), G->out.pay + se[0], deg * 8ull, cudaMemcpyDeviceToHost,
-                              G->stream));
-    TGXD_CUDA(cudaStreamSynchronize(G->stream));
-    for (uint32_t i = 0; i < deg; ++i) val[i] = (int32_t)pay[i].y;
-  }
-  P.cand_lo.clear();
-  P.cand_cnt.clear();
-  P.cand_key.clear();
-  uint32_t i = deg;
-  while (i > 0) {  // walk key groups from the top
-    uint32_t j = i;
-    const int32_t kv = key[i - 1];
-    bool any = false;
-    while (j > 0 && key[j - 1] == kv) {
-      any |= val[j - 1] <= p.vhi;
-      --j;
-    }
-    if (kv >= p.klo && kv <= p.vhi && any) {
-      P.cand_lo.push_back(se[0] + j);
-      P.cand_cnt.push_back(i - j);
-      P.cand_key.push_back(kv);
-    }
-    i = j;
-  }
+  G->max_out_deg = h;
+  G->max_out_deg_known = true;
   return TGXD_OK;
 }
 
@@ -386,7 +367,7 @@ static int ensure_workspace(tgxd_graph* G, uint32_t Q, bool need_r) {
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (traversal workspace)");
   if (slots > w.slots) {  // X / EP / params / seeds may have been reallocated
     w.xinv = false;
-    w.up_cache.clear();
+    w.up_valid = false;
   }
   w.slots = std::max(w.slots, slots);
   return TGXD_OK;
@@ -509,7 +490,7 @@ static int ensure_async(tgxd_graph* G, uint32_t Q, bool required = true) {
   return TGXD_OK;
 }
 
-static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint32_t ncand,
+static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g,
                         cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
   Workspace& w = G->ws;
   cudaStream_t s = G->stream;
@@ -536,7 +517,7 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   a.strict = P.strict;
   a.cutoff = (uint32_t)std::min<uint64_t>(G->index_cutoff, 0xffffffffULL);
   a.fastest = fast ? 1 : 0;
-  a.n_cand = ncand;
+  a.n_cand = w.cand_n.as<uint32_t>();
   a.cand_lo = w.cand_lo.as<uint32_t>();
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
@@ -547,7 +528,7 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   a.hctl = nullptr;
   a.hfa = a.hfb = nullptr;
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
-  if (!fast || ncand) {
+  {
     void* args[] = {&a};
     // 3 CTAs per SM: every idle warp polls a queue ticket, and with all 4
     // resident the polls slow the working warps (config 2: 1.7 vs 3.4 ms)
@@ -561,6 +542,28 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g, uint3
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   w.last_async = true;
+  return TGXD_OK;
+}
+
+// The one writer of the device's query parameters and seeds: uploads P's
+// unless the buffers already hold exactly these (a repeated query skips two
+// small copies). ensure_workspace drops the record whenever it may have
+// reallocated the buffers.
+static int upload_query(tgxd_graph* G, const Prepared& P) {
+  Workspace& w = G->ws;
+  const size_t nq = P.Q * sizeof(QueryParam), ns = P.Q * sizeof(Seed);
+  const bool same = w.up_valid && w.up_qp.size() == nq && w.up_seeds.size() == ns &&
+                    std::memcmp(w.up_qp.data(), P.qp.data(), nq) == 0 &&
+                    std::memcmp(w.up_seeds.data(), P.seeds.data(), ns) == 0;
+  if (same) return TGXD_OK;
+  TGXD_CUDA(cudaMemcpyAsync(w.params.p, P.qp.data(), nq, cudaMemcpyHostToDevice, G->stream));
+  TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), ns, cudaMemcpyHostToDevice, G->stream));
+  const char* a = reinterpret_cast<const char*>(P.qp.data());
+  const char* b = reinterpret_cast<const char*>(P.seeds.data());
+  w.up_qp.assign(a, a + nq);
+  w.up_seeds.assign(b, b + ns);
+  w.up_valid = true;
+  w.last_h2d += nq + ns;
   return TGXD_OK;
 }
 
@@ -595,8 +598,10 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   if (ok && kind == kEdgeShortest)
     ok = dalloc<long long>(w.eval, qcap) && dalloc<long long>(w.ey, G->n + 1);
   if (!ok) return fail(TGXD_ERR_CUDA, "device allocation failed (edge-state workspace)");
-  TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), sizeof(Seed), cudaMemcpyHostToDevice, s));
-  w.up_cache.clear();  // seeds rewritten here
+  {
+    const int rc = upload_query(G, P);
+    if (rc) return rc;
+  }
   init_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
       w.X.as<int32_t>(), w.EP.as<int2>(), kind == kEdgeFastest ? w.R.as<int32_t>() : nullptr,
       G->n);
@@ -763,36 +768,19 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   if (bfs && mode != TGXD_MODE_DENSE) mode = TGXD_MODE_SPARSE;
   const DevCsr& g = P.kind == TGXD_LATEST_DEPARTURE ? G->in : G->out;
   const uint64_t slots = (uint64_t)P.Q * G->n;
-  {  // the query's parameters and seeds, unless the device already holds them
-    std::vector<int64_t> key;
-    key.reserve(6 * P.Q + 3);
-    key.push_back((int64_t)P.Q);
-    key.push_back((int64_t)(uintptr_t)w.params.p);
-    key.push_back((int64_t)(uintptr_t)w.seeds.p);
-    for (uint32_t q = 0; q < P.Q; ++q) {
-      key.push_back(P.qp[q].root);
-      key.push_back(P.qp[q].klo);
-      key.push_back(P.qp[q].vhi);
-      key.push_back(P.qp[q].depart);
-      key.push_back(P.seeds[q].root);
-      key.push_back(P.seeds[q].value);
-    }
-    if (key != w.up_cache) {
-      TGXD_CUDA(cudaMemcpyAsync(w.params.p, P.qp.data(), P.Q * sizeof(QueryParam),
-                                cudaMemcpyHostToDevice, s));
-      TGXD_CUDA(cudaMemcpyAsync(w.seeds.p, P.seeds.data(), P.Q * sizeof(Seed),
-                                cudaMemcpyHostToDevice, s));
-      w.up_cache.swap(key);
-    }
+  {
+    const int rc = upload_query(G, P);
+    if (rc) return rc;
   }
-  const uint32_t ncand = (uint32_t)P.cand_key.size();
-  if (fast && ncand) {
-    if (!dalloc<uint32_t>(w.cand_lo, ncand) || !dalloc<uint32_t>(w.cand_cnt, ncand) ||
-        !dalloc<int32_t>(w.cand_key, ncand))
+  if (fast) {  // candidate departures, extracted on the device (candidates.cuh)
+    if (const int rc = ensure_max_out_degree(G)) return rc;
+    const size_t cap = (size_t)G->max_out_deg + 1;
+    if (!dalloc<uint32_t>(w.cand_lo, cap) || !dalloc<uint32_t>(w.cand_cnt, cap) ||
+        !dalloc<int32_t>(w.cand_key, cap) || !dalloc<uint32_t>(w.cand_n, 1))
       return fail(TGXD_ERR_CUDA, "device allocation failed (candidates)");
-    TGXD_CUDA(cudaMemcpyAsync(w.cand_lo.p, P.cand_lo.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
-    TGXD_CUDA(cudaMemcpyAsync(w.cand_cnt.p, P.cand_cnt.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
-    TGXD_CUDA(cudaMemcpyAsync(w.cand_key.p, P.cand_key.data(), ncand * 4ull, cudaMemcpyHostToDevice, s));
+    candidates_kernel<<<1, kCandThreads, 0, s>>>(
+        G->out, w.params.as<QueryParam>(), P.seeds[0].root, w.cand_lo.as<uint32_t>(),
+        w.cand_cnt.as<uint32_t>(), w.cand_key.as<int32_t>(), w.cand_n.as<uint32_t>());
   }
   // batches of EA / LD queries: one warp lane per query (AUTO's choice)
   const bool lanes_ok = P.Q >= 2 && P.Q <= 32 && G->n <= kLanesMaxN && !fast && !bfs &&
@@ -843,7 +831,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
                                                    w.X.as<int32_t>(), w.fa.as<uint32_t>(),
                                                    w.ctl.as<Control>(), fast);
   if (mode == TGXD_MODE_ASYNC) {
-    const int rc = launch_async(G, P, g, ncand, ev_k0, ev_k1);
+    const int rc = launch_async(G, P, g, ev_k0, ev_k1);
     if (rc) return rc;
     if (out_dev) convert_for(G, P, out_dev, width);
     TGXD_CUDA(cudaGetLastError());
@@ -908,7 +896,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   }
   a.rg = P.kind == TGXD_LATEST_DEPARTURE ? G->out : G->in;
   a.fastest = fast ? 1 : 0;
-  a.n_cand = ncand;
+  a.n_cand = w.cand_n.as<uint32_t>();
   a.cand_lo = w.cand_lo.as<uint32_t>();
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
   a.cand_key = w.cand_key.as<int32_t>();
@@ -918,14 +906,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   a.wtrace_on = getenv("TGXD_WTRACE") != nullptr;
   a.trace_cap = w.trace_cap;
   a.round_limit = (uint32_t)std::min<uint64_t>(
-      0xfffffff0ULL, ((uint64_t)ncand + 1) * ((uint64_t)slots + 2) + 16);
+      0xfffffff0ULL, ((uint64_t)(fast ? G->max_out_deg : 0) + 1) * ((uint64_t)slots + 2) + 16);
   if (w.trace_host) {
     TGXD_CUDA(cudaStreamSynchronize(s));
     std::memset(w.trace_host, 0, w.trace_cap * 64ull);
     TGXD_CUDA(cudaMemsetAsync(w.wtrace.p, 0, w.trace_cap * 32ull, s));
   }
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
-  if (!fast || ncand) {
+  {
     void* args[] = {&a};
     const bool early = w.early_req && !fast && !bfs;
     if (early && a.handoff_f) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
@@ -951,7 +939,7 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       h.strict = P.strict;
       h.cutoff = a.cutoff;
       h.fastest = 0;
-      h.n_cand = 0;
+      h.n_cand = nullptr;
       h.cand_lo = nullptr;
       h.cand_cnt = nullptr;
       h.cand_key = nullptr;
@@ -972,10 +960,6 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
             w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X,
             G->patch_dev);
     }
-  } else {
-    Control z;
-    std::memset(&z, 0, sizeof z);
-    TGXD_CUDA(cudaMemcpyAsync(w.ctl.p, &z, sizeof z, cudaMemcpyHostToDevice, s));
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   if (out_dev && !w.early_done) convert_for(G, P, out_dev, width);
@@ -1136,12 +1120,17 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     if (!verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "null query arrays");
     tgxd_stats acc;
     std::memset(&acc, 0, sizeof acc);
+    uint64_t h2d = 0, d2h = 0;
     for (uint32_t q = 0; q < k; ++q) {
       char* o = static_cast<char*>(out) + (size_t)q * G->n * width;
       tgxd_stats one;
       const int rc = query_impl(G, kind, 1, verts + q, ta + q, tb + q, ordering, mode, o, width,
                                 out_on_device, &one);
       if (rc) return rc;
+      h2d += G->ws.last_h2d;
+      d2h += G->ws.last_d2h;
+      G->ws.last_h2d = h2d;
+      G->ws.last_d2h = d2h;
       acc.rounds += one.rounds;
       acc.candidates += one.candidates;
       acc.expansions += one.expansions;
@@ -1155,13 +1144,10 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   }
   std::lock_guard<std::mutex> lock(G->mu);
   TGXD_CUDA(cudaSetDevice(G->device));
+  G->ws.last_h2d = 0;
   Prepared P;
   int rc = prepare(G, kind, k, verts, ta, tb, ordering, P);
   if (rc) return rc;
-  if (kind == TGXD_FASTEST && !P.edge) {
-    rc = fastest_candidates(G, P);
-    if (rc) return rc;
-  }
   rc = ensure_workspace(G, P.Q, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS);
   if (rc) return rc;
   Workspace& w = G->ws;
@@ -1862,6 +1848,13 @@ int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes) {
   return TGXD_OK;
 }
 
+int tgxd_last_h2d_bytes(tgxd_graph* g, uint64_t* bytes) {
+  if (!g || !bytes) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  *bytes = g->ws.last_h2d;
+  return TGXD_OK;
+}
+
 int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reached) {
   if (!g || !e_adm || !v_reached) return fail(TGXD_ERR_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lock(g->mu);
@@ -1885,22 +1878,31 @@ int tgxd_last_work(tgxd_graph* g, uint32_t q, uint64_t* e_adm, uint64_t* v_reach
   return TGXD_OK;
 }
 
-int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
-                      const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode, int warmup,
-                      int steps, float* total_ms, float* kernel_ms) {
-  if (!g || !total_ms || !kernel_ms || steps < 1 || warmup < 0)
+// Device time of `steps` launches after `warmup` untimed ones, outputs in
+// HBM. rotate = false: every step is the whole k-query batch; rotate =
+// true: step i is the single query i mod k (parameters uploaded per step).
+static int time_impl(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
+                     const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode, int warmup,
+                     int steps, bool rotate, float* total_ms, float* kernel_ms) {
+  if (!g || !total_ms || !kernel_ms || steps < 1 || warmup < 0 || k == 0 || !vertices || !t_a ||
+      !t_b)
     return fail(TGXD_ERR_ARGUMENT, "bad timing arguments");
-  if (kind == TGXD_FASTEST && k != 1) return fail(TGXD_ERR_ARGUMENT, "timed fastest: one source");
+  if (kind == TGXD_FASTEST && k != 1 && !rotate)
+    return fail(TGXD_ERR_ARGUMENT, "timed fastest: one source");
   std::lock_guard<std::mutex> lock(g->mu);
   TGXD_CUDA(cudaSetDevice(g->device));
-  Prepared P;
-  int rc = prepare(g, kind, k, vertices, t_a, t_b, ordering, P);
+  const uint32_t np = rotate ? k : 1;
+  std::vector<Prepared> Ps(np);
+  for (uint32_t i = 0; i < np; ++i) {
+    Prepared& P = Ps[i];
+    int rc = rotate ? prepare(g, kind, 1, vertices + i, t_a + i, t_b + i, ordering, P)
+                    : prepare(g, kind, k, vertices, t_a, t_b, ordering, P);
+    if (rc) return rc;
+  }
+  int rc = ensure_workspace(g, Ps[0].Q, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS);
   if (rc) return rc;
-  if (kind == TGXD_FASTEST && !P.edge && (rc = fastest_candidates(g, P))) return rc;
-  if ((rc = ensure_workspace(g, P.Q, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS)))
-    return rc;
   Workspace& w = g->ws;
-  const uint64_t slots = (uint64_t)P.Q * g->n;
+  const uint64_t slots = (uint64_t)Ps[0].Q * g->n;
   if (!dalloc<int32_t>(w.timing_out, slots)) return fail(TGXD_ERR_CUDA, "allocation (output)");
   std::vector<cudaEvent_t> ev(2 * (size_t)steps);
   for (auto& e : ev) TGXD_CUDA(cudaEventCreate(&e));
@@ -1908,11 +1910,13 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
     for (auto& e : ev) cudaEventDestroy(e);
   };
   for (int i = 0; i < warmup; ++i) {
-    if ((rc = launch(g, P, mode, w.timing_out.p, 4, nullptr, nullptr))) return destroy(), rc;
+    if ((rc = launch(g, Ps[i % np], mode, w.timing_out.p, 4, nullptr, nullptr)))
+      return destroy(), rc;
   }
   TGXD_CUDA(cudaEventRecord(w.ev[2], g->stream));
   for (int i = 0; i < steps; ++i) {
-    if ((rc = launch(g, P, mode, w.timing_out.p, 4, ev[2 * i], ev[2 * i + 1]))) return destroy(), rc;
+    if ((rc = launch(g, Ps[i % np], mode, w.timing_out.p, 4, ev[2 * i], ev[2 * i + 1])))
+      return destroy(), rc;
   }
   TGXD_CUDA(cudaEventRecord(w.ev[3], g->stream));
   TGXD_CUDA(cudaStreamSynchronize(g->stream));
@@ -1926,7 +1930,21 @@ int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* verti
   destroy();
   *total_ms = tot;
   *kernel_ms = ksum / steps;
-  return TGXD_OK;
+  return read_stats(g, nullptr, 0, 0);
+}
+
+int tgxd_time_queries(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
+                      const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode, int warmup,
+                      int steps, float* total_ms, float* kernel_ms) {
+  return time_impl(g, kind, k, vertices, t_a, t_b, ordering, mode, warmup, steps, false, total_ms,
+                   kernel_ms);
+}
+
+int tgxd_time_rotation(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertices,
+                       const uint64_t* t_a, const uint64_t* t_b, int ordering, int mode,
+                       int warmup, int steps, float* total_ms, float* kernel_ms) {
+  return time_impl(g, kind, k, vertices, t_a, t_b, ordering, mode, warmup, steps, true, total_ms,
+                   kernel_ms);
 }
 
 // The trace lives in mapped pinned host memory: the device writes it

@@ -86,7 +86,7 @@ struct AsyncArgs {
   int strict;
   uint32_t cutoff;
   int fastest;
-  uint32_t n_cand;
+  const uint32_t* n_cand;  // device count (candidates.cuh), ascending lists
   const uint32_t* cand_lo;
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
@@ -494,11 +494,14 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
   } else if (!a.fastest) {
     async_loop(a, rx, vb, 1, t_deadline, done, work, ix, nb, nc, wait_ns, busy_ns);
   } else {
-    for (uint32_t cand = 0; cand < a.n_cand; ++cand) {
+    const uint32_t n_cand = __ldcg(a.n_cand);
+    for (uint32_t cand = 0; cand < n_cand; ++cand) {
       // Seeds (path_algorithms.cpp:476-486): the candidate's first edges,
-      // relaxed without an admissibility check, 128-edge pieces over warps.
-      rx.depart = a.cand_key[cand];
-      const uint32_t lo = a.cand_lo[cand], cnt = a.cand_cnt[cand];
+      // relaxed without an admissibility check, 128-edge pieces over warps
+      // (descending: the lists are ascending).
+      const uint32_t ci = n_cand - 1 - cand;
+      rx.depart = a.cand_key[ci];
+      const uint32_t lo = a.cand_lo[ci], cnt = a.cand_cnt[ci];
       const uint32_t pieces = (cnt + 127) / 128;
       const uint32_t mine = gw < pieces ? (pieces - gw + nw - 1) / nw : 0u;
       grid.sync();  // the previous candidate is drained everywhere

@@ -74,12 +74,15 @@ struct Workspace {
   // only [0, xdirty) where X is finite instead of writing every slot
   bool xinv = false;
   uint64_t xdirty = 0;
-  // query parameters / seeds last uploaded to params / seeds (api.cu launch:
-  // a repeated query skips its two small host-to-device copies)
-  std::vector<int64_t> up_cache;
+  // the bytes of the query parameters / seeds last uploaded to params /
+  // seeds (api.cu upload_query: a repeated query skips its two small
+  // host-to-device copies)
+  std::vector<char> up_qp, up_seeds;
+  bool up_valid = false;
+  uint64_t last_h2d = 0;  // bytes the last query moved host -> device
   // lane-per-query batches (lanes.cuh): vertex-major labels, ranges, dirty masks
   DeviceBuffer lxm, leb, ldirty;
-  DeviceBuffer cand_lo, cand_cnt, cand_key, timing_out;
+  DeviceBuffer cand_lo, cand_cnt, cand_key, cand_n, timing_out;
   // asynchronous engine: queued flags, vertex / chunk rings, control block
   DeviceBuffer axq, aunits, actl;
   uint64_t a_slots = 0, a_units = 0;
@@ -196,6 +199,8 @@ struct tgxd_graph {
   tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax;
   tgxd::DeviceBuffer out2in;  // Out -> In position of each edge (shortest duration; lazy)
   bool out2in_ready = false;
+  uint32_t max_out_deg = 0;  // fastest: sizes the device candidate lists (lazy)
+  bool max_out_deg_known = false;
   tgxd::DevCsr out, in;
   // selective-index cost model (costmodel.cuh), per direction, built on first use
   struct Hist {

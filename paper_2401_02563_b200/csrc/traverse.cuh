@@ -100,7 +100,7 @@ struct TravArgs {
   unsigned int handoff_growth;  // ... or one growing by less than this factor per round
   // fastest sweep (Q == 1)
   int fastest;
-  uint32_t n_cand;
+  const uint32_t* n_cand;  // device: candidate count (candidates.cuh), ascending lists
   const uint32_t* cand_lo;
   const uint32_t* cand_cnt;
   const int32_t* cand_key;
@@ -1309,19 +1309,22 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   st.pending = 0;
   st.last_f = 0;
   bool handed = false;
+  const uint32_t n_cand = a.fastest ? __ldcg(a.n_cand) : 0u;
   for (uint32_t cand = 0;; ++cand) {
     int32_t depart = 0;
     uint32_t xlo = 0, xcnt = 0;
     if (a.fastest) {
-      if (cand >= a.n_cand) break;
+      if (cand >= n_cand) break;
       // the previous candidate's last post-barrier reads end before this
       // candidate's seeds move the counters
       if (cand) grid.sync();
       // Seed round (path_algorithms.cpp:476-486): the candidate's first
       // edges, relaxed without an admissibility check.
-      depart = a.cand_key[cand];
-      xlo = a.cand_lo[cand];
-      xcnt = a.cand_cnt[cand];
+      // (descending: the lists are ascending)
+      const uint32_t ci = n_cand - 1 - cand;
+      depart = a.cand_key[ci];
+      xlo = a.cand_lo[ci];
+      xcnt = a.cand_cnt[ci];
     }
     for (;;) {
       if (st.rounds > a.round_limit) {  // identical in every block: all stop together
@@ -1497,7 +1500,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
     ctl->t_end = gtimer();
     ctl->rounds = st.rounds;
     ctl->expansions = __ldcg(&ctl->chunks) + __ldcg(&ctl->smalls);
-    ctl->candidates = a.fastest ? a.n_cand : 0;
+    ctl->candidates = n_cand;
   }
 }
 

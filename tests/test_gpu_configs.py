@@ -144,3 +144,23 @@ def test_full_c3_queries_bit_exact():
             want = o.query(kind, q.vertex, q.window.t_a, q.window.t_b)
             assert np.array_equal(FN[kind](g, q.vertex, q.window).values, want), (kind, i)
             assert np.array_equal(batch[i], want), (kind, i)
+
+
+@pytest.mark.parametrize("mode", [T.Mode.AUTO, T.Mode.ASYNC])
+def test_fastest_from_the_hub_source(mode):
+    """Fastest from the top out-degree vertex (the reference CLI's default
+    source pick, tools/tgx.cpp:125-137): ~13K candidate departures, extracted
+    on the device (candidates.cuh) and swept in descending order."""
+    wl, g, qs = setup("c4", -7)
+    E = T.generate_edges(wl.gen)
+    o = Oracle(E, wl.gen.n_vertices)
+    deg = g.degrees(T.Direction.OUT)
+    hub = int(np.argmax(deg))
+    for w in (qs[0].window, T.QueryWindow(2_000_000, 6_000_000)):
+        st = T.EdgeMapStats()
+        got = T.fastest_path(g, hub, w, T.AlgoOptions(mode=mode, stats=st)).values
+        assert np.array_equal(got, o.query("fastest", hub, w.t_a, w.t_b)), (mode, w)
+        # one candidate per distinct start of the hub's window out-edges
+        sel = (E[0] == hub) & (E[2] >= w.t_a) & (E[3] <= w.t_b)
+        if mode == T.Mode.AUTO:
+            assert st.candidates == len(np.unique(E[2][sel]))

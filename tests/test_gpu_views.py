@@ -46,3 +46,22 @@ def test_view_errors_and_lifetime():
     v.close()
     assert np.array_equal(T.earliest_arrival(g, 0, T.QueryWindow(0, 999_999)).values, b)
     g.close()
+
+
+def test_views_are_released_when_the_stream_count_changes():
+    """concurrent_queries replaces its serve views when `streams` changes;
+    closed views leave the parent's list (no growth, no stale handles)."""
+    gen = T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 13, cube_root_starts=True)
+    g = T.TemporalGraph.generate(gen)
+    E = T.generate_edges(gen)
+    o = Oracle(E, gen.n_vertices)
+    deg = np.bincount(E[0], minlength=gen.n_vertices)
+    srcs = [int(x) for x in np.flatnonzero(deg)[:4]]
+    wins = [T.QueryWindow(0, 999_999)] * 4
+    for streams in (2, 3, 2, 4):
+        out = T.concurrent_queries(g, "earliest_arrival", srcs, wins, streams=streams)
+        assert len(g._views) == streams
+        for i, s in enumerate(srcs):
+            assert np.array_equal(out[i], o.query("earliest_arrival", s, 0, 999_999))
+    g.close()
+    assert g._views == []
