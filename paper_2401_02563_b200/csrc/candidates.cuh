@@ -5,12 +5,13 @@
 // query never synchronises with the host and a hub source with tens of
 // thousands of candidates costs one short kernel.
 //
-// Out segments are sorted by (start, end, ...) (tcsr.cpp:12-15), so a key
-// group's first entry holds the group's smallest end: the group is a
-// candidate iff klo <= key <= vhi and that end <= vhi (an edge of the group
-// lies inside the window). Candidates are written in ascending key order
-// with their whole group ({lo, count, key}); the sweep walks them from the
-// top (descending, path_algorithms.cpp:460).
+// A key group (equal starts) is a candidate iff klo <= key <= vhi and one of
+// its edges ends by vhi (an edge of the group lies inside the window). The
+// device layout orders a segment by key only (build.cuh: equal keys keep
+// input order), so the group's first thread looks for such an end.
+// Candidates are written in ascending key order with their whole group
+// ({lo, count, key}); the sweep walks them from the top (descending,
+// path_algorithms.cpp:460).
 #pragma once
 
 #include <cub/block/block_scan.cuh>
@@ -57,16 +58,24 @@ __global__ void __launch_bounds__(kCandThreads) candidates_kernel(
   const uint32_t b = cand_upper(g.key, a, s1, vhi);
   uint32_t base = 0;
   for (uint32_t t0 = a; t0 < b; t0 += kCandTile) {
-    uint32_t flag[kCandPerThread];
+    uint32_t flag[kCandPerThread], gend[kCandPerThread];
     uint32_t cnt = 0;
 #pragma unroll
     for (int k = 0; k < kCandPerThread; ++k) {
       const uint32_t j = t0 + threadIdx.x * kCandPerThread + k;
       flag[k] = 0;
+      gend[k] = j;
       if (j < b) {
         const int32_t kv = __ldg(g.key + j);
-        const bool start = j == s0 || __ldg(g.key + j - 1) != kv;
-        flag[k] = start && (int32_t)__ldg(&g.pay[j].y) <= vhi ? 1u : 0u;
+        if (j == s0 || __ldg(g.key + j - 1) != kv) {  // first edge of its key group
+          const uint32_t e = cand_upper(g.key, j, b, kv);
+          for (uint32_t i = j; i < e; ++i)
+            if ((int32_t)__ldg(&g.pay[i].y) <= vhi) {
+              flag[k] = 1;
+              break;
+            }
+          gend[k] = e;
+        }
       }
       cnt += flag[k];
     }
@@ -76,11 +85,9 @@ __global__ void __launch_bounds__(kCandThreads) candidates_kernel(
     for (int k = 0; k < kCandPerThread; ++k) {
       if (!flag[k]) continue;
       const uint32_t j = t0 + threadIdx.x * kCandPerThread + k;
-      const int32_t kv = __ldg(g.key + j);
-      const uint32_t e = cand_upper(g.key, j, s1, kv);  // end of the key group
       cand_lo[base + pos] = j;
-      cand_cnt[base + pos] = e - j;
-      cand_key[base + pos] = kv;
+      cand_cnt[base + pos] = gend[k] - j;
+      cand_key[base + pos] = __ldg(g.key + j);
       ++pos;
     }
     base += total;
