@@ -3,25 +3,34 @@
 // Header-only shim over the C-ABI (include/tgxd.h, libtgxd.so). It keeps the
 // reference signatures and semantics (/root/reference/proj/include/tgx/):
 //   TemporalGraph::build(edges, n_v, directed, config)   engine.hpp:32-33
+//   TemporalGraph::meta / degree / csr / out_csr / in_csr engine.hpp:35-44
+//     (GraphMeta types.hpp:98-108; TemporalCsr read access tcsr.hpp:36-50,
+//     materialized on the host from the device layout on first use)
 //   earliest_arrival / latest_departure / fastest_path    algorithms.hpp:46-58
 //   shortest_duration / temporal_bfs                      algorithms.hpp:62-67
 //   PathResult (int64 values, INT64_MAX / INT64_MIN)       algorithms.hpp:16-21
 //   digest_of                                             digest.hpp:42-52
 // and re-throws the reference's exception types: std::out_of_range for a bad
-// vertex or edge, std::invalid_argument for a bad window. Every ordering,
-// Overlaps included, runs on the device. Times outside [0, 2^31 - 2] and the
-// weighted shortest duration (edge weights are not stored on the device)
-// raise std::domain_error; there is no CPU fallback. force_access is accepted
-// and ignored: results are access-invariant (test_algorithms.cpp:196-217).
+// vertex or edge, std::invalid_argument for a bad window or (weighted
+// shortest duration) a reachable edge whose weight is not a non-negative
+// integer. Every ordering, Overlaps included, runs on the device. Times
+// outside [0, 2^31 - 2] raise std::domain_error; there is no CPU fallback.
+// force_access is accepted and ignored: results are access-invariant
+// (test_algorithms.cpp:196-217). EdgeMapStats counts one access decision per
+// vertex expansion (engine.hpp:316, 341): index_decisions for expansions that
+// went through the selective index, scan_decisions for the others.
 //
 // A user of the reference switches by replacing `#include "tgx/..."` and
 // `tgx::` with this header and `tgx_b200::`, and linking libtgxd.so.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
+#include <numeric>
 #include <cstdint>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -54,6 +63,17 @@ struct QueryWindow {
 enum class Ordering { Succeeds, StrictlySucceeds, Overlaps };
 enum class ForceAccess { Auto, Index, Scan };
 enum class Direction { Out, In };
+
+struct GraphMeta {  // types.hpp:98-108
+  VertexId n_v = 0;
+  EdgeId n_e = 0;  // logical edge count (undirected: before symmetrization)
+  bool directed = true;
+  std::vector<EdgeId> out_degree;
+  std::vector<EdgeId> in_degree;
+  EdgeId degree(VertexId v, Direction d) const {
+    return d == Direction::Out ? out_degree[v] : in_degree[v];
+  }
+};
 
 struct EngineConfig {
   EdgeId index_cutoff = 2048;
@@ -100,6 +120,75 @@ inline void check(int code) {
 }
 }  // namespace detail
 
+// Host view of one device T-CSR layout (tcsr.hpp:27-85 read access):
+// offsets and degrees from the device degrees, the edge arrays (segment
+// order: start, end, neighbor) copied from the device on first use.
+class TemporalCsr {
+ public:
+  VertexId vertex_count() const { return n_; }
+  EdgeId edge_count() const { return offsets_.empty() ? 0 : offsets_.back(); }
+  EdgeId degree(VertexId v) const { return offsets_[v + 1] - offsets_[v]; }
+  std::span<const EdgeId> offsets() const { return offsets_; }
+  std::span<const VertexId> neighbors() const { return edges().nbr; }
+  std::span<const Timestamp> starts() const { return edges().st; }
+  std::span<const Timestamp> ends() const { return edges().en; }
+  VertexId neighbor_at(EdgeId i) const { return edges().nbr[i]; }
+  Timestamp start_at(EdgeId i) const { return edges().st[i]; }
+  Timestamp end_at(EdgeId i) const { return edges().en[i]; }
+
+ private:
+  friend class TemporalGraph;
+  struct Edges {
+    std::vector<VertexId> nbr;
+    std::vector<Timestamp> st, en;
+  };
+  const Edges& edges() const {
+    std::call_once(*once_, [this] {
+      const EdgeId m = edge_count();
+      std::vector<std::uint32_t> s(m), d(m);
+      Edges e;
+      e.st.resize(m);
+      e.en.resize(m);
+      if (m)
+        detail::check(tgxd_graph_flatten(h_.get(), dir_ == Direction::Out ? 0 : 1, s.data(),
+                                         d.data(), e.st.data(), e.en.data()));
+      e.nbr = dir_ == Direction::Out ? std::move(d) : std::move(s);
+      // the reference's segment order (start, end, neighbor), tcsr.cpp:12-15
+      // (the device orders a segment by its search key only)
+      std::vector<EdgeId> p;
+      for (VertexId v = 0; v < n_; ++v) {
+        const EdgeId lo = offsets_[v], hi = offsets_[v + 1];
+        if (hi - lo < 2) continue;
+        p.resize(hi - lo);
+        std::iota(p.begin(), p.end(), lo);
+        std::sort(p.begin(), p.end(), [&](EdgeId x, EdgeId y) {
+          if (e.st[x] != e.st[y]) return e.st[x] < e.st[y];
+          if (e.en[x] != e.en[y]) return e.en[x] < e.en[y];
+          return e.nbr[x] < e.nbr[y];
+        });
+        std::vector<VertexId> nb(p.size());
+        std::vector<Timestamp> a(p.size()), b(p.size());
+        for (std::size_t i = 0; i < p.size(); ++i) {
+          nb[i] = e.nbr[p[i]];
+          a[i] = e.st[p[i]];
+          b[i] = e.en[p[i]];
+        }
+        std::copy(nb.begin(), nb.end(), e.nbr.begin() + lo);
+        std::copy(a.begin(), a.end(), e.st.begin() + lo);
+        std::copy(b.begin(), b.end(), e.en.begin() + lo);
+      }
+      *edges_ = std::move(e);
+    });
+    return *edges_;
+  }
+  std::shared_ptr<tgxd_graph> h_;
+  Direction dir_ = Direction::Out;
+  VertexId n_ = 0;
+  std::vector<EdgeId> offsets_;
+  std::shared_ptr<std::once_flag> once_ = std::make_shared<std::once_flag>();
+  std::shared_ptr<Edges> edges_ = std::make_shared<Edges>();
+};
+
 // Device-resident graph: both T-CSR layouts plus the selective index. Cheap
 // to copy (shared handle); immutable after build.
 class TemporalGraph {
@@ -110,19 +199,27 @@ class TemporalGraph {
     const std::size_t m = edges.size();
     std::vector<std::uint32_t> s(m), d(m);
     std::vector<std::uint64_t> a(m), b(m);
+    std::vector<double> w(m);
+    bool weighted = false;
     for (std::size_t i = 0; i < m; ++i) {
       s[i] = edges[i].source;
       d[i] = edges[i].destination;
       a[i] = edges[i].start;
       b[i] = edges[i].end;
+      w[i] = edges[i].weight;
+      weighted = weighted || w[i] != 1.0;
     }
     tgxd_graph* h = nullptr;
-    detail::check(tgxd_graph_build(n_v, m, s.data(), d.data(), a.data(), b.data(),
-                                   directed ? 1 : 0, config.index_cutoff, &h));
+    detail::check(tgxd_graph_build_weighted(n_v, m, s.data(), d.data(), a.data(), b.data(),
+                                            weighted ? w.data() : nullptr, directed ? 1 : 0,
+                                            config.index_cutoff, &h));
     TemporalGraph g;
     g.h_ = std::shared_ptr<tgxd_graph>(h, tgxd_graph_destroy);
     g.config_ = config;
     g.n_ = n_v;
+    g.meta_ = std::make_shared<Layouts>();
+    g.meta_->m_logical = m;
+    g.meta_->directed = directed;
     return g;
   }
 
@@ -143,10 +240,46 @@ class TemporalGraph {
   Ordering ordering() const { return config_.ordering; }
   tgxd_graph* handle() const { return h_.get(); }
 
+  // engine.hpp:35-44 (degrees read back from the device once per graph)
+  const GraphMeta& meta() const { return layouts().meta; }
+  const TemporalCsr& csr(Direction d) const { return d == Direction::Out ? out_csr() : in_csr(); }
+  const TemporalCsr& out_csr() const { return layouts().out; }
+  const TemporalCsr& in_csr() const { return layouts().in; }
+  EdgeId degree(VertexId v, Direction d) const { return csr(d).degree(v); }
+
  private:
+  struct Layouts {
+    std::once_flag once;
+    EdgeId m_logical = 0;
+    bool directed = true;
+    GraphMeta meta;
+    TemporalCsr out, in;
+  };
+  const Layouts& layouts() const {
+    std::call_once(meta_->once, [this] {
+      Layouts& L = *meta_;
+      L.meta.n_v = n_;
+      L.meta.n_e = L.m_logical;
+      L.meta.directed = L.directed;
+      for (int dir = 0; dir < 2; ++dir) {
+        std::vector<std::uint32_t> deg(n_);
+        if (n_) detail::check(tgxd_graph_degrees(h_.get(), dir, deg.data()));
+        std::vector<EdgeId>& md = dir == 0 ? L.meta.out_degree : L.meta.in_degree;
+        md.assign(deg.begin(), deg.end());
+        TemporalCsr& c = dir == 0 ? L.out : L.in;
+        c.h_ = h_;
+        c.dir_ = dir == 0 ? Direction::Out : Direction::In;
+        c.n_ = n_;
+        c.offsets_.assign(static_cast<std::size_t>(n_) + 1, 0);
+        for (VertexId v = 0; v < n_; ++v) c.offsets_[v + 1] = c.offsets_[v] + deg[v];
+      }
+    });
+    return *meta_;
+  }
   std::shared_ptr<tgxd_graph> h_;
   EngineConfig config_;
   VertexId n_ = 0;
+  std::shared_ptr<Layouts> meta_;
 };
 
 namespace detail {
@@ -182,11 +315,13 @@ inline PathResult fastest_path(const TemporalGraph& g, VertexId source, const Qu
   return detail::run(TGXD_FASTEST, g, source, w, opts);
 }
 
+// path_algorithms.cpp:196-258, 410-434: the least sum of end - start, or
+// with opts.weighted of the edges' weights (weight 1.0 unless the graph was
+// built with other weights).
 inline PathResult shortest_duration(const TemporalGraph& g, VertexId source, const QueryWindow& w,
                                     const AlgoOptions& opts = {}) {
-  if (opts.weighted)
-    throw std::domain_error("weighted shortest duration: edge weights are not on the device");
-  return detail::run(TGXD_SHORTEST_DURATION, g, source, w, opts);
+  return detail::run(opts.weighted ? TGXD_SHORTEST_DURATION_WEIGHTED : TGXD_SHORTEST_DURATION, g,
+                     source, w, opts);
 }
 
 inline PathResult temporal_bfs(const TemporalGraph& g, VertexId source, const QueryWindow& w,

@@ -52,7 +52,13 @@ enum tgxd_kind {
   TGXD_LATEST_DEPARTURE = 1,
   TGXD_FASTEST = 2,
   TGXD_SHORTEST_DURATION = 3,
-  TGXD_TEMPORAL_BFS = 4
+  TGXD_TEMPORAL_BFS = 4,
+  /* shortest_duration with AlgoOptions::weighted (algorithms.hpp:36): the
+   * sum of edge weights, which must be non-negative integers on every edge a
+   * path can reach (else TGXD_ERR_WINDOW, the reference's invalid_argument,
+   * path_algorithms.cpp:196-203); weights >= 2^62 give TGXD_ERR_TIME_RANGE.
+   * A graph built without weights has weight 1.0 on every edge. */
+  TGXD_SHORTEST_DURATION_WEIGHTED = 5
 };
 
 /* tgx::Ordering, types.hpp:64-68 (same numeric order). Overlaps runs every
@@ -80,7 +86,9 @@ enum tgxd_mode {
 typedef struct tgxd_stats {
   uint32_t rounds;          /* frontier rounds (all candidates for fastest) */
   uint32_t candidates;      /* fastest: departure candidates swept */
-  uint64_t expansions;      /* non-empty frontier ranges expanded */
+  uint64_t expansions;      /* frontier vertices expanded: one per for_each_window_edge call
+                               of the reference (engine.hpp:316, 341; a pull round visits
+                               every slot) */
   uint64_t edges_relaxed;   /* edges relaxed by push plus entries scanned by pull rounds */
   uint64_t index_lookups;   /* expansions that used the selective index */
   float kernel_ms;          /* traversal kernel time (CUDA events) */
@@ -115,6 +123,13 @@ int tgxd_device_count(int* count);
 int tgxd_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                      const uint64_t* start, const uint64_t* end, int directed,
                      uint64_t index_cutoff, tgxd_graph** out);
+
+/* Same, with per-edge weights (TemporalEdge::weight, types.hpp:29-40):
+ * stored on the device (int64, Out-layout order) for weighted shortest
+ * duration; NULL = every weight 1.0. */
+int tgxd_graph_build_weighted(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                              const uint64_t* start, const uint64_t* end, const double* weight,
+                              int directed, uint64_t index_cutoff, tgxd_graph** out);
 
 /* Same, but the edge list is generated on the device (no host copy). */
 int tgxd_graph_generate(const tgxd_gen_config* cfg, int directed, uint64_t index_cutoff,
@@ -156,6 +171,9 @@ int tgxd_shortest_duration(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_
                            int ordering, int64_t* out, tgxd_stats* stats);
 int tgxd_temporal_bfs(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int ordering,
                       int64_t* out, tgxd_stats* stats);
+/* shortest_duration with AlgoOptions::weighted = true (path_algorithms.cpp:196-258). */
+int tgxd_shortest_duration_weighted(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b,
+                                    int ordering, int64_t* out, tgxd_stats* stats);
 
 /* General form: k queries of one kind run as one batched traversal
  * (configs 3 and 5). out holds k x n labels of `width` bytes (4 or 8),

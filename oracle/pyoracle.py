@@ -27,7 +27,7 @@ _u32p = _P(ctypes.c_uint32)
 _u64p = _P(ctypes.c_uint64)
 _i64p = _P(ctypes.c_int64)
 KIND = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2, "shortest_duration": 3,
-        "temporal_bfs": 4}
+        "temporal_bfs": 4, "shortest_duration_weighted": 5}
 
 
 class OracleError(Exception):
@@ -60,6 +60,9 @@ class Oracle:
             vp = ctypes.c_void_p
             lib.tgxo_graph_build.argtypes = [ctypes.c_uint32, ctypes.c_uint64, _u32p, _u32p,
                                              _u64p, _u64p, ctypes.c_int, _P(vp)]
+            lib.tgxo_graph_build_weighted.argtypes = [ctypes.c_uint32, ctypes.c_uint64, _u32p,
+                                                      _u32p, _u64p, _u64p,
+                                                      _P(ctypes.c_double), ctypes.c_int, _P(vp)]
             lib.tgxo_graph_free.argtypes = [vp]
             lib.tgxo_graph_free.restype = None
             lib.tgxo_query.argtypes = [vp, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
@@ -72,15 +75,17 @@ class Oracle:
             cls._lib = lib
         return cls._lib
 
-    def __init__(self, edges, n: int, directed: bool = True):
+    def __init__(self, edges, n: int, directed: bool = True, weights=None):
         lib = self.lib()
         s, d, a, b = _arr(edges)
         self.n = n
         self._h = ctypes.c_void_p()
-        self._check(lib.tgxo_graph_build(n, len(s), s.ctypes.data_as(_u32p),
-                                         d.ctypes.data_as(_u32p), a.ctypes.data_as(_u64p),
-                                         b.ctypes.data_as(_u64p), 1 if directed else 0,
-                                         ctypes.byref(self._h)))
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        self._check(lib.tgxo_graph_build_weighted(
+            n, len(s), s.ctypes.data_as(_u32p), d.ctypes.data_as(_u32p),
+            a.ctypes.data_as(_u64p), b.ctypes.data_as(_u64p),
+            None if w is None else w.ctypes.data_as(_f64p), 1 if directed else 0,
+            ctypes.byref(self._h)))
 
     @classmethod
     def _check(cls, rc):
@@ -193,6 +198,9 @@ class Reference:
             vp = ctypes.c_void_p
             lib.tgxref_build.argtypes = [ctypes.c_uint32, ctypes.c_uint64, _u32p, _u32p, _u64p,
                                          _u64p, ctypes.c_int, ctypes.c_uint64, _P(vp)]
+            lib.tgxref_build_weighted.argtypes = [ctypes.c_uint32, ctypes.c_uint64, _u32p, _u32p,
+                                                  _u64p, _u64p, _P(ctypes.c_double),
+                                                  ctypes.c_int, ctypes.c_uint64, _P(vp)]
             lib.tgxref_free.argtypes = [vp]
             lib.tgxref_free.restype = None
             lib.tgxref_query.argtypes = [vp, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
@@ -216,14 +224,23 @@ class Reference:
     def workers(cls) -> int:
         return int(cls.lib().tgxref_num_workers())
 
-    def __init__(self, edges, n: int, directed: bool = True, index_cutoff: int = 0):
+    def __init__(self, edges, n: int, directed: bool = True, index_cutoff: int = 0,
+                 weights=None):
         lib = self.lib()
         s, d, a, b = _arr(edges)
         self.n = n
         self._h = ctypes.c_void_p()
-        self._check(lib.tgxref_build(n, len(s), s.ctypes.data_as(_u32p), d.ctypes.data_as(_u32p),
-                                     a.ctypes.data_as(_u64p), b.ctypes.data_as(_u64p),
-                                     1 if directed else 0, index_cutoff, ctypes.byref(self._h)))
+        if weights is None:
+            self._check(lib.tgxref_build(n, len(s), s.ctypes.data_as(_u32p),
+                                         d.ctypes.data_as(_u32p), a.ctypes.data_as(_u64p),
+                                         b.ctypes.data_as(_u64p), 1 if directed else 0,
+                                         index_cutoff, ctypes.byref(self._h)))
+        else:
+            w = np.ascontiguousarray(weights, np.float64)
+            self._check(lib.tgxref_build_weighted(
+                n, len(s), s.ctypes.data_as(_u32p), d.ctypes.data_as(_u32p),
+                a.ctypes.data_as(_u64p), b.ctypes.data_as(_u64p), w.ctypes.data_as(_f64p),
+                1 if directed else 0, index_cutoff, ctypes.byref(self._h)))
 
     @classmethod
     def _check(cls, rc):

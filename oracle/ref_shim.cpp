@@ -53,10 +53,11 @@ int guarded(F&& f) {
 
 std::vector<tgx::TemporalEdge> edges_of(std::uint64_t m, const std::uint32_t* src,
                                         const std::uint32_t* dst, const std::uint64_t* start,
-                                        const std::uint64_t* end) {
+                                        const std::uint64_t* end,
+                                        const double* weight = nullptr) {
   std::vector<tgx::TemporalEdge> edges(m);
   for (std::uint64_t i = 0; i < m; ++i) {
-    edges[i] = tgx::TemporalEdge{src[i], dst[i], start[i], end[i], 1.0};
+    edges[i] = tgx::TemporalEdge{src[i], dst[i], start[i], end[i], weight ? weight[i] : 1.0};
   }
   return edges;
 }
@@ -91,10 +92,25 @@ int tgxref_build(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
   });
 }
 
+// Same, with per-edge weights (TemporalEdge::weight, types.hpp:29-40).
+int tgxref_build_weighted(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
+                          const std::uint32_t* dst, const std::uint64_t* start,
+                          const std::uint64_t* end, const double* weight, int directed,
+                          std::uint64_t index_cutoff, void** out) {
+  *out = nullptr;
+  return guarded([&] {
+    tgx::EngineConfig cfg;
+    if (index_cutoff != 0) cfg.index_cutoff = index_cutoff;
+    auto* g = new tgx::TemporalGraph(tgx::TemporalGraph::build(
+        edges_of(m, src, dst, start, end, weight), n, directed != 0, cfg));
+    *out = g;
+  });
+}
+
 void tgxref_free(void* g) { delete static_cast<tgx::TemporalGraph*>(g); }
 
 // kind: 0 earliest arrival, 1 latest departure, 2 fastest, 3 shortest duration
-// (unweighted), 4 temporal BFS.
+// (unweighted), 4 temporal BFS, 5 shortest duration with AlgoOptions::weighted.
 // force: -1 graph default, 0 auto, 1 index, 2 scan.
 int tgxref_query(void* gp, int kind, std::uint32_t vertex, std::uint64_t ta, std::uint64_t tb,
                  int ordering, int force, std::int64_t* out) {
@@ -115,6 +131,10 @@ int tgxref_query(void* gp, int kind, std::uint32_t vertex, std::uint64_t ta, std
       case 2: r = tgx::fastest_path(g, vertex, w, opts); break;
       case 3: r = tgx::shortest_duration(g, vertex, w, opts); break;
       case 4: r = tgx::temporal_bfs(g, vertex, w, opts); break;
+      case 5:
+        opts.weighted = true;
+        r = tgx::shortest_duration(g, vertex, w, opts);
+        break;
       default: throw std::invalid_argument("unknown query kind");
     }
     std::memcpy(out, r.values.data(), r.values.size() * sizeof(std::int64_t));

@@ -44,6 +44,7 @@ typedef struct {
   uint32_t* nbr;
   uint64_t* st;
   uint64_t* en;
+  double* wt;
 } ocsr;
 
 struct tgxo_graph {
@@ -55,30 +56,32 @@ struct tgxo_graph {
 typedef struct {
   uint64_t s, e;
   uint32_t nbr;
+  double w;
 } orec;
 
-/* Segment order (start, end, neighbor), tcsr.cpp:12-15 (weights are all 1.0
- * through this interface, so the weight tiebreak never fires). */
+/* Segment order (start, end, neighbor, weight), tcsr.cpp:12-15. */
 static int rec_cmp(const void* a, const void* b) {
   const orec* x = (const orec*)a;
   const orec* y = (const orec*)b;
   if (x->s != y->s) return x->s < y->s ? -1 : 1;
   if (x->e != y->e) return x->e < y->e ? -1 : 1;
   if (x->nbr != y->nbr) return x->nbr < y->nbr ? -1 : 1;
+  if (x->w != y->w) return x->w < y->w ? -1 : 1;
   return 0;
 }
 
 /* TemporalCsr::build, tcsr.cpp:19-84: count, exclusive scan, placement,
  * per-segment sort, split into flat arrays. */
 static int build_csr(ocsr* c, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
-                     const uint64_t* st, const uint64_t* en, int by_dst) {
+                     const uint64_t* st, const uint64_t* en, const double* wt, int by_dst) {
   c->off = calloc((size_t)n + 1, sizeof(uint64_t));
   c->nbr = malloc((m ? m : 1) * sizeof(uint32_t));
   c->st = malloc((m ? m : 1) * sizeof(uint64_t));
   c->en = malloc((m ? m : 1) * sizeof(uint64_t));
+  c->wt = malloc((m ? m : 1) * sizeof(double));
   orec* rec = malloc((m ? m : 1) * sizeof(orec));
   uint64_t* cur = malloc(((size_t)n + 1) * sizeof(uint64_t));
-  if (!c->off || !c->nbr || !c->st || !c->en || !rec || !cur) {
+  if (!c->off || !c->nbr || !c->st || !c->en || !c->wt || !rec || !cur) {
     free(rec);
     free(cur);
     return fail(TGXO_INVALID_ARGUMENT, "oracle: out of host memory");
@@ -92,6 +95,7 @@ static int build_csr(ocsr* c, uint32_t n, uint64_t m, const uint32_t* src, const
     rec[slot].s = st[i];
     rec[slot].e = en[i];
     rec[slot].nbr = by_dst ? src[i] : dst[i];
+    rec[slot].w = wt ? wt[i] : 1.0;
   }
   for (uint32_t v = 0; v < n; ++v) {
     const uint64_t lo = c->off[v], hi = c->off[v + 1];
@@ -101,6 +105,7 @@ static int build_csr(ocsr* c, uint32_t n, uint64_t m, const uint32_t* src, const
     c->nbr[i] = rec[i].nbr;
     c->st[i] = rec[i].s;
     c->en[i] = rec[i].e;
+    c->wt[i] = rec[i].w;
   }
   free(rec);
   free(cur);
@@ -112,6 +117,7 @@ static void free_csr(ocsr* c) {
   free(c->nbr);
   free(c->st);
   free(c->en);
+  free(c->wt);
 }
 
 void tgxo_graph_free(tgxo_graph* g) {
@@ -129,6 +135,14 @@ uint64_t tgxo_graph_edges(const tgxo_graph* g) { return g->m; }
  * non-self-loop edge (engine.cpp:13-22). */
 int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                      const uint64_t* start, const uint64_t* end, int directed, tgxo_graph** out) {
+  return tgxo_graph_build_weighted(n, m, src, dst, start, end, NULL, directed, out);
+}
+
+/* Same with per-edge weights (TemporalEdge::weight, types.hpp:29-40; NULL:
+ * every weight 1.0, the TemporalEdge default). */
+int tgxo_graph_build_weighted(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                              const uint64_t* start, const uint64_t* end, const double* weight,
+                              int directed, tgxo_graph** out) {
   *out = NULL;
   for (uint64_t i = 0; i < m; ++i) {
     char msg[160];
@@ -150,8 +164,10 @@ int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
   const uint64_t* a = start;
   const uint64_t* b = end;
   uint64_t mm = m;
+  const double* w = weight;
   uint32_t *s2 = NULL, *d2 = NULL;
   uint64_t *a2 = NULL, *b2 = NULL;
+  double* w2 = NULL;
   if (!directed) {
     uint64_t extra = 0;
     for (uint64_t i = 0; i < m; ++i) extra += src[i] != dst[i];
@@ -160,10 +176,12 @@ int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
     d2 = malloc((mm ? mm : 1) * 4);
     a2 = malloc((mm ? mm : 1) * 8);
     b2 = malloc((mm ? mm : 1) * 8);
+    w2 = malloc((mm ? mm : 1) * 8);
     memcpy(s2, src, m * 4);
     memcpy(d2, dst, m * 4);
     memcpy(a2, start, m * 8);
     memcpy(b2, end, m * 8);
+    for (uint64_t i = 0; i < m; ++i) w2[i] = weight ? weight[i] : 1.0;
     uint64_t k = m;
     for (uint64_t i = 0; i < m; ++i) {
       if (src[i] == dst[i]) continue;
@@ -171,18 +189,21 @@ int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
       d2[k] = src[i];
       a2[k] = start[i];
       b2[k] = end[i];
+      w2[k] = w2[i];
       ++k;
     }
     s = s2;
     d = d2;
     a = a2;
     b = b2;
+    w = w2;
   }
   tgxo_graph* g = calloc(1, sizeof(tgxo_graph));
   g->n = n;
   g->m = mm;
-  int rc = build_csr(&g->out, n, mm, s, d, a, b, 0);
-  if (rc == TGXO_OK) rc = build_csr(&g->in, n, mm, s, d, a, b, 1);
+  int rc = build_csr(&g->out, n, mm, s, d, a, b, w, 0);
+  if (rc == TGXO_OK) rc = build_csr(&g->in, n, mm, s, d, a, b, w, 1);
+  free(w2);
   free(s2);
   free(d2);
   free(a2);
@@ -720,8 +741,25 @@ static void fastest_overlaps(const tgxo_graph* g, uint32_t source, uint64_t ta, 
  * out-edge states value[f] = min over valid paths ending with f of the sum of
  * (end - start); frontier by write_min + round stamp with base read at the
  * round's start; r[v] = min over reached in-edges, r[source] = 0. */
-static void shortest_duration(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb,
-                              int ord, int64_t* R) {
+/* duration_metric, path_algorithms.cpp:196-203: end - start, or the edge's
+ * weight, which must be a non-negative integer (else invalid_argument). */
+static int duration_metric(const ocsr* c, uint64_t f, int weighted, int64_t* d) {
+  if (!weighted) {
+    *d = (int64_t)(c->en[f] - c->st[f]);
+    return TGXO_OK;
+  }
+  const double w = c->wt[f];
+  const double r = nearbyint(w);
+  if (w < 0.0 || r != w)
+    return fail(TGXO_INVALID_ARGUMENT,
+                "weighted shortest duration needs non-negative integer weights");
+  *d = (int64_t)r;
+  return TGXO_OK;
+}
+
+static int shortest_duration(const tgxo_graph* g, uint32_t source, uint64_t ta, uint64_t tb,
+                             int ord, int weighted, int64_t* R) {
+  int rc = TGXO_OK;
   const ocsr* c = &g->out;
   const uint64_t m = g->m;
   int64_t* val = malloc((m ? m : 1) * sizeof(int64_t));
@@ -733,7 +771,8 @@ static void shortest_duration(const tgxo_graph* g, uint32_t source, uint64_t ta,
   uint64_t bcap = 0;
   uint32_t round = 1;
   FOR_WINDOW(c, source, ta, tb, f) {
-    const int64_t d = (int64_t)(c->en[f] - c->st[f]);
+    int64_t d;
+    if ((rc = duration_metric(c, f, weighted, &d))) goto done;
     if (d < val[f]) {
       val[f] = d;
       touched[f] = 1;
@@ -758,7 +797,9 @@ static void shortest_duration(const tgxo_graph* g, uint32_t source, uint64_t ta,
       if (!step_window(c->st[e], c->en[e], ord, 1, &wa, &wb)) continue;
       FOR_WINDOW(c, c->nbr[e], wa, wb, f) {
         if (!holds(c->st[e], c->en[e], c->st[f], c->en[f], ord)) continue;
-        const int64_t cand = base[i] + (int64_t)(c->en[f] - c->st[f]);
+        int64_t dm;
+        if ((rc = duration_metric(c, f, weighted, &dm))) goto done;
+        const int64_t cand = base[i] + dm;
         if (cand < val[f]) {
           val[f] = cand;
           touched[f] = 1;
@@ -778,12 +819,14 @@ static void shortest_duration(const tgxo_graph* g, uint32_t source, uint64_t ta,
   for (uint64_t e = 0; e < m; ++e)
     if (touched[e] && val[e] < R[c->nbr[e]]) R[c->nbr[e]] = val[e];
   R[source] = 0;
+done:
   free(val);
   free(stamp);
   free(touched);
   free(base);
   free(fr.v);
   free(nx.v);
+  return rc;
 }
 
 /* temporal_bfs, path_algorithms.cpp:359-408: round-synchronous earliest
@@ -857,7 +900,8 @@ int tgxo_query(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint
       case TGXO_LD:
       case TGXO_BFS: overlaps_reach(g, kind, vertex, ta, tb, out); return TGXO_OK;
       case TGXO_FASTEST: fastest_overlaps(g, vertex, ta, tb, out); return TGXO_OK;
-      case TGXO_SD: shortest_duration(g, vertex, ta, tb, ordering, out); return TGXO_OK;
+      case TGXO_SD: return shortest_duration(g, vertex, ta, tb, ordering, 0, out);
+      case TGXO_SD_WEIGHTED: return shortest_duration(g, vertex, ta, tb, ordering, 1, out);
       default: return fail(TGXO_INVALID_ARGUMENT, "unknown query kind");
     }
   }
@@ -865,7 +909,8 @@ int tgxo_query(const tgxo_graph* g, int kind, uint32_t vertex, uint64_t ta, uint
     case TGXO_EA: earliest_arrival(g, vertex, ta, tb, strict, out); break;
     case TGXO_LD: latest_departure(g, vertex, ta, tb, strict, out); break;
     case TGXO_FASTEST: fastest(g, vertex, ta, tb, strict, out); break;
-    case TGXO_SD: shortest_duration(g, vertex, ta, tb, ordering, out); break;
+    case TGXO_SD: return shortest_duration(g, vertex, ta, tb, ordering, 0, out);
+    case TGXO_SD_WEIGHTED: return shortest_duration(g, vertex, ta, tb, ordering, 1, out);
     case TGXO_BFS: temporal_bfs(g, vertex, ta, tb, strict, out); break;
     default: return fail(TGXO_INVALID_ARGUMENT, "unknown query kind");
   }

@@ -20,6 +20,8 @@ extern "C" {
 enum { TGXO_OK = 0, TGXO_OUT_OF_RANGE = 1, TGXO_INVALID_ARGUMENT = 2, TGXO_UNSUPPORTED = 3 };
 /* kinds: the reference's five path metrics (algorithms.hpp:46-66) */
 enum { TGXO_EA = 0, TGXO_LD = 1, TGXO_FASTEST = 2, TGXO_SD = 3, TGXO_BFS = 4 };
+/* shortest duration with AlgoOptions::weighted (sum of edge weights) */
+enum { TGXO_SD_WEIGHTED = 5 };
 /* Ordering values follow tgx::Ordering (types.hpp:64-68). */
 enum { TGXO_SUCCEEDS = 0, TGXO_STRICTLY_SUCCEEDS = 1, TGXO_OVERLAPS = 2 };
 
@@ -27,6 +29,9 @@ typedef struct tgxo_graph tgxo_graph;
 
 int tgxo_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                      const uint64_t* start, const uint64_t* end, int directed, tgxo_graph** out);
+int tgxo_graph_build_weighted(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                              const uint64_t* start, const uint64_t* end, const double* weight,
+                              int directed, tgxo_graph** out);
 void tgxo_graph_free(tgxo_graph* g);
 uint64_t tgxo_graph_edges(const tgxo_graph* g);
 

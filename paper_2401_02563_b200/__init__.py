@@ -211,6 +211,12 @@ def load_library() -> ctypes.CDLL:
                               ctypes.c_int, ctypes.c_uint64, _P(vp)], ctypes.c_int),
         "tgxd_graph_generate": ([_P(GenConfig), ctypes.c_int, ctypes.c_uint64, _P(vp)],
                                 ctypes.c_int),
+        "tgxd_graph_build_weighted": ([ctypes.c_uint32, ctypes.c_uint64, _u32p, _u32p, _u64p,
+                                       _u64p, _P(ctypes.c_double), ctypes.c_int,
+                                       ctypes.c_uint64, _P(vp)], ctypes.c_int),
+        "tgxd_shortest_duration_weighted": ([vp, ctypes.c_uint32, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_int, _i64p, _P(_Stats)],
+                                            ctypes.c_int),
         "tgxd_generate_host": ([_P(GenConfig), ctypes.c_uint64, _u64p, _u32p, _u32p, _u64p,
                                 _u64p], ctypes.c_int),
         "tgxd_graph_destroy": ([vp], None),
@@ -274,19 +280,29 @@ def device_count() -> int:
     return c.value
 
 
-def _edge_arrays(edges) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
-    if isinstance(edges, tuple) and len(edges) == 4:
-        s, d, a, b = edges
+def _edge_arrays(edges):
+    """(src u32, dst u32, start u64, end u64, weight f64 or None) from a
+    (src, dst, start, end[, weight]) tuple of arrays, a dict, or TemporalEdges."""
+    w = None
+    if isinstance(edges, tuple) and len(edges) in (4, 5):
+        s, d, a, b = edges[:4]
+        w = edges[4] if len(edges) == 5 else None
     elif isinstance(edges, dict):
         s, d, a, b = edges["src"], edges["dst"], edges["start"], edges["end"]
+        w = edges.get("weight")
     else:
         el = list(edges)
         s = [e.source for e in el]
         d = [e.destination for e in el]
         a = [e.start for e in el]
         b = [e.end for e in el]
+        w = [e.weight for e in el]
+    if w is not None:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        if np.all(w == 1.0):  # the TemporalEdge default: nothing to store
+            w = None
     return (np.ascontiguousarray(s, dtype=np.uint32), np.ascontiguousarray(d, dtype=np.uint32),
-            np.ascontiguousarray(a, dtype=np.uint64), np.ascontiguousarray(b, dtype=np.uint64))
+            np.ascontiguousarray(a, dtype=np.uint64), np.ascontiguousarray(b, dtype=np.uint64), w)
 
 
 class TemporalGraph:
@@ -310,17 +326,20 @@ class TemporalGraph:
     def build(edges, n_v: int, directed: bool = True,
               config: Optional[EngineConfig] = None) -> "TemporalGraph":
         """TemporalGraph::build (engine.cpp:7-34). `edges`: iterable of
-        TemporalEdge, a (src, dst, start, end) tuple of arrays, or a dict."""
+        TemporalEdge, a (src, dst, start, end[, weight]) tuple of arrays, or a
+        dict. Weights other than 1.0 are stored on the device for weighted
+        shortest duration."""
         config = config or EngineConfig()
         if config.index_cutoff < 1:
             raise InvalidArgument("index cutoff must be >= 1")  # selective_index.cpp:156
         lib = load_library()
-        s, d, a, b = _edge_arrays(edges)
+        s, d, a, b, w = _edge_arrays(edges)
         h = ctypes.c_void_p()
-        _check(lib.tgxd_graph_build(n_v, len(s), _ptr(s, ctypes.c_uint32),
-                                    _ptr(d, ctypes.c_uint32), _ptr(a, ctypes.c_uint64),
-                                    _ptr(b, ctypes.c_uint64), 1 if directed else 0,
-                                    config.index_cutoff, ctypes.byref(h)))
+        _check(lib.tgxd_graph_build_weighted(
+            n_v, len(s), _ptr(s, ctypes.c_uint32), _ptr(d, ctypes.c_uint32),
+            _ptr(a, ctypes.c_uint64), _ptr(b, ctypes.c_uint64),
+            None if w is None else _ptr(w, ctypes.c_double), 1 if directed else 0,
+            config.index_cutoff, ctypes.byref(h)))
         return TemporalGraph(h.value, config, directed)
 
     @staticmethod
@@ -454,11 +473,12 @@ def fastest_path(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
 
 def shortest_duration(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
                       opts: Optional[AlgoOptions] = None) -> PathResult:
-    """algorithms.hpp:62-63 / path_algorithms.cpp:410-434 (unweighted: the sum
-    of end - start over the path's edges; edge-state engine)."""
-    if opts is not None and opts.weighted:
-        raise Unsupported("weighted shortest duration: edge weights are not stored on the device")
-    return _run(3, g, source, w, opts)
+    """algorithms.hpp:62-63 / path_algorithms.cpp:196-258, 410-434: the least
+    sum of end - start over the path's edges, or with opts.weighted the sum
+    of edge weights (non-negative integers on every edge a path reaches,
+    else InvalidArgument as duration_metric throws; weight 1.0 on a graph
+    built without weights)."""
+    return _run(5 if opts is not None and opts.weighted else 3, g, source, w, opts)
 
 
 def temporal_bfs(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
@@ -468,7 +488,7 @@ def temporal_bfs(g: TemporalGraph, source: int, w: QueryWindow = QueryWindow(),
 
 
 KINDS = {"earliest_arrival": 0, "latest_departure": 1, "fastest": 2, "shortest_duration": 3,
-         "temporal_bfs": 4}
+         "temporal_bfs": 4, "shortest_duration_weighted": 5}
 
 
 def query_batch(g: TemporalGraph, kind: str, vertices: Sequence[int],

@@ -140,8 +140,17 @@ cudaError_t DeviceBuffer::ensure(size_t nbytes) {
 
 // Builds both layouts from device edge arrays (m edges, already validated and
 // materialized). Frees nothing it does not own.
+__global__ void gather_weights(const uint32_t* idx, const long long* w, uint64_t m,
+                               long long* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride)
+    out[j] = w[idx[j]];
+}
+
+// (d_w / out_w: optional per-edge weight codes, gathered into Out order)
 static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d_dst,
-                         const int32_t* d_st, const int32_t* d_en, uint64_t m) {
+                         const int32_t* d_st, const int32_t* d_en, uint64_t m,
+                         const long long* d_w = nullptr, long long* out_w = nullptr) {
   cudaStream_t s = G->stream;
   const uint32_t n = G->n;
   G->m = m;
@@ -188,6 +197,7 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
       TGXD_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
                                                 end_bit, s));
       gather_layout<<<gb, 256, 0, s>>>(ib, other, kk, vv, dir, m, key, pay);
+      if (dir == 0 && d_w && out_w) gather_weights<<<gb, 256, 0, s>>>(ib, d_w, m, out_w);
       make_fences<<<grid_for(nf, G->sm_count), 256, 0, s>>>(key, m, fence);
     }
     TGXD_CUDA(cudaMemsetAsync(dc, 0, ((size_t)n + 1) * 4, s));
@@ -268,6 +278,7 @@ struct Prepared {
   int strict;
   int ordering;
   bool edge;  // edge-state engine (edges.cuh): Overlaps, or shortest duration
+  bool weighted = false;  // shortest duration summing edge weights
   uint32_t Q;
   std::vector<QueryParam> qp;
   std::vector<Seed> seeds;
@@ -277,7 +288,9 @@ struct Prepared {
 // checked_window (invalid_argument), then the ordering.
 static int prepare(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts, const uint64_t* ta,
                    const uint64_t* tb, int ordering, Prepared& P) {
-  if (kind < 0 || kind > 4) return fail(TGXD_ERR_ARGUMENT, "unknown query kind");
+  if (kind < 0 || kind > 5) return fail(TGXD_ERR_ARGUMENT, "unknown query kind");
+  P.weighted = kind == TGXD_SHORTEST_DURATION_WEIGHTED;
+  if (P.weighted) kind = TGXD_SHORTEST_DURATION;
   if (k == 0 || !verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "empty or null query batch");
   if ((uint64_t)k * G->n >= 0xffffffffULL)
     return fail(TGXD_ERR_ARGUMENT, "batch too large: k * n must stay below 2^32");
@@ -635,6 +648,8 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
     d.nchunks = &w.ectl.as<EdgeCtl>()->nchunks;
     d.n = G->n;
     d.round_limit = m + 16;
+    d.weighted = P.weighted ? 1 : 0;
+    d.w = G->out_w;
     if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
     void* sargs[] = {&d};
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)sd_kernel, dim3(G->coop_blocks_sd),
@@ -670,6 +685,8 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   a.n = G->n;
   a.m = m;
   a.round_limit = m + 16;  // every round queues an edge state that strictly improved
+  a.weighted = P.weighted ? 1 : 0;
+  a.w = P.kind == TGXD_LATEST_DEPARTURE ? nullptr : G->out_w;
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   void* args[] = {&a};
   TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)edge_kernel, dim3(G->coop_blocks_edge),
@@ -989,6 +1006,11 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ectl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
     if (c.error) return fail(TGXD_ERR_CUDA, "edge traversal watchdog: round limit exceeded");
+    if (c.weight_err == 1)  // path_algorithms.cpp:196-203
+      return fail(TGXD_ERR_WINDOW,
+                  "weighted shortest duration needs non-negative integer weights");
+    if (c.weight_err == 2)
+      return fail(TGXD_ERR_TIME_RANGE, "edge weight beyond the device range (2^62)");
     if (!st) return TGXD_OK;
     st->rounds = c.rounds;
     st->candidates = 0;
@@ -1022,7 +1044,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     if (!st) return TGXD_OK;
     st->rounds = 0;
     st->candidates = 0;
-    st->expansions = c.batches + c.chunks;
+    st->expansions = c.visits;
     st->edges_relaxed = c.edges;
     st->index_lookups = c.index_lookups;
     st->kernel_ms = kernel_ms;
@@ -1056,7 +1078,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   if (!st) return TGXD_OK;
   st->rounds = c.rounds;
   st->candidates = c.candidates;
-  st->expansions = c.expansions + ac.batches + ac.chunks;
+  st->expansions = c.expansions + ac.visits;
   st->edges_relaxed = c.edges + c.pull_scanned + ac.edges;
   st->index_lookups = c.index_lookups + ac.index_lookups;
   st->kernel_ms = kernel_ms;
@@ -1115,7 +1137,8 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   if (!G) return fail(TGXD_ERR_ARGUMENT, "null graph");
   if (!out) return fail(TGXD_ERR_ARGUMENT, "null output");
   if (width != 4 && width != 8) return fail(TGXD_ERR_ARGUMENT, "width must be 4 or 8");
-  const bool edge_kind = ordering == TGXD_OVERLAPS || kind == TGXD_SHORTEST_DURATION;
+  const bool edge_kind = ordering == TGXD_OVERLAPS || kind == TGXD_SHORTEST_DURATION ||
+                         kind == TGXD_SHORTEST_DURATION_WEIGHTED;
   if ((kind == TGXD_FASTEST || edge_kind) && k > 1) {  // one sweep / edge traversal per source
     if (!verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "null query arrays");
     tgxd_stats acc;
@@ -1158,7 +1181,7 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   // crossing PCIe: half the bytes on the link, the widening hidden behind it.
   // (up to 2^26 slots: the pinned staging stays <= 256 MB per handle)
   const bool staged = !out_on_device && width == 8 && slots >= (1u << 20) &&
-                      slots <= (1ull << 26) && kind != TGXD_SHORTEST_DURATION;
+                      slots <= (1ull << 26) && P.kind != TGXD_SHORTEST_DURATION;
   void* dout = out;
   if (!out_on_device) {
     if (!dalloc<char>(w.timing_out, slots * width))
@@ -1515,6 +1538,13 @@ int tgxd_graph_generate(const tgxd_gen_config* cfg, int directed, uint64_t index
 int tgxd_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                      const uint64_t* start, const uint64_t* end, int directed,
                      uint64_t index_cutoff, tgxd_graph** out) {
+  return tgxd_graph_build_weighted(n, m, src, dst, start, end, nullptr, directed, index_cutoff,
+                                   out);
+}
+
+int tgxd_graph_build_weighted(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                              const uint64_t* start, const uint64_t* end, const double* weight,
+                              int directed, uint64_t index_cutoff, tgxd_graph** out) {
   if (!out) return fail(TGXD_ERR_ARGUMENT, "null out");
   *out = nullptr;
   if (m && (!src || !dst || !start || !end)) return fail(TGXD_ERR_ARGUMENT, "null edge arrays");
@@ -1547,6 +1577,17 @@ int tgxd_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
     hst[i] = (int32_t)start[i];
     hen[i] = (int32_t)end[i];
   }
+  // weights as int64 codes: the value when a non-negative integer below 2^62,
+  // -1 when not a non-negative integer (duration_metric's invalid_argument,
+  // raised only if a query reaches the edge), -2 when too large
+  std::vector<long long> hw;
+  if (weight) {
+    hw.resize(m);
+    for (uint64_t i = 0; i < m; ++i) {
+      const double x = weight[i], r = std::nearbyint(x);
+      hw[i] = (x < 0.0 || r != x) ? -1ll : (r >= 4611686018427387904.0 ? -2ll : (long long)r);
+    }
+  }
   if (!directed) {  // engine.cpp:13-22
     for (uint64_t i = 0; i < m; ++i) {
       if (src[i] == dst[i]) continue;
@@ -1554,6 +1595,7 @@ int tgxd_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
       hd.push_back(src[i]);
       hst.push_back((int32_t)start[i]);
       hen.push_back((int32_t)end[i]);
+      if (weight) hw.push_back(hw[i]);
     }
   }
   tgxd_graph* G = nullptr;
@@ -1574,7 +1616,20 @@ int tgxd_graph_build(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
     tgxd_graph_destroy(G);
     return fail(TGXD_ERR_CUDA, std::string("edge upload: ") + cudaGetErrorString(e));
   }
-  rc = build_layouts(G, ds, dd, dst_, den, mm);
+  DeviceBuffer bw;
+  long long* dw = nullptr;
+  if (weight) {
+    dw = dalloc<long long>(bw, mm);
+    long long* ow = dalloc<long long>(G->out_wbuf, mm);
+    if (!dw || !ow ||
+        (mm && cudaMemcpyAsync(dw, hw.data(), mm * 8, cudaMemcpyHostToDevice, G->stream) !=
+                   cudaSuccess)) {
+      tgxd_graph_destroy(G);
+      return fail(TGXD_ERR_CUDA, "edge weight upload failed");
+    }
+    G->out_w = ow;
+  }
+  rc = build_layouts(G, ds, dd, dst_, den, mm, dw, G->out_wbuf.as<long long>());
   if (rc) {
     tgxd_graph_destroy(G);
     return rc;
@@ -1615,6 +1670,7 @@ int tgxd_graph_view(tgxd_graph* g, int share, tgxd_graph** out) {
   v->indexed[1] = g->indexed[1];
   v->out = g->out;  // the device graph is the parent's: no buffers owned here
   v->in = g->in;
+  v->out_w = g->out_w;
   v->parent = g;
   v->share = share;
   // grids sized so `share` views fit on the GPU side by side
@@ -1833,6 +1889,12 @@ int tgxd_shortest_duration(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_
                            int ordering, int64_t* out, tgxd_stats* stats) {
   return query_impl(g, TGXD_SHORTEST_DURATION, 1, &source, &t_a, &t_b, ordering, TGXD_MODE_AUTO,
                     out, 8, 0, stats);
+}
+
+int tgxd_shortest_duration_weighted(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b,
+                                    int ordering, int64_t* out, tgxd_stats* stats) {
+  return query_impl(g, TGXD_SHORTEST_DURATION_WEIGHTED, 1, &source, &t_a, &t_b, ordering,
+                    TGXD_MODE_AUTO, out, 8, 0, stats);
 }
 
 int tgxd_temporal_bfs(tgxd_graph* g, uint32_t source, uint64_t t_a, uint64_t t_b, int ordering,

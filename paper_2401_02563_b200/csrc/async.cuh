@@ -66,6 +66,7 @@ struct AsyncCtl {
   unsigned int pad0;
   unsigned long long edges;
   unsigned long long index_lookups;
+  unsigned long long visits;  // vertex expansions (for_each_window_edge calls)
   unsigned long long batches, chunks;
   unsigned long long wait_ns, busy_ns, t_first, t_last;  // time accounting
   unsigned long long t_entry, t_loop;  // handoff: kernel entry, queue ready
@@ -326,6 +327,7 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
       const int32_t hik = min(old, qp.vhi + 1);
       uint32_t pos = kNoPos;
       if (lb < hik) {
+        ix += 1ull << 32;  // a vertex expansion (high word), index lookups (low word)
         if (t > s && km >= lb) {
           act = true;
           const bool fence = a.cutoff != 0 && t - s >= a.cutoff;
@@ -482,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
       a.c->abort = 0;
       a.c->error = 0;
       a.c->quiesce = 0;
-      a.c->edges = a.c->index_lookups = a.c->batches = a.c->chunks = 0;
+      a.c->edges = a.c->index_lookups = a.c->visits = a.c->batches = a.c->chunks = 0;
       a.c->wait_ns = a.c->busy_ns = 0;
       a.c->head.v = a.c->completed.v = t0;
       a.c->tail.v = t0 + (nh + kBatch - 1) / kBatch;
@@ -540,7 +542,8 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
   }
   if (lane_id() == 0) {
     if (work) atomicAdd(&a.c->edges, work);
-    if (ix) atomicAdd(&a.c->index_lookups, ix);
+    if (ix & 0xffffffffull) atomicAdd(&a.c->index_lookups, ix & 0xffffffffull);
+    if (ix >> 32) atomicAdd(&a.c->visits, ix >> 32);
     if (nb) atomicAdd(&a.c->batches, nb);
     if (nc) atomicAdd(&a.c->chunks, nc);
     atomicAdd(&a.c->wait_ns, wait_ns);
@@ -558,6 +561,7 @@ __global__ void async_seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n,
   c->quiesce = 0;
   c->edges = 0;
   c->index_lookups = 0;
+  c->visits = 0;
   c->batches = 0;
   c->chunks = 0;
   c->wait_ns = 0;

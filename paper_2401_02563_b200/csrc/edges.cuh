@@ -46,6 +46,7 @@ struct EdgeCtl {
   unsigned long long nchunks;  // shortest duration: out-edge chunks emitted
   unsigned int rounds;
   unsigned int error;
+  unsigned int weight_err;     // weighted: 1 a reachable edge's weight is invalid, 2 too large
   alignas(128) unsigned int bar_count;
   alignas(128) unsigned int bar_gen;
   unsigned int bar_pad[31];
@@ -67,6 +68,8 @@ struct EdgeArgs {
   EdgeCtl* ctl;
   uint32_t n, m;
   uint32_t round_limit;
+  int weighted;           // shortest: sum edge weights (w; null: every weight 1)
+  const long long* w;     // per position (Out layout) weight code, see tgxd_graph::out_w
 };
 
 constexpr long long kInf64 = 0x7fffffffffffffffLL;
@@ -136,6 +139,24 @@ __device__ __forceinline__ void edge_push_drain(uint32_t* buf, uint32_t& nb, Edg
   __syncwarp();
 }
 
+// The cost of edge f for shortest duration: its duration, or (weighted) its
+// weight; an invalid weight code records the reference's error
+// (path_algorithms.cpp:196-203) and the edge is not taken.
+__device__ __forceinline__ bool edge_cost(int weighted, const long long* w, uint32_t f, int32_t key,
+                                          int32_t val, unsigned int* err, long long* cost) {
+  if (!weighted) {
+    *cost = (long long)(val - key);
+    return true;
+  }
+  const long long c = w ? __ldg(w + f) : 1ll;
+  if (c < 0) {
+    atomicMax(err, c == -1 ? 1u : 2u);
+    return false;
+  }
+  *cost = c;
+  return true;
+}
+
 // Applies candidate f to its edge state; returns true when f joins the next
 // frontier. base: the expanding edge's departure (fastest) or sum (shortest).
 __device__ __forceinline__ bool edge_update(const EdgeArgs& a, uint32_t f, uint2 pf, int32_t kf,
@@ -153,7 +174,9 @@ __device__ __forceinline__ bool edge_update(const EdgeArgs& a, uint32_t f, uint2
     const int32_t b = (int32_t)base;
     if (b > __ldcg(a.dep + f)) improved = b > atomicMax(a.dep + f, b);
   } else {
-    const long long c = base + (long long)((int32_t)pf.y - kf);
+    long long cost;
+    if (!edge_cost(a.weighted, a.w, f, kf, (int32_t)pf.y, &a.ctl->weight_err, &cost)) return false;
+    const long long c = base + cost;
     if (c < (long long)__ldcg(reinterpret_cast<const unsigned long long*>(a.val + f)))
       improved = c < atomicMin(a.val + f, c);
   }
@@ -268,8 +291,9 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) edge_kernel(EdgeArg
             a.dep[f] = kf;  // write_max over an untouched edge (seeds are distinct)
             push = true;
           } else {
-            a.val[f] = (long long)((int32_t)pf.y - kf);
-            push = true;
+            long long cost;
+            push = edge_cost(a.weighted, a.w, f, kf, (int32_t)pf.y, &ctl->weight_err, &cost);
+            if (push) a.val[f] = cost;  // write_min over an untouched edge
           }
         }
       }
@@ -349,6 +373,7 @@ __global__ void edge_init_kernel(int kind, uint32_t m, uint32_t* reached, int32_
     ctl->nchunks = 0;
     ctl->rounds = 0;
     ctl->error = 0;
+    ctl->weight_err = 0;
     ctl->bar_count = 0;
     ctl->bar_gen = 0;
   }

@@ -42,6 +42,8 @@ struct SdArgs {
   unsigned long long* nchunks;  // chunk counter (monotone)
   uint32_t n;
   uint32_t round_limit;
+  int weighted;            // price = weight (w; null: 1) instead of end - start
+  const long long* w;
 };
 
 // Out -> In position map: the In entry of the same (src, dst, start, end)
@@ -112,7 +114,10 @@ __device__ __forceinline__ bool sd_price(const SdArgs& a, uint32_t w, uint32_t f
     }
   }
   if (best == kInf64) return false;
-  const long long c = best + (long long)((int32_t)pf.y - st);
+  // g is an admissible successor: the reference evaluates its cost here
+  long long cost;
+  if (!edge_cost(a.weighted, a.w, f, st, (int32_t)pf.y, &a.ctl->weight_err, &cost)) return false;
+  const long long c = best + cost;
   if (!(c < (long long)__ldcg(reinterpret_cast<const unsigned long long*>(a.val + f)))) return false;
   if (!(c < atomicMin(a.val + f, c))) return false;
   const uint32_t h = pf.x;

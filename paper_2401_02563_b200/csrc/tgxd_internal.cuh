@@ -119,7 +119,7 @@ struct Control {
   unsigned long long chunks;        // big-range chunks emitted
   unsigned long long smalls;        // small ranges emitted
   unsigned long long edges;         // edges handed to the relax step
-  unsigned long long expansions;    // non-empty ranges (chunks + small ranges)
+  unsigned long long expansions;    // vertex expansions (the reference's for_each_window_edge calls)
   unsigned long long index_lookups; // expansions that used the fence index
   unsigned long long pull_scanned;  // reverse-layout entries scanned by pull rounds
   unsigned long long pchunks;       // pull chunks emitted
@@ -198,6 +198,10 @@ struct tgxd_graph {
   tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence, out_kmax;
   tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax;
   tgxd::DeviceBuffer out2in;  // Out -> In position of each edge (shortest duration; lazy)
+  // weighted shortest duration: per Out position the edge's weight as int64
+  // (-1: not a non-negative integer, -2: >= 2^62); null = every weight 1
+  tgxd::DeviceBuffer out_wbuf;
+  const long long* out_w = nullptr;
   bool out2in_ready = false;
   uint32_t max_out_deg = 0;  // fastest: sizes the device candidate lists (lazy)
   bool max_out_deg_known = false;

@@ -474,6 +474,9 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
       const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
       uint32_t pos = kNoPos;
       if (lb < hik) {
+        // one for_each_window_edge call of the reference (engine.hpp:316),
+        // counted in ix's high word; index lookups in its low word
+        ix += 1ull << 32;
         // (s, t, km: segment bounds and last key, loaded with the label)
         if (t > s && km >= lb) {
           act = true;
@@ -1416,6 +1419,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
           trace_round(a, st.rounds, 5, 0);
         }
         phase_pull2(a, rx, pc_end - st.pc_cur, blockIdx.x, gridDim.x, wbuf, scanned);
+        if (tr) ix += (unsigned long long)a.Q * a.n << 32;  // a pull visits every slot (engine.hpp:341)
         st.pc_cur = pc_end;
         work_pull += scanned;
         trace_warp_done(a, st.rounds, 1);
@@ -1494,12 +1498,12 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
     ix += __shfl_xor_sync(0xffffffffu, ix, o);
     work_pull += __shfl_xor_sync(0xffffffffu, work_pull, o);
   }
-  if (lane_id() == 0 && ix) atomicAdd(&ctl->index_lookups, ix);
+  if (lane_id() == 0 && (ix & 0xffffffffull)) atomicAdd(&ctl->index_lookups, ix & 0xffffffffull);
+  if (lane_id() == 0 && (ix >> 32)) atomicAdd(&ctl->expansions, ix >> 32);
   if (lane_id() == 0 && work_pull) atomicAdd(&ctl->pull_scanned, work_pull);
   if (tr) {
     ctl->t_end = gtimer();
     ctl->rounds = st.rounds;
-    ctl->expansions = __ldcg(&ctl->chunks) + __ldcg(&ctl->smalls);
     ctl->candidates = n_cand;
   }
 }

@@ -21,6 +21,13 @@ inputs + outputs as compressed npz files next to this script:
                     test_engine.cpp:223-243 as a path query
   rmat12_ext.npz    the rmat12 graph, 4 sources x 2 windows x 5 metrics x 3
                     orderings
+  weighted.npz      weighted shortest duration (AlgoOptions::weighted,
+                    path_algorithms.cpp:196-258): 240 random small instances
+                    with integer weights 0..5 x all three orderings, a third
+                    of them with one non-integer or negative weight (the
+                    reference's invalid_argument iff a reachable edge carries
+                    it: code 2, labels zero), plus the rmat12 graph with
+                    seeded integer weights, 4 sources x 3 orderings
   cost_model.npz    the selective-index cost model (choose_access_method:
                     decision, beta_hat, k_hat; count_in_window) on the rmat12
                     graph indexed at 64 (both directions, every indexed vertex
@@ -298,6 +305,61 @@ def cost_model():
     np.savez_compressed(HERE / "cost_model.npz", **out)
 
 
+def weighted():
+    from oracle.pyoracle import OracleError, generate
+    rng = np.random.default_rng(20260105)
+    eoff, src, dst, st, en, wt, meta, labels = [0], [], [], [], [], [], [], []
+    for it in range(240):
+        n = int(rng.integers(1, 13))
+        m = int(rng.integers(0, 41))
+        s = rng.integers(0, n, m)
+        d = rng.integers(0, n, m)
+        a = rng.integers(0, 61, m)
+        b = a + rng.integers(0, 9, m)
+        w = rng.integers(0, 6, m).astype(np.float64)
+        if it % 3 == 0 and m:
+            w[int(rng.integers(0, m))] = (2.5, -1.0, 0.25)[it // 3 % 3]
+        ref = Reference((s, d, a, b), n, True, 0, w)
+        ta, tb = sorted(int(x) for x in rng.integers(0, 76, 2))
+        v = int(rng.integers(0, n))
+        for ordv in (0, 1, 2):
+            try:
+                out, code = ref.query("shortest_duration_weighted", v, ta, tb, ordv), 0
+            except OracleError as e:
+                out, code = np.zeros(n, np.int64), e.code
+            meta.append((it, n, v, ta, tb, ordv, code, sum(len(x) for x in labels)))
+            labels.append(out)
+        ref.close()
+        src.append(s); dst.append(d); st.append(a); en.append(b); wt.append(w)
+        eoff.append(eoff[-1] + m)
+    # the rmat12 graph with seeded integer weights
+    import paper_2401_02563_b200 as T
+    g = T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 7, cube_root_starts=True)
+    E = generate(g)
+    n = g.n_vertices
+    W = np.random.default_rng(5).integers(0, 1000, len(E[0])).astype(np.float64)
+    ref = Reference(E, n, True, 0, W)
+    deg = np.bincount(E[0], minlength=n)
+    srcs = [int(np.argmax(deg))] + [int(x) for x in np.random.default_rng(13).choice(
+        np.flatnonzero(deg), 3)]
+    rq, rl = [], []
+    for sidx, v in enumerate(srcs):
+        ta, tb = (0, 999_999) if sidx % 2 == 0 else (200_000, 800_000)
+        for ordv in (0, 1, 2):
+            rq.append((v, ta, tb, ordv))
+            rl.append(ref.query("shortest_duration_weighted", v, ta, tb, ordv))
+    ref.close()
+    np.savez_compressed(
+        HERE / "weighted.npz", eoff=np.array(eoff, np.int64),
+        src=np.concatenate(src).astype(np.uint32), dst=np.concatenate(dst).astype(np.uint32),
+        start=np.concatenate(st).astype(np.uint64), end=np.concatenate(en).astype(np.uint64),
+        weight=np.concatenate(wt), meta=np.array(meta, np.int64),
+        labels=np.concatenate(labels).astype(np.int64),
+        rmat_edge_digest=np.array([edge_digest(E)], np.uint64),
+        rmat_weight_seed=np.array([5], np.int64), rmat_meta=np.array(rq, np.int64),
+        rmat_labels=np.stack(rl).astype(np.int64))
+
+
 def main():
     import paper_2401_02563_b200 as T
     small_random()
@@ -318,6 +380,7 @@ def main():
     scaled("uniform14", g2, qs2)
     extended()
     cost_model()
+    weighted()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
@@ -325,5 +388,7 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["cost_model"]:
         cost_model()
+    elif sys.argv[1:] == ["weighted"]:
+        weighted()
     else:
         main()

@@ -92,8 +92,19 @@ def test_error_semantics():
         T.fastest_path(g, 0, T.QueryWindow(9, 3))
     with pytest.raises(T.InvalidArgument):     # internal.hpp:19-21
         T.earliest_arrival(g, 0, T.QueryWindow(1 << 63, (1 << 64) - 1))
-    with pytest.raises(T.Unsupported):         # weights are not stored on the device
-        T.shortest_duration(g, 0, T.QueryWindow(), T.AlgoOptions(weighted=True))
+    # weighted shortest duration: weight 1.0 without stored weights; a
+    # reachable non-integer weight is invalid_argument (path_algorithms.cpp:196-203)
+    assert T.shortest_duration(g, 0, T.QueryWindow(),
+                               T.AlgoOptions(weighted=True)).values[1] == 1
+    gw = T.TemporalGraph.build(S.hand_edges([(0, 1, 3, 5), (1, 0, 7, 8)]) + (
+        np.array([2.0, 0.5]),), 2)
+    with pytest.raises(T.InvalidArgument):
+        T.shortest_duration(gw, 0, T.QueryWindow(), T.AlgoOptions(weighted=True))
+    assert T.shortest_duration(gw, 0, T.QueryWindow(0, 6),  # the 0.5 edge is outside
+                               T.AlgoOptions(weighted=True)).values[1] == 2
+    with pytest.raises(T.TimeRangeError):      # beyond the device's int64 weight range
+        gb = T.TemporalGraph.build(S.hand_edges([(0, 1, 3, 5)]) + (np.array([2.0 ** 63]),), 2)
+        T.shortest_duration(gb, 0, T.QueryWindow(), T.AlgoOptions(weighted=True))
     with pytest.raises(T.OutOfRange):
         T.shortest_duration(g, 2)
     with pytest.raises(T.InvalidArgument):

@@ -91,3 +91,59 @@ def test_reduced_configs_edge_state_parity(name):
             want = o.query(kind, q.vertex, q.window.t_a, q.window.t_b, ordv)
             got = run(g, kind, q.vertex, q.window.t_a, q.window.t_b, ordv)
             assert np.array_equal(got, want), (name, kind, ordv)
+
+
+def test_weighted_shortest_duration_golden():
+    """AlgoOptions::weighted (path_algorithms.cpp:196-258) on the device:
+    the reference's fixtures, its invalid_argument (a reachable edge with a
+    non-integer or negative weight) as InvalidArgument, every ordering."""
+    z = np.load(S.GOLDEN / "weighted.npz")
+    eoff = z["eoff"]
+    errors = 0
+    for it, n, v, ta, tb, ordv, code, lo in z["meta"]:
+        a, b = eoff[it], eoff[it + 1]
+        E = (z["src"][a:b], z["dst"][a:b], z["start"][a:b], z["end"][a:b], z["weight"][a:b])
+        g = T.TemporalGraph.build(E, int(n))
+        opts = T.AlgoOptions(ordering=T.Ordering(int(ordv)), weighted=True)
+        if code:
+            errors += 1
+            with pytest.raises(T.InvalidArgument):
+                T.shortest_duration(g, int(v), T.QueryWindow(int(ta), int(tb)), opts)
+        else:
+            got = T.shortest_duration(g, int(v), T.QueryWindow(int(ta), int(tb)), opts).values
+            assert np.array_equal(got, z["labels"][lo:lo + n]), (it, ordv)
+        g.close()
+    assert errors > 0
+
+
+def test_weighted_shortest_duration_rmat12():
+    z = np.load(S.GOLDEN / "weighted.npz")
+    gen = T.GenConfig.rmat(12, 16, 0.57, 0.19, 0.19, 1_000_000, 0.02, 7, cube_root_starts=True)
+    E = T.generate_edges(gen)
+    assert S.edge_digest(E) == int(z["rmat_edge_digest"][0])
+    W = np.random.default_rng(int(z["rmat_weight_seed"][0])).integers(0, 1000, len(E[0]))
+    g = T.TemporalGraph.build(E + (W.astype(np.float64),), gen.n_vertices)
+    for (v, ta, tb, ordv), want in zip(z["rmat_meta"], z["rmat_labels"]):
+        got = T.shortest_duration(g, int(v), T.QueryWindow(int(ta), int(tb)),
+                                  T.AlgoOptions(ordering=T.Ordering(int(ordv)),
+                                                weighted=True)).values
+        assert np.array_equal(got, want), (v, ordv)
+    # unweighted queries on the weighted graph still sum durations
+    o = Oracle(E, gen.n_vertices)
+    v, ta, tb, _ = (int(x) for x in z["rmat_meta"][0])
+    assert np.array_equal(T.shortest_duration(g, v, T.QueryWindow(ta, tb)).values,
+                          o.query("shortest_duration", v, ta, tb))
+
+
+def test_weighted_on_unweighted_graph_counts_edges():
+    """Without stored weights every edge weighs 1.0 (TemporalEdge default)."""
+    gen = T.GenConfig.rmat(10, 8, 0.57, 0.19, 0.19, 1_000_000, 0.02, 9, cube_root_starts=True)
+    E = T.generate_edges(gen)
+    n = gen.n_vertices
+    g = T.TemporalGraph.build(E, n)
+    o = Oracle(E, n, True, np.ones(len(E[0])))
+    src = int(np.argmax(np.bincount(E[0], minlength=n)))
+    for ordv in (0, 1, 2):
+        got = T.shortest_duration(g, src, T.QueryWindow(0, 999_999),
+                                  T.AlgoOptions(ordering=T.Ordering(ordv), weighted=True)).values
+        assert np.array_equal(got, o.query("shortest_duration_weighted", src, 0, 999_999, ordv))
