@@ -25,6 +25,7 @@
 #include "sd.cuh"
 #include "lanes.cuh"
 #include "candidates.cuh"
+#include "tail.cuh"
 #include "costmodel.cuh"
 
 namespace tgxd {
@@ -224,6 +225,39 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
   return TGXD_OK;
 }
 
+// The cluster tail engine's size: 16 CTAs (non-portable) when the device can
+// co-schedule them, else the portable 8, else 0 (the async engine finishes
+// tails). TGXD_TAIL=async forces the async engine; TGXD_TAIL_CLUSTER=8/16.
+static int tail_cluster_size() {
+  static const int size = [] {
+    const char* e = getenv("TGXD_TAIL");
+    if (e && std::string(e) == "async") return 0;
+    int want = 16;
+    if (const char* c = getenv("TGXD_TAIL_CLUSTER")) want = atoi(c);
+    cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c : {16, 8}) {
+      if (c > want) continue;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(kTailThreads);
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = c;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, tail_kernel, &cfg) == cudaSuccess &&
+          clusters > 0)
+        return c;
+      cudaGetLastError();
+    }
+    return 0;
+  }();
+  return size;
+}
+
 static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph** out) {
   int dev = 0, count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
@@ -266,6 +300,7 @@ static int new_graph(uint32_t n, uint64_t index_cutoff, int directed, tgxd_graph
   int per_sm_l = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, lanes_kernel, kThreads, 0);
   G->coop_blocks_lanes = std::max(1, per_sm_l) * G->sm_count;
+  G->tail_cluster = tail_cluster_size();
   *out = G;
   return TGXD_OK;
 }
@@ -499,6 +534,21 @@ static int ensure_async(tgxd_graph* G, uint32_t Q, bool required = true) {
         w.aunits.as<uint32_t>(), nunits, w.actl.as<AsyncCtl>());
     w.a_slots = slots;
     w.a_units = nunits;
+  }
+  return TGXD_OK;
+}
+
+// The cluster tail engine's per-slot stamps (zeroed once; epochs keep them
+// valid across queries) and control block.
+static int ensure_tail(tgxd_graph* G, uint32_t Q) {
+  Workspace& w = G->ws;
+  const uint64_t slots = (uint64_t)Q * G->n;
+  if (w.t_slots < slots || !w.tctl.p) {
+    if (!dalloc<uint32_t>(w.tstamp, slots) || !dalloc<TailCtl>(w.tctl, 1))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (tail engine)");
+    TGXD_CUDA(cudaMemsetAsync(w.tstamp.p, 0, slots * 4, G->stream));
+    TGXD_CUDA(cudaMemsetAsync(w.tctl.p, 0, sizeof(TailCtl), G->stream));
+    w.t_slots = slots;
   }
   return TGXD_OK;
 }
@@ -890,23 +940,33 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   // (measured on config 2: the queue-driven expand is cheaper below that).
   a.dense_f = std::max<uint64_t>(1024, slots / 2);
   a.push_w = std::max<uint64_t>(4096, slots * 4);
-  // a frontier holding a quarter of the slots is pulled (direction switch;
-  // measured on configs 2 and 4: below that the pull's sweep over every slot
-  // costs more than it saves)
-  // (TGXD_PULL_DIV overrides the share's divisor; 0 turns AUTO's pulls off)
+  // a frontier holding half the slots is pulled (direction switch; a quarter
+  // for fastest sweeps). Measured over config 2's 8-source rotation: pulling
+  // from a quarter 1.255 ms per query, a third 1.136, half 1.102, never
+  // 1.144 — a pull scans every open slot's in-edges, which is wasted on the
+  // many vertices still unreachable; config 4 fastest 5.14 (quarter) vs 5.31
+  // ms (half) (TGXD_PULL_DIV overrides the divisor; 0 turns AUTO's pulls off)
   const char* pf = getenv("TGXD_PULL_DIV");
-  const int pdiv = pf ? atoi(pf) : 4;
+  const int pdiv = pf ? atoi(pf) : (fast ? 4 : 2);
   a.pull_f = pdiv <= 0 ? ~0ull : std::max<uint64_t>(1024, slots / pdiv);
   if (const char* pfx = getenv("TGXD_PULL_F")) a.pull_f = strtoull(pfx, nullptr, 10);  // tests
   // AUTO: a frontier past its peak and below 1/16 of the slots is finished by
   // the async engine (TGXD_HANDOFF_F overrides the size; 0 turns it off)
+  // (the cluster tail engine takes smaller frontiers: its 16 SMs are fast
+  // per round but a fraction of the GPU's throughput)
   a.handoff_f = 0;
+  const bool cluster_tail = G->tail_cluster > 0;
   if (mode == TGXD_MODE_AUTO && !fast) {
     const char* hf = getenv("TGXD_HANDOFF_F");
-    const uint64_t want = hf ? strtoull(hf, nullptr, 10) : std::max<uint64_t>(4096, slots / 16);
-    if (want && ensure_async(G, P.Q, false) == TGXD_OK) a.handoff_f = want;
+    const uint64_t want = hf             ? strtoull(hf, nullptr, 10)
+                          : cluster_tail ? std::min<uint64_t>(32768, std::max<uint64_t>(4096, slots / 16))
+                                         : std::max<uint64_t>(4096, slots / 16);
+    if (want && (cluster_tail ? ensure_tail(G, P.Q) : ensure_async(G, P.Q, false)) == TGXD_OK)
+      a.handoff_f = want;
   }
   w.last_handoff = a.handoff_f != 0;
+  w.last_tail = w.last_handoff && cluster_tail;
+  if (w.last_tail) tail_reset_kernel<<<1, 1, 0, s>>>(w.tctl.as<TailCtl>());
   {
     const char* hg = getenv("TGXD_HANDOFF_GROWTH");
     a.handoff_growth = hg ? (unsigned)std::max(1, atoi(hg)) : 8u;
@@ -940,7 +1000,44 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       TGXD_CUDA(cudaEventRecord(G->early_ev, s));
       w.early_done = true;
     }
-    if (a.handoff_f) {  // the continuation exits at once unless the round kernel handed off
+    if (a.handoff_f && cluster_tail) {  // exits at once unless the round kernel handed off
+      TailArgs t;
+      t.g = g;
+      t.qp = a.qp;
+      t.X = a.X;
+      t.EP = a.EP;
+      t.fa = a.fa;
+      t.fb = a.fb;
+      t.chunks = a.chunks;
+      t.stamp = w.tstamp.as<uint32_t>();
+      t.hctl = a.ctl;
+      t.tc = w.tctl.as<TailCtl>();
+      t.n = G->n;
+      t.Q = P.Q;
+      t.strict = P.strict;
+      t.cutoff = a.cutoff;
+      t.round_limit = (uint32_t)std::min<uint64_t>(0xfffffff0ULL, slots + 16);
+      t.slots = slots;
+      t.chg = early ? w.chg.as<uint32_t>() : nullptr;
+      t.chg_n = early ? w.chg_n.as<unsigned long long>() : nullptr;
+      t.chg_cap = early ? w.chg_cap : 0;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G->tail_cluster);
+      cfg.blockDim = dim3(kTailThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = G->tail_cluster;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      TGXD_CUDA(cudaLaunchKernelEx(&cfg, tail_kernel, t));
+      if (early)
+        tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
+            w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X,
+            G->patch_dev);
+    } else if (a.handoff_f) {  // the continuation exits at once unless the round kernel handed off
       AsyncArgs h;
       h.g = g;
       h.qp = a.qp;
@@ -1057,7 +1154,21 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   if (c.error) return fail(TGXD_ERR_CUDA, "traversal watchdog: round limit exceeded");
   AsyncCtl ac;
   std::memset(&ac, 0, sizeof ac);
-  if (G->ws.last_handoff && c.handoff_n) {  // the async engine finished the tail
+  uint32_t tail_rounds = 0;
+  if (G->ws.last_tail && c.handoff_n) {  // the cluster tail engine finished the query
+    TailCtl tc;
+    TGXD_CUDA(cudaMemcpyAsync(&tc, G->ws.tctl.p, sizeof tc, cudaMemcpyDeviceToHost, G->stream));
+    TGXD_CUDA(cudaStreamSynchronize(G->stream));
+    if (tc.error) return fail(TGXD_ERR_CUDA, "tail traversal watchdog: round limit exceeded");
+    if (getenv("TGXD_ASTATS"))
+      fprintf(stderr, "tail %llu: rounds %u edges %llu visits %llu gap %.1f us loop %.1f us\n",
+              c.handoff_n, tc.rounds, tc.edges, tc.visits, (tc.t_entry - c.t_end) / 1e3,
+              (tc.t_end - tc.t_entry) / 1e3);
+    tail_rounds = tc.rounds;
+    ac.edges = tc.edges;
+    ac.visits = tc.visits;
+    ac.index_lookups = tc.index_lookups;
+  } else if (G->ws.last_handoff && c.handoff_n) {  // the async engine finished the tail
     TGXD_CUDA(cudaMemcpyAsync(&ac, G->ws.actl.p, sizeof ac, cudaMemcpyDeviceToHost, G->stream));
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
     if (ac.error) {
@@ -1076,7 +1187,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
               (ac.t_last - ac.t_loop) / 1e3);
   }
   if (!st) return TGXD_OK;
-  st->rounds = c.rounds;
+  st->rounds = c.rounds + tail_rounds;
   st->candidates = c.candidates;
   st->expansions = c.expansions + ac.visits;
   st->edges_relaxed = c.edges + c.pull_scanned + ac.edges;

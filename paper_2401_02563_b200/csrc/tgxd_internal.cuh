@@ -91,6 +91,9 @@ struct Workspace {
   bool last_edge = false;
   bool last_async = false;
   bool last_handoff = false;  // round kernel may have handed its tail to the async engine
+  bool last_tail = false;     // ... to the cluster tail engine (tail.cuh)
+  DeviceBuffer tstamp, tctl;  // cluster tail engine: per-slot stamps, control block
+  uint64_t t_slots = 0;
   // early host copy (api.cu query_impl): the labels leave for the host while
   // the async tail runs; the tail's changed labels are patched afterwards
   bool early_req = false;   // set by the caller for one launch
@@ -220,6 +223,7 @@ struct tgxd_graph {
   int coop_blocks_sd = 0;
   int coop_blocks_lanes = 0;
   int tail_per_sm = 3;       // CTAs per SM of the async tail continuation
+  int tail_cluster = 0;      // CTAs of the cluster tail engine (0: async engine)
   int share = 1;             // views: handles meant to run side by side (grids divided)
   const tgxd_graph* parent = nullptr;  // views: the handle whose device graph is shared
   std::mutex mu;

@@ -94,7 +94,7 @@ int main() {
                       fill ? "INF " : "zero", ms, m / (ms * 1e6));
     }
   };
-  for (int bps : {3, 4, 8}) {
+  for (int bps : {2, 4, 6, 8}) {
     for (int fill : {0, 0x7f}) {
       run(relax<4, true>, "U=4 hints", bps, fill);
       run(relax<4, false>, "U=4 no hints", bps, fill);
