@@ -953,13 +953,16 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   // AUTO: a frontier past its peak and below 1/16 of the slots is finished by
   // the async engine (TGXD_HANDOFF_F overrides the size; 0 turns it off)
   // (the cluster tail engine takes smaller frontiers: its 16 SMs are fast
-  // per round but a fraction of the GPU's throughput)
+  // per round — 5-7 us for a few hundred slots against ~20 us on the grid —
+  // but a ninth of the GPU's throughput; config 2's rotation: handoff at 16K
+  // 1.096 ms, 32K 1.101, 64K 1.123, the async engine at 1/16 of the slots
+  // 1.106; config 5 query 2.81 vs 3.03 ms)
   a.handoff_f = 0;
   const bool cluster_tail = G->tail_cluster > 0;
   if (mode == TGXD_MODE_AUTO && !fast) {
     const char* hf = getenv("TGXD_HANDOFF_F");
     const uint64_t want = hf             ? strtoull(hf, nullptr, 10)
-                          : cluster_tail ? std::min<uint64_t>(32768, std::max<uint64_t>(4096, slots / 16))
+                          : cluster_tail ? std::min<uint64_t>(16384, std::max<uint64_t>(4096, slots / 16))
                                          : std::max<uint64_t>(4096, slots / 16);
     if (want && (cluster_tail ? ensure_tail(G, P.Q) : ensure_async(G, P.Q, false)) == TGXD_OK)
       a.handoff_f = want;
@@ -1021,6 +1024,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       t.chg = early ? w.chg.as<uint32_t>() : nullptr;
       t.chg_n = early ? w.chg_n.as<unsigned long long>() : nullptr;
       t.chg_cap = early ? w.chg_cap : 0;
+      t.trace = w.trace_dev;
+      t.trace_cap = w.trace_cap;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(G->tail_cluster);
       cfg.blockDim = dim3(kTailThreads);

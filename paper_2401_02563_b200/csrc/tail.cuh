@@ -73,46 +73,92 @@ struct TailArgs {
   uint32_t* chg;
   unsigned long long* chg_n;
   unsigned long long chg_cap;
+  // optional per-round trace (mapped host memory, rows after the round
+  // kernel's): t0, t after phase 1, t end, F, chunks, -, -, kind 4
+  unsigned long long* trace;
+  uint32_t trace_cap;
 };
+
+__device__ __forceinline__ void tail_trace(const TailArgs& a, uint32_t row, int slot,
+                                           unsigned long long v) {
+  if (a.trace && row < a.trace_cap) {
+    volatile unsigned long long* t = a.trace;
+    t[row * 8 + slot] = v;
+  }
+}
 
 namespace cgt = cooperative_groups;
 
-// One relax step: lane's edge f (when act) of query q.
-__device__ __forceinline__ void tail_relax_step(const TailArgs& a, bool act, uint32_t f,
-                                                uint32_t q, uint32_t epoch, uint64_t pol_stream,
-                                                uint64_t pol_keep, unsigned long long* push_cnt,
-                                                uint32_t* fout) {
-  bool imp = false, push = false;
-  uint32_t d = 0;
-  if (act) {
-    const uint2 pl = ld_stream2(a.g.pay + f, pol_stream);
-    d = q * a.n + pl.x;
-    const int32_t v = (int32_t)pl.y;
-    const int32_t vhi = a.Q == 1 ? a.qp[0].vhi : __ldg(&a.qp[q].vhi);
-    if (v <= vhi && v < ld_state(a.X + d, pol_keep)) {
-      const int32_t old = atomicMin(a.X + d, v);  // write_min, parallel.hpp:91-99
-      if (v < old) {
-        imp = true;
-        push = atomicExch(a.stamp + d, epoch) != epoch;  // claim_stamp, parallel.hpp:113-121
-      }
-    }
+// kTailU relax steps of 32 edges (lane's edge f[u] of query q[u] when
+// act[u]), every load and atomic of the batch in flight together; the
+// improved slots whose stamp this round claims are queued with one DSMEM
+// reservation for the whole batch.
+constexpr int kTailU = 4;
+__device__ __forceinline__ void tail_relax(const TailArgs& a, const bool (&act)[kTailU],
+                                           const uint32_t (&f)[kTailU],
+                                           const uint32_t (&q)[kTailU], uint32_t epoch,
+                                           uint64_t pol_stream, uint64_t pol_keep,
+                                           unsigned long long* push_cnt, uint32_t* fout) {
+  uint2 pl[kTailU];
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u)
+    pl[u] = act[u] ? ld_stream2(a.g.pay + f[u], pol_stream) : make_uint2(0u, (uint32_t)kInf);
+  uint32_t d[kTailU];
+  int32_t v[kTailU], cur[kTailU];
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u) {
+    d[u] = q[u] * a.n + pl[u].x;
+    v[u] = (int32_t)pl[u].y;
+    const int32_t vhi = a.Q == 1 ? a.qp[0].vhi : __ldg(&a.qp[q[u]].vhi);
+    if (!(act[u] && v[u] <= vhi)) v[u] = kInf;  // window containment, types.hpp:55-57
+    cur[u] = v[u] != kInf ? ld_state(a.X + d[u], pol_keep) : kInf;
+  }
+  int32_t old[kTailU];
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u)
+    old[u] = v[u] < cur[u] ? atomicMin(a.X + d[u], v[u]) : v[u];  // write_min, parallel.hpp:91-99
+  bool imp[kTailU], push[kTailU];
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u) {
+    imp[u] = v[u] < old[u];
+    // claim_stamp (parallel.hpp:113-121): queued once per round
+    push[u] = imp[u] && atomicExch(a.stamp + d[u], epoch) != epoch;
   }
   const uint32_t lane = lane_id();
-  const uint32_t pm = __ballot_sync(0xffffffffu, push);
-  if (pm) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(push_cnt, (unsigned long long)__popc(pm));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (push) fout[base + __popc(pm & ((1u << lane) - 1))] = d;
+  const uint32_t below = (1u << lane) - 1;
+  uint32_t pm[kTailU], tot = 0;
+#pragma unroll
+  for (int u = 0; u < kTailU; ++u) {
+    pm[u] = __ballot_sync(0xffffffffu, push[u]);
+    tot += __popc(pm[u]);
   }
-  if (a.chg) {
-    const uint32_t im = __ballot_sync(0xffffffffu, imp);
-    if (im) {
+  if (tot) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(push_cnt, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+    for (int u = 0; u < kTailU; ++u) {
+      if (push[u]) fout[base + __popc(pm[u] & below)] = d[u];
+      base += __popc(pm[u]);
+    }
+  }
+  if (a.chg) {  // early host copy: every lowered slot is listed
+    uint32_t im[kTailU], itot = 0;
+#pragma unroll
+    for (int u = 0; u < kTailU; ++u) {
+      im[u] = __ballot_sync(0xffffffffu, imp[u]);
+      itot += __popc(im[u]);
+    }
+    if (itot) {
       unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(a.chg_n, (unsigned long long)__popc(im));
+      if (lane == 0) base = atomicAdd(a.chg_n, (unsigned long long)itot);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const unsigned long long k = base + __popc(im & ((1u << lane) - 1));
-      if (imp && k < a.chg_cap) a.chg[k] = d;
+#pragma unroll
+      for (int u = 0; u < kTailU; ++u) {
+        const unsigned long long k = base + __popc(im[u] & below);
+        if (imp[u] && k < a.chg_cap) a.chg[k] = d[u];
+        base += __popc(im[u]);
+      }
     }
   }
 }
@@ -149,8 +195,14 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
   uint32_t* qout = qin == a.fa ? a.fb : a.fa;
   unsigned long long work = 0, ix = 0;
   uint32_t r = 0;
+  const uint32_t row0 = a.trace ? __ldcg(&a.hctl->rounds) : 0u;
   for (;; ++r) {
     const unsigned long long F = *(volatile unsigned long long*)&cnt[r % 3];
+    if (lead) {
+      tail_trace(a, row0 + r, 0, gtimer());
+      tail_trace(a, row0 + r, 3, F);
+      tail_trace(a, row0 + r, 7, 4);
+    }
     if (F == 0) break;
     if (r >= a.round_limit) {
       if (lead) a.tc->error = 1;
@@ -163,11 +215,13 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
     unsigned long long* push_cnt = &cnt[(r + 1) % 3];
     unsigned long long* ch_cnt = &cnt[3 + r % 3];
     const uint32_t epoch = base_epoch + r + 1;
-    // (1) expand 32 slots per warp, relax short ranges in place
-    for (unsigned long long b = (unsigned long long)gw * 32; b < F; b += (unsigned long long)nw * 32) {
+    // (1) each warp expands up to 32 slots (spread over all warps when the
+    // frontier is small) and relaxes their short ranges in place
+    const uint32_t ipw = (uint32_t)min(32ull, max(1ull, (F + nw - 1) / nw));
+    for (unsigned long long b = (unsigned long long)gw * ipw; b < F; b += (unsigned long long)nw * ipw) {
       const unsigned long long i = b + lane;
       uint32_t q = 0, p0 = 0, cnt_e = 0;
-      if (i < F) {
+      if (lane < ipw && i < F) {
         const uint32_t item = __ldcg(qin + i);
         q = a.Q == 1 ? 0u : item / a.n;
         const uint32_t v = item - q * a.n;
@@ -220,8 +274,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
           }
         }
       }
-      // short ranges: the warp's ranges packed 32 edges per step (the owner
-      // lane of item t is found from the mask of range starts)
+      // short ranges: the warp's ranges packed 32 edges per step, kTailU
+      // steps in flight (the owner lane of edge t is found from the mask of
+      // range starts)
       const uint32_t c = big ? 0u : cnt_e;
       uint32_t incl = c;
 #pragma unroll
@@ -232,36 +287,54 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
       const uint32_t start = incl - c;
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
       const uint32_t nonempty = __ballot_sync(0xffffffffu, c != 0);
-      for (uint32_t sb = 0; sb < total; sb += 32) {
-        const uint32_t before = __ballot_sync(0xffffffffu, c != 0 && start <= sb);
-        const uint32_t i0 = before ? 31 - __clz(before) : 0;
-        const uint32_t rel = start - sb;
-        const uint32_t bit = (c != 0 && start > sb && rel < 32) ? (1u << rel) : 0u;
-        const uint32_t mask = __reduce_or_sync(0xffffffffu, bit);
-        const uint32_t k = __popc(mask & ((2u << lane) - 1));
-        const uint32_t own = k ? __fns(nonempty, i0, (int)k + 1) & 31 : i0;
-        const uint32_t olo = __shfl_sync(0xffffffffu, p0, own);
-        const uint32_t ost = __shfl_sync(0xffffffffu, start, own);
-        const uint32_t oq = __shfl_sync(0xffffffffu, q, own);
-        const uint32_t tt = sb + lane;
-        tail_relax_step(a, tt < total, olo + (tt - ost), oq, epoch, pol_stream, pol_keep,
-                        push_cnt, qout);
+      for (uint32_t sb0 = 0; sb0 < total; sb0 += 32 * kTailU) {
+        bool act[kTailU];
+        uint32_t f[kTailU], oqs[kTailU];
+#pragma unroll
+        for (int u = 0; u < kTailU; ++u) {
+          const uint32_t sb = sb0 + 32 * u;
+          const uint32_t before = __ballot_sync(0xffffffffu, c != 0 && start <= sb);
+          const uint32_t i0 = before ? 31 - __clz(before) : 0;
+          const uint32_t rel = start - sb;
+          const uint32_t bit = (c != 0 && start > sb && rel < 32) ? (1u << rel) : 0u;
+          const uint32_t mask = __reduce_or_sync(0xffffffffu, bit);
+          const uint32_t k = __popc(mask & ((2u << lane) - 1));
+          const uint32_t own = k ? __fns(nonempty, i0, (int)k + 1) & 31 : i0;
+          const uint32_t olo = __shfl_sync(0xffffffffu, p0, own);
+          const uint32_t ost = __shfl_sync(0xffffffffu, start, own);
+          oqs[u] = __shfl_sync(0xffffffffu, q, own);
+          const uint32_t tt = sb + lane;
+          act[u] = tt < total;
+          f[u] = olo + (tt - ost);
+        }
+        tail_relax(a, act, f, oqs, epoch, pol_stream, pol_keep, push_cnt, qout);
       }
     }
     cluster.sync();
     // (2) chunks, when the round emitted any (the count is final after the barrier)
     const unsigned long long nch = *(volatile unsigned long long*)ch_cnt;
+    if (lead) {
+      tail_trace(a, row0 + r, 1, gtimer());
+      tail_trace(a, row0 + r, 4, nch);
+    }
     if (nch) {
+      static_assert(kTailChunk == 32 * kTailU, "a chunk is one relax batch");
       for (unsigned long long cix = gw; cix < nch; cix += nw) {
         const uint2 ch = __ldcg(a.chunks + cix);
         const uint32_t cq = ch.y >> 10, len = ch.y & 1023u;
-#pragma unroll 1
-        for (uint32_t u = 0; u < len; u += 32)
-          tail_relax_step(a, u + lane < len, ch.x + u + lane, cq, epoch, pol_stream, pol_keep,
-                          push_cnt, qout);
+        bool act[kTailU];
+        uint32_t f[kTailU], qs[kTailU];
+#pragma unroll
+        for (int u = 0; u < kTailU; ++u) {
+          act[u] = 32 * u + lane < len;
+          f[u] = ch.x + 32 * u + lane;
+          qs[u] = cq;
+        }
+        tail_relax(a, act, f, qs, epoch, pol_stream, pol_keep, push_cnt, qout);
       }
       cluster.sync();
     }
+    if (lead) tail_trace(a, row0 + r, 2, gtimer());
     uint32_t* tq = qin;
     qin = qout;
     qout = tq;

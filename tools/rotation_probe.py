@@ -29,8 +29,12 @@ for q in qs:
         for row in tr:
             if row[0] == 0:
                 break
-            kind = {1: "L", 2: "D", 3: "P"}.get(int(row[7]), "G")
-            rows.append([kind, int(row[3]), round((row[2] - row[0]) / 1e3, 1)])
+            kind = {1: "L", 2: "D", 3: "P", 4: "T"}.get(int(row[7]), "G")
+            if kind == "T":  # cluster tail round: phase 1 and chunk phase
+                rows.append([kind, int(row[3]), round((row[1] - row[0]) / 1e3, 1),
+                             round((row[2] - row[1]) / 1e3, 1) if row[2] else 0, int(row[4])])
+            else:
+                rows.append([kind, int(row[3]), round((row[2] - row[0]) / 1e3, 1)])
     tot, ker = T.time_queries(g, q.kind, [q.vertex], [q.window], warmup=2, steps=args.steps)
     ms = tot / args.steps
     tot_e += e
