@@ -1249,37 +1249,119 @@ static bool host_avx2() {
 
 static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts,
                       const uint64_t* ta, const uint64_t* tb, int ordering, int mode, void* out,
+                      int width, int out_on_device, tgxd_stats* stats);
+
+// Label bytes (4 per slot) above which a wide-window AUTO batch is split
+// (TGXD_BATCH_BUDGET_MB overrides): 256 MiB = groups of 4 on config 5, the
+// best measured grouping there (45 ms vs 47 one by one and 53 as one batch).
+static uint64_t batch_label_budget() {
+  const char* e = getenv("TGXD_BATCH_BUDGET_MB");
+  return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) << 20 : 256ull << 20;
+}
+
+__global__ void time_span_kernel(DevCsr g, int* span) {
+  int lo = INT32_MAX, hi = INT32_MIN;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < g.m; i += gridDim.x * blockDim.x) {
+    lo = min(lo, __ldg(g.key + i));
+    hi = max(hi, (int32_t)__ldg(&g.pay[i].y));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(span, lo);
+    atomicMax(span + 1, hi);
+  }
+}
+
+// [earliest start, latest end] of the graph's edges (once per graph).
+static int ensure_time_span(tgxd_graph* G) {
+  if (G->span_known) return TGXD_OK;
+  DeviceBuffer tmp;
+  int* d = dalloc<int>(tmp, 2);
+  if (!d) return fail(TGXD_ERR_CUDA, "allocation (time span)");
+  const int init[2] = {INT32_MAX, INT32_MIN};
+  TGXD_CUDA(cudaMemcpyAsync(d, init, 8, cudaMemcpyHostToDevice, G->stream));
+  if (G->out.m)
+    time_span_kernel<<<grid_for(G->out.m, G->sm_count), 256, 0, G->stream>>>(G->out, d);
+  TGXD_CUDA(cudaMemcpyAsync(G->span, d, 8, cudaMemcpyDeviceToHost, G->stream));
+  TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  G->span_known = true;
+  return TGXD_OK;
+}
+
+// Queries of a batch in groups of `group`, one traversal per group, results
+// and statistics accumulated (tgxd_last_work then refers to the last group).
+static int run_groups(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts,
+                      const uint64_t* ta, const uint64_t* tb, int ordering, int mode, void* out,
+                      int width, int out_on_device, tgxd_stats* stats, uint32_t group) {
+  if (!verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "null query arrays");
+  tgxd_stats acc;
+  std::memset(&acc, 0, sizeof acc);
+  uint64_t h2d = 0, d2h = 0;
+  for (uint32_t q = 0; q < k; q += group) {
+    const uint32_t kq = std::min(group, k - q);
+    char* o = static_cast<char*>(out) + (size_t)q * G->n * width;
+    tgxd_stats one;
+    const int rc = query_impl(G, kind, kq, verts + q, ta + q, tb + q, ordering, mode, o, width,
+                              out_on_device, &one);
+    if (rc) return rc;
+    h2d += G->ws.last_h2d;
+    d2h += G->ws.last_d2h;
+    G->ws.last_h2d = h2d;
+    G->ws.last_d2h = d2h;
+    acc.rounds += one.rounds;
+    acc.candidates += one.candidates;
+    acc.expansions += one.expansions;
+    acc.edges_relaxed += one.edges_relaxed;
+    acc.index_lookups += one.index_lookups;
+    acc.kernel_ms += one.kernel_ms;
+    acc.total_ms += one.total_ms;
+  }
+  if (stats) *stats = acc;
+  return TGXD_OK;
+}
+
+static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts,
+                      const uint64_t* ta, const uint64_t* tb, int ordering, int mode, void* out,
                       int width, int out_on_device, tgxd_stats* stats) {
   if (!G) return fail(TGXD_ERR_ARGUMENT, "null graph");
   if (!out) return fail(TGXD_ERR_ARGUMENT, "null output");
   if (width != 4 && width != 8) return fail(TGXD_ERR_ARGUMENT, "width must be 4 or 8");
   const bool edge_kind = ordering == TGXD_OVERLAPS || kind == TGXD_SHORTEST_DURATION ||
                          kind == TGXD_SHORTEST_DURATION_WEIGHTED;
-  if ((kind == TGXD_FASTEST || edge_kind) && k > 1) {  // one sweep / edge traversal per source
-    if (!verts || !ta || !tb) return fail(TGXD_ERR_ARGUMENT, "null query arrays");
-    tgxd_stats acc;
-    std::memset(&acc, 0, sizeof acc);
-    uint64_t h2d = 0, d2h = 0;
-    for (uint32_t q = 0; q < k; ++q) {
-      char* o = static_cast<char*>(out) + (size_t)q * G->n * width;
-      tgxd_stats one;
-      const int rc = query_impl(G, kind, 1, verts + q, ta + q, tb + q, ordering, mode, o, width,
-                                out_on_device, &one);
-      if (rc) return rc;
-      h2d += G->ws.last_h2d;
-      d2h += G->ws.last_d2h;
-      G->ws.last_h2d = h2d;
-      G->ws.last_d2h = d2h;
-      acc.rounds += one.rounds;
-      acc.candidates += one.candidates;
-      acc.expansions += one.expansions;
-      acc.edges_relaxed += one.edges_relaxed;
-      acc.index_lookups += one.index_lookups;
-      acc.kernel_ms += one.kernel_ms;
-      acc.total_ms += one.total_ms;
+  if ((kind == TGXD_FASTEST || edge_kind) && k > 1)  // one sweep / edge traversal per source
+    return run_groups(G, kind, k, verts, ta, tb, ordering, mode, out, width, out_on_device, stats,
+                      1);
+  // AUTO batches of wide-window EA / LD queries whose labels exceed a share of
+  // L2 run in groups that fit: a batch's rounds are shared, but when its
+  // queries reach most of the graph every label probe of a Q x n batch goes
+  // to DRAM (config 5: 32 queries x 2^24 slots = 2.1 GB of labels; slot-major
+  // batch 50.9 ms, one by one 46.5). Narrow windows (config 3, 1% of the
+  // timeline) reach little and keep the shared rounds.
+  if (k > 1 && mode == TGXD_MODE_AUTO && verts && ta && tb &&
+      (kind == TGXD_EARLIEST_ARRIVAL || kind == TGXD_LATEST_DEPARTURE) &&
+      (uint64_t)k * G->n * 4 > batch_label_budget() && !getenv("TGXD_NO_SPLIT")) {
+    {
+      std::lock_guard<std::mutex> lock(G->mu);
+      TGXD_CUDA(cudaSetDevice(G->device));
+      if (const int rc = ensure_time_span(G)) return rc;
     }
-    if (stats) *stats = acc;
-    return TGXD_OK;
+    const double span = std::max(1.0, (double)G->span[1] - (double)G->span[0]);
+    double frac = 0;
+    for (uint32_t q = 0; q < k; ++q) {
+      const double lo = std::max<double>((double)ta[q], G->span[0]);
+      const double hi = std::min<double>((double)std::min<uint64_t>(tb[q], kTimeLimit63), G->span[1]);
+      frac += std::max(0.0, hi - lo) / span;
+    }
+    if (frac / k >= 0.05) {
+      const uint32_t group =
+          (uint32_t)std::max<uint64_t>(1, batch_label_budget() / ((uint64_t)G->n * 4));
+      if (group < k)
+        return run_groups(G, kind, k, verts, ta, tb, ordering, mode, out, width, out_on_device,
+                          stats, group);
+    }
   }
   std::lock_guard<std::mutex> lock(G->mu);
   TGXD_CUDA(cudaSetDevice(G->device));

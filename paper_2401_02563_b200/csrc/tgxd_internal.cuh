@@ -207,6 +207,8 @@ struct tgxd_graph {
   const long long* out_w = nullptr;
   bool out2in_ready = false;
   uint32_t max_out_deg = 0;  // fastest: sizes the device candidate lists (lazy)
+  int span[2] = {0, 0};       // earliest start, latest end (lazy; batch splitting)
+  bool span_known = false;
   bool max_out_deg_known = false;
   tgxd::DevCsr out, in;
   // selective-index cost model (costmodel.cuh), per direction, built on first use

@@ -164,3 +164,19 @@ def test_fastest_from_the_hub_source(mode):
         sel = (E[0] == hub) & (E[2] >= w.t_a) & (E[3] <= w.t_b)
         if mode == T.Mode.AUTO:
             assert st.candidates == len(np.unique(E[2][sel]))
+
+
+@pytest.mark.parametrize("budget_mb", ["1", "2", "100000"])
+def test_split_batches_match_the_oracle(monkeypatch, budget_mb):
+    """AUTO splits wide-window EA / LD batches whose labels exceed the budget
+    into groups (1 MiB: one query per group on a 2^18-vertex graph, 2 MiB:
+    pairs, huge: one batch); every grouping gives the oracle's labels."""
+    monkeypatch.setenv("TGXD_BATCH_BUDGET_MB", budget_mb)
+    wl, g, qs = setup("c5", -6)
+    o = Oracle(T.generate_edges(wl.gen), wl.gen.n_vertices)
+    sub = qs[:5] + qs[16:19]
+    for kind in ("earliest_arrival", "latest_departure"):
+        out = T.query_batch(g, kind, [q.vertex for q in sub], [q.window for q in sub])
+        for i, q in enumerate(sub):
+            assert np.array_equal(out[i], o.query(kind, q.vertex, q.window.t_a, q.window.t_b)), \
+                (budget_mb, kind, i)
