@@ -1252,11 +1252,12 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
                       int width, int out_on_device, tgxd_stats* stats);
 
 // Label bytes (4 per slot) above which a wide-window AUTO batch is split
-// (TGXD_BATCH_BUDGET_MB overrides): 256 MiB = groups of 4 on config 5, the
-// best measured grouping there (45 ms vs 47 one by one and 53 as one batch).
+// (TGXD_BATCH_BUDGET_MB overrides). Config 5's 16-query groups (device ms):
+// budget 64 MiB (one query at a time) 41.9, 128 (2) 42.9, 256 (4) 43.9,
+// 512 (8) 47.5, one batch 53.1.
 static uint64_t batch_label_budget() {
   const char* e = getenv("TGXD_BATCH_BUDGET_MB");
-  return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) << 20 : 256ull << 20;
+  return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) << 20 : 64ull << 20;
 }
 
 __global__ void time_span_kernel(DevCsr g, int* span) {
@@ -1288,6 +1289,39 @@ static int ensure_time_span(tgxd_graph* G) {
   TGXD_CUDA(cudaMemcpyAsync(G->span, d, 8, cudaMemcpyDeviceToHost, G->stream));
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
   G->span_known = true;
+  return TGXD_OK;
+}
+
+// AUTO batches of wide-window EA / LD queries whose labels exceed
+// batch_label_budget() run in groups within it: a batch's rounds are shared,
+// but when its queries reach most of the graph every label probe of a Q x n
+// batch goes to DRAM (config 5: 32 queries x 2^24 slots = 2.1 GB of labels;
+// slot-major batch 50.9 ms, one by one 46.5). Narrow windows (config 3, 1% of
+// the timeline) reach little and keep the shared rounds. *group = 0: no split.
+// (`locked`: the caller already holds G->mu)
+static int split_group(tgxd_graph* G, int kind, uint32_t k, const uint64_t* ta,
+                       const uint64_t* tb, int mode, bool locked, uint32_t* group) {
+  *group = 0;
+  if (!(k > 1 && mode == TGXD_MODE_AUTO && ta && tb &&
+        (kind == TGXD_EARLIEST_ARRIVAL || kind == TGXD_LATEST_DEPARTURE) &&
+        (uint64_t)k * G->n * 4 > batch_label_budget() && !getenv("TGXD_NO_SPLIT")))
+    return TGXD_OK;
+  if (!G->span_known) {
+    std::unique_lock<std::mutex> lock(G->mu, std::defer_lock);
+    if (!locked) lock.lock();
+    TGXD_CUDA(cudaSetDevice(G->device));
+    if (const int rc = ensure_time_span(G)) return rc;
+  }
+  const double span = std::max(1.0, (double)G->span[1] - (double)G->span[0]);
+  double frac = 0;
+  for (uint32_t q = 0; q < k; ++q) {
+    const double lo = std::max<double>((double)ta[q], G->span[0]);
+    const double hi = std::min<double>((double)std::min<uint64_t>(tb[q], kTimeLimit63), G->span[1]);
+    frac += std::max(0.0, hi - lo) / span;
+  }
+  if (frac / k < 0.05) return TGXD_OK;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, batch_label_budget() / ((uint64_t)G->n * 4));
+  if (g < k) *group = g;
   return TGXD_OK;
 }
 
@@ -1334,34 +1368,12 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   if ((kind == TGXD_FASTEST || edge_kind) && k > 1)  // one sweep / edge traversal per source
     return run_groups(G, kind, k, verts, ta, tb, ordering, mode, out, width, out_on_device, stats,
                       1);
-  // AUTO batches of wide-window EA / LD queries whose labels exceed a share of
-  // L2 run in groups that fit: a batch's rounds are shared, but when its
-  // queries reach most of the graph every label probe of a Q x n batch goes
-  // to DRAM (config 5: 32 queries x 2^24 slots = 2.1 GB of labels; slot-major
-  // batch 50.9 ms, one by one 46.5). Narrow windows (config 3, 1% of the
-  // timeline) reach little and keep the shared rounds.
-  if (k > 1 && mode == TGXD_MODE_AUTO && verts && ta && tb &&
-      (kind == TGXD_EARLIEST_ARRIVAL || kind == TGXD_LATEST_DEPARTURE) &&
-      (uint64_t)k * G->n * 4 > batch_label_budget() && !getenv("TGXD_NO_SPLIT")) {
-    {
-      std::lock_guard<std::mutex> lock(G->mu);
-      TGXD_CUDA(cudaSetDevice(G->device));
-      if (const int rc = ensure_time_span(G)) return rc;
-    }
-    const double span = std::max(1.0, (double)G->span[1] - (double)G->span[0]);
-    double frac = 0;
-    for (uint32_t q = 0; q < k; ++q) {
-      const double lo = std::max<double>((double)ta[q], G->span[0]);
-      const double hi = std::min<double>((double)std::min<uint64_t>(tb[q], kTimeLimit63), G->span[1]);
-      frac += std::max(0.0, hi - lo) / span;
-    }
-    if (frac / k >= 0.05) {
-      const uint32_t group =
-          (uint32_t)std::max<uint64_t>(1, batch_label_budget() / ((uint64_t)G->n * 4));
-      if (group < k)
-        return run_groups(G, kind, k, verts, ta, tb, ordering, mode, out, width, out_on_device,
-                          stats, group);
-    }
+  {
+    uint32_t group = 0;
+    if (const int rc = split_group(G, kind, k, ta, tb, mode, false, &group)) return rc;
+    if (group)
+      return run_groups(G, kind, k, verts, ta, tb, ordering, mode, out, width, out_on_device,
+                        stats, group);
   }
   std::lock_guard<std::mutex> lock(G->mu);
   TGXD_CUDA(cudaSetDevice(G->device));
@@ -2151,33 +2163,43 @@ static int time_impl(tgxd_graph* g, int kind, uint32_t k, const uint32_t* vertic
     return fail(TGXD_ERR_ARGUMENT, "timed fastest: one source");
   std::lock_guard<std::mutex> lock(g->mu);
   TGXD_CUDA(cudaSetDevice(g->device));
-  const uint32_t np = rotate ? k : 1;
+  uint32_t group = 0;
+  int rc = rotate ? TGXD_OK : split_group(g, kind, k, t_a, t_b, mode, true, &group);
+  if (rc) return rc;
+  // rotate: one Prepared per query, step i runs query i mod k; a split batch:
+  // one per group, every step runs all groups; else one for the whole batch
+  const uint32_t np = rotate ? k : (group ? (k + group - 1) / group : 1);
+  const uint32_t per_step = rotate ? 1 : np;
   std::vector<Prepared> Ps(np);
+  uint32_t qmax = 1;
   for (uint32_t i = 0; i < np; ++i) {
     Prepared& P = Ps[i];
-    int rc = rotate ? prepare(g, kind, 1, vertices + i, t_a + i, t_b + i, ordering, P)
-                    : prepare(g, kind, k, vertices, t_a, t_b, ordering, P);
+    const uint32_t q0 = rotate ? i : i * (group ? group : k);
+    const uint32_t kq = rotate ? 1 : std::min(group ? group : k, k - q0);
+    rc = prepare(g, kind, kq, vertices + q0, t_a + q0, t_b + q0, ordering, P);
     if (rc) return rc;
+    qmax = std::max(qmax, P.Q);
   }
-  int rc = ensure_workspace(g, Ps[0].Q, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS);
+  rc = ensure_workspace(g, qmax, kind == TGXD_FASTEST || kind == TGXD_TEMPORAL_BFS);
   if (rc) return rc;
   Workspace& w = g->ws;
-  const uint64_t slots = (uint64_t)Ps[0].Q * g->n;
+  const uint64_t slots = (uint64_t)qmax * g->n;
   if (!dalloc<int32_t>(w.timing_out, slots)) return fail(TGXD_ERR_CUDA, "allocation (output)");
   std::vector<cudaEvent_t> ev(2 * (size_t)steps);
   for (auto& e : ev) TGXD_CUDA(cudaEventCreate(&e));
   auto destroy = [&] {
     for (auto& e : ev) cudaEventDestroy(e);
   };
-  for (int i = 0; i < warmup; ++i) {
-    if ((rc = launch(g, Ps[i % np], mode, w.timing_out.p, 4, nullptr, nullptr)))
-      return destroy(), rc;
-  }
+  for (int i = 0; i < warmup; ++i)
+    for (uint32_t j = 0; j < per_step; ++j)
+      if ((rc = launch(g, Ps[(i * per_step + j) % np], mode, w.timing_out.p, 4, nullptr, nullptr)))
+        return destroy(), rc;
   TGXD_CUDA(cudaEventRecord(w.ev[2], g->stream));
-  for (int i = 0; i < steps; ++i) {
-    if ((rc = launch(g, Ps[i % np], mode, w.timing_out.p, 4, ev[2 * i], ev[2 * i + 1])))
-      return destroy(), rc;
-  }
+  for (int i = 0; i < steps; ++i)
+    for (uint32_t j = 0; j < per_step; ++j)
+      if ((rc = launch(g, Ps[(i * per_step + j) % np], mode, w.timing_out.p, 4,
+                       j == 0 ? ev[2 * i] : nullptr, j + 1 == per_step ? ev[2 * i + 1] : nullptr)))
+        return destroy(), rc;
   TGXD_CUDA(cudaEventRecord(w.ev[3], g->stream));
   TGXD_CUDA(cudaStreamSynchronize(g->stream));
   float tot = 0, ksum = 0;

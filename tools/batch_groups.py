@@ -17,16 +17,9 @@ if args.child:
     out = {"config": args.config, "budget_mb": os.environ.get("TGXD_BATCH_BUDGET_MB")}
     for kind in sorted({q.kind for q in qs}):
         sub = [q for q in qs if q.kind == kind]
-        st = T.EdgeMapStats()
-        import time
-        T.query_batch(g, kind, [q.vertex for q in sub], [q.window for q in sub], width=4)
-        ts = []
-        for _ in range(3):
-            st = T.EdgeMapStats()
-            T.query_batch(g, kind, [q.vertex for q in sub], [q.window for q in sub], width=4,
-                          stats=st)
-            ts.append(st.total_ms)
-        out[kind + "_ms"] = round(min(ts), 3)
+        tot, ker = T.time_queries(g, kind, [q.vertex for q in sub], [q.window for q in sub],
+                                  warmup=1, steps=3)
+        out[kind + "_ms"] = round(tot / 3, 3)
     print(json.dumps(out), flush=True)
 else:
     for b in args.budgets.split(","):
