@@ -79,25 +79,32 @@ if args.extras:
     sys.exit(0)
 
 
-def ref_time(wl, edges, n, groups):
-    """Median seconds per reference call for each (kind, vertex, window)."""
-    from oracle.pyoracle import Reference
+def ref_time(wl, edges, n, groups, g=None):
+    """Median seconds per reference call for each (kind, vertex, window); with
+    a device graph `g`, also whether the device's labels for the same query
+    are identical, and both FNV-1a digests (digest.hpp:42-52)."""
+    from oracle.pyoracle import Reference, digest
     if not Reference.available():
-        return None, None
+        return None, None, None
     Reference.set_workers(os.cpu_count() or 1)
     t0 = time.perf_counter()
     ref = Reference(edges, n, True, wl.index_cutoff)
     build = time.perf_counter() - t0
-    out = []
+    out, checks = [], []
     for kind, v, w, steps in groups:
         ts = []
         for _ in range(steps):
             t = time.perf_counter()
-            ref.query(kind, v, w.t_a, w.t_b)
+            want = ref.query(kind, v, w.t_a, w.t_b)
             ts.append(time.perf_counter() - t)
         out.append(float(np.median(ts)))
+        if g is not None:
+            got = FN[kind](g, v, w).values
+            checks.append({"vertex": v, "window": [w.t_a, w.t_b],
+                           "identical": bool(np.array_equal(got, want)),
+                           "ref_digest": digest(want), "gpu_digest": digest(got)})
     ref.close()
-    return out, build
+    return out, build, checks
 
 
 for name in args.configs.split(","):
@@ -172,8 +179,11 @@ for name in args.configs.split(","):
             steps = 1 if kind == "fastest" else args.ref_steps
             # bounded sample: at most 8 queries of a group on the CPU
             samp = sub[:8]
-            times, rbuild = ref_time(wl, edges, n, [(kind, q.vertex, q.window, steps) for q in samp])
+            times, rbuild, checks = ref_time(wl, edges, n,
+                                             [(kind, q.vertex, q.window, steps) for q in samp], g)
             if times is not None:
+                line["parity"] = checks
+                line["identical"] = all(c["identical"] for c in checks)
                 e_s = sum(per_q[i][0] for i in range(len(samp)))
                 line["ref"] = {"kind": "reference", "cores": os.cpu_count(), "queries": len(samp),
                                "s_per_query": float(np.mean(times)),
