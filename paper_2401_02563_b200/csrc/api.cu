@@ -950,26 +950,33 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   const int pdiv = pf ? atoi(pf) : (fast ? 4 : 2);
   a.pull_f = pdiv <= 0 ? ~0ull : std::max<uint64_t>(1024, slots / pdiv);
   if (const char* pfx = getenv("TGXD_PULL_F")) a.pull_f = strtoull(pfx, nullptr, 10);  // tests
-  // AUTO: a frontier past its peak and below 1/16 of the slots is finished by
-  // the async engine (TGXD_HANDOFF_F overrides the size; 0 turns it off)
-  // (the cluster tail engine takes smaller frontiers: its 16 SMs are fast
-  // per round — 5-7 us for a few hundred slots against ~20 us on the grid —
-  // but a ninth of the GPU's throughput; config 2's rotation: handoff at 16K
-  // 1.096 ms, 32K 1.101, 64K 1.123, the async engine at 1/16 of the slots
-  // 1.106; config 5 query 2.81 vs 3.03 ms)
+  // AUTO tail handoff (traverse.cuh): a frontier past its peak and at most
+  // 16K slots goes to the cluster tail engine — its 16 SMs are fast per round
+  // (5-7 us for a few hundred slots against ~20 us on the grid) but a ninth
+  // of the GPU's throughput (config 2's rotation: handoff at 16K 1.096 ms,
+  // 32K 1.101, 64K 1.123); a frontier of at most 1/16 of the slots that grows
+  // by less than 8x per round goes to the async engine on every SM (config 1:
+  // 27 such rounds, 0.45 ms there against 0.76 ms on the cluster engine).
+  // Without a cluster, the async engine takes both (the round-1 rule).
+  // TGXD_HANDOFF_F / TGXD_ASYNC_F override the sizes (0 turns one off).
   a.handoff_f = 0;
+  a.async_f = 0;
+  a.async_grow_only = 0;
   const bool cluster_tail = G->tail_cluster > 0;
   if (mode == TGXD_MODE_AUTO && !fast) {
     const char* hf = getenv("TGXD_HANDOFF_F");
-    const uint64_t want = hf             ? strtoull(hf, nullptr, 10)
-                          : cluster_tail ? std::min<uint64_t>(16384, std::max<uint64_t>(4096, slots / 16))
-                                         : std::max<uint64_t>(4096, slots / 16);
-    if (want && (cluster_tail ? ensure_tail(G, P.Q) : ensure_async(G, P.Q, false)) == TGXD_OK)
-      a.handoff_f = want;
+    const char* af = getenv("TGXD_ASYNC_F");
+    const uint64_t sixteenth = std::max<uint64_t>(4096, slots / 16);
+    const uint64_t want_c = !cluster_tail ? 0
+                            : hf          ? strtoull(hf, nullptr, 10)
+                                          : std::min<uint64_t>(16384, sixteenth);
+    const uint64_t want_a = af ? strtoull(af, nullptr, 10) : sixteenth;
+    if (want_c && ensure_tail(G, P.Q) == TGXD_OK) a.handoff_f = want_c;
+    if (want_a && ensure_async(G, P.Q, false) == TGXD_OK) a.async_f = want_a;
+    a.async_grow_only = a.handoff_f != 0;
   }
-  w.last_handoff = a.handoff_f != 0;
-  w.last_tail = w.last_handoff && cluster_tail;
-  if (w.last_tail) tail_reset_kernel<<<1, 1, 0, s>>>(w.tctl.as<TailCtl>());
+  w.last_handoff = a.handoff_f != 0 || a.async_f != 0;
+  if (a.handoff_f) tail_reset_kernel<<<1, 1, 0, s>>>(w.tctl.as<TailCtl>());
   {
     const char* hg = getenv("TGXD_HANDOFF_GROWTH");
     a.handoff_growth = hg ? (unsigned)std::max(1, atoi(hg)) : 8u;
@@ -996,14 +1003,14 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   {
     void* args[] = {&a};
     const bool early = w.early_req && !fast && !bfs;
-    if (early && a.handoff_f) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
+    if (early && w.last_handoff) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)traverse_kernel, dim3(G->coop_blocks),
                                           dim3(kThreads), args, 0, s));
     if (early) {  // the caller's copy of the labels may start now
       TGXD_CUDA(cudaEventRecord(G->early_ev, s));
       w.early_done = true;
     }
-    if (a.handoff_f && cluster_tail) {  // exits at once unless the round kernel handed off
+    if (a.handoff_f) {  // exits at once unless the round kernel handed off to it
       TailArgs t;
       t.g = g;
       t.qp = a.qp;
@@ -1038,11 +1045,8 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       cfg.attrs = &at;
       cfg.numAttrs = 1;
       TGXD_CUDA(cudaLaunchKernelEx(&cfg, tail_kernel, t));
-      if (early)
-        tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
-            w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X,
-            G->patch_dev);
-    } else if (a.handoff_f) {  // the continuation exits at once unless the round kernel handed off
+    }
+    if (a.async_f) {  // the continuation exits at once unless the round kernel handed off to it
       AsyncArgs h;
       h.g = g;
       h.qp = a.qp;
@@ -1074,11 +1078,10 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       const int tail_blocks = std::min(G->coop_blocks_async, G->tail_per_sm * G->sm_count);
       TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(tail_blocks),
                                             dim3(kThreads), hargs, 0, s));
-      if (early)
-        tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
-            w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X,
-            G->patch_dev);
     }
+    if (early && w.last_handoff)  // the labels a tail engine lowered after the early copy
+      tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
+          w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X, G->patch_dev);
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   if (out_dev && !w.early_done) convert_for(G, P, out_dev, width);
@@ -1160,7 +1163,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   AsyncCtl ac;
   std::memset(&ac, 0, sizeof ac);
   uint32_t tail_rounds = 0;
-  if (G->ws.last_tail && c.handoff_n) {  // the cluster tail engine finished the query
+  if (G->ws.last_handoff && c.handoff_n && c.handoff_kind == 1) {  // the cluster engine finished it
     TailCtl tc;
     TGXD_CUDA(cudaMemcpyAsync(&tc, G->ws.tctl.p, sizeof tc, cudaMemcpyDeviceToHost, G->stream));
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
@@ -1173,7 +1176,7 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
     ac.edges = tc.edges;
     ac.visits = tc.visits;
     ac.index_lookups = tc.index_lookups;
-  } else if (G->ws.last_handoff && c.handoff_n) {  // the async engine finished the tail
+  } else if (G->ws.last_handoff && c.handoff_n) {  // the async engine finished it
     TGXD_CUDA(cudaMemcpyAsync(&ac, G->ws.actl.p, sizeof ac, cudaMemcpyDeviceToHost, G->stream));
     TGXD_CUDA(cudaStreamSynchronize(G->stream));
     if (ac.error) {

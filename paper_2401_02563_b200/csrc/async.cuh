@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
     // Continuation of a round-kernel query (traverse.cuh, tail handoff):
     // labels become label words, the handed-over queue becomes batch units.
     const unsigned long long nh = __ldcg(&a.hctl->handoff_n);
-    if (nh == 0) return;  // the round kernel finished the query itself
+    // the round kernel finished the query itself, or handed it to the
+    // cluster engine
+    if (nh == 0 || __ldcg(&a.hctl->handoff_kind) != 2) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.c->t_entry = gtimer();
     const uint32_t* fin = __ldcg(&a.hctl->handoff_flip) ? a.hfb : a.hfa;
     const unsigned long long t0 = __ldcg(&a.c->tail.v);

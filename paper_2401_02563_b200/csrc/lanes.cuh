@@ -302,6 +302,7 @@ __global__ void lanes_seed_kernel(const QueryParam* qp, uint32_t Q, int32_t* XM,
   ctl->pull_scanned = 0;
   ctl->pchunks = 0;
   ctl->handoff_n = 0;
+  ctl->handoff_kind = 0;
   ctl->error = 0;
   ctl->bar_count = 0;
   ctl->bar_gen = 0;

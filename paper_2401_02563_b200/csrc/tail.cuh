@@ -171,7 +171,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
   __shared__ unsigned long long s_cnt[6];
   cgt::cluster_group cluster = cgt::this_cluster();
   const unsigned long long nh = __ldcg(&a.hctl->handoff_n);
-  if (nh == 0) return;  // the round kernel finished the query itself (uniform)
+  // the round kernel finished the query itself, or handed it to the async
+  // engine (uniform)
+  if (nh == 0 || __ldcg(&a.hctl->handoff_kind) != 1) return;
   const uint32_t rank = cluster.block_rank();
   const uint32_t ncta = cluster.num_blocks();
   const bool lead = rank == 0 && threadIdx.x == 0;

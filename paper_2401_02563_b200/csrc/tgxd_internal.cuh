@@ -90,8 +90,7 @@ struct Workspace {
   DeviceBuffer ereached, edep, eval, estamp, efa, efb, ectl, ey, esm;
   bool last_edge = false;
   bool last_async = false;
-  bool last_handoff = false;  // round kernel may have handed its tail to the async engine
-  bool last_tail = false;     // ... to the cluster tail engine (tail.cuh)
+  bool last_handoff = false;  // round kernel may have handed its tail to a tail engine
   DeviceBuffer tstamp, tctl;  // cluster tail engine: per-slot stamps, control block
   uint64_t t_slots = 0;
   // early host copy (api.cu query_impl): the labels leave for the host while
@@ -130,7 +129,8 @@ struct Control {
   unsigned int candidates;
   unsigned int error;               // watchdog tripped
   unsigned int handoff_flip;        // handoff: the queue holding the frontier (fb if 1)
-  unsigned long long handoff_n;     // handoff: frontier size left to the async engine
+  unsigned long long handoff_n;     // handoff: frontier size left to a tail engine
+  unsigned long long handoff_kind;  // handoff: 1 the cluster tail engine, 2 the async engine
   unsigned long long t_end;         // globaltimer when the round kernel finished
   unsigned long long state[12];     // CTA-local rounds hand their state over here
   // grid barrier of the round kernel (traverse.cuh GridBarrier), own lines

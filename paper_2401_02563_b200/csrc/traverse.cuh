@@ -96,8 +96,12 @@ struct TravArgs {
   unsigned long long dense_f;  // AUTO: frontier above this expands densely
   unsigned long long push_w;   // AUTO: rounds relaxing more edges do not push
   unsigned long long pull_f;   // AUTO: a frontier at least this big is pulled
-  unsigned long long handoff_f; // AUTO: a shrinking frontier this small goes to the async engine
-  unsigned int handoff_growth;  // ... or one growing by less than this factor per round
+  unsigned long long handoff_f;  // AUTO: a shrinking frontier this small goes to the cluster tail engine
+  unsigned long long async_f;    // AUTO: a frontier this small goes to the async engine when it
+                                 // grows by less than handoff_growth per round (or shrinks,
+                                 // with async_grow_only == 0)
+  unsigned int handoff_growth;
+  int async_grow_only;
   // fastest sweep (Q == 1)
   int fastest;
   const uint32_t* n_cand;  // device: candidate count (candidates.cuh), ascending lists
@@ -268,7 +272,14 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
     const int32_t vhi = a.Q == 1 ? rx.vhi0 : __ldg(&a.qp[q[u]].vhi);
     // window containment: end <= t_b (types.hpp:55-57)
     if (!(act[u] && v[u] <= vhi)) v[u] = kInf;
+#ifdef TGXD_L1_PROBE
+    // L1-cached probe: a stale (higher) label only costs an extra atomicMin,
+    // which returns the true old value; a stale label is never lower
+    if (v[u] != kInf) asm volatile("ld.global.ca.b32 %0, [%1];" : "=r"(cur[u]) : "l"(a.X + idx[u]));
+    else cur[u] = kInf;
+#else
     cur[u] = v[u] != kInf ? ld_state(a.X + idx[u], rx.pol_keep) : kInf;
+#endif
   }
   // all atomics of the batch are in flight before any result is used
   int32_t old[kUnroll], ex[kUnroll];
@@ -1343,14 +1354,26 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       // ~10 us latency floor per round.
       // (past its peak, or growing by less than handoff_growth per round: a
       // frontier that stays small for many rounds is latency-bound in rounds)
-      if (!xcnt && !st.dense && !a.fastest && F <= a.handoff_f && st.rounds >= 2 &&
-          F < (unsigned long long)st.last_f * a.handoff_growth) {
-        if (tr) {
-          ctl->handoff_n = F;
-          ctl->handoff_flip = st.flip;
+      // Two engines: the cluster engine (tail.cuh) for a small frontier past
+      // its peak; the barrier-free engine on every SM (async.cuh) for a
+      // frontier that grows slowly — a long thin traversal (config 1: 27
+      // rounds of <= 103K slots) needs the whole GPU, not one cluster.
+      if (!xcnt && !st.dense && !a.fastest && st.rounds >= 2) {
+        const unsigned long long lf = st.last_f;
+        unsigned long long kind = 0;
+        if (F <= a.handoff_f && F < lf)
+          kind = 1;
+        else if (F <= a.async_f && F < lf * a.handoff_growth && (!a.async_grow_only || F >= lf))
+          kind = 2;
+        if (kind) {
+          if (tr) {
+            ctl->handoff_n = F;
+            ctl->handoff_kind = kind;
+            ctl->handoff_flip = st.flip;
+          }
+          handed = true;
+          break;
         }
-        handed = true;
-        break;
       }
       if (!xcnt) st.last_f = (uint32_t)min(F, 0xffffffffull);
       const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
@@ -1591,6 +1614,7 @@ __global__ void reset_seed_kernel(int32_t* X, int2* EP, size_t nl, uint32_t root
     ctl->pull_scanned = 0;
     ctl->pchunks = 0;
     ctl->handoff_n = 0;
+    ctl->handoff_kind = 0;
     ctl->error = 0;
     ctl->bar_count = 0;
     ctl->bar_gen = 0;
@@ -1612,6 +1636,7 @@ __global__ void seed_kernel(const QueryParam* qp, uint32_t Q, uint32_t n, int32_
     ctl->pull_scanned = 0;
     ctl->pchunks = 0;
     ctl->handoff_n = 0;
+    ctl->handoff_kind = 0;
     ctl->error = 0;
     ctl->bar_count = 0;
     ctl->bar_gen = 0;

@@ -34,7 +34,9 @@ for q in qs:
                 rows.append([kind, int(row[3]), round((row[1] - row[0]) / 1e3, 1),
                              round((row[2] - row[1]) / 1e3, 1) if row[2] else 0, int(row[4])])
             else:
-                rows.append([kind, int(row[3]), round((row[2] - row[0]) / 1e3, 1)])
+                # expand (or P1) and relax (or P2) separately, chunks, smalls
+                rows.append([kind, int(row[3]), round((row[1] - row[0]) / 1e3, 1),
+                             round((row[2] - row[1]) / 1e3, 1), int(row[4]), int(row[5])])
     tot, ker = T.time_queries(g, q.kind, [q.vertex], [q.window], warmup=2, steps=args.steps)
     ms = tot / args.steps
     tot_e += e
