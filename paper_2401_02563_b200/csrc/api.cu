@@ -816,6 +816,46 @@ static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void*
   return TGXD_OK;
 }
 
+// Query slots of a fastest query's split sweep (traverse.cuh
+// split_seed_step): sized from the source's out-degree, which bounds its
+// candidate count, so no read back is needed; the kernel decides from the
+// candidates how many slots work (split_width). TGXD_FASTEST_SPLIT forces a
+// width (1 = one sweep).
+static int fastest_split(tgxd_graph* G, uint32_t src, uint32_t* split, int* forced) {
+  const char* e = getenv("TGXD_FASTEST_SPLIT");  // read per query (tests vary it)
+  *forced = e != nullptr;
+  if (e) {
+    *split = (uint32_t)std::max(1, atoi(e));
+    return TGXD_OK;
+  }
+  if (G->h_out_off.size() != (size_t)G->n + 1) {  // once per handle
+    G->h_out_off.resize((size_t)G->n + 1);
+    TGXD_CUDA(cudaMemcpyAsync(G->h_out_off.data(), G->out.off, ((size_t)G->n + 1) * 4,
+                              cudaMemcpyDeviceToHost, G->stream));
+    TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  }
+  *split = split_width(G->h_out_off[src + 1] - G->h_out_off[src], G->n, 64);
+  return TGXD_OK;
+}
+
+// r[v] = min over the sub-sweeps of their r (and the arrival labels, for the
+// work count: the minimum over the subsets is the sweep over all candidates).
+__global__ void split_reduce_kernel(int32_t* R, int32_t* X, uint32_t n, uint32_t k) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t r = R[v], x = X[v];
+    for (uint32_t q = 1; q < k; ++q) {
+      r = min(r, R[(size_t)q * n + v]);
+      x = min(x, X[(size_t)q * n + v]);
+    }
+    R[v] = r;
+    X[v] = x;
+  }
+}
+
+static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, uint32_t split,
+                       int forced, int mode, void* out_dev, int width, cudaEvent_t ev_k0,
+                       cudaEvent_t ev_k1);
+
 // Enqueues one traversal (init, seeds, the persistent kernel, widening into
 // out_dev). ev_k0/ev_k1 bracket the traversal kernel when non-null.
 static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int width,
@@ -824,6 +864,24 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
     G->ws.xinv = false;
     return launch_edges(G, P, out_dev, width, ev_k0, ev_k1);
   }
+  uint32_t split = 1;
+  int forced = 0;
+  if (P.kind == TGXD_FASTEST && P.Q == 1 && mode != TGXD_MODE_ASYNC)
+    if (const int rc = fastest_split(G, P.seeds[0].root, &split, &forced)) return rc;
+  if (split <= 1) return launch_body(G, P, P, 1, 0, mode, out_dev, width, ev_k0, ev_k1);
+  Prepared Pk = P;
+  Pk.Q = split;
+  Pk.qp.assign(split, P.qp[0]);
+  Pk.seeds.assign(split, P.seeds[0]);
+  if (const int rc = ensure_workspace(G, split, true)) return rc;
+  if (!dalloc<int32_t>(G->ws.dep, split))
+    return fail(TGXD_ERR_CUDA, "device allocation failed (split sweep)");
+  return launch_body(G, Pk, P, split, forced, mode, out_dev, width, ev_k0, ev_k1);
+}
+
+static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, uint32_t split,
+                       int forced, int mode, void* out_dev, int width, cudaEvent_t ev_k0,
+                       cudaEvent_t ev_k1) {
   Workspace& w = G->ws;
   w.last_edge = false;
   cudaStream_t s = G->stream;
@@ -983,6 +1041,9 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
   }
   a.rg = P.kind == TGXD_LATEST_DEPARTURE ? G->out : G->in;
   a.fastest = fast ? 1 : 0;
+  a.split = split;
+  a.split_forced = forced;
+  a.dep = split > 1 ? w.dep.as<int32_t>() : nullptr;
   a.n_cand = w.cand_n.as<uint32_t>();
   a.cand_lo = w.cand_lo.as<uint32_t>();
   a.cand_cnt = w.cand_cnt.as<uint32_t>();
@@ -1083,13 +1144,16 @@ static int launch(tgxd_graph* G, const Prepared& P, int mode, void* out_dev, int
       tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
           w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X, G->patch_dev);
   }
+  if (split > 1)
+    split_reduce_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
+        w.R.as<int32_t>(), w.X.as<int32_t>(), G->n, split);
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
-  if (out_dev && !w.early_done) convert_for(G, P, out_dev, width);
+  if (out_dev && !w.early_done) convert_for(G, Pout, out_dev, width);
   TGXD_CUDA(cudaGetLastError());
-  w.last_kind = P.kind;
-  w.last_q = P.Q;
-  w.last_strict = P.strict;
-  w.last_params = P.qp;
+  w.last_kind = Pout.kind;
+  w.last_q = Pout.Q;
+  w.last_strict = Pout.strict;
+  w.last_params = Pout.qp;
   if (fast) {  // count the arrival fixpoint with the source as root (all seeds)
     w.last_params[0].root = P.seeds[0].root;
   }

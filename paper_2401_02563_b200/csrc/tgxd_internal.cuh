@@ -83,6 +83,7 @@ struct Workspace {
   // lane-per-query batches (lanes.cuh): vertex-major labels, ranges, dirty masks
   DeviceBuffer lxm, leb, ldirty;
   DeviceBuffer cand_lo, cand_cnt, cand_key, cand_n, timing_out;
+  DeviceBuffer dep;    // split fastest sweeps: each sub-sweep's current departure
   // asynchronous engine: queued flags, vertex / chunk rings, control block
   DeviceBuffer axq, aunits, actl;
   uint64_t a_slots = 0, a_units = 0;
@@ -207,6 +208,7 @@ struct tgxd_graph {
   const long long* out_w = nullptr;
   bool out2in_ready = false;
   uint32_t max_out_deg = 0;  // fastest: sizes the device candidate lists (lazy)
+  std::vector<uint32_t> h_out_off;  // fastest: host copy of the Out offsets (lazy; split width)
   int span[2] = {0, 0};       // earliest start, latest end (lazy; batch splitting)
   bool span_known = false;
   bool max_out_deg_known = false;

@@ -102,8 +102,13 @@ struct TravArgs {
                                  // with async_grow_only == 0)
   unsigned int handoff_growth;
   int async_grow_only;
-  // fastest sweep (Q == 1)
+  // fastest sweep: one query (split == 1), or `split` sub-sweeps over
+  // interleaved candidate subsets, one query slot each (Q == split; see
+  // split_seed_step)
   int fastest;
+  uint32_t split;
+  int split_forced;        // split is the width (tests), not a cap for split_width
+  int32_t* dep;            // split > 1: departure of each sub-sweep's current candidate
   const uint32_t* n_cand;  // device: candidate count (candidates.cuh), ascending lists
   const uint32_t* cand_lo;
   const uint32_t* cand_cnt;
@@ -246,6 +251,15 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
                                             const bool (&act)[kUnroll], RelaxCtx& rx,
                                             PushBuf& pb);
 
+// Split fastest sweeps (split_seed_step) give every query slot its own
+// departure, so r is not updated per improvement there (a per-edge lookup of
+// the slot's departure measured 3 % on config 4's one-sweep fastest) but per
+// expansion, from the label the slot is expanded with (expand_warp, P1):
+// every improvement is followed by an expansion of the improved slot within
+// the step, the last one with the step's final label, and r needs only the
+// minimum of label - departure (path_algorithms.cpp:519-523).
+constexpr int32_t kSplitDepart = INT32_MIN;
+
 __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&e)[kUnroll],
                                             const uint32_t (&q)[kUnroll],
                                             const bool (&act)[kUnroll], RelaxCtx& rx,
@@ -301,7 +315,7 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
       // (compare_and_swap(r[d], inf, round), path_algorithms.cpp:395-397)
       if (a.hops) {
         if (old[u] == kInf) a.R[idx[u]] = rx.hop;
-      } else if (a.R) {
+      } else if (a.R && rx.depart != kSplitDepart) {
         atomicMin(a.R + idx[u], v[u] - rx.depart);
       }
       if (rx.push) p[u] = bound_of(old[u], a.strict) == ex[u];
@@ -481,6 +495,10 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
     int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
     if (lb < qp.klo) lb = qp.klo;
     const int32_t old = ep.x;
+    if (a.split > 1 && lb < old) {  // split fastest sweep: r from the expanded label
+      const int32_t r = x - __ldcg(a.dep + q);
+      if (r < __ldcg(a.R + item)) atomicMin(a.R + item, r);
+    }
     if (lb < old) {
       const int32_t hik = min(old, qp.vhi + 1);  // keys above vhi cannot fit the window
       uint32_t pos = kNoPos;
@@ -962,7 +980,7 @@ __device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs
   const bool improved = best != kInf;
   if (improved) {
     a.X[i] = best;
-    if (a.R) atomicMin(a.R + i, best - rx.depart);
+    if (a.R && rx.depart != kSplitDepart) atomicMin(a.R + i, best - rx.depart);
   }
   const uint32_t bal = __ballot_sync(0xffffffffu, improved);
   if (bal) {
@@ -1020,6 +1038,10 @@ __device__ TGXD_PHASE void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned
           int32_t lb = (i - q * a.n == qp.root) ? qp.klo : bound_of(x[u], a.strict);
           if (lb < qp.klo) lb = qp.klo;
           a.EP[i] = make_int2(lb, (int32_t)kNoPos);
+          if (a.split > 1) {  // split fastest sweep: r from the label pulled from
+            const int32_t r = x[u] - __ldcg(a.dep + q);
+            if (r < __ldcg(a.R + i)) atomicMin(a.R + i, r);
+          }
         }
       }
       slot_list_push4(b.obuf, b.no, open, make_uint4(i, (uint32_t)lim, sg[u], tg[u]));
@@ -1069,7 +1091,7 @@ __device__ TGXD_PHASE void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned
     if (lane == 0 && m != kInf && m < ld_state(a.X + slot, rx.pol_keep)) {
       const int32_t old = atomicMin(a.X + slot, m);
       if (m < old) {
-        if (a.R) atomicMin(a.R + slot, m - rx.depart);
+        if (a.R && rx.depart != kSplitDepart) atomicMin(a.R + slot, m - rx.depart);
         first = bound_of(old, a.strict) == __ldcg(&a.EP[slot].x);
       }
     }
@@ -1278,6 +1300,75 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
   }
 }
 
+// Sub-sweeps a fastest query's n_cand candidates are split over. A split
+// sweep costs ~ K full traversals (every sub-sweep starts from scratch) plus
+// n_cand / K steps of shared rounds, so K ~ sqrt(c n_cand / n): config 4's
+// graph (scale 23) 241K candidates 4.0 s at 64 (5.4 at 32, 4.7 at 128), 24K
+// 1.25 s at 20 (1.82 at 64); scale 20, 6.9K candidates 0.19 s at 27, 0.36 at
+// 10 — c ~ 1.2e5. One sweep below K = 2 (config 4's own source: 3
+// candidates). At most `cap`.
+__host__ __device__ __forceinline__ uint32_t split_width(uint32_t n_cand, uint32_t n, uint32_t cap) {
+  const unsigned long long t = 120000ull * n_cand;  // K^2 n <= t
+  uint32_t k = 1;
+  while (k < cap && (unsigned long long)(k + 1) * (k + 1) * n <= t) ++k;
+  return k;
+}
+
+// One step of a split fastest sweep (split > 1). The closed form
+// r[v] = min over candidates d of (A_d[v] - d), A_d the arrivals of the
+// paths whose first edge leaves the source at d (a path has exactly one
+// first edge, so arrivals from a set of departures are the pointwise minimum
+// of the single-departure arrivals), lets the candidates be split into
+// `split` subsets, each swept in decreasing order with incremental labels
+// exactly as path_algorithms.cpp:460-524 sweeps all of them; the sub-sweeps'
+// r are then reduced by a minimum (api.cu split_reduce_kernel). Subset q
+// takes candidates q, q + split, q + 2 split, ... of the descending list, so
+// every step advances all sub-sweeps by one candidate and their rounds are
+// shared: ~n_cand / split steps instead of n_cand.
+//
+// The step emits each sub-sweep's seed group (its candidate's first edges,
+// relaxed without an admissibility check, :476-486) as chunks of query slot
+// q, records the candidate's departure in dep[q] and relaxes the chunks with
+// the push rule; st is left as after a round that pushed.
+__device__ TGXD_PHASE void split_seed_step(const TravArgs& a, TState& st, uint32_t step,
+                                           uint32_t n_cand, uint32_t keff, GridBarrier& grid,
+                                           int32_t vhi0, uint64_t pol_stream, uint64_t pol_keep,
+                                           uint32_t* wbuf) {
+  Control* ctl = a.ctl;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nthr = gridDim.x * blockDim.x;
+  for (uint32_t q = tid; q < keff; q += nthr) {
+    const uint32_t j = step * keff + q;  // position in the descending candidate order
+    if (j >= n_cand) continue;
+    const uint32_t ci = n_cand - 1 - j;     // the lists are ascending
+    a.dep[q] = a.cand_key[ci];
+    const uint32_t lo = a.cand_lo[ci], cnt = a.cand_cnt[ci];
+    const uint32_t nch = (cnt + kChunk - 1) / kChunk;
+    const unsigned long long base = atomicAdd(&ctl->chunks, (unsigned long long)nch) - st.c_cur;
+    for (uint32_t k = 0; k < nch; ++k)
+      if (TGXD_IN_CAP(base + k, 1))
+        a.chunks[base + k] = make_uint2(lo + k * kChunk, (q << kChunkLenBits) | min(kChunk, cnt - k * kChunk));
+  }
+  grid.sync();
+  const Counters c0 = read_counters(ctl);
+  const unsigned long long p_now = st.p_known;
+  uint32_t* fout = st.flip ? a.fa : a.fb;
+  RelaxCtx rx{vhi0, kSplitDepart, true, p_now, fout, pol_stream, pol_keep, 0,
+              (int32_t)st.rounds + 1};
+  phase_b(a, c0.chunks - st.c_cur, 0, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
+  grid.sync();
+  const Counters c1 = read_counters(ctl);
+  st.p_known = c1.pushes;
+  st.i_known = c1.improved;
+  st.c_cur = c0.chunks;
+  st.e_cur = c0.edges;
+  st.prev_p = p_now;
+  st.flip ^= 1u;
+  ++st.rounds;
+  st.dense = a.mode == TGXD_MODE_AUTO && st.p_known - p_now > a.dense_f;
+  if (st.dense) st.prev_i = st.i_known - (st.p_known - p_now);
+}
+
 #ifdef TGXD_TMA_RELAX
 __shared__ __align__(128) uint2 s_tma_buf[kWarps][2 * kTmaEntries];
 __shared__ __align__(8) unsigned long long s_tma_bar[kWarps][2];
@@ -1324,14 +1415,33 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   st.last_f = 0;
   bool handed = false;
   const uint32_t n_cand = a.fastest ? __ldcg(a.n_cand) : 0u;
+  // split sweeps take `split` candidates per step, one per query slot
+  // (the host sized `split` query slots from the source's degree; the
+  // candidates decide how many of them work: slots beyond keff stay idle)
+  const uint32_t keff = a.split <= 1 ? 1u
+                        : a.split_forced ? min(a.split, max(n_cand, 1u))
+                                         : split_width(n_cand, a.n, a.split);
+  const uint32_t n_steps = (n_cand + keff - 1) / keff;
   for (uint32_t cand = 0;; ++cand) {
     int32_t depart = 0;
     uint32_t xlo = 0, xcnt = 0;
     if (a.fastest) {
-      if (cand >= n_cand) break;
+      if (cand >= n_steps) break;
       // the previous candidate's last post-barrier reads end before this
       // candidate's seeds move the counters
       if (cand) grid.sync();
+      if (keff > 1) {
+        depart = kSplitDepart;  // per slot, dep[q]
+        if (tr) trace_round(a, st.rounds, 0, gtimer());
+        split_seed_step(a, st, cand, n_cand, keff, grid, vhi0, pol_stream, pol_keep, wbuf);
+        if (tr) {
+          trace_round(a, st.rounds - 1, 1, gtimer());
+          trace_round(a, st.rounds - 1, 2, gtimer());
+          trace_round(a, st.rounds - 1, 6, st.p_known - st.prev_p);
+          trace_round(a, st.rounds - 1, 7, 5);
+        }
+        // the rounds below propagate every sub-sweep's delta
+      } else {
       // Seed round (path_algorithms.cpp:476-486): the candidate's first
       // edges, relaxed without an admissibility check.
       // (descending: the lists are ascending)
@@ -1339,6 +1449,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       depart = a.cand_key[ci];
       xlo = a.cand_lo[ci];
       xcnt = a.cand_cnt[ci];
+      }
     }
     for (;;) {
       if (st.rounds > a.round_limit) {  // identical in every block: all stop together
