@@ -187,11 +187,12 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     DeviceBuffer& b_fence = dir == 0 ? G->out_fence : G->in_fence;
     DeviceBuffer& b_kmax = dir == 0 ? G->out_kmax : G->in_kmax;
     int32_t* kmax = dalloc<int32_t>(b_kmax, (size_t)n + 1);
+    uint2* okm = dalloc<uint2>(dir == 0 ? G->out_okm : G->in_okm, (size_t)n + 1);
     uint32_t* off = dalloc<uint32_t>(b_off, (size_t)n + 1);
     int32_t* key = dalloc<int32_t>(b_key, m);
     uint2* pay = dalloc<uint2>(b_pay, m);
     int32_t* fence = dalloc<int32_t>(b_fence, nf);
-    if (!off || !key || !pay || !fence || !kmax)
+    if (!off || !key || !pay || !fence || !kmax || !okm)
       return fail(TGXD_ERR_CUDA, "device allocation failed (T-CSR arrays)");
     if (m) {
       make_sort_keys<<<gb, 256, 0, s>>>(owner, kk, dir, m, ka, ia);
@@ -207,12 +208,14 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     TGXD_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, sb, dc, off, (int64_t)n + 1, s));
     if (n) count_indexed<<<grid_for(n, G->sm_count), 256, 0, s>>>(off, n, G->index_cutoff, dctr + dir);
     if (n) segment_kmax<<<grid_for(n, G->sm_count), 256, 0, s>>>(off, key, n, kmax);
+    make_okm<<<grid_for((size_t)n + 1, G->sm_count), 256, 0, s>>>(off, kmax, n, okm);
     DevCsr& c = dir == 0 ? G->out : G->in;
     c.off = off;
     c.key = key;
     c.pay = pay;
     c.fence = fence;
     c.kmax = kmax;
+    c.okm = okm;
     c.n = n;
     c.m = (uint32_t)m;
   }
@@ -1055,6 +1058,9 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
   a.trace_cap = w.trace_cap;
   a.round_limit = (uint32_t)std::min<uint64_t>(
       0xfffffff0ULL, ((uint64_t)(fast ? G->max_out_deg : 0) + 1) * ((uint64_t)slots + 2) + 16);
+  // profiling only: stop after this many rounds (tools/phase_profile.sh takes
+  // per-round differences of ncu captures); the labels are then incomplete
+  if (const char* sr = getenv("TGXD_STOP_ROUND")) a.round_limit = (uint32_t)atoi(sr);
   if (w.trace_host) {
     TGXD_CUDA(cudaStreamSynchronize(s));
     std::memset(w.trace_host, 0, w.trace_cap * 64ull);
@@ -1223,7 +1229,8 @@ static int read_stats(tgxd_graph* G, tgxd_stats* st, float kernel_ms, float tota
   Control c;
   TGXD_CUDA(cudaMemcpyAsync(&c, G->ws.ctl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
   TGXD_CUDA(cudaStreamSynchronize(G->stream));
-  if (c.error) return fail(TGXD_ERR_CUDA, "traversal watchdog: round limit exceeded");
+  if (c.error && !getenv("TGXD_STOP_ROUND"))
+    return fail(TGXD_ERR_CUDA, "traversal watchdog: round limit exceeded");
   AsyncCtl ac;
   std::memset(&ac, 0, sizeof ac);
   uint32_t tail_rounds = 0;

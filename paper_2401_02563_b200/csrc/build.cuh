@@ -116,6 +116,12 @@ __global__ void segment_kmax(const uint32_t* off, const int32_t* key, uint32_t n
   }
 }
 
+__global__ void make_okm(const uint32_t* off, const int32_t* kmax, uint32_t n, uint2* okm) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += stride)
+    okm[v] = make_uint2(off[v], v < n ? (uint32_t)kmax[v] : (uint32_t)INT32_MIN);
+}
+
 __global__ void count_indexed(const uint32_t* off, uint32_t n, uint64_t cutoff,
                               unsigned long long* out) {
   unsigned long long c = 0;

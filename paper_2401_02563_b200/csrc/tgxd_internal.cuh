@@ -41,6 +41,9 @@ struct DevCsr {
   const uint2* pay = nullptr;     // m: relax payload {neighbor, val} (one 8-byte load)
   const int32_t* fence = nullptr; // ceil(m / 32): key[32 j]
   const int32_t* kmax = nullptr;  // n: last (largest) key of each segment, INT32_MIN if empty
+  // n + 1: {off[v], kmax[v]} side by side — an expansion's segment bounds and
+  // last key come from one 128-byte line (a random miss fetches the whole line)
+  const uint2* okm = nullptr;
   uint32_t n = 0;
   uint32_t m = 0;
 };
@@ -199,8 +202,8 @@ struct tgxd_graph {
   int directed = 1;
   uint64_t index_cutoff = 2048;
   uint64_t indexed[2] = {0, 0};
-  tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence, out_kmax;
-  tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax;
+  tgxd::DeviceBuffer out_off, out_key, out_pay, out_fence, out_kmax, out_okm;
+  tgxd::DeviceBuffer in_off, in_key, in_pay, in_fence, in_kmax, in_okm;
   tgxd::DeviceBuffer out2in;  // Out -> In position of each edge (shortest duration; lazy)
   // weighted shortest duration: per Out position the edge's weight as int64
   // (-1: not a non-negative integer, -2: >= 2^62); null = every weight 1
