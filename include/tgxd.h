@@ -197,6 +197,11 @@ int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes);
  * candidate lists. */
 int tgxd_last_h2d_bytes(tgxd_graph* g, uint64_t* bytes);
 
+/* Kernels this handle's queries have launched so far (a running total;
+ * measurement: bench.py's gpu_launches is the difference over its timed
+ * loops). Not in the reference. */
+int tgxd_launch_count(tgxd_graph* g, uint64_t* count);
+
 /* Device time of `steps` back-to-back queries with device-resident output,
  * after `warmup` untimed ones: total ms (CUDA events on the handle's stream)
  * and the mean traversal-kernel ms per query. */

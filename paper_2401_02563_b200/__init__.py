@@ -239,6 +239,7 @@ def load_library() -> ctypes.CDLL:
         "tgxd_last_work": ([vp, ctypes.c_uint32, _u64p, _u64p], ctypes.c_int),
         "tgxd_last_d2h_bytes": ([vp, _u64p], ctypes.c_int),
         "tgxd_last_h2d_bytes": ([vp, _u64p], ctypes.c_int),
+        "tgxd_launch_count": ([vp, _u64p], ctypes.c_int),
         "tgxd_time_rotation": ([vp, ctypes.c_int, ctypes.c_uint32, _u32p, _u64p, _u64p,
                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 _P(ctypes.c_float), _P(ctypes.c_float)], ctypes.c_int),
@@ -521,6 +522,13 @@ def last_d2h_bytes(g: TemporalGraph) -> int:
     b = ctypes.c_uint64()
     _check(load_library().tgxd_last_d2h_bytes(g.handle, ctypes.byref(b)))
     return b.value
+
+
+def launch_count(g: TemporalGraph) -> int:
+    """Kernels g's queries have launched so far (running total)."""
+    b = ctypes.c_uint64()
+    _check(load_library().tgxd_launch_count(g.handle, ctypes.byref(b)))
+    return int(b.value)
 
 
 def last_h2d_bytes(g: TemporalGraph) -> int:

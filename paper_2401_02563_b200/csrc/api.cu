@@ -504,6 +504,7 @@ static void convert_for(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   }
   convert_kernel<<<grid_for(slots, G->sm_count), 256, 0, G->stream>>>(
       form, V, V64, slots, G->n, w.seeds.as<Seed>(), out_dev, width);
+  ++G->ws.launches;
 }
 
 static uint64_t next_pow2(uint64_t x) {
@@ -535,6 +536,7 @@ static int ensure_async(tgxd_graph* G, uint32_t Q, bool required = true) {
     TGXD_CUDA(cudaMemsetAsync(w.actl.p, 0, sizeof(AsyncCtl), s));
     async_reset_kernel<<<grid_for(nunits, G->sm_count), 256, 0, s>>>(
         w.aunits.as<uint32_t>(), nunits, w.actl.as<AsyncCtl>());
+    ++G->ws.launches;
     w.a_slots = slots;
     w.a_units = nunits;
   }
@@ -565,9 +567,11 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g,
   if (const int rc = ensure_async(G, P.Q)) return rc;
   async_init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
       w.axq.as<unsigned long long>(), slots);
+  ++G->ws.launches;
   async_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
                                      w.axq.as<unsigned long long>(), w.aunits.as<uint32_t>(),
                                      w.a_units - 1, w.actl.as<AsyncCtl>(), fast);
+  ++G->ws.launches;
   AsyncArgs a;
   a.g = g;
   a.qp = w.params.as<QueryParam>();
@@ -605,6 +609,7 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g,
     const int blocks = std::min(G->coop_blocks_async, per_sm * G->sm_count);
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(blocks), dim3(kThreads),
                                           args, 0, s));
+    ++G->ws.launches;
   }
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   w.last_async = true;
@@ -657,6 +662,7 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
     if (ok && G->out.m) {
       out2in_kernel<<<grid_for(G->out.m, G->sm_count), 256, 0, s>>>(G->out, G->in,
                                                                     G->out2in.as<uint32_t>());
+      ++G->ws.launches;
       G->out2in_ready = true;
     }
   }
@@ -671,11 +677,13 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   init_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
       w.X.as<int32_t>(), w.EP.as<int2>(), kind == kEdgeFastest ? w.R.as<int32_t>() : nullptr,
       G->n);
+  ++G->ws.launches;
   edge_init_kernel<<<grid_for(qcap, G->sm_count), 256, 0, s>>>(
       kind, sd ? (uint32_t)(qcap - 1) : m, w.ereached.as<uint32_t>(), w.edep.as<int32_t>(),
       w.eval.as<long long>(), w.estamp.as<uint32_t>(),
       kind == kEdgeShortest ? w.ey.as<long long>() : nullptr, G->n, w.ectl.as<EdgeCtl>(),
       sd ? w.esm.as<long long>() : nullptr, sd ? G->in.m : 0u);
+  ++G->ws.launches;
 #ifdef TGXD_CHECK
   {
     const unsigned long long caps[2] = {qcap, (uint64_t)G->n + (uint64_t)(G->m / kChunk + 1)};
@@ -707,8 +715,10 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
     void* sargs[] = {&d};
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)sd_kernel, dim3(G->coop_blocks_sd),
                                           dim3(kThreads), sargs, 0, s));
+    ++G->ws.launches;
     edge_fold_kernel<<<grid_for(m, G->sm_count), 256, 0, s>>>(
         g, kEdgeShortest, nullptr, d.val, w.R.as<int32_t>(), w.ey.as<long long>());
+    ++G->ws.launches;
     if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
     if (out_dev) convert_for(G, P, out_dev, width);
     TGXD_CUDA(cudaGetLastError());
@@ -744,9 +754,11 @@ static int launch_edges(tgxd_graph* G, const Prepared& P, void* out_dev, int wid
   void* args[] = {&a};
   TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)edge_kernel, dim3(G->coop_blocks_edge),
                                         dim3(kThreads), args, 0, s));
+  ++G->ws.launches;
   if (kind != kEdgeReach)
     edge_fold_kernel<<<grid_for(m, G->sm_count), 256, 0, s>>>(
         g, kind, a.dep, a.val, w.R.as<int32_t>(), w.ey.as<long long>());
+  if (kind != kEdgeReach) ++G->ws.launches;
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   if (out_dev) convert_for(G, P, out_dev, width);
   TGXD_CUDA(cudaGetLastError());
@@ -772,9 +784,11 @@ static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void*
     return fail(TGXD_ERR_CUDA, "device allocation failed (lane-per-query labels)");
   lanes_init_kernel<<<grid_for(n * 8, G->sm_count), 256, 0, s>>>(
       w.lxm.as<int32_t>(), w.leb.as<int2>(), w.ldirty.as<uint32_t>(), n);
+  ++G->ws.launches;
   lanes_seed_kernel<<<1, 32, 0, s>>>(w.params.as<QueryParam>(), P.Q, w.lxm.as<int32_t>(),
                                      w.ldirty.as<uint32_t>(), w.fa.as<uint32_t>(),
                                      w.ctl.as<Control>());
+  ++G->ws.launches;
 #ifdef TGXD_CHECK
   {  // frontier: distinct vertices; chunks: segments / 128 + one per vertex
     const unsigned long long caps[2] = {(uint64_t)P.Q * G->n,
@@ -804,9 +818,11 @@ static int launch_lanes(tgxd_graph* G, const Prepared& P, const DevCsr& g, void*
   void* args[] = {&a};
   TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)lanes_kernel, dim3(G->coop_blocks_lanes),
                                         dim3(kThreads), args, 0, s));
+  ++G->ws.launches;
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   lanes_transpose_kernel<<<std::min<uint64_t>((n + 31) / 32, 8ull * G->sm_count), 256, 0, s>>>(
       w.lxm.as<int32_t>(), w.X.as<int32_t>(), G->n, P.Q);
+  ++G->ws.launches;
   if (out_dev) convert_for(G, P, out_dev, width);
   TGXD_CUDA(cudaGetLastError());
   w.last_edge = false;
@@ -909,6 +925,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
     candidates_kernel<<<1, kCandThreads, 0, s>>>(
         G->out, w.params.as<QueryParam>(), P.seeds[0].root, w.cand_lo.as<uint32_t>(),
         w.cand_cnt.as<uint32_t>(), w.cand_key.as<int32_t>(), w.cand_n.as<uint32_t>());
+    ++G->ws.launches;
   }
   // batches of EA / LD queries: one warp lane per query (AUTO's choice)
   const bool lanes_ok = P.Q >= 2 && P.Q <= 32 && G->n <= kLanesMaxN && !fast && !bfs &&
@@ -938,26 +955,31 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
     if (!w.xinv) {
       init_kernel<<<grid_for(w.slots, G->sm_count), 256, 0, s>>>(w.X.as<int32_t>(),
                                                                   w.EP.as<int2>(), nullptr, w.slots);
+      ++G->ws.launches;
       w.xinv = true;
     } else if (P.Q == 1) {  // reset + seed in one launch
       reset_seed_kernel<<<grid_for(std::max<uint64_t>(w.xdirty / 4, 1), G->sm_count), 256, 0, s>>>(
           w.X.as<int32_t>(), w.EP.as<int2>(), w.xdirty, P.qp[0].root, P.qp[0].klo,
           w.fa.as<uint32_t>(), w.ctl.as<Control>());
+      ++G->ws.launches;
       seeded = true;
     } else if (w.xdirty) {
       reset_kernel<<<grid_for(w.xdirty, G->sm_count), 256, 0, s>>>(w.X.as<int32_t>(),
                                                                     w.EP.as<int2>(), w.xdirty);
+      ++G->ws.launches;
     }
     w.xdirty = slots;
   } else {
     init_kernel<<<grid_for(slots, G->sm_count), 256, 0, s>>>(
         w.X.as<int32_t>(), w.EP.as<int2>(), fast || bfs ? w.R.as<int32_t>() : nullptr, slots);
+    ++G->ws.launches;
     w.xinv = false;
   }
   if (!seeded)
     seed_kernel<<<(P.Q + 127) / 128, 128, 0, s>>>(w.params.as<QueryParam>(), P.Q, G->n,
                                                    w.X.as<int32_t>(), w.fa.as<uint32_t>(),
                                                    w.ctl.as<Control>(), fast);
+  if (!seeded) ++G->ws.launches;
   if (mode == TGXD_MODE_ASYNC) {
     const int rc = launch_async(G, P, g, ev_k0, ev_k1);
     if (rc) return rc;
@@ -1038,6 +1060,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
   }
   w.last_handoff = a.handoff_f != 0 || a.async_f != 0;
   if (a.handoff_f) tail_reset_kernel<<<1, 1, 0, s>>>(w.tctl.as<TailCtl>());
+  if (a.handoff_f) ++G->ws.launches;
   {
     const char* hg = getenv("TGXD_HANDOFF_GROWTH");
     a.handoff_growth = hg ? (unsigned)std::max(1, atoi(hg)) : 8u;
@@ -1073,6 +1096,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
     if (early && w.last_handoff) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)traverse_kernel, dim3(G->coop_blocks),
                                           dim3(kThreads), args, 0, s));
+    ++G->ws.launches;
     if (early) {  // the caller's copy of the labels may start now
       TGXD_CUDA(cudaEventRecord(G->early_ev, s));
       w.early_done = true;
@@ -1112,6 +1136,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
       cfg.attrs = &at;
       cfg.numAttrs = 1;
       TGXD_CUDA(cudaLaunchKernelEx(&cfg, tail_kernel, t));
+      ++G->ws.launches;
     }
     if (a.async_f) {  // the continuation exits at once unless the round kernel handed off to it
       AsyncArgs h;
@@ -1145,14 +1170,17 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
       const int tail_blocks = std::min(G->coop_blocks_async, G->tail_per_sm * G->sm_count);
       TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)async_kernel, dim3(tail_blocks),
                                             dim3(kThreads), hargs, 0, s));
+      ++G->ws.launches;
     }
     if (early && w.last_handoff)  // the labels a tail engine lowered after the early copy
       tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
           w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X, G->patch_dev);
+    if (early && w.last_handoff) ++G->ws.launches;
   }
   if (split > 1)
     split_reduce_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
         w.R.as<int32_t>(), w.X.as<int32_t>(), G->n, split);
+  if (split > 1) ++G->ws.launches;
   if (ev_k1) TGXD_CUDA(cudaEventRecord(ev_k1, s));
   if (out_dev && !w.early_done) convert_for(G, Pout, out_dev, width);
   TGXD_CUDA(cudaGetLastError());
@@ -2191,6 +2219,13 @@ int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes) {
   if (!g || !bytes) return fail(TGXD_ERR_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lock(g->mu);
   *bytes = g->ws.last_d2h;
+  return TGXD_OK;
+}
+
+int tgxd_launch_count(tgxd_graph* g, uint64_t* count) {
+  if (!g || !count) return fail(TGXD_ERR_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  *count = g->ws.launches;
   return TGXD_OK;
 }
 

@@ -71,6 +71,7 @@ constexpr uint32_t kNoRoot = 0xffffffffu;
 struct Workspace {
   uint64_t slots = 0;  // Q x n label slots currently allocated
   DeviceBuffer X, EP, R, fa, fb, chunks, smalls, ctl, params, seeds;
+  uint64_t launches = 0;  // kernels this handle's queries launched (running total)
   // lazy label reset (api.cu launch): while `xinv` holds, every slot whose
   // expansion state is not the initial one has a finite label, and slots at
   // or above `xdirty` are untouched — so the next round-kernel query resets

@@ -61,7 +61,10 @@ namespace tgxd {
 #ifndef TGXD_LOCAL_F
 #define TGXD_LOCAL_F 128
 #endif
-constexpr int kThreads = 256;
+#ifndef TGXD_THREADS
+#define TGXD_THREADS 256
+#endif
+constexpr int kThreads = TGXD_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = TGXD_UNROLL;             // 32-edge steps in flight per warp
 constexpr uint32_t kChunk = 32u * kUnroll;       // edges per chunk of a big range
