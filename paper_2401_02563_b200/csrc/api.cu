@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1084,6 +1085,22 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
   // profiling only: stop after this many rounds (tools/phase_profile.sh takes
   // per-round differences of ncu captures); the labels are then incomplete
   if (const char* sr = getenv("TGXD_STOP_ROUND")) a.round_limit = (uint32_t)atoi(sr);
+  {
+    // early host copy from inside the round kernel (traverse.cuh): EA / LD
+    // with a host result; TGXD_LOG_F overrides the frontier size (0 = off:
+    // the copy starts after the round kernel)
+    const bool early = w.early_req && !fast && !bfs;
+    const char* lf = getenv("TGXD_LOG_F");
+    const uint64_t log_f = lf ? strtoull(lf, nullptr, 10) : std::max<uint64_t>(4096, slots / 16);
+    const bool in_kernel = early && log_f && G->copy_flag_dev;
+    a.copy_flag = in_kernel ? G->copy_flag_dev : nullptr;
+    a.log_f = log_f;
+    a.p24 = early && w.p24_req ? w.p24.as<uint32_t>() : nullptr;
+    a.p24_neg = P.kind == TGXD_LATEST_DEPARTURE ? 1 : 0;
+    a.chg = early ? w.chg.as<uint32_t>() : nullptr;
+    a.chg_n = early ? w.chg_n.as<unsigned long long>() : nullptr;
+    a.chg_cap = early ? w.chg_cap : 0;
+  }
   if (w.trace_host) {
     TGXD_CUDA(cudaStreamSynchronize(s));
     std::memset(w.trace_host, 0, w.trace_cap * 64ull);
@@ -1093,7 +1110,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
   {
     void* args[] = {&a};
     const bool early = w.early_req && !fast && !bfs;
-    if (early && w.last_handoff) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
+    if (early) TGXD_CUDA(cudaMemsetAsync(w.chg_n.p, 0, 8, s));
     TGXD_CUDA(cudaLaunchCooperativeKernel((const void*)traverse_kernel, dim3(G->coop_blocks),
                                           dim3(kThreads), args, 0, s));
     ++G->ws.launches;
@@ -1172,10 +1189,10 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
                                             dim3(kThreads), hargs, 0, s));
       ++G->ws.launches;
     }
-    if (early && w.last_handoff)  // the labels a tail engine lowered after the early copy
+    if (early)  // the labels lowered after the early copy started (round kernel, tail engine)
       tail_patch_kernel<<<2 * G->sm_count, 256, 0, s>>>(
           w.chg.as<uint32_t>(), w.chg_n.as<unsigned long long>(), w.chg_cap, a.X, G->patch_dev);
-    if (early && w.last_handoff) ++G->ws.launches;
+    if (early) ++G->ws.launches;
   }
   if (split > 1)
     split_reduce_kernel<<<grid_for(G->n, G->sm_count), 256, 0, s>>>(
@@ -1338,6 +1355,38 @@ __attribute__((target("avx2"))) static uint64_t widen_avx2(const int32_t* src, i
     _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i + 4), hi);
   }
   return i;
+}
+
+// 24-bit labels (pack24, traverse.cuh) -> int64 PathResult values: 8 per
+// step (bytes 0-11 of the group to the low lane, 12-23 to the high lane, one
+// byte shuffle, the 0xFFFFFF sentinel blended). `src` is readable 8 bytes
+// past the last group.
+__attribute__((target("avx2"))) static uint64_t widen24_avx2(const uint8_t* src, int64_t* dst,
+                                                           uint64_t a, uint64_t b, bool neg) {
+  const __m256i perm = _mm256_setr_epi32(0, 1, 2, 3, 3, 4, 5, 6);
+  const __m256i shuf = _mm256_setr_epi8(0, 1, 2, -1, 3, 4, 5, -1, 6, 7, 8, -1, 9, 10, 11, -1,
+                                        0, 1, 2, -1, 3, 4, 5, -1, 6, 7, 8, -1, 9, 10, 11, -1);
+  const __m256i sent = _mm256_set1_epi32(0xFFFFFF);
+  const __m256i inf64 = _mm256_set1_epi64x(neg ? INT64_MIN : INT64_MAX);
+  uint64_t i = a;
+  for (; i + 8 <= b; i += 8) {
+    const __m256i raw = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + 3 * i));
+    const __m256i x = _mm256_shuffle_epi8(_mm256_permutevar8x32_epi32(raw, perm), shuf);
+    const __m256i is_inf = _mm256_cmpeq_epi32(x, sent);
+    const __m256i lo = _mm256_cvtepu32_epi64(_mm256_castsi256_si128(x));
+    const __m256i hi = _mm256_cvtepu32_epi64(_mm256_extracti128_si256(x, 1));
+    const __m256i mlo = _mm256_cvtepi32_epi64(_mm256_castsi256_si128(is_inf));
+    const __m256i mhi = _mm256_cvtepi32_epi64(_mm256_extracti128_si256(is_inf, 1));
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), _mm256_blendv_epi8(lo, inf64, mlo));
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i + 4), _mm256_blendv_epi8(hi, inf64, mhi));
+  }
+  return i;
+}
+
+static inline int64_t widen24_one(const uint8_t* src, uint64_t i, bool neg) {
+  const uint32_t u = (uint32_t)src[3 * i] | ((uint32_t)src[3 * i + 1] << 8) |
+                     ((uint32_t)src[3 * i + 2] << 16);
+  return u == 0xFFFFFFu ? (neg ? INT64_MIN : INT64_MAX) : (int64_t)u;
 }
 
 static bool host_avx2() {
@@ -1539,27 +1588,91 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
       G->patch_dev = static_cast<unsigned long long*>(dp);
       G->patch_cap = cap;
     }
+    if (!G->copy_flag_host) {
+      void* hp = nullptr;
+      TGXD_CUDA(cudaHostAlloc(&hp, 64, cudaHostAllocMapped));
+      G->copy_flag_host = static_cast<volatile unsigned int*>(hp);
+      void* dp = nullptr;
+      TGXD_CUDA(cudaHostGetDevicePointer(&dp, hp, 0));
+      G->copy_flag_dev = static_cast<unsigned int*>(dp);
+    }
+    *G->copy_flag_host = 0u;
     if (!dalloc<uint32_t>(w.chg, cap) || !dalloc<unsigned long long>(w.chg_n, 1))
       return fail(TGXD_ERR_CUDA, "device allocation failed (tail patch list)");
     w.chg_cap = cap;
     G->patch_host[0] = 0;  // no tail: nothing to patch
   }
+  // the early copy moves 24-bit labels when every time of the graph fits
+  // (config 2: 12.6 MB over PCIe instead of 16.8; TGXD_NO_PACK24 turns it off)
+  bool pack = false;
+  if (early_ok && !getenv("TGXD_NO_PACK24")) {
+    if (const int rc2 = ensure_time_span(G)) return rc2;
+    pack = G->span[0] >= 0 && G->span[1] < 0xFFFFFE;
+    if (pack && !dalloc<uint32_t>(w.p24, (slots * 3 + 3) / 4 + 16))
+      return fail(TGXD_ERR_CUDA, "device allocation failed (packed labels)");
+  }
+  w.p24_req = pack;
   w.early_req = early_ok;
   w.early_done = false;
+  // TGXD_E2E_TRACE: host timeline of this call on stderr (diagnostics)
+  static const bool e2e_trace = getenv("TGXD_E2E_TRACE") != nullptr;
+  auto host_us = [] {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double h0 = e2e_trace ? host_us() : 0.0;
+  double h_flag = 0, h_enq = 0, h_c0 = 0, h_clast = 0, h_widen = 0;
+  bool by_flag = false;
   TGXD_CUDA(cudaEventRecord(w.ev[2], G->stream));
   rc = launch(G, P, mode, dout, staged ? 4 : width, w.ev[0], w.ev[1]);
+  const double h_launched = e2e_trace ? host_us() : 0.0;
   w.early_req = false;
+  w.p24_req = false;
   if (rc) return rc;
   const bool early = w.early_done;  // the traversal took the round kernel
-  const uint64_t chunk = (slots + kChunks - 1) / kChunks;
+  const bool p24 = early && pack;
+  // chunk c covers [bound(c), bound(c + 1)): shrinking chunks (1 - ((K - c) / K)^2
+  // of the slots before chunk c), so the widening exposed after the last copy
+  // is short (config 2: the last of 8 chunks is 1.6 % of the labels instead
+  // of 12.5 %); TGXD_FLAT_CHUNKS=1 makes them equal
+  static const bool flat = getenv("TGXD_FLAT_CHUNKS") != nullptr;
+  auto bound = [&](int c) -> uint64_t {
+    if (c >= kChunks) return slots;
+    if (flat) return std::min<uint64_t>(slots, c * ((slots + kChunks - 1) / kChunks));
+    const double r = (double)(kChunks - c) / kChunks;
+    return std::min<uint64_t>(slots, (uint64_t)((1.0 - r * r) * (double)slots) & ~(uint64_t)7);
+  };
   cudaStream_t cs = early ? G->copy_stream : G->stream;
   const int32_t* csrc = early ? w.X.as<int32_t>() : static_cast<int32_t*>(dout);
-  if (early) TGXD_CUDA(cudaStreamWaitEvent(cs, G->early_ev, 0));
+  if (early) {
+    // the copies may start once the round kernel raises the copy flag (its
+    // heavy rounds are over; later changes are listed for the patch) or,
+    // at the latest, when it is done
+    for (;;) {
+      if (*G->copy_flag_host) {
+        by_flag = true;
+        break;
+      }
+      const cudaError_t q = cudaEventQuery(G->early_ev);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) return fail(TGXD_ERR_CUDA, cudaGetErrorString(q));
+    }
+    if (e2e_trace) h_flag = host_us();
+    if (p24 && !by_flag) {  // the round kernel ended without packing: pack beside the tail
+      TGXD_CUDA(cudaStreamWaitEvent(cs, G->early_ev, 0));
+      pack24_kernel<<<grid_for((slots + 3) / 4, G->sm_count), 256, 0, cs>>>(
+          w.X.as<int32_t>(), w.p24.as<uint32_t>(), slots, kind == TGXD_LATEST_DEPARTURE ? 1 : 0);
+      ++G->ws.launches;
+    }
+  }
   if (staged) {
     for (int c = 0; c < kChunks; ++c) {
-      const uint64_t lo = std::min<uint64_t>(slots, c * chunk);
-      const uint64_t len = std::min<uint64_t>(slots, lo + chunk) - lo;
-      if (len)
+      const uint64_t lo = bound(c);
+      const uint64_t len = bound(c + 1) - lo;
+      if (len && p24)
+        TGXD_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(G->pinned) + 3 * lo,
+                                  w.p24.as<char>() + 3 * lo, len * 3, cudaMemcpyDeviceToHost, cs));
+      else if (len)
         TGXD_CUDA(cudaMemcpyAsync(G->pinned + lo, csrc + lo, len * 4, cudaMemcpyDeviceToHost, cs));
       TGXD_CUDA(cudaEventRecord(G->chunk_ev[c], cs));
     }
@@ -1568,6 +1681,7 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     TGXD_CUDA(cudaMemcpyAsync(out, dout, slots * width, cudaMemcpyDeviceToHost, G->stream));
   }
   TGXD_CUDA(cudaEventRecord(w.ev[3], G->stream));
+  if (e2e_trace) h_enq = host_us();
   if (staged) {
     if (G->pool.size() == 0)
       G->pool.start([&] {
@@ -1596,15 +1710,26 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     const volatile unsigned long long* ph = G->patch_host;
     G->pool.run([&](int wi) {
       for (int c = 0; c < kChunks; ++c) {
-        const uint64_t lo = std::min<uint64_t>(slots, c * chunk);
-        const uint64_t hi = std::min<uint64_t>(slots, lo + chunk);
+        const uint64_t lo = bound(c);
+        const uint64_t hi = bound(c + 1);
         const uint64_t per = (hi - lo + T - 1) / T;
         const uint64_t a = std::min(hi, lo + wi * per), b = std::min(hi, a + per);
         if (cudaEventSynchronize(G->chunk_ev[c]) != cudaSuccess) {
           bad = 1;
           break;
         }
+        if (e2e_trace && wi == 0 && c == 0) h_c0 = host_us();
+        if (e2e_trace && wi == 0 && c == kChunks - 1) h_clast = host_us();
         uint64_t i = a;
+        if (p24) {  // 24-bit labels (times, sentinel 0xFFFFFF)
+          const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
+          // the vector loads read 8 bytes past their 8 labels: stay clear of
+          // the staging's end
+          const uint64_t vb = b + 8 <= slots ? b : (b > 8 ? b - 8 : a);
+          if (host_avx2() && vb > a) i = widen24_avx2(s8, o64, a, vb, neg);
+          for (; i < b; ++i) o64[i] = widen24_one(s8, i, neg);
+          continue;
+        }
         if (host_avx2()) i = widen_avx2(src, o64, a, b, neg);  // 8 labels per step
         if (neg) {
           for (; i < b; ++i) o64[i] = widen(src[i]);
@@ -1637,6 +1762,7 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
         o64[(uint32_t)e] = widen((int32_t)(uint32_t)(e >> 32));
       }
     });
+    if (e2e_trace) h_widen = host_us();
     if (bad) return fail(TGXD_ERR_CUDA, "result copy failed");
     if (recopy) {
       TGXD_CUDA(cudaMemcpyAsync(G->pinned, w.X.p, slots * 4, cudaMemcpyDeviceToHost, G->stream));
@@ -1649,7 +1775,7 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
     }
     for (uint32_t q = 0; q < P.Q; ++q)  // the roots' exact values (t_a, t_b, 0)
       o64[(uint64_t)q * G->n + P.seeds[q].root] = P.seeds[q].value;
-    w.last_d2h = slots * 4;
+    w.last_d2h = slots * (p24 ? 3 : 4);
     if (early) {
       const unsigned long long np = G->patch_host[0];
       w.last_d2h += np > w.chg_cap ? slots * 4 : 8 * (np + 1);
@@ -1661,6 +1787,13 @@ static int query_impl(tgxd_graph* G, int kind, uint32_t k, const uint32_t* verts
   float km = 0, tm = 0;
   TGXD_CUDA(cudaEventElapsedTime(&km, w.ev[0], w.ev[1]));
   TGXD_CUDA(cudaEventElapsedTime(&tm, w.ev[2], w.ev[3]));
+  if (e2e_trace)
+    fprintf(stderr,
+            "e2e us: launched %.0f copy-start %.0f (%s) enqueued %.0f chunk0 %.0f last-chunk %.0f "
+            "widened+patched %.0f end %.0f | kernels %.0f span %.0f patch %llu\n",
+            h_launched - h0, h_flag - h0, by_flag ? "flag" : "event", h_enq - h0, h_c0 - h0,
+            h_clast - h0, h_widen - h0, host_us() - h0, km * 1e3, tm * 1e3,
+            G->patch_host ? (unsigned long long)G->patch_host[0] : 0ull);
   return read_stats(G, stats, km, tm);
 }
 
@@ -1959,6 +2092,7 @@ void tgxd_graph_destroy(tgxd_graph* g) {
   if (g->ws.trace_host) cudaFreeHost(g->ws.trace_host);
   if (g->pinned) cudaFreeHost(g->pinned);
   if (g->patch_host) cudaFreeHost(g->patch_host);
+  if (g->copy_flag_host) cudaFreeHost(const_cast<unsigned int*>(g->copy_flag_host));
   if (g->early_ev) cudaEventDestroy(g->early_ev);
   if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
   for (auto& e : g->chunk_ev)

@@ -102,6 +102,8 @@ struct Workspace {
   // the async tail runs; the tail's changed labels are patched afterwards
   bool early_req = false;   // set by the caller for one launch
   bool early_done = false;  // launch recorded early_ev (and the patch list)
+  bool p24_req = false;     // the early copy reads 24-bit packed labels (p24)
+  DeviceBuffer p24;
   uint64_t last_d2h = 0;    // bytes the last host-result query moved to the host
   DeviceBuffer chg, chg_n;
   unsigned long long chg_cap = 0;
@@ -243,6 +245,8 @@ struct tgxd_graph {
   cudaStream_t copy_stream = nullptr;  // early host copies
   cudaEvent_t early_ev = nullptr;      // the round kernel is done
   unsigned long long* patch_host = nullptr;  // mapped: count, {slot, label} pairs
+  volatile unsigned int* copy_flag_host = nullptr;  // mapped: the round kernel's copy signal
+  unsigned int* copy_flag_dev = nullptr;
   unsigned long long* patch_dev = nullptr;
   size_t patch_cap = 0;
   WidenPool pool;

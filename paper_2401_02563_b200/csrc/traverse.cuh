@@ -123,6 +123,16 @@ struct TravArgs {
   int wtrace_on;
   uint32_t trace_cap;
   uint32_t round_limit;  // watchdog: a correct traversal never gets near it
+  // early host copy of EA / LD labels (api.cu): a frontier past its peak and
+  // at most log_f slots raises *copy_flag (mapped host memory) and from then
+  // on every lowered slot is listed in chg
+  uint32_t* chg;
+  unsigned long long* chg_n;
+  unsigned long long chg_cap;
+  volatile unsigned int* copy_flag;
+  unsigned long long log_f;
+  uint32_t* p24;         // non-null: the copy reads labels packed to 24 bits here
+  int p24_neg;
   unsigned long long init_pushes;  // queue position / improvements after seeding
 };
 
@@ -235,7 +245,50 @@ struct RelaxCtx {
   uint64_t pol_stream, pol_keep;
   uint32_t improved;         // per-lane improvement count (no-push rounds)
   int32_t hop;               // temporal BFS: this round's number (1-based)
+  bool log = false;          // list every lowered slot (the host copy has started)
 };
+
+// 24-bit packing of key-space labels for the early host copy (api.cu): 4
+// labels per 12 bytes, INF as 0xFFFFFF, LD labels negated back to times.
+// Threads [tid, nthr) of the caller pack groups [0, ceil(slots / 4)).
+__device__ __forceinline__ uint32_t pack24_one(int32_t x, int neg) {
+  return x == kInf ? 0xFFFFFFu : (uint32_t)(neg ? -x : x) & 0xFFFFFFu;
+}
+__device__ __forceinline__ void pack24(const int32_t* X, uint32_t* P, uint64_t slots, int neg,
+                                       uint64_t tid, uint64_t nthr) {
+  const uint64_t groups = (slots + 3) / 4;
+  for (uint64_t i = tid; i < groups; i += nthr) {
+    uint32_t u[4];
+    if (4 * i + 4 <= slots) {
+      const int4 x = __ldcg(reinterpret_cast<const int4*>(X) + i);
+      u[0] = pack24_one(x.x, neg);
+      u[1] = pack24_one(x.y, neg);
+      u[2] = pack24_one(x.z, neg);
+      u[3] = pack24_one(x.w, neg);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = 4 * i + k < slots ? pack24_one(__ldcg(X + 4 * i + k), neg) : 0u;
+    }
+    P[3 * i] = u[0] | (u[1] << 24);
+    P[3 * i + 1] = (u[1] >> 8) | (u[2] << 16);
+    P[3 * i + 2] = (u[2] >> 16) | (u[3] << 8);
+  }
+}
+
+// Early host copy (api.cu): once the round kernel signals the copy, every
+// slot it lowers afterwards is listed (the tail engines do the same); the
+// host patches the listed slots with their final labels. One reservation
+// per warp and call.
+__device__ __forceinline__ void log_lowered(const TravArgs& a, bool lowered, uint32_t slot) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, lowered);
+  if (!bal) return;
+  const uint32_t lane = lane_id();
+  unsigned long long base = 0;
+  if (lane == __ffs(bal) - 1) base = atomicAdd(a.chg_n, (unsigned long long)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+  const unsigned long long k = base + __popc(bal & ((1u << lane) - 1));
+  if (lowered && k < a.chg_cap) a.chg[k] = slot;
+}
 
 // Relax kUnroll 32-edge steps: e[u] edge ids, q[u] query slots, act[u] lane
 // validity. write_min (parallel.hpp:91-99) is a plain label probe followed by
@@ -254,13 +307,15 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
                                             const bool (&act)[kUnroll], RelaxCtx& rx,
                                             PushBuf& pb);
 
-// Split fastest sweeps (split_seed_step) give every query slot its own
-// departure, so r is not updated per improvement there (a per-edge lookup of
-// the slot's departure measured 3 % on config 4's one-sweep fastest) but per
-// expansion, from the label the slot is expanded with (expand_warp, P1):
-// every improvement is followed by an expansion of the improved slot within
-// the step, the last one with the step's final label, and r needs only the
-// minimum of label - departure (path_algorithms.cpp:519-523).
+// Fastest: r = min over improvements of (label - departure) is not taken per
+// improving edge but per expansion, from the label the slot is expanded
+// with (expand_warp, P1): every improvement is followed by an expansion of
+// the improved slot before the candidate's rounds end, the last one with
+// the candidate's final label, and r needs only the minimum of label -
+// departure (path_algorithms.cpp:519-523) — one probe and at most one
+// atomicMin per expansion instead of one per improving edge (config 4
+// fastest 5.09 -> ... ms). Split sweeps (split_seed_step) give every query
+// slot its own departure (dep[q]); the round's `depart` is then kSplitDepart.
 constexpr int32_t kSplitDepart = INT32_MIN;
 
 __device__ __forceinline__ void relax_steps(const TravArgs& a, const uint32_t (&e)[kUnroll],
@@ -303,24 +358,32 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     old[u] = v[u];  // no atomic issued: not an improvement
-    ex[u] = 0;
+    ex[u] = kInf;
     if (v[u] < cur[u]) {
+      // the expansion bound decides the first improvement; a slot probed
+      // unreached was never expanded (bound INF, no load): its improver that
+      // finds old == INF pushes it, later ones see a finite old
+#ifdef TGXD_EP_ALWAYS
       if (rx.push) ex[u] = ld_state(reinterpret_cast<const int32_t*>(a.EP + idx[u]), rx.pol_keep);
+#else
+      if (rx.push && cur[u] != kInf)
+        ex[u] = ld_state(reinterpret_cast<const int32_t*>(a.EP + idx[u]), rx.pol_keep);
+#endif
       old[u] = atomicMin(a.X + idx[u], v[u]);  // write_min, parallel.hpp:91-99
     }
+  }
+  if (rx.log) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) log_lowered(a, v[u] < old[u], idx[u]);
   }
   bool p[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     p[u] = false;
     if (v[u] < old[u]) {
-      // fastest: r = min(arrival - departure); BFS: the first improving round
-      // (compare_and_swap(r[d], inf, round), path_algorithms.cpp:395-397)
-      if (a.hops) {
-        if (old[u] == kInf) a.R[idx[u]] = rx.hop;
-      } else if (a.R && rx.depart != kSplitDepart) {
-        atomicMin(a.R + idx[u], v[u] - rx.depart);
-      }
+      // BFS: the first improving round (compare_and_swap(r[d], inf, round),
+      // path_algorithms.cpp:395-397); fastest's r is taken at expansion
+      if (a.hops && old[u] == kInf) a.R[idx[u]] = rx.hop;
       if (rx.push) p[u] = bound_of(old[u], a.strict) == ex[u];
       else ++rx.improved;
     }
@@ -484,7 +547,7 @@ struct ExpandBufs {
 __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint32_t item, int32_t x,
                                             int2 ep, uint32_t s, uint32_t t, int32_t km,
                                             ExpandBufs& eb, unsigned long long& work,
-                                            unsigned long long& ix) {
+                                            unsigned long long& ix, int32_t depart) {
   const uint32_t lane = lane_id();
   uint32_t q = 0, p0 = 0, p1 = 0;
   bool act = false;
@@ -498,8 +561,8 @@ __device__ __forceinline__ void expand_warp(const TravArgs& a, bool valid, uint3
     int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);
     if (lb < qp.klo) lb = qp.klo;
     const int32_t old = ep.x;
-    if (a.split > 1 && lb < old) {  // split fastest sweep: r from the expanded label
-      const int32_t r = x - __ldcg(a.dep + q);
+    if (a.fastest && lb < old) {  // fastest: r from the expanded label
+      const int32_t r = x - (depart == kSplitDepart ? __ldcg(a.dep + q) : depart);
       if (r < __ldcg(a.R + item)) atomicMin(a.R + item, r);
     }
     if (lb < old) {
@@ -588,7 +651,8 @@ __device__ __forceinline__ void flush_work(Control* ctl, unsigned long long work
 // bound is below its expansion bound.
 __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint32_t F,
                         unsigned long long cstart, unsigned long long sstart, uint32_t bid,
-                        uint32_t nblk, uint64_t pol_keep, uint2* ebuf, unsigned long long& ix) {
+                        uint32_t nblk, uint64_t pol_keep, uint2* ebuf, unsigned long long& ix,
+                        int32_t depart) {
   const uint32_t lane = lane_id();
   const uint32_t gw = bid * kWarps + (threadIdx.x >> 5);
   const uint32_t nw = nblk * kWarps;
@@ -619,7 +683,7 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
       t0 = __ldg(&a.g.okm[v + 1].x);
       valid = x != kInf;
     }
-    expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix);
+    expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix, depart);
   }
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
@@ -999,8 +1063,8 @@ __device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs
   const bool improved = best != kInf;
   if (improved) {
     a.X[i] = best;
-    if (a.R && rx.depart != kSplitDepart) atomicMin(a.R + i, best - rx.depart);
   }
+  if (rx.log) log_lowered(a, improved, i);
   const uint32_t bal = __ballot_sync(0xffffffffu, improved);
   if (bal) {
     if (improved) b.pb.buf[b.pb.n + __popc(bal & ((1u << lane) - 1))] = i;
@@ -1057,8 +1121,8 @@ __device__ TGXD_PHASE void phase_pull1(const TravArgs& a, RelaxCtx& rx, unsigned
           int32_t lb = (i - q * a.n == qp.root) ? qp.klo : bound_of(x[u], a.strict);
           if (lb < qp.klo) lb = qp.klo;
           a.EP[i] = make_int2(lb, (int32_t)kNoPos);
-          if (a.split > 1) {  // split fastest sweep: r from the label pulled from
-            const int32_t r = x[u] - __ldcg(a.dep + q);
+          if (a.fastest) {  // fastest: r from the label the pull starts from
+            const int32_t r = x[u] - (rx.depart == kSplitDepart ? __ldcg(a.dep + q) : rx.depart);
             if (r < __ldcg(a.R + i)) atomicMin(a.R + i, r);
           }
         }
@@ -1106,14 +1170,15 @@ __device__ TGXD_PHASE void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     scanned += lane == 0 ? hi - ch.x : 0u;
-    bool first = false;
+    bool first = false, lowered = false;
     if (lane == 0 && m != kInf && m < ld_state(a.X + slot, rx.pol_keep)) {
       const int32_t old = atomicMin(a.X + slot, m);
       if (m < old) {
-        if (a.R && rx.depart != kSplitDepart) atomicMin(a.R + slot, m - rx.depart);
-        first = bound_of(old, a.strict) == __ldcg(&a.EP[slot].x);
+        lowered = true;
+        first = old == kInf || bound_of(old, a.strict) == __ldcg(&a.EP[slot].x);
       }
     }
+    if (rx.log) log_lowered(a, lowered, slot);
     const uint32_t bal = __ballot_sync(0xffffffffu, first);
     if (bal) {
       if (lane == 0) pb.buf[pb.n] = slot;
@@ -1187,6 +1252,7 @@ struct TState {
   int dense;                   // the next expand scans densely
   int pending;                 // CTA expand done, grid relax of its work pending
   uint32_t last_f;             // previous round's frontier size
+  int logging;                 // early host copy running: list lowered slots
 };
 
 __device__ __forceinline__ void save_state(Control* ctl, const TState& s) {
@@ -1273,6 +1339,7 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
     uint32_t* fin = st.flip ? a.fb : a.fa;
     uint32_t* fout = st.flip ? a.fa : a.fb;
     RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
+    rx.log = st.logging;
     if (seed) {
       if (tr) {
         trace_round(a, st.rounds, 0, gtimer());
@@ -1289,7 +1356,7 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
         trace_round(a, st.rounds, 3, F);
         trace_round(a, st.rounds, 7, 1);
       }
-      phase_a(a, fin, F, st.c_cur, st.s_cur, 0, 1, pol_keep, ebuf, ix);
+      phase_a(a, fin, F, st.c_cur, st.s_cur, 0, 1, pol_keep, ebuf, ix, depart);
       const unsigned long long c_end = block_read(&ctl->chunks);
       const unsigned long long s_end = block_read(&ctl->smalls);
       const unsigned long long e_end = block_read(&ctl->edges);
@@ -1432,6 +1499,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
   st.dense = a.mode == TGXD_MODE_DENSE;
   st.pending = 0;
   st.last_f = 0;
+  st.logging = 0;
   bool handed = false;
   const uint32_t n_cand = a.fastest ? __ldcg(a.n_cand) : 0u;
   // split sweeps take `split` candidates per step, one per query slot
@@ -1505,6 +1573,22 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
           break;
         }
       }
+      // early host copy: a frontier past its peak and small enough starts
+      // the labels' copy to the host now (the heavy rounds are over); what
+      // the remaining rounds lower is listed for the host's patch
+      if (a.copy_flag && !st.logging && !xcnt && st.rounds >= 2 && F <= a.log_f &&
+          F < (unsigned long long)st.last_f) {
+        st.logging = 1;
+        if (a.p24) {  // the copy reads 24-bit labels: pack them first
+          pack24(a.X, a.p24, (uint64_t)a.Q * a.n, a.p24_neg,
+                 (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
+          grid.sync();
+        }
+        if (tr) {
+          __threadfence_system();
+          *a.copy_flag = 1u;
+        }
+      }
       if (!xcnt) st.last_f = (uint32_t)min(F, 0xffffffffull);
       const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
                             (xcnt ? xcnt <= kLocalMaxW : F <= kLocalMaxF);
@@ -1524,6 +1608,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         const unsigned long long p_now = st.p_known;
         uint32_t* fout = st.flip ? a.fa : a.fb;
         RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
+        rx.log = st.logging;
         phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
         trace_warp_done(a, st.rounds, 1);
         grid.sync();
@@ -1557,6 +1642,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       }
       if (pull) {
         RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
+        rx.log = st.logging;
         unsigned long long scanned = 0;
         // P1 queues slots right away: every block's post-barrier read of the
         // pushes counter must be over first (counter discipline)
@@ -1593,7 +1679,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       unsigned long long c_end = st.c_cur, s_end = st.s_cur, e_end = st.e_cur;
       if (!xcnt) {
         phase_a(a, st.dense ? nullptr : fin, (uint32_t)F, st.c_cur, st.s_cur, blockIdx.x,
-                gridDim.x, pol_keep, ebuf, ix);
+                gridDim.x, pol_keep, ebuf, ix, depart);
         trace_warp_done(a, st.rounds, 0);
         grid.sync();
         const Counters c0 = read_counters(ctl);
@@ -1610,6 +1696,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       const bool push = a.mode == TGXD_MODE_SPARSE ||
                         (a.mode == TGXD_MODE_AUTO && w <= a.push_w);
       RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
+      rx.log = st.logging;
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, xlo, xcnt, rx, blockIdx.x, gridDim.x, wbuf);
       if (!push) {  // improvements only feed the dense frontier's size
         uint32_t imp = rx.improved;
@@ -1659,6 +1746,13 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
     ctl->rounds = st.rounds;
     ctl->candidates = n_cand;
   }
+}
+
+// 24-bit packing when the copy starts after the round kernel (api.cu; it
+// runs beside the tail engine).
+__global__ void pack24_kernel(const int32_t* X, uint32_t* P, uint64_t slots, int neg) {
+  pack24(X, P, slots, neg, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+         (uint64_t)gridDim.x * blockDim.x);
 }
 
 // Labels, expansion bounds and durations to INF.

@@ -51,12 +51,21 @@ def test_early_copy_matches(c2_small, kind):
             assert np.array_equal(_run(fn, g, v, w, {"TGXD_NO_EARLY_COPY": "1"}), want)
             # a patch list of one entry forces the re-copy after the tail
             assert np.array_equal(_run(fn, g, v, w, {"TGXD_PATCH_CAP": "1"}), want)
+            # the copy started from inside the round kernel: as early as
+            # possible (every later round lists its changes), never, and with
+            # the whole tail left to the round kernel
+            for env in ({"TGXD_LOG_F": "1000000000"}, {"TGXD_LOG_F": "0"},
+                        {"TGXD_LOG_F": "1000000000", "TGXD_HANDOFF_F": "0",
+                         "TGXD_ASYNC_F": "0"},
+                        {"TGXD_LOG_F": "1000000000", "TGXD_PATCH_CAP": "64"},
+                        {"TGXD_NO_PACK24": "1"}, {"TGXD_NO_PACK24": "1", "TGXD_LOG_F": "0"}):
+                assert np.array_equal(_run(fn, g, v, w, env), want), env
 
 
 def test_early_copy_batch(c2_small):
     g, o, n = c2_small
     deg = g.degrees(T.Direction.OUT)
-    srcs = [int(x) for x in np.argsort(-deg)[:3]]
+    srcs = [int(x) for x in np.argsort(deg.astype(np.int64))[::-1][:3]]
     wins = [T.QueryWindow(0, 999_999), T.QueryWindow(100_000, 999_999), T.QueryWindow(0, 500_000)]
     for mode in (T.Mode.SPARSE, T.Mode.AUTO):
         out = T.query_batch(g, "earliest_arrival", srcs, wins, mode=mode)
