@@ -598,6 +598,7 @@ static int launch_async(tgxd_graph* G, const Prepared& P, const DevCsr& g,
   a.chg_cap = 0;
   a.hctl = nullptr;
   a.hfa = a.hfb = nullptr;
+  a.hfresh = 0;
   if (ev_k0) TGXD_CUDA(cudaEventRecord(ev_k0, s));
   {
     void* args[] = {&a};
@@ -1095,6 +1096,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
     const bool in_kernel = early && log_f && G->copy_flag_dev;
     a.copy_flag = in_kernel ? G->copy_flag_dev : nullptr;
     a.log_f = log_f;
+    a.fresh = slots < (1ull << 31) && !getenv("TGXD_NO_FRESH") ? 0x80000000u : 0u;
     a.p24 = early && w.p24_req ? w.p24.as<uint32_t>() : nullptr;
     a.p24_neg = P.kind == TGXD_LATEST_DEPARTURE ? 1 : 0;
     a.chg = early ? w.chg.as<uint32_t>() : nullptr;
@@ -1136,6 +1138,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
       t.cutoff = a.cutoff;
       t.round_limit = (uint32_t)std::min<uint64_t>(0xfffffff0ULL, slots + 16);
       t.slots = slots;
+      t.fresh = a.fresh;
       t.chg = early ? w.chg.as<uint32_t>() : nullptr;
       t.chg_n = early ? w.chg_n.as<unsigned long long>() : nullptr;
       t.chg_cap = early ? w.chg_cap : 0;
@@ -1182,6 +1185,7 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
       h.hctl = a.ctl;
       h.hfa = a.fa;
       h.hfb = a.fb;
+      h.hfresh = a.fresh;
       void* hargs[] = {&h};
       // the tail on fewer CTAs per SM (new_graph: G->tail_per_sm)
       const int tail_blocks = std::min(G->coop_blocks_async, G->tail_per_sm * G->sm_count);

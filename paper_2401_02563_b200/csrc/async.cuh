@@ -101,6 +101,7 @@ struct AsyncArgs {
   const Control* hctl;  // nullptr: a query of its own
   const uint32_t* hfa;
   const uint32_t* hfb;
+  uint32_t hfresh;       // the round kernel's queue-item mark (cleared on read)
 };
 
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) async_kernel(AsyncA
     for (size_t i = slots / 4 * 4 + tid; i < slots; i += nthr) a.XQ[i] = xq_pack(a.X[i], 0u);
     grid.sync();
     for (size_t k = tid; k < nh; k += nthr) {
-      const uint32_t item = __ldcg(fin + k);
+      const uint32_t item = __ldcg(fin + k) & ~a.hfresh;  // (round kernel's marks)
       a.XQ[item] = xq_pack(a.X[item], 1u);
       uint32_t* u = unit_ptr(a, t0 + k / kBatch);
       u[1 + k % kBatch] = item;

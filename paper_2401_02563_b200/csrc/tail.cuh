@@ -69,6 +69,7 @@ struct TailArgs {
   uint32_t cutoff;
   uint32_t round_limit;
   unsigned long long slots;
+  uint32_t fresh;            // the round kernel's queue-item mark (cleared on read)
   // early host copy: every slot the tail lowers is listed (api.cu)
   uint32_t* chg;
   unsigned long long* chg_n;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
       const unsigned long long i = b + lane;
       uint32_t q = 0, p0 = 0, cnt_e = 0;
       if (lane < ipw && i < F) {
-        const uint32_t item = __ldcg(qin + i);
+        const uint32_t item = __ldcg(qin + i) & ~a.fresh;  // (round kernel's marks)
         q = a.Q == 1 ? 0u : item / a.n;
         const uint32_t v = item - q * a.n;
         const int32_t x = ld_state(a.X + item, pol_keep);

@@ -133,6 +133,10 @@ struct TravArgs {
   unsigned long long log_f;
   uint32_t* p24;         // non-null: the copy reads labels packed to 24 bits here
   int p24_neg;
+  // frontier queue items of slots first reached in the round that queued
+  // them carry this bit (0: not used, slots >= 2^31): their expansion state
+  // is the initial one, so the expansion skips its load
+  uint32_t fresh;
   unsigned long long init_pushes;  // queue position / improvements after seeding
 };
 
@@ -314,7 +318,7 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
 // the candidate's final label, and r needs only the minimum of label -
 // departure (path_algorithms.cpp:519-523) — one probe and at most one
 // atomicMin per expansion instead of one per improving edge (config 4
-// fastest 5.09 -> ... ms). Split sweeps (split_seed_step) give every query
+// fastest 5.11 -> 4.66 ms). Split sweeps (split_seed_step) give every query
 // slot its own departure (dep[q]); the round's `depart` is then kSplitDepart.
 constexpr int32_t kSplitDepart = INT32_MIN;
 
@@ -394,7 +398,7 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
       const uint32_t bal = __ballot_sync(0xffffffffu, p[u]);
       if (bal) {
         const uint32_t lane = lane_id();
-        if (p[u]) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = idx[u];
+        if (p[u]) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = idx[u] | (old[u] == kInf ? a.fresh : 0u);
         pb.n += __popc(bal);
         if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
       }
@@ -668,9 +672,14 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
     uint32_t s0 = 0, t0 = 0;
     int32_t km0 = INT32_MIN;
     if (valid) {
-      if (fin) item = __ldcg(fin + i);
+      bool fresh = false;
+      if (fin) {
+        item = __ldcg(fin + i);
+        fresh = (item & a.fresh) != 0;
+        item &= ~a.fresh;
+      }
       x = ld_state(a.X + item, pol_keep);
-      ep = __ldcg(a.EP + item);
+      if (!fresh) ep = __ldcg(a.EP + item);  // (a fresh slot's is the initial state)
       // the segment's bounds and last key do not depend on the label: issue
       // them with it (one dependent load less per expansion)
       const uint32_t v = a.Q == 1 ? item : item % a.n;
@@ -1067,7 +1076,9 @@ __device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs
   if (rx.log) log_lowered(a, improved, i);
   const uint32_t bal = __ballot_sync(0xffffffffu, improved);
   if (bal) {
-    if (improved) b.pb.buf[b.pb.n + __popc(bal & ((1u << lane) - 1))] = i;
+    // (lim == vhi + 1: the slot was unreached — a reached label lies in the window)
+    const bool fresh = a.Q == 1 ? lim == a.qp[0].vhi + 1 : lim == a.qp[i / a.n].vhi + 1;
+    if (improved) b.pb.buf[b.pb.n + __popc(bal & ((1u << lane) - 1))] = i | (fresh ? a.fresh : 0u);
     b.pb.n += __popc(bal);
     if (b.pb.n >= 32) push_flush32(b.pb, a.ctl, rx.pstart, rx.fout);
   }
@@ -1170,18 +1181,19 @@ __device__ TGXD_PHASE void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     scanned += lane == 0 ? hi - ch.x : 0u;
-    bool first = false, lowered = false;
+    bool first = false, lowered = false, fresh = false;
     if (lane == 0 && m != kInf && m < ld_state(a.X + slot, rx.pol_keep)) {
       const int32_t old = atomicMin(a.X + slot, m);
       if (m < old) {
         lowered = true;
-        first = old == kInf || bound_of(old, a.strict) == __ldcg(&a.EP[slot].x);
+        fresh = old == kInf;
+        first = fresh || bound_of(old, a.strict) == __ldcg(&a.EP[slot].x);
       }
     }
     if (rx.log) log_lowered(a, lowered, slot);
     const uint32_t bal = __ballot_sync(0xffffffffu, first);
     if (bal) {
-      if (lane == 0) pb.buf[pb.n] = slot;
+      if (lane == 0) pb.buf[pb.n] = slot | (fresh ? a.fresh : 0u);
       pb.n += 1;
       if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
     }
