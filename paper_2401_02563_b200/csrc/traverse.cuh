@@ -888,8 +888,17 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
     const unsigned long long i = w * 32 + lane;
     return (w < nwin && i < nsmall) ? __ldcg(a.smalls + i) : make_uint2(0u, 0u);
   };
-  uint2 sv = win_load(gw);
-  for (unsigned long long w = gw; w < nwin; w += nw) {
+  // chunks and windows are one sequence of work units dealt round-robin:
+  // the windows continue where the chunks end, so the warps that took one
+  // chunk fewer start on the windows first
+#ifdef TGXD_SPLIT_UNITS
+  const unsigned long long w0 = gw;
+#else
+  const unsigned long long w0 =
+      (gw >= nchunks ? gw : gw + (nchunks - gw + nw - 1) / nw * nw) - nchunks;
+#endif
+  uint2 sv = win_load(w0);
+  for (unsigned long long w = w0; w < nwin; w += nw) {
     const uint2 snx = win_load(w + nw);  // next window prefetched
     relax_window(a, sv, rx, pb);
     sv = snx;
