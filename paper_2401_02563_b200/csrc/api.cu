@@ -2508,6 +2508,16 @@ int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds) {
 // extremes (device memory; copied only when `with_device` is set).
 int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds, int with_device) {
   if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
+#ifdef TGXD_WTRACE_ALL
+  if (const char* path = getenv("TGXD_WTRACE_ALL_FILE")) {  // diagnostics: every warp's times
+    std::vector<unsigned long long> all(sizeof(g_wdone) / 8);
+    TGXD_CUDA(cudaMemcpyFromSymbol(all.data(), g_wdone, sizeof(g_wdone)));
+    if (FILE* f = fopen(path, "wb")) {
+      fwrite(all.data(), 8, all.size(), f);
+      fclose(f);
+    }
+  }
+#endif
   const uint32_t r = std::min(max_rounds, g->ws.trace_cap);
   volatile unsigned long long* src = g->ws.trace_host;
   std::vector<unsigned long long> wt(r * 4ull, 0);

@@ -1326,11 +1326,19 @@ __device__ __forceinline__ void trace_round(const TravArgs& a, uint32_t r, int s
 // Per-warp phase completion: wtrace[r*4 + 2*phase] = latest, [+1] = earliest
 // (stored as kTBig - t so both are maxima).
 constexpr unsigned long long kTBig = 1ull << 62;
+#ifdef TGXD_WTRACE_ALL
+// diagnostics build: every warp's completion time of rounds < 16 (api.cu
+// dumps it to TGXD_WTRACE_ALL_FILE; tools/warp_spread.py)
+__device__ unsigned long long g_wdone[16][2][148 * TGXD_MIN_BLOCKS * kWarps];
+#endif
 __device__ __forceinline__ void trace_warp_done(const TravArgs& a, uint32_t r, int phase) {
   if (a.wtrace && a.wtrace_on && r < a.trace_cap && lane_id() == 0) {
     const unsigned long long t = gtimer();
     atomicMax(a.wtrace + r * 4 + 2 * phase, t);
     atomicMax(a.wtrace + r * 4 + 2 * phase + 1, kTBig - t);
+#ifdef TGXD_WTRACE_ALL
+    if (r < 16) g_wdone[r][phase][blockIdx.x * kWarps + (threadIdx.x >> 5)] = t;
+#endif
   }
 }
 
