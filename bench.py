@@ -132,6 +132,21 @@ def profile_traffic():
     return None
 
 
+RANDOM_LINE_GBS = 4830.0  # profiles/r02k/micro_gather_ncu.txt: 9.52 GB in 1.97 ms
+
+
+def random_line_roofline(kernel_ms):
+    traffic = profile_traffic()
+    if not traffic:
+        return None
+    achieved = traffic / (kernel_ms * 1e-3) / 1e9
+    return {"bound": "random 128-byte DRAM lines", "traffic_per_launch": traffic,
+            "achieved": achieved, "peak": RANDOM_LINE_GBS, "unit": "GB/s",
+            "frac": achieved / RANDOM_LINE_GBS,
+            "note": "traffic from the committed ncu capture of the same rotation; the kernel "
+                    "time includes the tail engine, so this understates the round kernel's rate"}
+
+
 def bench_config(wl, queries, n, m, work):
     """The `config` object both arms print (identical keys and values)."""
     return {"workload": f"{CONFIG}: {wl.describe}",
@@ -263,6 +278,9 @@ def run_ours(args):
         dist = dist_mod
         red_dev = "cpu" if shared else "cuda"
 
+    if world > 1 and "TGXD_HOST_THREADS" not in os.environ:
+        # replicas on one node share the host: split the widening threads
+        os.environ["TGXD_HOST_THREADS"] = str(max(2, ((os.cpu_count() or 8) - 4) // world))
     lib = T.load_library()
     wl = workload(CONFIG)
     g = T.TemporalGraph.generate(wl.gen, True, T.EngineConfig(index_cutoff=wl.index_cutoff))
@@ -348,6 +366,11 @@ def run_ours(args):
                      "timed": "CUDA events on the graph stream around the traversal kernels",
                      "algorithmic_bytes_per_step": b_steps / args.steps,
                      "algorithmic_bytes_per_query": b_alg, "peak_kind": peak_kind},
+        # what the kernel actually moves: DRAM line traffic (ncu, profiles/traffic.json,
+        # traverse_kernel only) over its time, against the random-line ceiling of
+        # this GPU (tools/micro_gather.cu: random reads cost 128-byte lines and
+        # saturate at 4.8 TB/s, profiles/r02k) — DESIGN.md §7
+        "memory_system": random_line_roofline(kernel_ms),
         "e2e": {"value": e2e_value, "unit": "edges/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "host_buffer": "pageable", "ms_per_step": e2e_s * 1e3,
