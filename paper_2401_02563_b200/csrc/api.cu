@@ -1097,6 +1097,10 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
     a.copy_flag = in_kernel ? G->copy_flag_dev : nullptr;
     a.log_f = log_f;
     a.fresh = slots < (1ull << 31) && !getenv("TGXD_NO_FRESH") ? 0x80000000u : 0u;
+#ifdef TGXD_EXPERIMENTS
+    const char* xs = getenv("TGXD_X_STOP_A");
+    a.x_stop_a = xs ? (uint32_t)atoi(xs) : 0xffffffffu;
+#endif
     a.p24 = early && w.p24_req ? w.p24.as<uint32_t>() : nullptr;
     a.p24_neg = P.kind == TGXD_LATEST_DEPARTURE ? 1 : 0;
     a.chg = early ? w.chg.as<uint32_t>() : nullptr;
@@ -2359,6 +2363,66 @@ int tgxd_last_d2h_bytes(tgxd_graph* g, uint64_t* bytes) {
   *bytes = g->ws.last_d2h;
   return TGXD_OK;
 }
+
+#ifdef TGXD_EXPERIMENTS
+// Experiment (tools/x_relax.py): runs an EA query whose round kernel stops
+// before round `round`'s relax (TGXD_X_STOP_A), then times that relax as
+// relax_only_kernel with `upw` units per warp. out: {ms, chunks, smalls, push}.
+extern "C" int tgxd_x_relax(tgxd_graph* G, uint32_t src, uint32_t round, uint32_t upw,
+                            double* out) {
+  std::lock_guard<std::mutex> lock(G->mu);
+  TGXD_CUDA(cudaSetDevice(G->device));
+  const uint64_t ta = 0, tb = 999999;
+  Prepared P;
+  int rc = prepare(G, TGXD_EARLIEST_ARRIVAL, 1, &src, &ta, &tb, 1, P);
+  if (rc) return rc;
+  if ((rc = ensure_workspace(G, 1, false))) return rc;
+  setenv("TGXD_X_STOP_A", std::to_string(round).c_str(), 1);
+  setenv("TGXD_HANDOFF_F", "0", 1);
+  setenv("TGXD_ASYNC_F", "0", 1);
+  rc = launch(G, P, TGXD_MODE_AUTO, nullptr, 4, nullptr, nullptr);
+  unsetenv("TGXD_X_STOP_A");
+  unsetenv("TGXD_HANDOFF_F");
+  unsetenv("TGXD_ASYNC_F");
+  if (rc) return rc;
+  Workspace& w = G->ws;
+  Control c;
+  TGXD_CUDA(cudaMemcpyAsync(&c, w.ctl.p, sizeof c, cudaMemcpyDeviceToHost, G->stream));
+  TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  const unsigned long long nch = c.state[0], nsm = c.state[1], pstart = c.state[2];
+  const int flip = (int)c.state[3], push = (int)c.state[4];
+  TravArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.g = G->out;
+  a.qp = w.params.as<QueryParam>();
+  a.X = w.X.as<int32_t>();
+  a.EP = w.EP.as<int2>();
+  a.chunks = w.chunks.as<uint2>();
+  a.smalls = w.smalls.as<uint2>();
+  a.ctl = w.ctl.as<Control>();
+  a.n = G->n;
+  a.Q = 1;
+  a.strict = P.strict;
+  a.fresh = 0x80000000u;
+  const unsigned long long units = nch + (nsm + 31) / 32;
+  const unsigned long long warps = (units + upw - 1) / upw;
+  const unsigned blocks = (unsigned)std::max<unsigned long long>(1, (warps + kWarps - 1) / kWarps);
+  uint32_t* fout = flip ? w.fa.as<uint32_t>() : w.fb.as<uint32_t>();
+  TGXD_CUDA(cudaEventRecord(w.ev[0], G->stream));
+  relax_only_kernel<<<blocks, kThreads, 0, G->stream>>>(a, nch, nsm, pstart, fout, push, upw);
+  TGXD_CUDA(cudaEventRecord(w.ev[1], G->stream));
+  TGXD_CUDA(cudaStreamSynchronize(G->stream));
+  TGXD_CUDA(cudaGetLastError());
+  float ms = 0;
+  TGXD_CUDA(cudaEventElapsedTime(&ms, w.ev[0], w.ev[1]));
+  out[0] = ms;
+  out[1] = (double)nch;
+  out[2] = (double)nsm;
+  out[3] = push;
+  w.xinv = false;  // the labels are a partial traversal's: the next query initializes
+  return TGXD_OK;
+}
+#endif
 
 int tgxd_launch_count(tgxd_graph* g, uint64_t* count) {
   if (!g || !count) return fail(TGXD_ERR_ARGUMENT, "null argument");

@@ -137,6 +137,9 @@ struct TravArgs {
   // them carry this bit (0: not used, slots >= 2^31): their expansion state
   // is the initial one, so the expansion skips its load
   uint32_t fresh;
+#ifdef TGXD_EXPERIMENTS
+  uint32_t x_stop_a;     // experiment: stop before this round's relax (api.cu tgxd_x_relax)
+#endif
   unsigned long long init_pushes;  // queue position / improvements after seeding
 };
 
@@ -1724,6 +1727,20 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       const unsigned long long w = (e_end - st.e_cur) + xcnt;
       const bool push = a.mode == TGXD_MODE_SPARSE ||
                         (a.mode == TGXD_MODE_AUTO && w <= a.push_w);
+#ifdef TGXD_EXPERIMENTS
+      if (st.rounds == a.x_stop_a) {  // experiment: leave this round's relax to relax_only_kernel
+        if (tr) {
+          ctl->state[0] = c_end - st.c_cur;
+          ctl->state[1] = s_end - st.s_cur;
+          ctl->state[2] = p_now;
+          ctl->state[3] = st.flip;
+          ctl->state[4] = push;
+          ctl->state[5] = st.c_cur;
+          ctl->state[6] = st.s_cur;
+        }
+        break;
+      }
+#endif
       RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
       rx.log = st.logging;
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, xlo, xcnt, rx, blockIdx.x, gridDim.x, wbuf);
@@ -1776,6 +1793,46 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
     ctl->candidates = n_cand;
   }
 }
+
+#ifdef TGXD_EXPERIMENTS
+#ifndef TGXD_X_BLOCKS
+#define TGXD_X_BLOCKS 8
+#endif
+// Experiment: one round's relax as a non-persistent kernel (own register
+// budget and occupancy, the hardware block scheduler balancing the units):
+// units of `upw` per warp, chunks then windows, push rule as phase_b.
+__global__ void __launch_bounds__(kThreads, TGXD_X_BLOCKS)
+    relax_only_kernel(TravArgs a, unsigned long long nchunks, unsigned long long nsmall,
+                      unsigned long long pstart, uint32_t* fout, int push, uint32_t upw) {
+  __shared__ uint32_t s_buf[kWarps][64];
+  const uint32_t lane = lane_id();
+  const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  PushBuf pb{s_buf[threadIdx.x >> 5], 0};
+  RelaxCtx rx{a.qp[0].vhi, 0, push != 0, pstart, fout, policy_evict_first(), policy_evict_last(),
+              0, 1};
+  const unsigned long long nwin = (nsmall + 31) / 32;
+  for (unsigned long long u = gw * upw; u < (gw + 1) * upw && u < nchunks + nwin; ++u) {
+    if (u < nchunks) {
+      const uint2 ch = __ldcg(a.chunks + u);
+      const uint32_t len = ch.y & ((1u << kChunkLenBits) - 1);
+      uint32_t e[kUnroll], q[kUnroll];
+      bool act[kUnroll];
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        const uint32_t off = k * 32 + lane;
+        act[k] = off < len;
+        e[k] = ch.x + off;
+        q[k] = ch.y >> kChunkLenBits;
+      }
+      relax_steps(a, e, q, act, rx, pb);
+    } else {
+      const unsigned long long i = (u - nchunks) * 32 + lane;
+      relax_window(a, i < nsmall ? __ldcg(a.smalls + i) : make_uint2(0u, 0u), rx, pb);
+    }
+  }
+  if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
+}
+#endif
 
 // 24-bit packing when the copy starts after the round kernel (api.cu; it
 // runs beside the tail engine).
