@@ -168,9 +168,21 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
   int end_bit = 32;
   while (end_bit < 64 && (1ULL << (end_bit - 32)) < (uint64_t)n) ++end_bit;
   if (end_bit == 32) end_bit = 33;
+  // without weights the sort moves the payloads (keys + 8-byte values; no
+  // random gathers after it: config 2's two gathers took 4.5 ms each); with
+  // weights it moves edge indices, which also order the weights
+  const bool kv = d_w == nullptr && !getenv("TGXD_BUILD_GATHER");
+  DeviceBuffer vals_a;
+  unsigned long long* va = kv ? dalloc<unsigned long long>(vals_a, std::max<uint64_t>(m, 1)) : nullptr;
+  if (kv && !va) return fail(TGXD_ERR_CUDA, "device allocation failed while building the graph");
   size_t temp_bytes = 0, scan_bytes = 0;
-  TGXD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
-                                            end_bit, s));
+  if (kv) {
+    TGXD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, ka, kb, va, va, (int64_t)m, 0,
+                                              end_bit, s));
+  } else {
+    TGXD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
+                                              end_bit, s));
+  }
   TGXD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, dc, dc, (int64_t)n + 1, s));
   if (temp.ensure(std::max(temp_bytes, scan_bytes) + 16) != cudaSuccess)
     return fail(TGXD_ERR_CUDA, "device allocation failed (sort scratch)");
@@ -196,10 +208,18 @@ static int build_layouts(tgxd_graph* G, const uint32_t* d_src, const uint32_t* d
     if (!off || !key || !pay || !fence || !kmax || !okm)
       return fail(TGXD_ERR_CUDA, "device allocation failed (T-CSR arrays)");
     if (m) {
-      make_sort_keys<<<gb, 256, 0, s>>>(owner, kk, dir, m, ka, ia);
-      TGXD_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, ka, kb, ia, ib, (int64_t)m, 0,
-                                                end_bit, s));
-      gather_layout<<<gb, 256, 0, s>>>(ib, other, kk, vv, dir, m, key, pay);
+      if (kv) {
+        make_sort_kv<<<gb, 256, 0, s>>>(owner, other, kk, vv, dir, m, ka, va);
+        TGXD_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, ka, kb, va,
+                                                  reinterpret_cast<unsigned long long*>(pay),
+                                                  (int64_t)m, 0, end_bit, s));
+        keys_from_sorted<<<gb, 256, 0, s>>>(kb, m, key);
+      } else {
+        make_sort_keys<<<gb, 256, 0, s>>>(owner, kk, dir, m, ka, ia);
+        TGXD_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, ka, kb, ia, ib, (int64_t)m,
+                                                  0, end_bit, s));
+        gather_layout<<<gb, 256, 0, s>>>(ib, other, kk, vv, dir, m, key, pay);
+      }
       if (dir == 0 && d_w && out_w) gather_weights<<<gb, 256, 0, s>>>(ib, d_w, m, out_w);
       make_fences<<<grid_for(nf, G->sm_count), 256, 0, s>>>(key, m, fence);
     }
@@ -2001,56 +2021,90 @@ int tgxd_graph_build_weighted(uint32_t n, uint64_t m, const uint32_t* src, const
   if (!out) return fail(TGXD_ERR_ARGUMENT, "null out");
   *out = nullptr;
   if (m && (!src || !dst || !start || !end)) return fail(TGXD_ERR_ARGUMENT, "null edge arrays");
+  // Host passes over the m input edges run on up to 16 threads (config 5:
+  // 268M edges; one thread took seconds per pass).
+  const unsigned nthreads = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>({16, std::max(1u, std::thread::hardware_concurrency()), m / 65536 + 1}));
+  auto par = [&](auto&& fn) {  // fn(t, lo, hi) over nthreads contiguous ranges
+    std::vector<std::thread> th;
+    const uint64_t per = (m + nthreads - 1) / nthreads;
+    for (unsigned t = 0; t < nthreads; ++t)
+      th.emplace_back([&, t] { fn(t, std::min<uint64_t>(m, t * per), std::min<uint64_t>(m, (t + 1) * per)); });
+    for (auto& x : th) x.join();
+  };
   // compute_meta (types.cpp:29-54): first offending edge, reference wording.
-  for (uint64_t i = 0; i < m; ++i) {
-    if (src[i] >= n || dst[i] >= n)
-      return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": endpoint (" +
-                                     std::to_string(src[i]) + " -> " + std::to_string(dst[i]) +
-                                     ") outside vertex range [0, " + std::to_string(n) + ")");
-    if (end[i] < start[i])
-      return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": end " + std::to_string(end[i]) +
-                                     " precedes start " + std::to_string(start[i]));
-    if (end[i] > kTimeLimit63)
+  {
+    std::vector<uint64_t> bad(nthreads, UINT64_MAX), far(nthreads, UINT64_MAX);
+    par([&](unsigned t, uint64_t lo, uint64_t hi) {
+      for (uint64_t i = lo; i < hi; ++i)
+        if (src[i] >= n || dst[i] >= n || end[i] < start[i] || end[i] > kTimeLimit63) {
+          bad[t] = i;
+          break;
+        }
+      for (uint64_t i = lo; i < hi; ++i)
+        if (end[i] > (uint64_t)kTimeMax) {
+          far[t] = i;
+          break;
+        }
+    });
+    const uint64_t i = *std::min_element(bad.begin(), bad.end());
+    if (i != UINT64_MAX) {
+      if (src[i] >= n || dst[i] >= n)
+        return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": endpoint (" +
+                                       std::to_string(src[i]) + " -> " + std::to_string(dst[i]) +
+                                       ") outside vertex range [0, " + std::to_string(n) + ")");
+      if (end[i] < start[i])
+        return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": end " +
+                                       std::to_string(end[i]) + " precedes start " +
+                                       std::to_string(start[i]));
       return fail(TGXD_ERR_EDGE, "edge " + std::to_string(i) + ": end " + std::to_string(end[i]) +
                                      " beyond the supported time range (2^63 - 1)");
-  }
-  for (uint64_t i = 0; i < m; ++i) {
-    if (end[i] > (uint64_t)kTimeMax)
-      return fail(TGXD_ERR_TIME_RANGE, "edge " + std::to_string(i) + ": end " +
-                                           std::to_string(end[i]) +
+    }
+    const uint64_t j = *std::min_element(far.begin(), far.end());
+    if (j != UINT64_MAX)
+      return fail(TGXD_ERR_TIME_RANGE, "edge " + std::to_string(j) + ": end " +
+                                           std::to_string(end[j]) +
                                            " outside the device time domain [0, 2^31 - 2]");
   }
-  uint64_t mm = m;
+  // undirected graphs add the reverse of every non-loop edge (engine.cpp:13-22),
+  // in input order after the originals: per-thread counts give each range's slot
+  std::vector<uint64_t> extra(nthreads + 1, 0);
   if (!directed)
-    for (uint64_t i = 0; i < m; ++i) mm += src[i] != dst[i];
+    par([&](unsigned t, uint64_t lo, uint64_t hi) {
+      uint64_t c = 0;
+      for (uint64_t i = lo; i < hi; ++i) c += src[i] != dst[i];
+      extra[t + 1] = c;
+    });
+  for (unsigned t = 0; t < nthreads; ++t) extra[t + 1] += extra[t];
+  const uint64_t mm = m + extra[nthreads];
   if (mm >= 0xffffffffULL) return fail(TGXD_ERR_ARGUMENT, "edge count must stay below 2^32");
-  std::vector<uint32_t> hs(src, src + m), hd(dst, dst + m);
-  std::vector<int32_t> hst(m), hen(m);
-  for (uint64_t i = 0; i < m; ++i) {
-    hst[i] = (int32_t)start[i];
-    hen[i] = (int32_t)end[i];
-  }
+  std::vector<uint32_t> hs(mm), hd(mm);
+  std::vector<int32_t> hst(mm), hen(mm);
   // weights as int64 codes: the value when a non-negative integer below 2^62,
   // -1 when not a non-negative integer (duration_metric's invalid_argument,
   // raised only if a query reaches the edge), -2 when too large
-  std::vector<long long> hw;
-  if (weight) {
-    hw.resize(m);
-    for (uint64_t i = 0; i < m; ++i) {
-      const double x = weight[i], r = std::nearbyint(x);
-      hw[i] = (x < 0.0 || r != x) ? -1ll : (r >= 4611686018427387904.0 ? -2ll : (long long)r);
+  std::vector<long long> hw(weight ? mm : 0);
+  par([&](unsigned t, uint64_t lo, uint64_t hi) {
+    uint64_t k = m + extra[t];
+    for (uint64_t i = lo; i < hi; ++i) {
+      hs[i] = src[i];
+      hd[i] = dst[i];
+      hst[i] = (int32_t)start[i];
+      hen[i] = (int32_t)end[i];
+      if (weight) {
+        const double x = weight[i], r = std::nearbyint(x);
+        hw[i] = (x < 0.0 || r != x) ? -1ll : (r >= 4611686018427387904.0 ? -2ll : (long long)r);
+      }
+      if (!directed && src[i] != dst[i]) {
+        hs[k] = dst[i];
+        hd[k] = src[i];
+        hst[k] = hst[i];
+        hen[k] = hen[i];
+        if (weight) hw[k] = hw[i];
+        ++k;
+      }
     }
-  }
-  if (!directed) {  // engine.cpp:13-22
-    for (uint64_t i = 0; i < m; ++i) {
-      if (src[i] == dst[i]) continue;
-      hs.push_back(dst[i]);
-      hd.push_back(src[i]);
-      hst.push_back((int32_t)start[i]);
-      hen.push_back((int32_t)end[i]);
-      if (weight) hw.push_back(hw[i]);
-    }
-  }
+  });
   tgxd_graph* G = nullptr;
   int rc = new_graph(n, index_cutoff, directed, &G);
   if (rc) return rc;

@@ -82,6 +82,27 @@ __global__ void make_sort_keys(const uint32_t* owner, const int32_t* kk, int neg
   }
 }
 
+// Sort keys and their payloads {other, val} as one 64-bit value (the sort
+// moves the payload: no random gathers afterwards; used without weights).
+__global__ void make_sort_kv(const uint32_t* owner, const uint32_t* other, const int32_t* kk,
+                             const int32_t* vv, int negate, uint64_t m, unsigned long long* keys,
+                             unsigned long long* vals) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int32_t k = negate ? -kk[i] : kk[i];
+    keys[i] = ((unsigned long long)owner[i] << 32) | key_bits(k);
+    const uint32_t v = (uint32_t)(negate ? -vv[i] : vv[i]);
+    vals[i] = ((unsigned long long)v << 32) | other[i];  // = uint2 {other, val}
+  }
+}
+
+// The layout's keys from the sorted sort keys.
+__global__ void keys_from_sorted(const unsigned long long* keys, uint64_t m, int32_t* key) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride)
+    key[j] = (int32_t)((uint32_t)keys[j] ^ 0x80000000u);
+}
+
 __global__ void gather_layout(const uint32_t* idx, const uint32_t* other, const int32_t* kk,
                               const int32_t* vv, int negate, uint64_t m, int32_t* key,
                               uint2* pay) {
