@@ -375,8 +375,14 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "host_buffer": "pageable", "ms_per_step": e2e_s * 1e3,
                 "call": "tgxd_earliest_arrival (int64 PathResult values in host memory)"},
+        # BASELINE config 2 as defined (its one seeded source, repeated): TEPS and the
+        # HBM roofline of north_star's target on it
         "single_source": {"source": srcs[0], "ms_per_step": tot1 / args.steps,
-                          "kernel_ms": ker1, "value": work[0][0] / (tot1 / args.steps * 1e-3)},
+                          "kernel_ms": ker1, "value": work[0][0] / (tot1 / args.steps * 1e-3),
+                          "roofline": {"bound": "hbm", "achieved": b_alg[0] / (ker1 * 1e-3) / 1e9,
+                                       "peak": peak, "unit": "GB/s",
+                                       "frac": b_alg[0] / (ker1 * 1e-3) / 1e9 / peak,
+                                       "algorithmic_bytes": b_alg[0]}},
         "gpu_launches": round(launches),
         "kernels_per_step": kernels,
         "clocks": sampler.summary(),
