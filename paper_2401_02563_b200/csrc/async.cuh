@@ -235,6 +235,11 @@ __device__ __forceinline__ void relax_async(const AsyncArgs& a, const uint32_t (
     if (imp[u] && a.R) atomicMin(a.R + idx[u], v[u] - rx.depart);
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) vb_append(a, vb, was[u] == 0u, idx[u]);
+#if TGXD_PF_ASYNC
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (was[u] == 0u) prefetch_expansion<TGXD_PF_ASYNC>(a.g.okm, a.g.key, a.g.pay, idx[u] - q[u] * a.n);
+#endif
 }
 
 // Relax ranges given one per lane (lo, cnt, q), packed 32 per warp: range l
@@ -317,8 +322,15 @@ __device__ __forceinline__ void expand_batch(const AsyncArgs& a, bool valid, uin
     // label, bounds and the segment's extent all issued together
     const int32_t x = xq_label(atomicAnd(a.XQ + item, ~1ull));
     const int2 ep = __ldcg(a.EP + item);
+#if TGXD_OKM_ENGINES
+    // segment bounds and last key from one {off, kmax} line
+    const uint2 ok = __ldg(a.g.okm + v);
+    const uint32_t s = ok.x, t = __ldg(&a.g.okm[v + 1].x);
+    const int32_t km = (int32_t)ok.y;
+#else
     const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
     const int32_t km = __ldg(a.g.kmax + v);  // no key at or above lb: nothing to do
+#endif
     const QueryParam& qp = a.qp[q];
     // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342)
     int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);

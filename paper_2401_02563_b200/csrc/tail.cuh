@@ -142,6 +142,11 @@ __device__ __forceinline__ void tail_relax(const TailArgs& a, const bool (&act)[
       if (push[u]) fout[base + __popc(pm[u] & below)] = d[u];
       base += __popc(pm[u]);
     }
+#if TGXD_PF_TAIL
+#pragma unroll
+    for (int u = 0; u < kTailU; ++u)
+      if (push[u]) prefetch_expansion<TGXD_PF_TAIL>(a.g.okm, a.g.key, a.g.pay, pl[u].x);
+#endif
   }
   if (a.chg) {  // early host copy: every lowered slot is listed
     uint32_t im[kTailU], itot = 0;
@@ -230,8 +235,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailArgs a) {
         const uint32_t v = item - q * a.n;
         const int32_t x = ld_state(a.X + item, pol_keep);
         const int2 ep = __ldcg(a.EP + item);
+#if TGXD_OKM_ENGINES
+        // segment bounds and last key from one {off, kmax} line
+        const uint2 ok = __ldg(a.g.okm + v);
+        const uint32_t s = ok.x, t = __ldg(&a.g.okm[v + 1].x);
+        const int32_t km = (int32_t)ok.y;
+#else
         const uint32_t s = __ldg(a.g.off + v), t = __ldg(a.g.off + v + 1);
         const int32_t km = __ldg(a.g.kmax + v);
+#endif
         const QueryParam& qp = a.qp[q];
         // min_start / max_end hooks (path_algorithms.cpp:287-291, :337-342)
         int32_t lb = (v == qp.root) ? qp.klo : bound_of(x, a.strict);

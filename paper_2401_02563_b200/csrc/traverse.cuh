@@ -189,6 +189,52 @@ __device__ __forceinline__ int32_t ld_state(const int32_t* p, uint64_t pol) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Expansion prefetch at push time: a slot queued for expansion has the
+// {off, kmax} line its expansion starts from pulled into L2 by its pusher
+// (level 1, fire and forget), or the pusher reads the segment bounds and
+// prefetches the first key and payload lines of a short segment (level 2:
+// one DRAM latency for the pushing warp, up to three fewer for the
+// expansion). Measured (tools/runs/p1.sh, p2.sh; ms): level 1 in the async
+// engine — config 1 0.482 -> 0.461, everything else unchanged — is on;
+// level 1 in thin grid rounds (config 2 rotation 1.070 -> 1.075), in the
+// cluster tail (neutral) and level 2 anywhere (rotation 1.103, config 1
+// 0.49) are off. The engines' expansions read {off, kmax} from the
+// interleaved okm line (TGXD_OKM_ENGINES; config 1 -1 %).
+#ifndef TGXD_PF_GRID
+#define TGXD_PF_GRID 0
+#endif
+#ifndef TGXD_PF_TAIL
+#define TGXD_PF_TAIL 0
+#endif
+#ifndef TGXD_PF_ASYNC
+#define TGXD_PF_ASYNC 1
+#endif
+#ifndef TGXD_OKM_ENGINES
+#define TGXD_OKM_ENGINES 1
+#endif
+#ifndef TGXD_PF_MAXW
+#define TGXD_PF_MAXW (1u << 18)
+#endif
+constexpr unsigned long long kPfMaxW = TGXD_PF_MAXW;  // a round relaxing more is not latency-bound
+__device__ __forceinline__ void pf_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+template <int kLevel>
+__device__ __forceinline__ void prefetch_expansion(const uint2* okm, const int32_t* key,
+                                                   const uint2* pay, uint32_t v) {
+  if (kLevel >= 2) {
+    const uint32_t s = __ldg(&okm[v].x), t = __ldg(&okm[v + 1].x);
+    if (t > s && t - s <= 32) {
+      pf_l2(key + s);
+      if (((s ^ (t - 1)) >> 5) != 0) pf_l2(key + t - 1);
+      pf_l2(pay + s);
+      if (((s ^ (t - 1)) >> 4) != 0) pf_l2(pay + t - 1);
+    }
+  } else if (kLevel == 1) {
+    pf_l2(okm + v);
+  }
+}
+
 // Debug builds (-DTGXD_CHECK): every queue / work-list store is checked
 // against its allocation; a violation is recorded (and the store skipped)
 // and reported by the host as an internal error.
@@ -253,6 +299,7 @@ struct RelaxCtx {
   uint32_t improved;         // per-lane improvement count (no-push rounds)
   int32_t hop;               // temporal BFS: this round's number (1-based)
   bool log = false;          // list every lowered slot (the host copy has started)
+  bool pf = false;           // prefetch pushed slots' expansion lines (thin rounds)
 };
 
 // 24-bit packing of key-space labels for the early host copy (api.cu): 4
@@ -406,6 +453,13 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
         if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
       }
     }
+#if TGXD_PF_GRID
+    if (rx.pf) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (p[u]) prefetch_expansion<TGXD_PF_GRID>(a.g.okm, a.g.key, a.g.pay, pl[u].x);
+    }
+#endif
   }
 }
 
@@ -1372,6 +1426,7 @@ __device__ TGXD_PHASE void local_rounds(const TravArgs& a, TState& st, uint32_t 
     uint32_t* fout = st.flip ? a.fa : a.fb;
     RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
     rx.log = st.logging;
+    rx.pf = TGXD_PF_GRID != 0;
     if (seed) {
       if (tr) {
         trace_round(a, st.rounds, 0, gtimer());
@@ -1641,6 +1696,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
         uint32_t* fout = st.flip ? a.fa : a.fb;
         RelaxCtx rx{vhi0, depart, true, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
         rx.log = st.logging;
+        rx.pf = TGXD_PF_GRID != 0 && e_end - st.e_cur <= kPfMaxW;
         phase_b(a, c_end - st.c_cur, s_end - st.s_cur, 0, 0, rx, blockIdx.x, gridDim.x, wbuf);
         trace_warp_done(a, st.rounds, 1);
         grid.sync();
@@ -1743,6 +1799,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
 #endif
       RelaxCtx rx{vhi0, depart, push, p_now, fout, pol_stream, pol_keep, 0, (int32_t)st.rounds + 1};
       rx.log = st.logging;
+      rx.pf = TGXD_PF_GRID != 0 && push && w <= kPfMaxW;
       phase_b(a, c_end - st.c_cur, s_end - st.s_cur, xlo, xcnt, rx, blockIdx.x, gridDim.x, wbuf);
       if (!push) {  // improvements only feed the dense frontier's size
         uint32_t imp = rx.improved;
