@@ -1044,6 +1044,8 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
   // slot count; expand densely only when the queue holds half the slots
   // (measured on config 2: the queue-driven expand is cheaper below that).
   a.dense_f = std::max<uint64_t>(1024, slots / 2);
+  if (const char* dd = getenv("TGXD_DENSE_DIV"))  // experiments: dense expand above slots / div
+    a.dense_f = std::max<uint64_t>(1024, slots / (uint64_t)std::max(1, atoi(dd)));
   a.push_w = std::max<uint64_t>(4096, slots * 4);
   // a frontier holding half the slots is pulled (direction switch; a quarter
   // for fastest sweeps). Measured over config 2's 8-source rotation: pulling
