@@ -7,7 +7,10 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum",
         "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum",
         "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
-        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "smsp__inst_executed.sum"]
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "smsp__inst_executed.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors_op_atom.sum",
+        "lts__t_sectors_op_red.sum"]
 STALL = re.compile(r"smsp__pcsamp_warps_issue_stalled_(\w+)$")
 
 
@@ -55,6 +58,10 @@ for k in ks:
               f"  L2 req {req / 1e6:6.2f} M ({req / max(t, 1e-9) / 1e3:6.1f} G/s)"
               f"  L2 rd sectors {rd / 1e6:6.2f} M hit {100 * hit / max(rd, 1):4.1f}%"
               f"  atom {dm.get('lts__t_requests_srcunit_tex_op_atom_dot_alu.sum', 0) / 1e6:5.2f} M"
+              f"  L1 ld sectors {dm.get('l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum', 0) / 1e6:6.2f} M"
+              f" hit {100 * dm.get('l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum', 0) / max(dm.get('l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum', 0), 1):4.1f}%"
+              f"  smem wavefronts {dm.get('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum', 0) / 1e6:6.2f} M"
+              f"  L2 atom+red sectors {(dm.get('lts__t_sectors_op_atom.sum', 0) + dm.get('lts__t_sectors_op_red.sum', 0)) / 1e6:5.2f} M"
               f"  stalls " + ", ".join(f"{n} {100 * x / tot:.0f}%" for n, x in top))
     else:
         print(f"rounds 0..{k}: {m['gpu__time_duration.sum'] / 1e3:.1f} us")
