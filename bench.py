@@ -435,14 +435,52 @@ def concurrent_rotation(T, g, srcs, wins, work, steps, barrier, streams=4):
     all_streams(0, per)
     barrier()
     dt = time.perf_counter() - t0
+
+    # the same through the C-ABI call with int64 results in host memory (one
+    # caller thread and one host array per view; the views split the host
+    # widening threads)
+    import ctypes
+    lib = T.load_library()
+    n = g.vertex_count()
+    outs = [np.empty(n, np.int64) for _ in range(streams)]
+
+    def run_e2e(si, n_steps):
+        try:
+            optr = outs[si].ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            for j in range(n_steps):
+                i = (si + streams * j) % k
+                T._check(lib.tgxd_earliest_arrival(views[si].handle, srcs[i], wins[i].t_a,
+                                                   wins[i].t_b, 1, optr, None))
+        except Exception as e:  # surfaced below
+            err.append(e)
+
+    def all_e2e(n_steps):
+        th = [threading.Thread(target=run_e2e, args=(si, n_steps)) for si in range(streams)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    per_e = max(1, per // 2)
+    all_e2e(2)
+    barrier()
+    t1 = time.perf_counter()
+    all_e2e(per_e)
+    barrier()
+    dte = time.perf_counter() - t1
     for v in views:
         v.close()
     if err:
         return {"error": str(err[0])}
     edges = sum(work[(si + streams * j) % k][0] for si in range(streams) for j in range(per))
+    edges_e = sum(work[(si + streams * j) % k][0] for si in range(streams) for j in range(per_e))
     return {"streams": streams, "queries": streams * per, "ms_per_query": dt * 1e3 / (streams * per),
             "value": edges / dt, "unit": "edges/s",
-            "timed": "host clock between device synchronisations around all streams"}
+            "timed": "host clock between device synchronisations around all streams",
+            "e2e": {"value": edges_e / dte, "unit": "edges/s", "queries": streams * per_e,
+                    "ms_per_query": dte * 1e3 / (streams * per_e),
+                    "call": "tgxd_earliest_arrival on each view from its own host thread "
+                            "(int64 PathResult values in host memory)"}}
 
 
 def cpu_baseline(wl, queries, n, work):
