@@ -2628,6 +2628,16 @@ int tgxd_set_trace(tgxd_graph* g, uint32_t max_rounds) {
 // extremes (device memory; copied only when `with_device` is set).
 int tgxd_get_trace(tgxd_graph* g, uint64_t* out, uint32_t max_rounds, int with_device) {
   if (!g || !out) return fail(TGXD_ERR_ARGUMENT, "null argument");
+#ifdef TGXD_CHAIN
+  if (const char* path = getenv("TGXD_CHAIN_FILE")) {  // diagnostics: block 0 / warp 0 chain marks
+    std::vector<unsigned long long> all(sizeof(g_chain) / 8);
+    TGXD_CUDA(cudaMemcpyFromSymbol(all.data(), g_chain, sizeof(g_chain)));
+    if (FILE* f = fopen(path, "wb")) {
+      fwrite(all.data(), 8, all.size(), f);
+      fclose(f);
+    }
+  }
+#endif
 #ifdef TGXD_WTRACE_ALL
   if (const char* path = getenv("TGXD_WTRACE_ALL_FILE")) {  // diagnostics: every warp's times
     std::vector<unsigned long long> all(sizeof(g_wdone) / 8);

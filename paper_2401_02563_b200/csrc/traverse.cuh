@@ -149,6 +149,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+#ifdef TGXD_CHAIN
+// diagnostics build: timestamps along the dependent chain of block 0 / warp 0
+// in the rounds' phases (api.cu dumps them to TGXD_CHAIN_FILE; tools/chain_trace.py)
+__device__ unsigned long long g_chain[64][16];
+__device__ unsigned int g_chain_round;
+__device__ __forceinline__ void chain_mark(int k, unsigned int consume = 0) {
+  __shared__ volatile unsigned int s_sink;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s_sink = consume;  // issues once `consume` is available
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
+    if (g_chain_round < 64) g_chain[g_chain_round][k] = t;
+  }
+}
+#define TGXD_MARK(k, v) chain_mark(k, (unsigned int)(v))
+#else
+#define TGXD_MARK(k, v)
+#endif
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -720,6 +739,7 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
   const uint32_t total = fin ? F : a.Q * a.n;
   ExpandBufs eb{{ebuf, 0}, {ebuf + kListCap, 0}, cstart, sstart};
   unsigned long long work = 0;
+  TGXD_MARK(0, 0);
   for (uint32_t base = gw * 32; base < total; base += nw * 32) {
     const uint32_t i = base + lane;
     bool valid = i < total;
@@ -749,11 +769,18 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
       t0 = __ldg(&a.g.okm[v + 1].x);
       valid = x != kInf;
     }
+    if (base == gw * 32) {
+      TGXD_MARK(1, item);
+      TGXD_MARK(2, x + ep.x + s0 + t0 + km0);
+    }
     expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix, depart);
+    if (base == gw * 32) TGXD_MARK(3, eb.sm.n + eb.ch.n + (uint32_t)work);
   }
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
+  TGXD_MARK(4, eb.sm.n);
   flush_work(a.ctl, work);
+  TGXD_MARK(5, 0);
 }
 
 #ifdef TGXD_TMA_RELAX
@@ -954,13 +981,17 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
   const unsigned long long w0 =
       (gw >= nchunks ? gw : gw + (nchunks - gw + nw - 1) / nw * nw) - nchunks;
 #endif
+  TGXD_MARK(8, 0);
   uint2 sv = win_load(w0);
+  TGXD_MARK(9, sv.x + sv.y);
   for (unsigned long long w = w0; w < nwin; w += nw) {
     const uint2 snx = win_load(w + nw);  // next window prefetched
     relax_window(a, sv, rx, pb);
+    if (w == w0) TGXD_MARK(10, pb.n);
     sv = snx;
   }
   if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
+  TGXD_MARK(11, pb.n);
 }
 
 // ---------------------------------------------------------------------------
@@ -1766,11 +1797,16 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       }
       unsigned long long c_end = st.c_cur, s_end = st.s_cur, e_end = st.e_cur;
       if (!xcnt) {
+#ifdef TGXD_CHAIN
+        if (tr) g_chain_round = st.rounds;
+#endif
         phase_a(a, st.dense ? nullptr : fin, (uint32_t)F, st.c_cur, st.s_cur, blockIdx.x,
                 gridDim.x, pol_keep, ebuf, ix, depart);
         trace_warp_done(a, st.rounds, 0);
         grid.sync();
+        TGXD_MARK(6, 0);
         const Counters c0 = read_counters(ctl);
+        TGXD_MARK(7, c0.chunks);
         c_end = c0.chunks;
         s_end = c0.smalls;
         e_end = c0.edges;
@@ -1809,7 +1845,9 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       }
       trace_warp_done(a, st.rounds, 1);
       grid.sync();
+      TGXD_MARK(12, 0);
       const Counters c1 = read_counters(ctl);
+      TGXD_MARK(13, c1.pushes);
       st.p_known = c1.pushes;
       st.i_known = c1.improved;
       st.c_cur = c_end;

@@ -3,6 +3,7 @@
 // or two (lines homed in the SM's near L2 partition / in the other die's)?
 // build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/micro_l2_home tools/micro_l2_home.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 #include <algorithm>
@@ -15,7 +16,8 @@ __global__ void warm(const uint32_t* buf, size_t n, uint32_t* sink) {
   if (acc == 0x12345678u) *sink = acc;
 }
 
-__global__ void probe(const uint32_t* buf, size_t lines, uint32_t* lat, uint32_t* smid, int reps) {
+__global__ void probe(const uint32_t* buf, size_t lines, uint32_t* lat, uint32_t* smid, int reps,
+                      int fresh) {
   __shared__ volatile uint32_t sh[2];
   if (threadIdx.x != 0) return;
   uint32_t sm;
@@ -23,7 +25,7 @@ __global__ void probe(const uint32_t* buf, size_t lines, uint32_t* lat, uint32_t
   smid[blockIdx.x] = sm;
   uint32_t x = 12345u + blockIdx.x * 7919u;
   for (int pass = 0; pass < 2; ++pass) {  // pass 0 warms this lane's own path
-    uint32_t s = x;
+    uint32_t s = fresh && pass ? x ^ 0x9e3779b9u : x;  // fresh: the timed pass touches new lines (DRAM)
     for (int i = 0; i < reps; ++i) {
       s = s * 1664525u + 1013904223u;
       const size_t line = (size_t)(s >> 8) % lines;
@@ -38,8 +40,8 @@ __global__ void probe(const uint32_t* buf, size_t lines, uint32_t* lat, uint32_t
   }
 }
 
-int main() {
-  const size_t bytes = 16u << 20, n = bytes / 4, lines = bytes / 128;
+int main(int argc, char** argv) {
+  const size_t bytes = (size_t)(argc > 1 ? atoi(argv[1]) : 16) << 20, n = bytes / 4, lines = bytes / 128;
   const int reps = 4096, blocks = 8;
   uint32_t *buf, *lat, *smid, *sink;
   cudaMalloc(&buf, bytes);
@@ -48,7 +50,7 @@ int main() {
   cudaMalloc(&smid, blocks * 4);
   cudaMalloc(&sink, 4);
   warm<<<592, 256>>>(buf, n, sink);
-  probe<<<blocks, 32>>>(buf, lines, lat, smid, reps);
+  probe<<<blocks, 32>>>(buf, lines, lat, smid, reps, bytes > (64u << 20));
   cudaDeviceSynchronize();
   std::vector<uint32_t> h((size_t)blocks * reps), sm(blocks);
   cudaMemcpy(h.data(), lat, h.size() * 4, cudaMemcpyDeviceToHost);
@@ -56,11 +58,11 @@ int main() {
   for (int b = 0; b < blocks; ++b) {
     std::vector<uint32_t> v(h.begin() + (size_t)b * reps, h.begin() + (size_t)(b + 1) * reps);
     std::sort(v.begin(), v.end());
-    printf("sm %3u: latency cycles p5 %u p25 %u p50 %u p75 %u p95 %u | histogram (50-cycle bins from 200):", sm[b],
-           v[reps / 20], v[reps / 4], v[reps / 2], v[3 * reps / 4], v[19 * reps / 20]);
-    int hist[16] = {0};
-    for (uint32_t x : v) { int k = x < 200 ? 0 : std::min(15, (int)((x - 200) / 50)); ++hist[k]; }
-    for (int k = 0; k < 16; ++k) printf(" %d", hist[k]);
+    printf("sm %3u: latency cycles p5 %u p25 %u p50 %u p75 %u p95 %u | histogram (50-cycle bins from 200, %zu MB):", sm[b],
+           v[reps / 20], v[reps / 4], v[reps / 2], v[3 * reps / 4], v[19 * reps / 20], bytes >> 20);
+    int hist[40] = {0};
+    for (uint32_t x : v) { int k = x < 200 ? 0 : std::min(39, (int)((x - 200) / 50)); ++hist[k]; }
+    for (int k = 0; k < 40; ++k) printf(" %d", hist[k]);
     printf("\n");
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));

@@ -19,7 +19,8 @@ for _ in range(3):
 tr = T.get_trace(g, 64).astype(np.int64)
 nw = 148 * 4 * 8
 W = np.fromfile("/tmp/wdone.bin", dtype=np.uint64).astype(np.int64).reshape(16, 2, nw)
-for r in range(2, 8):
+detail = "--detail" in sys.argv
+for r in range(2, 12 if detail else 8):
     for ph in range(2):
         t = W[r, ph]
         if not (t > 0).any():
@@ -29,6 +30,13 @@ for r in range(2, 8):
         blk = d.reshape(-1, 8)                  # 8 warps per block
         inblock = (blk.max(1) - blk.min(1)).mean()
         bmean = blk.mean(1)
+        if detail:
+            bmax = blk.max(1)
+            order = np.argsort(bmax)
+            pct = [np.percentile(bmax, p) for p in (50, 90, 99, 100)]
+            slow = ", ".join(f"b{int(b)}(sm~{int(b) % 148}):{bmax[b]:.1f}" for b in order[-6:][::-1])
+            print(f"   r{r} {'AB'[ph]} block completion p50 {pct[0]:.1f} p90 {pct[1]:.1f} p99 {pct[2]:.1f} "
+                  f"max {pct[3]:.1f} us; slowest: {slow}")
         print(f"r{r} {'AB'[ph]}: warps first {d.min():6.1f} median {np.median(d):6.1f} last {d.max():6.1f} us;"
               f" block means {bmean.min():6.1f}..{bmean.max():6.1f} (sd {bmean.std():5.1f});"
               f" mean in-block spread {inblock:5.1f}; "
