@@ -740,9 +740,17 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
   ExpandBufs eb{{ebuf, 0}, {ebuf + kListCap, 0}, cstart, sstart};
   unsigned long long work = 0;
   TGXD_MARK(0, 0);
-  for (uint32_t base = gw * 32; base < total; base += nw * 32) {
+  // a queue that does not fill every warp is spread over all of them (ipw
+  // slots per warp): a thin round's time is the one warp-iteration that has
+  // work, and 32 lanes in different branches of the search serialise in it
+#ifndef TGXD_NO_SPREAD
+  const uint32_t ipw = fin ? min(32u, max(1u, (total + nw - 1) / nw)) : 32u;
+#else
+  const uint32_t ipw = 32u;
+#endif
+  for (uint32_t base = gw * ipw; base < total; base += nw * ipw) {
     const uint32_t i = base + lane;
-    bool valid = i < total;
+    bool valid = lane < ipw && i < total;
     uint32_t item = i;
     int32_t x = kInf;
     int2 ep = make_int2(kInf, (int32_t)kNoPos);
@@ -769,12 +777,12 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
       t0 = __ldg(&a.g.okm[v + 1].x);
       valid = x != kInf;
     }
-    if (base == gw * 32) {
+    if (base == gw * ipw) {
       TGXD_MARK(1, item);
       TGXD_MARK(2, x + ep.x + s0 + t0 + km0);
     }
     expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix, depart);
-    if (base == gw * 32) TGXD_MARK(3, eb.sm.n + eb.ch.n + (uint32_t)work);
+    if (base == gw * ipw) TGXD_MARK(3, eb.sm.n + eb.ch.n + (uint32_t)work);
   }
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
@@ -967,10 +975,16 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
   // small ranges: 32 per warp window, static shares (a window holds 32 to
   // ~1000 edges; taking windows from an atomic cursor instead measured 4 %
   // slower on config 2's rotation — the cursor's line slows its L2 slice)
-  const unsigned long long nwin = (nsmall + 31) / 32;
+  // (a list that does not fill every warp's window is spread: epw ranges per window)
+#ifndef TGXD_NO_SPREAD
+  const uint32_t epw = (uint32_t)min(32ull, max(1ull, (nsmall + nw - 1) / nw));
+#else
+  const uint32_t epw = 32u;
+#endif
+  const unsigned long long nwin = (nsmall + epw - 1) / epw;
   auto win_load = [&](unsigned long long w) -> uint2 {
-    const unsigned long long i = w * 32 + lane;
-    return (w < nwin && i < nsmall) ? __ldcg(a.smalls + i) : make_uint2(0u, 0u);
+    const unsigned long long i = w * epw + lane;
+    return (w < nwin && lane < epw && i < nsmall) ? __ldcg(a.smalls + i) : make_uint2(0u, 0u);
   };
   // chunks and windows are one sequence of work units dealt round-robin:
   // the windows continue where the chunks end, so the warps that took one
