@@ -726,6 +726,83 @@ __device__ __forceinline__ void flush_work(Control* ctl, unsigned long long work
   __syncthreads();
 }
 
+// End of an expand phase: the warps' staged list entries and work counts go
+// out with ONE reservation per block and list (a spread thin round would
+// otherwise end with ~5K same-address atomics on each counter).
+__device__ __forceinline__ void block_finish_expand(const TravArgs& a, ExpandBufs& eb,
+                                                    unsigned long long work) {
+  __shared__ uint32_t s_n[2][kWarps];
+  __shared__ unsigned long long s_w[kWarps];
+  __shared__ unsigned long long s_base[2];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
+  if (lane == 0) {
+    s_n[0][w] = eb.sm.n;
+    s_n[1][w] = eb.ch.n;
+    s_w[w] = work;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t0 = 0, t1 = 0;
+    unsigned long long tw = 0;
+#pragma unroll
+    for (int k = 0; k < kWarps; ++k) {
+      const uint32_t c0 = s_n[0][k], c1 = s_n[1][k];
+      s_n[0][k] = t0;
+      s_n[1][k] = t1;
+      t0 += c0;
+      t1 += c1;
+      tw += s_w[k];
+    }
+    unsigned long long b0 = 0, b1 = 0;
+    if (t0) b0 = atomicAdd(&a.ctl->smalls, (unsigned long long)t0);
+    if (t1) b1 = atomicAdd(&a.ctl->chunks, (unsigned long long)t1);
+    if (tw) atomicAdd(&a.ctl->edges, tw);
+    s_base[0] = b0;
+    s_base[1] = b1;
+  }
+  __syncthreads();
+  {
+    const unsigned long long b = s_base[0] + s_n[0][w] - eb.sstart;
+    for (uint32_t i = lane; i < eb.sm.n; i += 32)
+      if (TGXD_IN_CAP(b + i, 1)) a.smalls[b + i] = eb.sm.buf[i];
+  }
+  {
+    const unsigned long long b = s_base[1] + s_n[1][w] - eb.cstart;
+    for (uint32_t i = lane; i < eb.ch.n; i += 32)
+      if (TGXD_IN_CAP(b + i, 1)) a.chunks[b + i] = eb.ch.buf[i];
+  }
+  eb.sm.n = eb.ch.n = 0;
+  __syncthreads();
+}
+
+// End of a relax phase: the warps' staged queue entries with one reservation per block.
+__device__ __forceinline__ void block_push_drain(PushBuf& pb, Control* ctl, unsigned long long pstart,
+                                                 uint32_t* fout) {
+  __shared__ uint32_t s_pn[kWarps];
+  __shared__ unsigned long long s_pbase;
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  if (lane == 0) s_pn[w] = pb.n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 0; k < kWarps; ++k) {
+      const uint32_t c = s_pn[k];
+      s_pn[k] = t;
+      t += c;
+    }
+    s_pbase = t ? atomicAdd(&ctl->pushes, (unsigned long long)t) : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long b = s_pbase + s_pn[w] - pstart;
+  for (uint32_t i = lane; i < pb.n; i += 32)
+    if (TGXD_IN_CAP(b + i, 0)) fout[b + i] = pb.buf[i];
+  pb.n = 0;
+  __syncthreads();
+}
+
 // Phase A over a sparse frontier queue (items [0, F) of fin) or, with
 // fin == nullptr, over the implicit dense frontier: every slot whose label
 // bound is below its expansion bound.
@@ -784,10 +861,15 @@ __device__ TGXD_PHASE void phase_a(const TravArgs& a, const uint32_t* fin, uint3
     expand_warp(a, valid, item, x, ep, s0, t0, km0, eb, work, ix, depart);
     if (base == gw * ipw) TGXD_MARK(3, eb.sm.n + eb.ch.n + (uint32_t)work);
   }
+#ifdef TGXD_WARP_DRAIN
   list_drain(eb.sm, &a.ctl->smalls, sstart, a.smalls);
   list_drain(eb.ch, &a.ctl->chunks, cstart, a.chunks);
   TGXD_MARK(4, eb.sm.n);
   flush_work(a.ctl, work);
+#else
+  TGXD_MARK(4, eb.sm.n);
+  block_finish_expand(a, eb, work);
+#endif
   TGXD_MARK(5, 0);
 }
 
@@ -1004,7 +1086,11 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
     if (w == w0) TGXD_MARK(10, pb.n);
     sv = snx;
   }
+#ifdef TGXD_WARP_DRAIN
   if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
+#else
+  if (rx.push) block_push_drain(pb, a.ctl, rx.pstart, rx.fout);
+#endif
   TGXD_MARK(11, pb.n);
 }
 
