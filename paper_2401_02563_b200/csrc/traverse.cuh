@@ -1490,12 +1490,25 @@ struct Counters {
 __device__ __forceinline__ Counters read_counters(const Control* ctl) {
   __shared__ Counters s_c;
   if (threadIdx.x == 0) {
+#ifdef TGXD_SCALAR_COUNTERS
     s_c.pushes = __ldcg(&ctl->pushes);
     s_c.improved = __ldcg(&ctl->improved);
     s_c.chunks = __ldcg(&ctl->chunks);
     s_c.smalls = __ldcg(&ctl->smalls);
     s_c.edges = __ldcg(&ctl->edges);
     s_c.pchunks = __ldcg(&ctl->pchunks);
+#else
+    static_assert(offsetof(Control, pushes) == 0 && offsetof(Control, pchunks) == 40,
+                  "the six post-barrier counters lead the control block");
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(ctl);
+    const ulonglong2 c0 = __ldcg(p), c1 = __ldcg(p + 1), c2 = __ldcg(p + 2);
+    s_c.pushes = c0.x;
+    s_c.improved = c0.y;
+    s_c.chunks = c1.x;
+    s_c.smalls = c1.y;
+    s_c.edges = c2.x;
+    s_c.pchunks = c2.y;
+#endif
   }
   __syncthreads();
   const Counters c = s_c;
