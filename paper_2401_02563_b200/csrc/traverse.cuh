@@ -295,6 +295,37 @@ __device__ __forceinline__ void push_flush32(PushBuf& pb, Control* ctl,
   __syncwarp();
 }
 
+// The relax's variant: kPushFlush staged entries per reservation (buffers of
+// kPushFlush + 32 entries: the round kernel's). The pushes counter is one
+// address: at 0.66 ns per atomic a heavy round's ~85K 32-entry reservations
+// kept it busy for half the phase. Config 2 rotation / config 4 fastest, ms:
+// 32 entries 1.020 / 4.23, 64 0.969 / 3.97, 128 0.964 / 3.91, 256 0.965 / 3.93
+// (profiles/r02ap; the work lists' granule kListFlush stays 32: 64 equal, 128 slower).
+#ifndef TGXD_PUSH_FLUSH
+#define TGXD_PUSH_FLUSH 128
+#endif
+constexpr uint32_t kPushFlush = TGXD_PUSH_FLUSH;
+static_assert(kPushFlush % 32 == 0 && kPushFlush >= 32, "whole 32-entry rows");
+__device__ __forceinline__ void push_flush_n(PushBuf& pb, Control* ctl,
+                                             unsigned long long pstart, uint32_t* fout) {
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  uint32_t v[kPushFlush / 32];
+#pragma unroll
+  for (uint32_t j = 0; j < kPushFlush / 32; ++j) v[j] = pb.buf[32 * j + lane];
+  const uint32_t tail = pb.buf[kPushFlush + lane];
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&ctl->pushes, (unsigned long long)kPushFlush);
+  base = __shfl_sync(0xffffffffu, base, 0) - pstart;
+#pragma unroll
+  for (uint32_t j = 0; j < kPushFlush / 32; ++j)
+    if (TGXD_IN_CAP(base + 32 * j + lane, 0)) fout[base + 32 * j + lane] = v[j];
+  __syncwarp();
+  if (lane + kPushFlush < pb.n) pb.buf[lane] = tail;
+  pb.n -= kPushFlush;
+  __syncwarp();
+}
+
 __device__ __forceinline__ void push_drain(PushBuf& pb, Control* ctl, unsigned long long pstart,
                                            uint32_t* fout) {
   if (pb.n == 0) return;
@@ -302,8 +333,9 @@ __device__ __forceinline__ void push_drain(PushBuf& pb, Control* ctl, unsigned l
   __syncwarp();
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(&ctl->pushes, (unsigned long long)pb.n);
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (lane < pb.n && TGXD_IN_CAP(base - pstart + lane, 0)) fout[base - pstart + lane] = pb.buf[lane];
+  base = __shfl_sync(0xffffffffu, base, 0) - pstart;
+  for (uint32_t i = lane; i < pb.n; i += 32)
+    if (TGXD_IN_CAP(base + i, 0)) fout[base + i] = pb.buf[i];
   pb.n = 0;
   __syncwarp();
 }
@@ -469,7 +501,7 @@ __device__ __forceinline__ void relax_apply(const TravArgs& a, const uint2 (&pl)
         const uint32_t lane = lane_id();
         if (p[u]) pb.buf[pb.n + __popc(bal & ((1u << lane) - 1))] = idx[u] | (old[u] == kInf ? a.fresh : 0u);
         pb.n += __popc(bal);
-        if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
+        if (pb.n >= kPushFlush) push_flush_n(pb, a.ctl, rx.pstart, rx.fout);
       }
     }
 #if TGXD_PF_GRID
@@ -1086,11 +1118,7 @@ __device__ TGXD_PHASE void phase_b(const TravArgs& a, unsigned long long nchunks
     if (w == w0) TGXD_MARK(10, pb.n);
     sv = snx;
   }
-#ifdef TGXD_WARP_DRAIN
-  if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
-#else
   if (rx.push) block_push_drain(pb, a.ctl, rx.pstart, rx.fout);
-#endif
   TGXD_MARK(11, pb.n);
 }
 
@@ -1277,7 +1305,7 @@ __device__ TGXD_PHASE void pull_scan32(const TravArgs& a, RelaxCtx& rx, PullBufs
     const bool fresh = a.Q == 1 ? lim == a.qp[0].vhi + 1 : lim == a.qp[i / a.n].vhi + 1;
     if (improved) b.pb.buf[b.pb.n + __popc(bal & ((1u << lane) - 1))] = i | (fresh ? a.fresh : 0u);
     b.pb.n += __popc(bal);
-    if (b.pb.n >= 32) push_flush32(b.pb, a.ctl, rx.pstart, rx.fout);
+    if (b.pb.n >= kPushFlush) push_flush_n(b.pb, a.ctl, rx.pstart, rx.fout);
   }
   slot_list_push(b.rbuf, b.nr, open, make_uint2(o.x, o.y));
   if (b.nr >= 32) pull_search32(a, b, 32);
@@ -1392,7 +1420,7 @@ __device__ TGXD_PHASE void phase_pull2(const TravArgs& a, RelaxCtx& rx, unsigned
     if (bal) {
       if (lane == 0) pb.buf[pb.n] = slot | (fresh ? a.fresh : 0u);
       pb.n += 1;
-      if (pb.n >= 32) push_flush32(pb, a.ctl, rx.pstart, rx.fout);
+      if (pb.n >= kPushFlush) push_flush_n(pb, a.ctl, rx.pstart, rx.fout);
     }
   }
   push_drain(pb, a.ctl, rx.pstart, rx.fout);
@@ -1696,7 +1724,7 @@ __device__ TmaBufs tma_bufs_of_warp() {
 }
 #endif
 __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(TravArgs a) {
-  __shared__ uint32_t s_buf[kWarps][64];
+  __shared__ uint32_t s_buf[kWarps][kPushFlush + 32];
   __shared__ uint2 s_ebuf[kWarps][2 * kListCap];
   __shared__ uint2 s_rbuf[kWarps][64];
   __shared__ uint4 s_obuf[kWarps][64];
@@ -2012,7 +2040,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
 __global__ void __launch_bounds__(kThreads, TGXD_X_BLOCKS)
     relax_only_kernel(TravArgs a, unsigned long long nchunks, unsigned long long nsmall,
                       unsigned long long pstart, uint32_t* fout, int push, uint32_t upw) {
-  __shared__ uint32_t s_buf[kWarps][64];
+  __shared__ uint32_t s_buf[kWarps][kPushFlush + 32];
   const uint32_t lane = lane_id();
   const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
   PushBuf pb{s_buf[threadIdx.x >> 5], 0};
@@ -2038,7 +2066,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_X_BLOCKS)
       relax_window(a, i < nsmall ? __ldcg(a.smalls + i) : make_uint2(0u, 0u), rx, pb);
     }
   }
-  if (rx.push) push_drain(pb, a.ctl, rx.pstart, rx.fout);
+  if (rx.push) block_push_drain(pb, a.ctl, rx.pstart, rx.fout);
 }
 #endif
 
