@@ -1057,6 +1057,15 @@ static int launch_body(tgxd_graph* G, const Prepared& P, const Prepared& Pout, u
   const int pdiv = pf ? atoi(pf) : (fast ? 4 : 2);
   a.pull_f = pdiv <= 0 ? ~0ull : std::max<uint64_t>(1024, slots / pdiv);
   if (const char* pfx = getenv("TGXD_PULL_F")) a.pull_f = strtoull(pfx, nullptr, 10);  // tests
+  // ... and only when it jumped there from a much smaller frontier. A big
+  // frontier reached by a jump (config 2's own source: 43K -> 2.58M slots)
+  // is about to push the bulk of the query's edges at labels the pull can
+  // prune against; one reached by steady growth (config 4 LD: 1.17M -> 5.44M)
+  // follows a round that already relaxed most of them, and the pull then
+  // rescans long in-segments for little (621 vs 473 us for that round,
+  // profiles/r02at). Fastest sweeps keep the plain size rule.
+  a.pull_grow = fast ? 0u : 6u;
+  if (const char* pg = getenv("TGXD_PULL_GROW")) a.pull_grow = (unsigned)std::max(0, atoi(pg));
   // AUTO tail handoff (traverse.cuh): a frontier past its peak and at most
   // 16K slots goes to the cluster tail engine — its 16 SMs are fast per round
   // (5-7 us for a few hundred slots against ~20 us on the grid) but a ninth

@@ -99,6 +99,8 @@ struct TravArgs {
   unsigned long long dense_f;  // AUTO: frontier above this expands densely
   unsigned long long push_w;   // AUTO: rounds relaxing more edges do not push
   unsigned long long pull_f;   // AUTO: a frontier at least this big is pulled
+  unsigned int pull_grow;      // ... if it also grew by at least this factor over the previous
+                               // round's (0: no growth condition)
   unsigned long long handoff_f;  // AUTO: a shrinking frontier this small goes to the cluster tail engine
   unsigned long long async_f;    // AUTO: a frontier this small goes to the async engine when it
                                  // grows by less than handoff_growth per round (or shrinks,
@@ -1848,6 +1850,7 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
           *a.copy_flag = 1u;
         }
       }
+      const unsigned long long f_prev = st.last_f;
       if (!xcnt) st.last_f = (uint32_t)min(F, 0xffffffffull);
       const bool go_local = a.mode != TGXD_MODE_DENSE && !st.dense &&
                             (xcnt ? xcnt <= kLocalMaxW : F <= kLocalMaxF);
@@ -1894,7 +1897,8 @@ __global__ void __launch_bounds__(kThreads, TGXD_MIN_BLOCKS) traverse_kernel(Tra
       uint32_t* fin = st.flip ? a.fb : a.fa;
       uint32_t* fout = st.flip ? a.fa : a.fb;
       const bool pull = !xcnt && (a.mode == TGXD_MODE_PULL ||
-                                  (a.mode == TGXD_MODE_AUTO && F >= a.pull_f));
+                                  (a.mode == TGXD_MODE_AUTO && F >= a.pull_f &&
+                                   F >= f_prev * a.pull_grow));
       if (tr) {
         trace_round(a, st.rounds, 0, gtimer());
         trace_round(a, st.rounds, 3, F);
